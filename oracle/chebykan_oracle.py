@@ -1,0 +1,309 @@
+"""CPU oracle for the fused Chebyshev-KAN layer -- TEST INFRASTRUCTURE ONLY.
+
+This module is a float64 NumPy restatement of the reference's LUT-mode hot
+path (arxiv 2511.14852 / PolyKAN, package ``polykan`` under
+/root/reference/pkg/src/polykan).  It is the *checker*: only ``tests/``,
+``__graft_entry__.smoke()`` and the ``cpu_baseline`` / ``--impl reference``
+legs of ``bench.py`` may import it.  The product path
+(``paper_2511_14852_b200``) never imports, links or calls anything here and
+fails loudly when its CUDA library is missing.
+
+Pinning: every function below is checked bit-for-bit (or to <=1e-13 where
+BLAS summation order may differ) against golden vectors produced by running
+the reference itself in the build container (``tests/golden/make_golden.py``
+-> ``tests/golden/*.npz``; test ``tests/test_oracle_golden.py``).
+
+Citations are ``path:line`` relative to /root/reference/pkg/src/polykan/.
+"""
+from __future__ import annotations
+
+import math
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+# lut.py:28 -- positions within this distance of a node snap onto it.
+SNAP_EPS = 1e-9
+# lut.py:32 -- the reference's default table size.
+REFERENCE_DEFAULT_LUT_SIZE = 32768
+# kernels.py:81-82 -- default CPU tile shape of TileSchedule.for_dims.
+REF_TILE_IN = 64
+REF_TILE_OUT = 32
+
+
+# ---------------------------------------------------------------------------
+# Basis and table construction
+
+
+def chebyshev_rows(degree: int, t: np.ndarray) -> np.ndarray:
+    """T_0..T_degree at every point by the three-term recurrence.
+
+    basis.py:112-119 with the Chebyshev coefficients of basis.py:54-60
+    (alpha=1, beta=2x, gamma=1); the division by alpha=1.0 is kept so the
+    float64 rounding sequence is the reference's.
+    """
+    t = np.asarray(t, dtype=np.float64)
+    rows = np.empty((degree + 1,) + t.shape, dtype=np.float64)
+    rows[0] = np.ones_like(t)
+    if degree >= 1:
+        rows[1] = t.copy()
+    for k in range(1, degree):
+        rows[k + 1] = ((2.0 * t) * rows[k] - 1.0 * rows[k - 1]) / 1.0
+    return rows
+
+
+def chebyshev_trig_rows(degree: int, t: np.ndarray) -> np.ndarray:
+    """cos(k * arccos t), the exact path used for the interpolation report.
+
+    basis.py:144-152.
+    """
+    t = np.asarray(t, dtype=np.float64)
+    theta = np.arccos(t)
+    k = np.arange(degree + 1, dtype=np.float64).reshape((degree + 1,) + (1,) * t.ndim)
+    return np.cos(k * theta)
+
+
+def build_table(degree: int, lut_size: int):
+    """Uniform-grid table of T_k values (f64) and per-cell slopes (f32).
+
+    lut.py:76-94: grid x_i = -1 + i*step with step = 2/(N-1) and the last
+    node forced to exactly 1.0; slopes are float64 first differences over
+    step, stored as float32.  Returns (values[K,N] f64, slopes[K,N-1] f32,
+    step).
+    """
+    if lut_size < 2:
+        raise ValueError("lut_size must be >= 2")
+    if degree < 0:
+        raise ValueError(f"degree must be >= 0, got {degree}")
+    step = 2.0 / (lut_size - 1)
+    nodes = -1.0 + step * np.arange(lut_size, dtype=np.float64)
+    nodes[-1] = 1.0
+    values = chebyshev_rows(degree, nodes)
+    slopes = ((values[:, 1:] - values[:, :-1]) / step).astype(np.float32)
+    return values, slopes, step
+
+
+def interp_error_bound(degree: int, lut_size: int) -> np.ndarray:
+    """Per-feature bound step^2/8 * max|T_k''| = step^2/8 * k^2 (k^2-1)/3.
+
+    lut.py:143-153 (Chebyshev closed form, basis.py:215-217).
+    """
+    step = 2.0 / (lut_size - 1)
+    k = np.arange(degree + 1, dtype=np.float64)
+    return (step * step / 8.0) * np.maximum(k * k * (k * k - 1.0) / 3.0, 0.0)
+
+
+def cell_positions(t: np.ndarray, lut_size: int):
+    """Clamp to [-1,1], locate the cell, snap node echoes.  lut.py:97-106."""
+    tc = np.clip(np.asarray(t, dtype=np.float64), -1.0, 1.0)
+    pos = (tc + 1.0) * 0.5 * (lut_size - 1)
+    idx = np.minimum(pos.astype(np.int64), lut_size - 2)
+    frac = pos - idx
+    frac = np.where(frac < SNAP_EPS, 0.0, frac)
+    frac = np.where(frac > 1.0 - SNAP_EPS, 1.0, frac)
+    return idx, frac
+
+
+def lut_values(t: np.ndarray, values: np.ndarray) -> np.ndarray:
+    """v[idx](1-f) + v[idx+1] f for every point; (...,) -> (..., K).
+
+    lut.py:109-115 (the position-major copy of lut.py:64 is values.T).
+    """
+    idx, frac = cell_positions(t, values.shape[1])
+    by_pos = np.ascontiguousarray(values.T)
+    f = frac[..., None]
+    return by_pos[idx] * (1.0 - f) + by_pos[idx + 1] * f
+
+
+def lut_values_and_slopes(t: np.ndarray, values: np.ndarray, slopes: np.ndarray):
+    """Interpolated values plus the active cell's float32 slope (as f64).
+
+    lut.py:118-123 (slope copy lifted to f64 as in lut.py:66).
+    """
+    idx, frac = cell_positions(t, values.shape[1])
+    by_pos = np.ascontiguousarray(values.T)
+    s_by_pos = np.ascontiguousarray(slopes.T.astype(np.float64))
+    f = frac[..., None]
+    return by_pos[idx] * (1.0 - f) + by_pos[idx + 1] * f, s_by_pos[idx]
+
+
+# ---------------------------------------------------------------------------
+# Coefficient layouts (tensor.py:26-90)
+
+
+def jod_to_doj(c_jod: np.ndarray) -> np.ndarray:
+    """[I,O,K] -> contiguous [K,O,I]; tensor.py:77-82."""
+    return np.ascontiguousarray(np.asarray(c_jod).transpose(2, 1, 0))
+
+
+def doj_to_jod(c_doj: np.ndarray) -> np.ndarray:
+    """[K,O,I] -> contiguous [I,O,K]; tensor.py:85-90."""
+    return np.ascontiguousarray(np.asarray(c_doj).transpose(2, 1, 0))
+
+
+# ---------------------------------------------------------------------------
+# Fused LUT-mode layer
+
+
+def _tiles(n: int, width: int):
+    return [slice(s, min(s + width, n)) for s in range(0, n, width)]
+
+
+def _run(fn, items, threads: int) -> None:
+    # kernels.py:236-242: tasks own disjoint outputs, so order is irrelevant.
+    if threads <= 1:
+        for it in items:
+            fn(it)
+    else:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(fn, items))
+
+
+def _planes(t: np.ndarray, values: np.ndarray, slopes=None):
+    """(K,B,I) contiguous basis planes (and slope planes); kernels.py:194-217."""
+    if slopes is None:
+        v = lut_values(t, values)
+        return np.ascontiguousarray(v.transpose(2, 0, 1)), None
+    v, s = lut_values_and_slopes(t, values, slopes)
+    return (np.ascontiguousarray(v.transpose(2, 0, 1)),
+            np.ascontiguousarray(s.transpose(2, 0, 1)))
+
+
+def layer_forward(x, c_doj, values, bias=None, *, tile_in=REF_TILE_IN,
+                  tile_out=REF_TILE_OUT, threads=1) -> np.ndarray:
+    """y[b,o] = sum_i sum_k T_k(tanh x[b,i]) C[k,o,i] (+ bias[o]).
+
+    Follows fused_forward (kernels.py:351-371): tanh (288), basis planes
+    (289), per-(input tile, output tile) batched matmul summed over the
+    order axis into a unique slot (293-318), then the combine stage folding
+    input tiles in ascending order and adding the bias (321-348).
+    """
+    x = np.asarray(x, dtype=np.float64)
+    c = np.asarray(c_doj, dtype=np.float64)
+    n_feat, d_out, d_in = c.shape
+    if x.ndim != 2 or x.shape[1] != d_in:
+        raise ValueError(f"input must be (batch, {d_in}), got {x.shape}")
+    if values.shape[0] != n_feat:
+        raise ValueError(f"LUT has {values.shape[0]} features, coefficients expect {n_feat}")
+    batch = x.shape[0]
+    planes, _ = _planes(np.tanh(x), values)
+    ins, outs = _tiles(d_in, tile_in), _tiles(d_out, tile_out)
+    partial = np.zeros((len(outs), len(ins), batch, tile_out))
+
+    def task(pair):
+        a, b = pair
+        js, os_ = ins[a], outs[b]
+        prod = np.matmul(planes[:, :, js], c[:, os_, js].swapaxes(1, 2))
+        partial[b, a, :, : os_.stop - os_.start] = prod.sum(axis=0)
+
+    _run(task, [(a, b) for a in range(len(ins)) for b in range(len(outs))], threads)
+    y = np.zeros((batch, d_out))
+    for b, os_ in enumerate(outs):
+        acc = partial[b, 0, :, : os_.stop - os_.start].copy()
+        for a in range(1, len(ins)):
+            acc += partial[b, a, :, : os_.stop - os_.start]
+        y[:, os_] = acc
+    if bias is not None:
+        y += np.asarray(bias, dtype=np.float64)
+    return y
+
+
+def layer_backward(x, c_doj, dy, values, slopes, *, include_tanh_jacobian=True,
+                   tile_in=REF_TILE_IN, tile_out=REF_TILE_OUT, threads=1):
+    """(dC in DOJ [K,O,I], dX [B,I], db [O]) for loss gradient dy.
+
+    Follows backward_fused (kernels.py:374-447): per tile pair, dC tile =
+    dy^T . planes (429); x-grad stage = sum_{k>=1} (dy . C_k) * slope_k
+    (430-434); ordered merge over output tiles (439-442); tanh Jacobian
+    (443-444).  db = dy.sum(0) is Layer.backward's bias gradient
+    (model.py:147).
+    """
+    x = np.asarray(x, dtype=np.float64)
+    dy = np.asarray(dy, dtype=np.float64)
+    c = np.asarray(c_doj, dtype=np.float64)
+    n_feat, d_out, d_in = c.shape
+    batch = x.shape[0]
+    if dy.shape != (batch, d_out):
+        raise ValueError(f"dy must have shape ({batch}, {d_out}), got {dy.shape}")
+    t = np.tanh(x)
+    planes, slope_planes = _planes(t, values, slopes)
+    ins, outs = _tiles(d_in, tile_in), _tiles(d_out, tile_out)
+    dc = np.zeros_like(c)
+    stage = np.zeros((len(outs), batch, d_in))
+
+    def task(pair):
+        a, b = pair
+        js, os_ = ins[a], outs[b]
+        dyt = dy[:, os_]
+        dc[:, os_, js] = np.matmul(dyt.T[None, :, :], planes[:, :, js])
+        if n_feat > 1:
+            g = np.matmul(dyt[None, :, :], c[1:, os_, js])
+            stage[b, :, js] = (g * slope_planes[1:, :, js]).sum(axis=0)
+
+    _run(task, [(a, b) for a in range(len(ins)) for b in range(len(outs))], threads)
+    dx = np.zeros((batch, d_in))
+    for b in range(len(outs)):
+        dx += stage[b]
+    if include_tanh_jacobian:
+        dx *= 1.0 - t * t
+    return dc, dx, dy.sum(axis=0)
+
+
+def exact_forward(x, c_doj, bias=None) -> np.ndarray:
+    """Unfused exact cos(k acos tanh x) contraction; kernels.py:450-478 (trig=True)."""
+    x = np.asarray(x, dtype=np.float64)
+    c = np.asarray(c_doj, dtype=np.float64)
+    planes = chebyshev_trig_rows(c.shape[0] - 1, np.tanh(x))
+    y = np.einsum("kbi,koi->bo", planes, c)
+    if bias is not None:
+        y = y + bias
+    return y
+
+
+# ---------------------------------------------------------------------------
+# Error measures
+
+
+def max_rel_err(got, want, floor: float = 1e-9) -> float:
+    """Elementwise relative error with a magnitude-aware floor; verify.py:45-57."""
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    if got.size == 0:
+        return 0.0
+    big = float(np.abs(want).max(initial=0.0))
+    scale = np.maximum(np.abs(want), max(floor, 1e-7 * big))
+    return float(np.max(np.abs(got - want) / scale))
+
+
+def normwise_err(got, want) -> float:
+    """max|got-want| / max|want| -- the tolerance measure of SURVEY.md F1."""
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    if got.size == 0:
+        return 0.0
+    big = float(np.abs(want).max(initial=0.0))
+    return float(np.abs(got - want).max() / max(big, 1e-30))
+
+
+# ---------------------------------------------------------------------------
+# Seeded inputs (perf.py:157-169 distribution, generated in float32)
+
+
+def bench_inputs(batch, d_in, d_out, degree, seed=0):
+    """x ~ U(-1.5,1.5), C ~ U(-s,s) with s=1/sqrt(I*K) (JOD), dy ~ N(0,1).
+
+    Mirrors perf.py:157-169 but draws in float32 so the GPU and the oracle
+    see identical, exactly representable inputs.
+    """
+    rng = np.random.default_rng(seed)
+    k = degree + 1
+    s = 1.0 / math.sqrt(d_in * k)
+    x = rng.uniform(-1.5, 1.5, size=(batch, d_in)).astype(np.float32)
+    c_jod = rng.uniform(-s, s, size=(d_in, d_out, k)).astype(np.float32)
+    dy = rng.standard_normal((batch, d_out)).astype(np.float32)
+    return x, c_jod, dy
+
+
+def default_threads() -> int:
+    return max(1, os.cpu_count() or 1)

@@ -1,0 +1,22 @@
+import pathlib
+import sys
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")
+
+
+def golden_layer_cases():
+    return sorted(GOLDEN.glob("layer_*.npz"))
+
+
+def golden_lut_cases():
+    return sorted(p for p in GOLDEN.glob("lut_d*_n*.npz"))
