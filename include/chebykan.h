@@ -1,0 +1,120 @@
+/*
+ * chebykan.h -- C ABI of the B200-native fused Chebyshev-KAN layer.
+ *
+ * Drop-in boundary for the hot path of PolyKAN (arxiv 2511.14852).  The
+ * reference's operator API is Python/NumPy (package `polykan`, citations
+ * below are relative to /root/reference/pkg/src/polykan/); each entry point
+ * states the reference interface it replaces.  All tensors are plain device
+ * pointers owned by the caller (torch tensors on the host side), fp32 unless
+ * noted, row-major, contiguous.  Calls are asynchronous on the given stream.
+ * Return value: 0 = ok, otherwise a ck_status code; ck_last_error() returns
+ * the (thread-local) message.  No exceptions cross the ABI.
+ *
+ * Coefficient layout: DOJ = [K][O][I] (order, output, input; input innermost),
+ * the kernel layout of tensor.py:26-28 / doj_index tensor.py:72-74.
+ * K = degree + 1.
+ */
+#ifndef CHEBYKAN_H_
+#define CHEBYKAN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CK_API __attribute__((visibility("default")))
+#else
+#define CK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CK_OK = 0,
+  CK_INVALID_ARGUMENT = 1, /* reference raises ValueError (kernels.py:245-260, 281-282, 395-408) */
+  CK_CUDA_ERROR = 2,
+  CK_UNSUPPORTED = 3,
+  CK_WORKSPACE_TOO_SMALL = 4
+} ck_status;
+
+typedef struct ck_lut ck_lut; /* device-resident LUT (LutTable, lut.py:43-73) */
+
+/* Library version (major*10000 + minor*100 + patch). */
+CK_API int ck_version(void);
+/* Message of the last failing call on this host thread. */
+CK_API const char* ck_last_error(void);
+/* 1 when the current device is sm_100 (B200) and the kernels can launch. */
+CK_API int ck_device_supported(int device);
+
+/* --- LUT ------------------------------------------------------------------
+ * ck_lut_build replaces lut_build(BasisKind.CHEBYSHEV, degree, lut_size)
+ * (lut.py:76-94): float64 grid -1 + i*step with the last node forced to 1.0,
+ * values by the T_k recurrence (basis.py:112-119), slopes = float64 first
+ * differences / step rounded to float32.  Built on the device in float64
+ * (bit-identical to the reference table); stored as float32 values and
+ * float32 slopes, position-major, for the kernels.  Errors as lut.py:78-81.
+ */
+CK_API int ck_lut_build(int degree, int lut_size, int device, ck_lut** out);
+/* Wrap a caller-provided table (e.g. a PKLT file, load_lut lut.py:180-206):
+ * values[K][N] float64 and slopes[K][N-1] float32, host memory. */
+CK_API int ck_lut_create(int degree, int lut_size, const double* values_host, const float* slopes_host,
+                  int device, ck_lut** out);
+CK_API void ck_lut_destroy(ck_lut* lut);
+/* degree, lut_size and step of a table (LutTable fields, lut.py:52-56). */
+CK_API int ck_lut_info(const ck_lut* lut, int* degree, int* lut_size, double* step);
+/* Copy the float64 values [K][N] and float32 slopes [K][N-1] to host memory
+ * (either pointer may be NULL); synchronous. */
+CK_API int ck_lut_read(const ck_lut* lut, double* values_host, float* slopes_host);
+
+/* --- Basis expansion ---------------------------------------------------------
+ * phi[b][i][k] = interp of T_k at tanh(x[b][i]) and, when slopes != NULL,
+ * slopes[b][i][k] = the active cell's slope: interp_rows_with_slope
+ * (lut.py:97-123) applied to np.tanh(x) (kernels.py:288, 414).  The cell
+ * (clip, idx, frac, snap) is computed in float64 so it matches the
+ * reference's choice exactly; values are interpolated in float32. */
+CK_API int ck_expand(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi, float* slopes,
+              void* stream);
+
+/* --- Coefficient preparation (reorder_to_doj consumer, tensor.py:77-82) ---
+ * Converts fp32 DOJ coefficients into the kernels' tensor-core operands:
+ * bf16 hi/lo split copies in DOJ [K][O][I] (forward, unit stride in i) and
+ * DJO [K][I][O] (input-gradient GEMM), plus sum_i C[0][o][i].  Call once
+ * per parameter update; `prep` is an opaque caller-owned device buffer of
+ * ck_coeff_prep_bytes(...) bytes. */
+CK_API size_t ck_coeff_prep_bytes(int d_in, int d_out, int n_feat);
+CK_API int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int n_feat, void* prep,
+                     size_t prep_bytes, void* stream);
+
+/* --- Forward: replaces fused_forward (kernels.py:351-371) ------------------
+ * y[b][o] = sum_i sum_k T_k(tanh x[b][i]) C[k][o][i] + bias[o]
+ * x [B][I], y [B][O]; bias nullable.  Workspace: ck_forward_workspace_bytes. */
+CK_API size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
+CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
+               const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream);
+
+/* --- Backward: replaces backward_fused (kernels.py:374-447) plus the bias
+ * gradient of Layer.backward (model.py:147) --------------------------------
+ * dc_doj[k][o][i] = sum_b dy[b][o] T_k(tanh x[b][i])
+ * dx[b][i] = J * sum_o sum_{k>=1} dy[b][o] C[k][o][i] slope_k(b,i),
+ *            J = 1 - tanh^2 x when include_tanh_jacobian (KernelMode, kernels.py:35-44)
+ * db[o] = sum_b dy[b][o]
+ * Any of dx / dc_doj / db may be NULL to skip.  dc is reduced by a
+ * fixed-order two-stage merge: bit-reproducible run to run. */
+CK_API size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
+CK_API int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
+                const void* prep, int include_tanh_jacobian, float* dx, float* dc_doj, float* db,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+/* --- Deterministic merge: replaces combine's ordered fold (kernels.py:321-348)
+ * and the ordered x-grad merge (kernels.py:438-442) as a standalone op.
+ * out[n] = (accumulate ? out[n] : 0) + sum_{s=0}^{S-1} partials[s*stride + n],
+ * summed in ascending s. */
+CK_API int ck_merge(const float* partials, int num_partials, int64_t stride, int64_t n, float* out,
+             int accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHEBYKAN_H_ */

@@ -1,0 +1,35 @@
+"""B200-native fused Chebyshev-KAN layer (hot path of arxiv 2511.14852 / PolyKAN).
+
+Public surface mirrors the reference package ``polykan`` for this path:
+``lut_build`` / ``LutTable`` (lut.py), ``CoeffTensor`` / ``Layout`` /
+``reorder_to_doj`` (tensor.py), ``fused_forward`` / ``backward_fused`` /
+``KernelMode`` / ``TileSchedule`` (kernels.py), plus the torch module
+``ChebyKANLayer`` and data-parallel helpers.  All compute runs in the
+sm_100a kernels of ``lib/libchebykan.so``; there is no CPU fallback.
+"""
+from .kernels import (
+    LUT_MODE,
+    BasisPath,
+    KernelMode,
+    NonFiniteInputError,
+    PreparedCoeff,
+    TileSchedule,
+    backward_fused,
+    count_flops,
+    fused_forward,
+)
+from .layer import ChebyKANFunction, ChebyKANLayer
+from .lut import (
+    DEFAULT_LUT_SIZE,
+    LutTable,
+    expand,
+    interp_error_bound,
+    lut_build,
+    lut_from_arrays,
+    lut_max_error_bound,
+    lut_size_for_budget,
+)
+from .parallel import GradientAllreducer, allreduce_gradients, chebykan_parameters, shard_bounds
+from .tensor import CoeffTensor, Layout, doj_index, jod_index, reorder_to_doj, reorder_to_jod
+
+__version__ = "1.0.0"

@@ -1,0 +1,317 @@
+// extern "C" entry points (include/chebykan.h): argument validation with
+// the reference's error wording, workspace carving, and the orchestration of
+// the forward / backward kernels on the caller's stream.
+#include <string>
+
+#include "ck_common.cuh"
+#include "ck_internal.h"
+
+namespace ck {
+
+namespace {
+thread_local std::string g_error;
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+// Opaque coefficient-prep buffer: bf16 hi/lo DOJ [K][O][ldI], DJO [K][I][ldO],
+// and c0sum[O] = sum_i C[0][o][i].
+struct PrepLayout {
+  int64_t ldI, ldO;
+  size_t doj_hi, doj_lo, djo_hi, djo_lo, c0sum, total;
+  PrepLayout(int I, int O, int K) {
+    ldI = round_up(I, 8);
+    ldO = round_up(O, 8);
+    const size_t doj = align_up(sizeof(__nv_bfloat16) * K * O * ldI);
+    const size_t djo = align_up(sizeof(__nv_bfloat16) * K * I * ldO);
+    doj_hi = 0;
+    doj_lo = doj_hi + doj;
+    djo_hi = doj_lo + doj;
+    djo_lo = djo_hi + djo;
+    c0sum = djo_lo + djo;
+    total = c0sum + align_up(sizeof(float) * O);
+  }
+};
+
+struct FwdLayout {
+  int64_t chunk, ldI;
+  size_t hi, lo, split, total;
+  int64_t split_elems;
+  FwdLayout(int64_t B, int I, int O, int K) {
+    chunk = B < kChunkRows ? B : kChunkRows;
+    if (chunk < 1) chunk = 1;
+    ldI = round_up(I, 8);
+    const int d = K - 1;
+    const size_t planes = align_up(sizeof(__nv_bfloat16) * (d > 0 ? d : 0) * chunk * ldI);
+    split_elems = d > 0 ? gemm_split_ws_elems(chunk, O, 1, I) : 0;
+    hi = 0;
+    lo = planes;
+    split = lo + planes;
+    total = split + align_up(sizeof(float) * split_elems) + kAlign;
+  }
+};
+
+constexpr int kDbSlots = 32;
+
+struct BwdLayout {
+  int64_t chunk, n_chunks, ldO, ldB;
+  size_t dy_hi, dy_lo, dyt_hi, dyt_lo, g, pt_hi, pt_lo, db_part, db_tmp, split, total;
+  int64_t split_elems;
+  BwdLayout(int64_t B, int I, int O, int K) {
+    chunk = B < kChunkRows ? B : kChunkRows;
+    if (chunk < 1) chunk = 1;
+    n_chunks = ceil_div(B > 0 ? B : 1, chunk);
+    ldO = round_up(O, 8);
+    ldB = round_up(chunk, 8);
+    const int64_t d = K - 1;
+    const size_t dy = align_up(sizeof(__nv_bfloat16) * chunk * ldO);
+    const size_t dyt = align_up(sizeof(__nv_bfloat16) * O * ldB);
+    const size_t gb = align_up(sizeof(float) * d * chunk * I);
+    const size_t pt = align_up(sizeof(__nv_bfloat16) * d * I * ldB);
+    const size_t dbp = align_up(sizeof(double) * n_chunks * kDbSlots * O);
+    int64_t s1 = d > 0 ? gemm_split_ws_elems(chunk, I, static_cast<int>(d), O) : 0;
+    int64_t s2 = d > 0 ? gemm_split_ws_elems(O, I, static_cast<int>(d), chunk) : 0;
+    split_elems = s1 > s2 ? s1 : s2;
+    dy_hi = 0;
+    dy_lo = dy_hi + dy;
+    dyt_hi = dy_lo + dy;
+    dyt_lo = dyt_hi + dyt;
+    g = dyt_lo + dyt;
+    pt_hi = g + gb;
+    pt_lo = pt_hi + pt;
+    db_part = pt_lo + pt;
+    db_tmp = db_part + dbp;
+    split = db_tmp + align_up(sizeof(float) * O);
+    total = split + align_up(sizeof(float) * split_elems) + kAlign;
+  }
+};
+
+template <typename T>
+T* at(void* base, size_t off) {
+  uintptr_t b = (reinterpret_cast<uintptr_t>(base) + kAlign - 1) / kAlign * kAlign;
+  return reinterpret_cast<T*>(b + off);
+}
+
+int check_dims(int64_t batch, int d_in, int d_out, const ck_lut* lut) {
+  CK_CHECK(lut != nullptr, "LUT mode requires a LutTable");
+  CK_CHECK(batch >= 0, "batch must be >= 0");
+  CK_CHECK(d_in >= 1 && d_out >= 1, "d_in and d_out must be >= 1");
+  CK_CHECK(batch * static_cast<int64_t>(d_in) < (int64_t(1) << 40), "input too large");
+  return kOk;
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_error = msg; }
+const char* last_error() { return g_error.c_str(); }
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cached[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
+}  // namespace ck
+
+using ck::kOk;
+
+extern "C" int ck_version(void) { return 1 * 10000 + 0 * 100 + 0; }
+
+extern "C" const char* ck_last_error(void) { return ck::last_error(); }
+
+extern "C" int ck_device_supported(int device) {
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device) != cudaSuccess) return 0;
+  return (major == 10 && minor == 0) ? 1 : 0;
+}
+
+extern "C" int ck_expand(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi, float* slopes,
+                         void* stream) {
+  CK_TRY(ck::check_dims(rows, cols, 1, lut));
+  CK_CHECK(x != nullptr && phi != nullptr, "ck_expand: NULL tensor");
+  return ck::launch_expand_f32(x, rows, cols, lut, phi, slopes, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" size_t ck_coeff_prep_bytes(int d_in, int d_out, int n_feat) {
+  if (d_in < 1 || d_out < 1 || n_feat < 1) return 0;
+  return ck::PrepLayout(d_in, d_out, n_feat).total + ck::kAlign;
+}
+
+extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int n_feat, void* prep,
+                                size_t prep_bytes, void* stream) {
+  CK_CHECK(d_in >= 1 && d_out >= 1, "d_in and d_out must be >= 1");
+  CK_CHECK(n_feat >= 1, "degree must be >= 0");
+  CK_CHECK(coeff_doj != nullptr && prep != nullptr, "ck_coeff_prepare: NULL tensor");
+  CK_CHECK(prep_bytes >= ck_coeff_prep_bytes(d_in, d_out, n_feat), "coefficient prep buffer too small");
+  auto s = static_cast<cudaStream_t>(stream);
+  const ck::PrepLayout L(d_in, d_out, n_feat);
+  const int64_t I = d_in, O = d_out, K = n_feat;
+  // DOJ copies: rows (k,o), unit stride in i
+  CK_TRY(ck::launch_split_rows(coeff_doj, 1, K * O, I, 0, ck::at<__nv_bfloat16>(prep, L.doj_hi),
+                               ck::at<__nv_bfloat16>(prep, L.doj_lo), L.ldI, 0, s));
+  // DJO copies: per k, transpose [O][I] -> [I][O]
+  CK_TRY(ck::launch_split_transpose(coeff_doj, K, O, I, O * I, ck::at<__nv_bfloat16>(prep, L.djo_hi),
+                                    ck::at<__nv_bfloat16>(prep, L.djo_lo), L.ldO, I * L.ldO, s));
+  // k = 0 term: T_0 == 1 so its contribution is the per-output constant
+  CK_TRY(ck::launch_row_sum(coeff_doj, O, I, ck::at<float>(prep, L.c0sum), s));
+  return kOk;
+}
+
+extern "C" size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat) {
+  if (d_in < 1 || d_out < 1 || n_feat < 1 || batch < 0) return 0;
+  return ck::FwdLayout(batch, d_in, d_out, n_feat).total;
+}
+
+extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
+                          const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream) {
+  CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
+  CK_CHECK(x != nullptr && y != nullptr && prep != nullptr, "ck_forward: NULL tensor");
+  const int K = lut->n_feat, d = K - 1;
+  const ck::FwdLayout W(batch, d_in, d_out, K);
+  if (workspace_bytes < W.total) {
+    ck::set_error("forward workspace too small: need " + std::to_string(W.total) + " bytes");
+    return ck::kWorkspace;
+  }
+  if (batch == 0) return kOk;
+  auto s = static_cast<cudaStream_t>(stream);
+  const ck::PrepLayout P(d_in, d_out, K);
+  void* pv = const_cast<void*>(prep);
+  const float* c0sum = ck::at<float>(pv, P.c0sum);
+  auto* phi_hi = ck::at<__nv_bfloat16>(workspace, W.hi);
+  auto* phi_lo = ck::at<__nv_bfloat16>(workspace, W.lo);
+  for (int64_t r0 = 0; r0 < batch; r0 += W.chunk) {
+    const int64_t rows = batch - r0 < W.chunk ? batch - r0 : W.chunk;
+    float* yc = y + r0 * d_out;
+    if (d == 0) {
+      CK_TRY(ck::launch_fill_rows(yc, rows, d_out, bias, c0sum, s));
+      continue;
+    }
+    const int64_t plane = W.chunk * W.ldI;
+    CK_TRY(ck::launch_expand_planes(x + r0 * d_in, rows, d_in, lut, 1, phi_hi, phi_lo, W.ldI, plane, s));
+    ck::GemmProblem g{};
+    g.a = {phi_hi, phi_lo, rows, W.ldI, plane, d};
+    g.b = {ck::at<__nv_bfloat16>(pv, P.doj_hi), ck::at<__nv_bfloat16>(pv, P.doj_lo), d_out, P.ldI,
+           static_cast<int64_t>(d_out) * P.ldI, K};
+    g.R = d_in;
+    g.S = d;           // k = 1..d; the k = 0 term is c0sum (T_0 == 1)
+    g.a_seg0 = 0;
+    g.b_seg0 = 1;
+    g.nz = 1;
+    g.out = yc;
+    g.ldo = d_out;
+    g.out_z_stride = rows * d_out;
+    g.bias0 = bias;
+    g.bias1 = c0sum;
+    g.split_ws = ck::at<float>(workspace, W.split);
+    g.split_ws_elems = W.split_elems;
+    CK_TRY(ck::gemm_bf16x3(g, s));
+  }
+  return kOk;
+}
+
+extern "C" size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat) {
+  if (d_in < 1 || d_out < 1 || n_feat < 1 || batch < 0) return 0;
+  return ck::BwdLayout(batch, d_in, d_out, n_feat).total;
+}
+
+extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
+                           const void* prep, int include_tanh_jacobian, float* dx, float* dc_doj, float* db,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
+  CK_CHECK(x != nullptr && dy != nullptr && prep != nullptr, "ck_backward: NULL tensor");
+  const int K = lut->n_feat, d = K - 1;
+  const ck::BwdLayout W(batch, d_in, d_out, K);
+  if (workspace_bytes < W.total) {
+    ck::set_error("backward workspace too small: need " + std::to_string(W.total) + " bytes");
+    return ck::kWorkspace;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t I = d_in, O = d_out;
+  if (batch == 0) {
+    if (dc_doj) CK_CUDA(cudaMemsetAsync(dc_doj, 0, sizeof(float) * K * O * I, s));
+    if (db) CK_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * O, s));
+    return kOk;
+  }
+  const ck::PrepLayout P(d_in, d_out, K);
+  void* pv = const_cast<void*>(prep);
+  auto* dy_hi = ck::at<__nv_bfloat16>(workspace, W.dy_hi);
+  auto* dy_lo = ck::at<__nv_bfloat16>(workspace, W.dy_lo);
+  auto* dyt_hi = ck::at<__nv_bfloat16>(workspace, W.dyt_hi);
+  auto* dyt_lo = ck::at<__nv_bfloat16>(workspace, W.dyt_lo);
+  float* g = ck::at<float>(workspace, W.g);
+  auto* pt_hi = ck::at<__nv_bfloat16>(workspace, W.pt_hi);
+  auto* pt_lo = ck::at<__nv_bfloat16>(workspace, W.pt_lo);
+  double* db_part = ck::at<double>(workspace, W.db_part);
+  float* split_ws = ck::at<float>(workspace, W.split);
+  // db is needed for dC_0 as well; keep a private copy when the caller skips it
+  const bool need_db = db != nullptr || dc_doj != nullptr;
+
+  int64_t ci = 0;
+  for (int64_t r0 = 0; r0 < batch; r0 += W.chunk, ++ci) {
+    const int64_t rows = batch - r0 < W.chunk ? batch - r0 : W.chunk;
+    const float* xc = x + r0 * I;
+    const float* dyc = dy + r0 * O;
+    if (need_db) CK_TRY(ck::launch_col_partial(dyc, rows, O, db_part + ci * ck::kDbSlots * O, ck::kDbSlots, s));
+    if (d == 0) {
+      if (dx) CK_CUDA(cudaMemsetAsync(dx + r0 * I, 0, sizeof(float) * rows * I, s));
+      continue;
+    }
+    if (dx) {
+      CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
+      ck::GemmProblem gx{};
+      gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
+      gx.b = {ck::at<__nv_bfloat16>(pv, P.djo_hi), ck::at<__nv_bfloat16>(pv, P.djo_lo), I, P.ldO, I * P.ldO, K};
+      gx.R = O;
+      gx.S = 1;
+      gx.b_seg0 = 1;   // z = k - 1
+      gx.b_seg_z = 1;
+      gx.nz = d;
+      gx.out = g;
+      gx.ldo = I;
+      gx.out_z_stride = rows * I;
+      gx.split_ws = split_ws;
+      gx.split_ws_elems = W.split_elems;
+      CK_TRY(ck::gemm_bf16x3(gx, s));
+      CK_TRY(ck::launch_dx_combine(g, rows * I, xc, rows, d_in, lut, include_tanh_jacobian, dx + r0 * I, s));
+    }
+    if (dc_doj) {
+      CK_TRY(ck::launch_split_transpose(dyc, 1, rows, O, 0, dyt_hi, dyt_lo, W.ldB, 0, s));
+      CK_TRY(ck::launch_expand_planes_t(xc, rows, d_in, lut, 1, pt_hi, pt_lo, W.ldB, I * W.ldB, s));
+      ck::GemmProblem gc{};
+      gc.a = {dyt_hi, dyt_lo, O, W.ldB, O * W.ldB, 1};
+      gc.b = {pt_hi, pt_lo, I, W.ldB, I * W.ldB, d};
+      gc.R = rows;
+      gc.S = 1;
+      gc.b_seg_z = 1;  // plane z holds k = z + 1
+      gc.nz = d;
+      gc.out = dc_doj + O * I;
+      gc.ldo = I;
+      gc.out_z_stride = O * I;
+      gc.accumulate = ci > 0 ? 1 : 0;  // ascending chunk order: reproducible
+      gc.split_ws = split_ws;
+      gc.split_ws_elems = W.split_elems;
+      CK_TRY(ck::gemm_bf16x3(gc, s));
+    }
+  }
+  if (need_db) {
+    float* dbo = db != nullptr ? db : ck::at<float>(workspace, W.db_tmp);
+    CK_TRY(ck::launch_col_finish(db_part, static_cast<int>(W.n_chunks * ck::kDbSlots), O, dbo, s));
+    if (dc_doj) CK_TRY(ck::launch_broadcast_cols(dc_doj, O, I, dbo, s));  // dC_0 = db (T_0 == 1)
+  }
+  return kOk;
+}
+
+extern "C" int ck_merge(const float* partials, int num_partials, int64_t stride, int64_t n, float* out,
+                        int accumulate, void* stream) {
+  CK_CHECK(num_partials >= 0 && n >= 0 && stride >= n, "ck_merge: bad extents");
+  CK_CHECK(out != nullptr && (partials != nullptr || num_partials == 0), "ck_merge: NULL tensor");
+  return ck::launch_merge(partials, num_partials, stride, n, out, accumulate, static_cast<cudaStream_t>(stream));
+}

@@ -1,0 +1,113 @@
+// Internal (non-exported) interfaces shared by the ChebyKAN .cu files.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/chebykan.h"
+
+struct ck_lut {
+  int degree = 0;
+  int n_feat = 0;      // K = degree + 1
+  int lut_size = 0;    // N
+  double step = 0.0;   // 2 / (N - 1)
+  int device = 0;
+  double* values64 = nullptr;  // [K][N]   float64 build-precision table (validation)
+  float* values_pm = nullptr;  // [N][K]   float32, position-major (gather rows idx, idx+1)
+  float* slopes_pm = nullptr;  // [N-1][K] float32 cell slopes, position-major
+};
+
+namespace ck {
+
+// Rows processed per internal chunk by ck_forward / ck_backward (bounds the
+// workspace; chunks are processed in ascending order on one stream, so the
+// accumulated dC is bit-reproducible).
+constexpr int64_t kChunkRows = 32768;
+
+// --- LUT view passed by value to kernels ----------------------------------
+struct LutView {
+  const float* values_pm;
+  const float* slopes_pm;
+  int K;
+  int N;
+};
+inline LutView view(const ck_lut* l) { return LutView{l->values_pm, l->slopes_pm, l->n_feat, l->lut_size}; }
+
+// --- expansion (ck_expand.cu) ---------------------------------------------
+// phi[r][c][k] (f32) and optional slopes[r][c][k] for every k.
+int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi,
+                      float* slopes, cudaStream_t s);
+// Split planes hi/lo [nk][rows][ld] for k = k0..K-1 (bf16, ld % 8 == 0).
+int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
+                         __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t plane_stride,
+                         cudaStream_t s);
+// Transposed split planes hi/lo [nk][cols][ldr] (element (r,c) at [k][c][r]).
+int launch_expand_planes_t(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
+                           __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ldr, int64_t plane_stride,
+                           cudaStream_t s);
+// dx[r][c] = J * sum_{k>=1} slope_k(cell(tanh x)) * g[k-1][r][c]
+int launch_dx_combine(const float* g, int64_t g_plane_stride, const float* x, int64_t rows, int cols,
+                      const ck_lut* lut, int jacobian, float* dx, cudaStream_t s);
+
+// --- elementwise / reductions (ck_split.cu) -------------------------------
+// hi/lo [z][rows][ld] <- in [z][rows][cols] (input pitch = cols)
+int launch_split_rows(const float* in, int64_t nz, int64_t rows, int64_t cols, int64_t in_z_stride,
+                      __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t out_z_stride,
+                      cudaStream_t s);
+// hi/lo [z][cols][ld] <- transpose of in [z][rows][cols]
+int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t cols, int64_t in_z_stride,
+                           __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t out_z_stride,
+                           cudaStream_t s);
+// out[r] = sum_c in[r][c]  (float64 accumulation in a fixed order)
+int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s);
+// part[slot][c] = sum over rows of in[rows][cols]  (float64, fixed order)
+int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part, int slots,
+                       cudaStream_t s);
+// out[c] = sum_{s<slots} part[s][c] -> float
+int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s);
+// out[n] = (accumulate ? out[n] : 0) + sum_{s<S} partials[s * stride + n]
+int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate,
+                 cudaStream_t s);
+// out[r][c] = a[c] + b[c] (either nullable)
+int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b,
+                     cudaStream_t s);
+// out[r][c] += a[c] + b[c] (either nullable)
+int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s);
+// out[r][c] = v[r]  (dC_0 = db broadcast over inputs)
+int launch_broadcast_cols(float* out, int64_t rows, int64_t cols, const float* v, cudaStream_t s);
+
+// --- tcgen05 split-precision GEMM (ck_gemm.cu) ----------------------------
+// out[z][m][n] (+)= sum_{s<S} sum_r A[aseg][m][r] * B[bseg][n][r]
+//   aseg = a_seg0 + s + a_seg_z * z,  bseg = b_seg0 + s + b_seg_z * z
+// A and B are bf16 hi/lo pairs, K-major, row pitch lda/ldb (multiple of 8),
+// segment stride a_seg_stride/b_seg_stride elements.  BF16x3: the MMA sums
+// hi*hi + hi*lo + lo*hi in fp32 TMEM accumulators.
+struct GemmOperand {
+  const __nv_bfloat16* hi;
+  const __nv_bfloat16* lo;
+  int64_t rows;        // M (for A) or N (for B)
+  int64_t ld;          // row pitch in elements
+  int64_t seg_stride;  // elements between segments
+  int64_t segs;        // number of segments addressable
+};
+struct GemmProblem {
+  GemmOperand a, b;
+  int64_t R;          // reduction extent per segment
+  int S;              // segments summed into each output
+  int a_seg0, a_seg_z, b_seg0, b_seg_z;
+  int nz;             // number of outputs along z
+  float* out;
+  int64_t ldo, out_z_stride;
+  const float* bias0;  // nullable, added per column n
+  const float* bias1;  // nullable
+  int accumulate;      // out += result
+  float* split_ws;     // workspace for split-R partials (nullable -> no split)
+  int64_t split_ws_elems;
+};
+int gemm_bf16x3(const GemmProblem& p, cudaStream_t s);
+// Workspace (floats) the split-R path may want for this problem shape.
+int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R);
+
+}  // namespace ck

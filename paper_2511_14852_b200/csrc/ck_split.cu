@@ -1,0 +1,236 @@
+// Memory-bound helpers: bf16x3 operand splitting (with optional transpose),
+// fixed-order reductions (the two-stage deterministic merges) and fills.
+#include "ck_common.cuh"
+#include "ck_internal.h"
+
+namespace ck {
+namespace {
+
+constexpr int kThreads = 256;
+
+int blocks_for(int64_t items, int per_sm = 8) {
+  const int64_t want = ceil_div(items, kThreads);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
+  return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+// hi/lo [z][r][ld] from in [z][r][cols]; two columns per thread.
+__global__ void split_rows_kernel(const float* __restrict__ in, int64_t nz, int64_t rows, int64_t cols,
+                                  int64_t in_zs, uint32_t* __restrict__ hi, uint32_t* __restrict__ lo,
+                                  int64_t ld, int64_t out_zs) {
+  const int64_t pairs = (cols + 1) >> 1;
+  const int64_t n = nz * rows * pairs;
+  for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n;
+       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t z = it / (rows * pairs);
+    const int64_t rem = it - z * rows * pairs;
+    const int64_t r = rem / pairs;
+    const int64_t c = (rem - r * pairs) * 2;
+    const float* src = in + z * in_zs + r * cols + c;
+    const float a = src[0];
+    const float b = c + 1 < cols ? src[1] : 0.0f;
+    uint32_t h2, l2;
+    split_pack2(a, b, h2, l2);
+    const int64_t o = (z * out_zs + r * ld + c) >> 1;
+    hi[o] = h2;
+    lo[o] = l2;
+  }
+}
+
+// hi/lo [z][c][ld] = transpose of in [z][r][c] via 32x32 smem tiles.
+__global__ void split_transpose_kernel(const float* __restrict__ in, int64_t nz, int64_t rows, int64_t cols,
+                                       int64_t in_zs, __nv_bfloat16* __restrict__ hi,
+                                       __nv_bfloat16* __restrict__ lo, int64_t ld, int64_t out_zs) {
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+  const int64_t rt = ceil_div(rows, 32), ct = ceil_div(cols, 32);
+  for (int64_t t = blockIdx.x; t < nz * rt * ct; t += gridDim.x) {
+    const int64_t z = t / (rt * ct);
+    const int64_t rem = t - z * rt * ct;
+    const int64_t r0 = (rem / ct) * 32, c0 = (rem % ct) * 32;
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t r = r0 + j, c = c0 + tx;
+      tile[j][tx] = (r < rows && c < cols) ? in[z * in_zs + r * cols + c] : 0.0f;
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t c = c0 + j, r = r0 + tx;
+      if (c < cols && r < ld) {
+        __nv_bfloat16 h, l;
+        split_bf16(tile[tx][j], h, l);
+        const int64_t o = z * out_zs + c * ld + r;
+        hi[o] = h;
+        lo[o] = l;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// one warp per row, float64 lane partials combined by a fixed shuffle tree
+__global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    double acc = 0.0;
+    for (int64_t c = lane; c < cols; c += 32) acc += static_cast<double>(in[r * cols + c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[r] = static_cast<float>(acc);
+  }
+}
+
+// part[s][c] = sum of rows [s*chunk, min((s+1)*chunk, rows)) of column c
+__global__ void col_partial_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, int64_t chunk,
+                                   double* __restrict__ part, int slots) {
+  const int64_t n = static_cast<int64_t>(slots) * cols;
+  for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n;
+       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = it / cols, c = it - s * cols;
+    const int64_t r1 = (s + 1) * chunk < rows ? (s + 1) * chunk : rows;
+    double acc = 0.0;
+    for (int64_t r = s * chunk; r < r1; ++r) acc += static_cast<double>(in[r * cols + c]);
+    part[it] = acc;
+  }
+}
+
+__global__ void col_finish_kernel(const double* __restrict__ part, int slots, int64_t cols, float* __restrict__ out) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < slots; ++s) acc += part[s * cols + c];
+    out[c] = static_cast<float>(acc);
+  }
+}
+
+// out[n] = (acc ? out[n] : 0) + sum_s partials[s*stride + n], ascending s
+__global__ void merge_kernel(const float* __restrict__ partials, int S, int64_t stride, int64_t n,
+                             float* __restrict__ out, int accumulate) {
+  const bool vec = (stride % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(partials) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (vec) {
+    for (int64_t i = t0; i < n / 4; i += step) {
+      float4 a = accumulate ? reinterpret_cast<const float4*>(out)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < S; ++s) {
+        const float4 p = __ldg(reinterpret_cast<const float4*>(partials + s * stride) + i);
+        a.x += p.x;
+        a.y += p.y;
+        a.z += p.z;
+        a.w += p.w;
+      }
+      reinterpret_cast<float4*>(out)[i] = a;
+    }
+  } else {
+    for (int64_t i = t0; i < n; i += step) {
+      float a = accumulate ? out[i] : 0.0f;
+      for (int s = 0; s < S; ++s) a += partials[s * stride + i];
+      out[i] = a;
+    }
+  }
+}
+
+__global__ void fill_rows_kernel(float* __restrict__ out, int64_t rows, int64_t cols, const float* __restrict__ a,
+                                 const float* __restrict__ b) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = i % cols;
+    out[i] = (a ? a[c] : 0.0f) + (b ? b[c] : 0.0f);
+  }
+}
+
+__global__ void add_rows_kernel(float* __restrict__ out, int64_t rows, int64_t cols, const float* __restrict__ a,
+                                const float* __restrict__ b) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = i % cols;
+    out[i] += (a ? a[c] : 0.0f) + (b ? b[c] : 0.0f);
+  }
+}
+
+__global__ void broadcast_cols_kernel(float* __restrict__ out, int64_t rows, int64_t cols, const float* __restrict__ v) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    out[i] = v[i / cols];
+  }
+}
+
+}  // namespace
+
+int launch_split_rows(const float* in, int64_t nz, int64_t rows, int64_t cols, int64_t in_zs, __nv_bfloat16* hi,
+                      __nv_bfloat16* lo, int64_t ld, int64_t out_zs, cudaStream_t s) {
+  if (nz * rows * cols == 0) return kOk;
+  CK_CHECK(ld % 2 == 0 && out_zs % 2 == 0, "split_rows: pitch must be even");
+  split_rows_kernel<<<blocks_for(nz * rows * ((cols + 1) / 2)), kThreads, 0, s>>>(
+      in, nz, rows, cols, in_zs, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, out_zs);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t cols, int64_t in_zs,
+                           __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t out_zs, cudaStream_t s) {
+  if (nz * rows * cols == 0) return kOk;
+  const int64_t tiles = nz * ceil_div(rows, 32) * ceil_div(cols, 32);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  split_transpose_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s>>>(in, nz, rows, cols, in_zs,
+                                                                                         hi, lo, ld, out_zs);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s) {
+  if (rows == 0) return kOk;
+  row_sum_kernel<<<blocks_for(rows * 32), kThreads, 0, s>>>(in, rows, cols, out);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part, int slots, cudaStream_t s) {
+  if (cols == 0) return kOk;
+  const int64_t chunk = ceil_div(rows > 0 ? rows : 1, slots);
+  col_partial_kernel<<<blocks_for(slots * cols), kThreads, 0, s>>>(in, rows, cols, chunk, part, slots);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s) {
+  if (cols == 0) return kOk;
+  col_finish_kernel<<<blocks_for(cols), kThreads, 0, s>>>(part, slots, cols, out);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate, cudaStream_t s) {
+  if (n == 0) return kOk;
+  merge_kernel<<<blocks_for(ceil_div(n, 4)), kThreads, 0, s>>>(partials, S, stride, n, out, accumulate);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s) {
+  if (rows * cols == 0) return kOk;
+  fill_rows_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, a, b);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s) {
+  if (rows * cols == 0) return kOk;
+  add_rows_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, a, b);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_broadcast_cols(float* out, int64_t rows, int64_t cols, const float* v, cudaStream_t s) {
+  if (rows * cols == 0) return kOk;
+  broadcast_cols_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, v);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+}  // namespace ck

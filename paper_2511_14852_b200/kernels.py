@@ -1,0 +1,229 @@
+"""Operator API of the fused ChebyKAN layer (drop-in for polykan.kernels).
+
+Reference: /root/reference/pkg/src/polykan/kernels.py.  ``fused_forward``
+(kernels.py:351-371) and ``backward_fused`` (kernels.py:374-447) keep their
+names, argument meaning and ValueError wording; the work runs in the sm_100a
+kernels of libchebykan.so on the caller's current CUDA stream.  Tensors are
+torch CUDA tensors (fp32 compute; inputs of other dtypes are converted like
+the reference's ``np.asarray(x, dtype=float64)``).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from enum import Enum
+
+import torch
+
+from . import _lib
+from .lut import LutTable
+from .tensor import CoeffTensor, Layout
+
+
+class BasisPath(Enum):
+    LUT_INTERP = "lut"
+    EXACT_RECURRENCE = "exact"
+
+
+@dataclass(frozen=True)
+class KernelMode:
+    """Basis evaluation path and tanh chain-rule choice (kernels.py:35-44)."""
+
+    basis_path: BasisPath = BasisPath.LUT_INTERP
+    include_tanh_jacobian: bool = True
+
+
+LUT_MODE = KernelMode(BasisPath.LUT_INTERP)
+
+
+@dataclass(frozen=True)
+class TileSchedule:
+    """Reference CPU tiling descriptor (kernels.py:51-105).
+
+    Accepted for signature compatibility and validated the same way; the
+    B200 kernels choose their own tensor-core tiling (128 x 256 MMA tiles),
+    so the schedule does not change results.
+    """
+
+    tile_in: int
+    tile_out: int
+    lane_x: int
+    lane_y: int
+    g_x: int
+    g_y: int
+    d_in: int
+    d_out: int
+
+    def __post_init__(self) -> None:
+        if min(self.tile_in, self.tile_out, self.lane_x, self.lane_y) < 1:
+            raise ValueError("tile and lane sizes must be >= 1")
+        if self.tile_out != self.lane_y:
+            raise ValueError("output-aligned schedule requires tile_out == lane_y")
+        if self.d_in < 1 or self.d_out < 1:
+            raise ValueError("d_in and d_out must be >= 1")
+        if self.g_x != math.ceil(self.d_in / self.tile_in):
+            raise ValueError("g_x does not match ceil(d_in / tile_in)")
+        if self.g_y != math.ceil(self.d_out / self.tile_out):
+            raise ValueError("g_y does not match ceil(d_out / tile_out)")
+
+    @classmethod
+    def for_dims(cls, d_in: int, d_out: int, tile_in: int = 64, tile_out: int = 32, lane_x: int = 8,
+                 lane_y: int | None = None) -> "TileSchedule":
+        if d_in < 1 or d_out < 1:
+            raise ValueError("d_in and d_out must be >= 1")
+        lane_y = tile_out if lane_y is None else lane_y
+        return cls(tile_in, tile_out, lane_x, lane_y, math.ceil(d_in / tile_in), math.ceil(d_out / tile_out),
+                   d_in, d_out)
+
+
+class NonFiniteInputError(ValueError):
+    """Raised under validate=True; names the first offending element (kernels.py:170-183)."""
+
+    def __init__(self, b: int, j: int):
+        self.b = b
+        self.j = j
+        super().__init__(f"non-finite input at (b={b}, j={j})")
+
+
+def _check_finite(x: torch.Tensor) -> None:
+    bad = ~torch.isfinite(x)
+    if bool(bad.any()):
+        b, j = (int(v) for v in torch.nonzero(bad)[0].tolist())
+        raise NonFiniteInputError(b, j)
+
+
+class PreparedCoeff:
+    """Tensor-core operands derived from fp32 DOJ coefficients.
+
+    Holds the opaque prep buffer of ck_coeff_prepare: bf16 hi/lo split copies
+    in DOJ and DJO order plus sum_i C[0,o,i].  Rebuild after every update of
+    the coefficients (the Module does this by tracking the tensor version).
+    """
+
+    def __init__(self, coeff_doj: torch.Tensor):
+        if coeff_doj.dim() != 3:
+            raise ValueError("coefficients must be 3-D DOJ [K, O, I]")
+        k, o, i = coeff_doj.shape
+        self.n_feat, self.d_out, self.d_in = int(k), int(o), int(i)
+        self.device = coeff_doj.device
+        nbytes = _lib.lib().ck_coeff_prep_bytes(self.d_in, self.d_out, self.n_feat)
+        self.buffer = torch.empty(nbytes, dtype=torch.uint8, device=coeff_doj.device)
+        self.update(coeff_doj)
+
+    def update(self, coeff_doj: torch.Tensor) -> None:
+        c = coeff_doj.detach()
+        if c.dtype != torch.float32 or not c.is_contiguous():
+            c = c.to(torch.float32).contiguous()
+        rc = _lib.lib().ck_coeff_prepare(c.data_ptr(), self.d_in, self.d_out, self.n_feat, self.buffer.data_ptr(),
+                                         self.buffer.numel(), _lib.stream_handle(c.device))
+        _lib.check(rc, "ck_coeff_prepare")
+        self.key = (coeff_doj.data_ptr(), coeff_doj._version)
+
+
+def _as_f32(t: torch.Tensor, device) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(t)
+    return t.to(device=device, dtype=torch.float32).contiguous()
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut: LutTable, bias: torch.Tensor | None) -> torch.Tensor:
+    """y = fused layer forward on prepared coefficients (x fp32 contiguous [B, I])."""
+    b = x.shape[0]
+    y = torch.empty((b, prep.d_out), dtype=torch.float32, device=x.device)
+    lb = _lib.lib()
+    ws = _workspace(lb.ck_forward_workspace_bytes(b, prep.d_in, prep.d_out, prep.n_feat), x.device)
+    rc = lb.ck_forward(x.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(), _lib.ptr(bias),
+                       y.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle(x.device))
+    _lib.check(rc, "ck_forward")
+    return y
+
+
+def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut: LutTable, jacobian: bool,
+                 want_dx: bool = True, want_dc: bool = True, want_db: bool = True):
+    """(dC DOJ, dX, db) on prepared coefficients; unrequested outputs are None."""
+    b = x.shape[0]
+    dev = x.device
+    dx = torch.empty((b, prep.d_in), dtype=torch.float32, device=dev) if want_dx else None
+    dc = torch.empty((prep.n_feat, prep.d_out, prep.d_in), dtype=torch.float32, device=dev) if want_dc else None
+    db = torch.empty((prep.d_out,), dtype=torch.float32, device=dev) if want_db else None
+    lb = _lib.lib()
+    ws = _workspace(lb.ck_backward_workspace_bytes(b, prep.d_in, prep.d_out, prep.n_feat), dev)
+    rc = lb.ck_backward(x.data_ptr(), dy.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(),
+                        1 if jacobian else 0, _lib.ptr(dx), _lib.ptr(dc), _lib.ptr(db), ws.data_ptr(), ws.numel(),
+                        _lib.stream_handle(dev))
+    _lib.check(rc, "ck_backward")
+    return dc, dx, db
+
+
+def _check_common(coeff: CoeffTensor, lut: LutTable | None, sched: TileSchedule | None, mode: KernelMode,
+                  what: str) -> None:
+    if coeff.layout is not Layout.DOJ:
+        raise ValueError(f"{what} requires DOJ coefficient layout")
+    if mode.basis_path is not BasisPath.LUT_INTERP:
+        raise NotImplementedError("only the LUT-interpolation basis path runs on the B200 kernels")
+    if lut is None:
+        raise ValueError("LUT mode requires a LutTable")
+    if lut.n_features != coeff.n_feat:
+        raise ValueError(f"LUT has {lut.n_features} features, coefficients expect {coeff.n_feat}")
+    if sched is not None and (sched.d_in != coeff.d_in or sched.d_out != coeff.d_out):
+        raise ValueError("schedule dimensions do not match the coefficient tensor")
+
+
+def _device_of(coeff: CoeffTensor, lut: LutTable) -> torch.device:
+    return torch.device("cuda", lut.device)
+
+
+def fused_forward(x, coeff: CoeffTensor, lut: LutTable, sched: TileSchedule | None = None,
+                  mode: KernelMode = LUT_MODE, bias=None, *, validate: bool = False) -> torch.Tensor:
+    """y[b,o] = sum_j sum_k C[k,o,j] T_k(tanh x[b,j]) + bias[o]; returns (B, d_out) fp32.
+
+    kernels.py:351-371 (forward_partial 263-290 + combine 321-348).
+    """
+    _check_common(coeff, lut, sched, mode, "forward_partial")
+    dev = _device_of(coeff, lut)
+    x = _as_f32(x, dev)
+    if x.dim() != 2:
+        raise ValueError(f"input must be 2-D (batch, d_in), got shape {tuple(x.shape)}")
+    if x.shape[1] != coeff.d_in:
+        raise ValueError(f"input width {x.shape[1]} != coefficient d_in {coeff.d_in}")
+    if bias is not None:
+        bias = _as_f32(bias, dev)
+        if tuple(bias.shape) != (coeff.d_out,):
+            raise ValueError(f"bias must have shape ({coeff.d_out},), got {tuple(bias.shape)}")
+    if validate:
+        _check_finite(x)
+    prep = PreparedCoeff(_as_f32(coeff.as3d(), dev))
+    return forward_raw(x, prep, lut, bias)
+
+
+def backward_fused(x, coeff: CoeffTensor, dy, lut: LutTable, sched: TileSchedule | None = None,
+                   mode: KernelMode = LUT_MODE, *, validate: bool = False):
+    """(coeff_grad DOJ CoeffTensor, x_grad (B, d_in)); kernels.py:374-447."""
+    _check_common(coeff, lut, sched, mode, "backward_fused")
+    dev = _device_of(coeff, lut)
+    x = _as_f32(x, dev)
+    dy = _as_f32(dy, dev)
+    if x.dim() != 2 or dy.dim() != 2:
+        raise ValueError("x and dy must be 2-D")
+    if x.shape[1] != coeff.d_in:
+        raise ValueError(f"input width {x.shape[1]} != coefficient d_in {coeff.d_in}")
+    if tuple(dy.shape) != (x.shape[0], coeff.d_out):
+        raise ValueError(f"dy must have shape ({x.shape[0]}, {coeff.d_out}), got {tuple(dy.shape)}")
+    if validate:
+        _check_finite(x)
+        _check_finite(dy)
+    prep = PreparedCoeff(_as_f32(coeff.as3d(), dev))
+    dc, dx, _ = backward_raw(x, dy, prep, lut, mode.include_tanh_jacobian, want_db=False)
+    return CoeffTensor(coeff.d_in, coeff.d_out, coeff.degree, Layout.DOJ, dc), dx
+
+
+def count_flops(batch: int, d_in: int, d_out: int, degree: int) -> dict:
+    """Algorithmic FLOPs of one layer call."""
+    k = degree + 1
+    fwd = 2 * batch * d_in * d_out * k
+    bwd = 2 * batch * d_in * d_out * k + 2 * batch * d_in * d_out * degree
+    return {"fwd": fwd, "bwd": bwd, "train": fwd + bwd}

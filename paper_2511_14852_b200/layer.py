@@ -1,0 +1,147 @@
+"""ChebyKAN layer as a torch module with an autograd Function over the C ABI.
+
+Drop-in for the reference's ``Layer`` (model.py:86-148): constructor
+(input_dim, output_dim, degree), coefficients held in DOJ for the model's
+lifetime (model.py:97-101), seeded U(-s, s) init with s = 1/sqrt(I*K)
+(model.py:72-83), zero bias, forward caching x, backward returning dC, db,
+dX.  Leading dimensions are flattened like nn.Linear (the speech model feeds
+[batch, frames, bins]).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+from torch import nn
+
+from .kernels import PreparedCoeff, backward_raw, forward_raw
+from .lut import DEFAULT_LUT_SIZE, LutTable, lut_build
+
+
+class _LayerState:
+    """Per-module LUT and coefficient-prep cache (not a parameter)."""
+
+    def __init__(self, degree: int, lut_size: int, jacobian: bool):
+        self.degree = degree
+        self.lut_size = lut_size
+        self.jacobian = jacobian
+        self._luts: dict[int, LutTable] = {}
+        self._prep: PreparedCoeff | None = None
+
+    def lut(self, device: torch.device) -> LutTable:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        t = self._luts.get(idx)
+        if t is None:
+            t = lut_build(self.degree, self.lut_size, device=torch.device("cuda", idx))
+            self._luts[idx] = t
+        return t
+
+    def prepared(self, coeff_doj: torch.Tensor) -> PreparedCoeff:
+        key = (coeff_doj.data_ptr(), coeff_doj._version)
+        p = self._prep
+        if p is None or p.device != coeff_doj.device or tuple(coeff_doj.shape) != (p.n_feat, p.d_out, p.d_in):
+            p = PreparedCoeff(coeff_doj)
+            self._prep = p
+        elif p.key != key:
+            p.update(coeff_doj)
+        return p
+
+
+class ChebyKANFunction(torch.autograd.Function):
+    """y = ChebyKAN(x; C, b).  Forward: ck_forward.  Backward: ck_backward."""
+
+    @staticmethod
+    def forward(ctx, x, coeff_doj, bias, state: _LayerState):
+        if not x.is_cuda:
+            raise ValueError("ChebyKAN kernels run on CUDA tensors only (no CPU fallback)")
+        x = x.to(torch.float32).contiguous()
+        lut = state.lut(x.device)
+        prep = state.prepared(coeff_doj)
+        y = forward_raw(x, prep, lut, None if bias is None else bias.detach())
+        ctx.save_for_backward(x, coeff_doj)
+        ctx.state = state
+        ctx.has_bias = bias is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, coeff_doj = ctx.saved_tensors
+        state: _LayerState = ctx.state
+        dy = dy.to(torch.float32).contiguous()
+        need_x, need_c, need_b = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
+        prep = state.prepared(coeff_doj)
+        dc, dx, db = backward_raw(x, dy, prep, state.lut(x.device), state.jacobian, want_dx=need_x,
+                                  want_dc=need_c, want_db=need_b and ctx.has_bias)
+        return dx, dc, db, None
+
+
+class ChebyKANLayer(nn.Module):
+    """Chebyshev-KAN layer y = sum_i sum_k C[k,o,i] T_k(tanh x_i) + b_o.
+
+    Parameters
+    ----------
+    input_dim, output_dim, degree : layer shape (LayerSpec, model.py:37-54)
+    bias : learnable bias, zero-initialised (model.py:82)
+    lut_size : interpolation table size (reference default 32768, lut.py:32)
+    include_tanh_jacobian : KernelMode flag (kernels.py:35-44)
+    seed : when given, coefficients are drawn exactly as init_params
+        (numpy default_rng(seed).uniform(-s, s) in JOD order, model.py:72-83)
+    """
+
+    def __init__(self, input_dim: int, output_dim: int, degree: int, bias: bool = True,
+                 lut_size: int = DEFAULT_LUT_SIZE, include_tanh_jacobian: bool = True, seed: int | None = None,
+                 device=None):
+        super().__init__()
+        if input_dim < 1 or output_dim < 1:
+            raise ValueError("layer dimensions must be >= 1")
+        if degree < 0:
+            raise ValueError("degree must be >= 0")
+        self.input_dim, self.output_dim, self.degree = int(input_dim), int(output_dim), int(degree)
+        self.lut_size = int(lut_size)
+        k = self.degree + 1
+        self.coeff_doj = nn.Parameter(torch.empty((k, self.output_dim, self.input_dim), device=device))
+        self.bias = nn.Parameter(torch.zeros(self.output_dim, device=device)) if bias else None
+        self._state = _LayerState(self.degree, self.lut_size, include_tanh_jacobian)
+        self.reset_parameters(seed)
+
+    @property
+    def n_feat(self) -> int:
+        return self.degree + 1
+
+    @property
+    def cheby_coeffs(self) -> torch.Tensor:
+        """JOD [input, output, degree+1] view (tensor.py:26-28; original ChebyKAN layout)."""
+        return self.coeff_doj.permute(2, 1, 0)
+
+    @torch.no_grad()
+    def reset_parameters(self, seed: int | None = None) -> None:
+        s = 1.0 / math.sqrt(self.input_dim * self.n_feat)
+        if seed is None:
+            self.coeff_doj.uniform_(-s, s)
+        else:
+            rng = np.random.default_rng(seed)
+            jod = rng.uniform(-s, s, size=self.input_dim * self.output_dim * self.n_feat)
+            jod = jod.reshape(self.input_dim, self.output_dim, self.n_feat).transpose(2, 1, 0)
+            self.coeff_doj.copy_(torch.from_numpy(np.ascontiguousarray(jod)).to(torch.float32))
+        if self.bias is not None:
+            self.bias.zero_()
+
+    @torch.no_grad()
+    def load_jod(self, c_jod) -> None:
+        """Load coefficients given in JOD [I, O, K] order (reorder_to_doj, tensor.py:77-82)."""
+        c = torch.as_tensor(c_jod, dtype=torch.float32)
+        if tuple(c.shape) != (self.input_dim, self.output_dim, self.n_feat):
+            raise ValueError(f"expected JOD shape {(self.input_dim, self.output_dim, self.n_feat)}, got {tuple(c.shape)}")
+        self.coeff_doj.copy_(c.permute(2, 1, 0).contiguous())
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if x.shape[-1] != self.input_dim:
+            raise ValueError(f"expected input shape (batch, {self.input_dim}), got {tuple(x.shape)}")
+        lead = x.shape[:-1]
+        y = ChebyKANFunction.apply(x.reshape(-1, self.input_dim), self.coeff_doj, self.bias, self._state)
+        return y.reshape(*lead, self.output_dim)
+
+    def extra_repr(self) -> str:
+        return (f"input_dim={self.input_dim}, output_dim={self.output_dim}, degree={self.degree}, "
+                f"bias={self.bias is not None}, lut_size={self.lut_size}")

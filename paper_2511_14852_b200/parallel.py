@@ -1,0 +1,88 @@
+"""Data-parallel training of ChebyKAN layers: batch sharded, dC/db allreduced.
+
+One process per GPU (torchrun), ``torch.distributed`` with NCCL over
+NVLink/NVSwitch.  The forward and the input gradient are row-independent,
+so the only exchange per step is one allreduce(sum) of the concatenated
+fp32 coefficient and bias gradients of every ChebyKAN layer (SURVEY.md
+section 8(e)).  Rank shards are contiguous row blocks of the global batch.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+from torch import nn
+
+from .layer import ChebyKANLayer
+
+
+def shard_bounds(global_batch: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [start, stop) rows of rank's shard; earlier ranks take the remainder."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank must be in [0, world)")
+    base, rem = divmod(global_batch, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+def chebykan_parameters(module: nn.Module) -> list[torch.nn.Parameter]:
+    """Gradient-carrying parameters in a fixed order (module traversal order)."""
+    params: list[torch.nn.Parameter] = []
+    for m in module.modules():
+        if isinstance(m, ChebyKANLayer):
+            params.append(m.coeff_doj)
+            if m.bias is not None:
+                params.append(m.bias)
+    return params
+
+
+class GradientAllreducer:
+    """Flatten -> one allreduce -> scatter back, for a fixed parameter list.
+
+    The flat buffer is allocated once; per step the gradients are packed in a
+    fixed order, reduced with a single collective (sum, or mean when
+    ``average``), and copied back.  With NCCL the reduction order is fixed
+    for a given world size, so results are run-to-run reproducible.
+    """
+
+    def __init__(self, params: list[torch.nn.Parameter], group=None, average: bool = False):
+        self.params = list(params)
+        self.group = group
+        self.average = average
+        n = sum(p.numel() for p in self.params)
+        dev = self.params[0].device if self.params else torch.device("cpu")
+        self.flat = torch.empty(n, dtype=torch.float32, device=dev)
+
+    @property
+    def nbytes(self) -> int:
+        return self.flat.numel() * 4
+
+    def __call__(self) -> None:
+        if not dist.is_available() or not dist.is_initialized():
+            return
+        world = dist.get_world_size(self.group)
+        if world == 1:
+            return
+        off = 0
+        views = []
+        for p in self.params:
+            n = p.numel()
+            v = self.flat[off:off + n]
+            if p.grad is None:
+                v.zero_()
+            else:
+                v.copy_(p.grad.reshape(-1))
+            views.append((p, v))
+            off += n
+        dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+        if self.average:
+            self.flat.div_(world)
+        for p, v in views:
+            if p.grad is None:
+                p.grad = v.view_as(p).clone()
+            else:
+                p.grad.copy_(v.view_as(p))
+
+
+def allreduce_gradients(module: nn.Module, group=None, average: bool = False) -> None:
+    """One-shot helper: allreduce every ChebyKAN gradient of ``module``."""
+    GradientAllreducer(chebykan_parameters(module), group, average)()

@@ -1,0 +1,68 @@
+"""CPU-side checks of the C ABI: the in-tree library loads, exports every
+symbol include/chebykan.h declares, and validates arguments with the
+reference's error wording without touching a GPU."""
+import ctypes
+import re
+
+import pytest
+
+from conftest import ROOT
+from paper_2511_14852_b200 import _lib
+
+HEADER = ROOT / "include" / "chebykan.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"CK_API\s+[\w\s\*]+?\b(ck_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for name in ("ck_lut_build", "ck_expand", "ck_coeff_prepare", "ck_forward", "ck_backward", "ck_merge"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    syms = declared_symbols()
+    assert syms, "no symbols parsed from the header"
+    for name in syms:
+        assert hasattr(lib, name), f"{name} not exported by {_lib.LIB_PATH}"
+    assert set(syms) == set(_lib.SIGNATURES), "ctypes signatures out of sync with the header"
+
+
+def test_version_and_sizes_are_host_only():
+    lib = _lib.lib()
+    assert lib.ck_version() >= 10000
+    small = lib.ck_coeff_prep_bytes(64, 64, 5)
+    big = lib.ck_coeff_prep_bytes(4096, 4096, 9)
+    assert 0 < small < big
+    # bf16 hi/lo in two layouts: >= 4 bytes per coefficient per layout
+    assert big >= 2 * 4 * 4096 * 4096 * 9
+    assert lib.ck_forward_workspace_bytes(16384, 4096, 4096, 9) > 0
+    assert lib.ck_backward_workspace_bytes(16384, 4096, 4096, 9) > 0
+    assert lib.ck_coeff_prep_bytes(0, 4, 2) == 0
+
+
+def test_forward_without_lut_is_a_value_error():
+    lib = _lib.lib()
+    rc = lib.ck_forward(None, 4, 8, 8, None, None, None, None, None, 0, None)
+    assert rc == _lib.CK_INVALID_ARGUMENT
+    assert "LUT mode requires a LutTable" in _lib.last_error()
+    with pytest.raises(ValueError, match="LUT mode requires a LutTable"):
+        _lib.check(rc, "ck_forward")
+
+
+def test_lut_build_argument_errors_match_reference_wording():
+    lib = _lib.lib()
+    h = ctypes.c_void_p()
+    assert lib.ck_lut_build(4, 1, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
+    assert "lut_size must be >= 2" in _lib.last_error()       # lut.py:78-79
+    assert lib.ck_lut_build(-1, 16, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
+    assert "degree must be >= 0" in _lib.last_error()          # lut.py:80-81
+
+
+def test_merge_rejects_bad_extents():
+    lib = _lib.lib()
+    assert lib.ck_merge(None, 2, 4, 8, None, 0, None) == _lib.CK_INVALID_ARGUMENT

@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a kernels through the C ABI vs the reference.
+
+Gates (north star): normwise error max|got-want|/max|want|
+<= 1e-4 for y, dX, dC and db against the float64 reference on identical
+float32 inputs at the same LUT size; the float64 LUT itself and the cell
+slopes are bit-exact; repeated runs are bitwise identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, golden_layer_cases, golden_lut_cases
+from oracle import chebykan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # normwise, fp32 I/O + BF16x3 tensor-core contractions
+
+if torch.cuda.is_available():
+    import paper_2511_14852_b200 as ck
+    from paper_2511_14852_b200 import _lib
+
+
+def _dev():
+    return torch.device("cuda", 0)
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device=_dev())
+
+
+def test_device_is_b200_and_library_loads():
+    assert torch.cuda.is_available()
+    assert _lib.lib().ck_device_supported(0) == 1, torch.cuda.get_device_name(0)
+
+
+@pytest.mark.parametrize("degree,n", [(2, 3), (8, 1024), (8, 4096), (3, 512), (15, 16384), (5, 32768), (0, 16)])
+def test_lut_build_bit_identical_to_oracle(degree, n):
+    table = ck.lut_build(degree, n, device=_dev())
+    v, s, step = orc.build_table(degree, n)
+    assert table.step == step
+    assert np.array_equal(table.values, v)
+    assert np.array_equal(table.slopes, s)
+
+
+@pytest.mark.parametrize("path", golden_lut_cases(), ids=lambda p: p.stem)
+def test_expand_matches_reference_interp(path):
+    g = np.load(path)
+    degree = int(path.stem.split("_")[1][1:])
+    n = int(path.stem.split("_")[2][1:])
+    table = ck.lut_build(degree, n, device=_dev())
+    # feed pre-images so the kernel's tanh lands on the reference's points
+    t = g["points"].astype(np.float64)
+    x = np.arctanh(np.clip(t, -1 + 1e-7, 1 - 1e-7)).astype(np.float32)
+    tt = np.tanh(x.astype(np.float64))
+    want_v, want_s = orc.lut_values_and_slopes(tt, *orc.build_table(degree, n)[:2])
+    phi, slopes = ck.expand(_t(x).reshape(1, -1), table, with_slopes=True)
+    phi = phi.reshape(-1, degree + 1).cpu().numpy()
+    slopes = slopes.reshape(-1, degree + 1).cpu().numpy()
+    assert np.abs(phi - want_v).max() <= 2e-6
+    # float64 cell choice: slopes are the reference's float32 table entries
+    assert np.array_equal(slopes.astype(np.float64), want_s)
+
+
+def _run_layer(g):
+    degree, n = int(g["degree"]), int(g["lut_size"])
+    table = ck.lut_build(degree, n, device=_dev())
+    c = ck.reorder_to_doj(ck.CoeffTensor(g["x"].shape[1], g["dy"].shape[1], degree, ck.Layout.JOD,
+                                          _t(g["c_jod"])))
+    bias = _t(g["bias"]) if "bias" in g else None
+    mode = ck.KernelMode(include_tanh_jacobian=bool(g["jacobian"]))
+    y = ck.fused_forward(_t(g["x"]), c, table, None, mode, bias)
+    cg, dx = ck.backward_fused(_t(g["x"]), c, _t(g["dy"]), table, None, mode)
+    return y.cpu().numpy(), cg.data.cpu().numpy(), dx.cpu().numpy()
+
+
+@pytest.mark.parametrize("path", golden_layer_cases(), ids=lambda p: p.stem)
+def test_layer_matches_reference_golden(path):
+    g = np.load(path)
+    y, dc, dx = _run_layer(g)
+    errs = {
+        "y": orc.normwise_err(y, g["y"]),
+        "dc": orc.normwise_err(dc, g["dc_doj"]),
+        "dx": orc.normwise_err(dx, g["dx"]),
+    }
+    print(path.stem, {k: f"{v:.2e}" for k, v in errs.items()})
+    for k, e in errs.items():
+        assert e <= TOL, (k, e)
+
+
+@pytest.mark.parametrize("path", golden_layer_cases(), ids=lambda p: p.stem)
+def test_module_autograd_matches_reference_golden(path):
+    g = np.load(path)
+    degree, n = int(g["degree"]), int(g["lut_size"])
+    i, o = g["x"].shape[1], g["dy"].shape[1]
+    layer = ck.ChebyKANLayer(i, o, degree, bias="bias" in g, lut_size=n,
+                             include_tanh_jacobian=bool(g["jacobian"])).to(_dev())
+    layer.load_jod(g["c_jod"])
+    if "bias" in g:
+        with torch.no_grad():
+            layer.bias.copy_(_t(g["bias"]))
+    x = _t(g["x"]).requires_grad_(True)
+    y = layer(x)
+    y.backward(_t(g["dy"]))
+    assert orc.normwise_err(y.detach().cpu().numpy(), g["y"]) <= TOL
+    assert orc.normwise_err(layer.coeff_doj.grad.cpu().numpy(), g["dc_doj"]) <= TOL
+    assert orc.normwise_err(x.grad.cpu().numpy(), g["dx"]) <= TOL
+    if "bias" in g:
+        assert orc.normwise_err(layer.bias.grad.cpu().numpy(), g["db"]) <= 1e-6
+
+
+@pytest.mark.parametrize("shape", [(512, 1024, 1024, 8, 32768), (300, 257, 130, 3, 512),
+                                   (1024, 64, 64, 4, 4096), (2048, 512, 512, 5, 1024),
+                                   (257, 96, 1, 5, 1024), (64, 257, 512, 15, 16384)])
+def test_random_shapes_vs_oracle(shape):
+    b, i, o, d, n = shape
+    x, c_jod, dy = orc.bench_inputs(b, i, o, d, seed=b + i + o)
+    vals, slopes, _ = orc.build_table(d, n)
+    c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
+    want_y = orc.layer_forward(x, c_doj, vals, threads=8)
+    want_dc, want_dx, want_db = orc.layer_backward(x, c_doj, dy, vals, slopes, threads=8)
+    table = ck.lut_build(d, n, device=_dev())
+    c = ck.CoeffTensor(i, o, d, ck.Layout.DOJ, _t(c_doj.astype(np.float32)))
+    y = ck.fused_forward(_t(x), c, table).cpu().numpy()
+    cg, dx = ck.backward_fused(_t(x), c, _t(dy), table)
+    e = (orc.normwise_err(y, want_y), orc.normwise_err(cg.data.cpu().numpy(), want_dc),
+         orc.normwise_err(dx.cpu().numpy(), want_dx))
+    print(shape, [f"{v:.2e}" for v in e])
+    assert max(e) <= TOL, e
+
+
+def test_bitwise_determinism():
+    b, i, o, d = 4096, 512, 384, 6
+    x, c_jod, dy = orc.bench_inputs(b, i, o, d, seed=7)
+    table = ck.lut_build(d, 4096, device=_dev())
+    c = ck.reorder_to_doj(ck.CoeffTensor(i, o, d, ck.Layout.JOD, _t(c_jod)))
+    outs = []
+    for _ in range(3):
+        y = ck.fused_forward(_t(x), c, table)
+        cg, dx = ck.backward_fused(_t(x), c, _t(dy), table)
+        outs.append((y, cg.data, dx))
+    for other in outs[1:]:
+        for a, bb in zip(outs[0], other):
+            assert torch.equal(a, bb)
+
+
+def test_error_paths_match_reference_wording():
+    table = ck.lut_build(2, 64, device=_dev())
+    c_jod = ck.CoeffTensor(3, 2, 2, ck.Layout.JOD, torch.ones(18, device=_dev()))
+    with pytest.raises(ValueError, match="DOJ"):
+        ck.fused_forward(torch.zeros(1, 3, device=_dev()), c_jod, table)
+    c = ck.reorder_to_doj(c_jod)
+    with pytest.raises(ValueError, match="input width 4 != coefficient d_in 3"):
+        ck.fused_forward(torch.zeros(2, 4, device=_dev()), c, table)
+    with pytest.raises(ValueError, match="dy must have shape"):
+        ck.backward_fused(torch.zeros(2, 3, device=_dev()), c, torch.zeros(2, 3, device=_dev()), table)
+    other = ck.lut_build(3, 64, device=_dev())
+    with pytest.raises(ValueError, match="LUT has 4 features, coefficients expect 3"):
+        ck.fused_forward(torch.zeros(2, 3, device=_dev()), c, other)
+    x = torch.zeros(2, 3, device=_dev())
+    x[1, 2] = float("inf")
+    with pytest.raises(ck.NonFiniteInputError, match=r"b=1, j=2"):
+        ck.fused_forward(x, c, table, validate=True)
+
+
+def test_hand_examples():
+    # test_kernels.py:63-70 (LUT mode at N=32768: linear features are exact
+    # up to float32): all-ones coefficients, X = [0, 10] -> 1 + (1 + tanh 10)
+    table = ck.lut_build(1, 32768, device=_dev())
+    c = ck.CoeffTensor(2, 1, 1, ck.Layout.DOJ, torch.ones(4, device=_dev()))
+    y = ck.fused_forward(torch.tensor([[0.0, 10.0]], device=_dev()), c, table)
+    assert abs(float(y[0, 0]) - (2.0 + np.tanh(10.0))) <= 1e-6
+    # degree 0: dC = sum_b dy for every j, dX = 0 (test_kernels.py:152-162)
+    t0 = ck.lut_build(0, 16, device=_dev())
+    c0 = ck.CoeffTensor(3, 2, 0, ck.Layout.DOJ, torch.ones(6, device=_dev()))
+    x = torch.tensor([[0.1, -0.4, 2.0], [1.0, 0.0, -1.0]], device=_dev())
+    dy = torch.tensor([[1.0, 2.0], [3.0, 4.0]], device=_dev())
+    cg, dx = ck.backward_fused(x, c0, dy, t0)
+    assert torch.count_nonzero(dx) == 0
+    for j in range(3):
+        assert torch.equal(cg.data[0, :, j], dy.sum(0))

@@ -1,0 +1,96 @@
+"""Host-side logic of the product package (no GPU): schedule validation,
+layouts, LUT sizing, sharding -- mirroring the reference's own unit tests."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import chebykan_oracle as orc
+from paper_2511_14852_b200 import (
+    DEFAULT_LUT_SIZE,
+    ChebyKANLayer,
+    CoeffTensor,
+    Layout,
+    TileSchedule,
+    doj_index,
+    interp_error_bound,
+    jod_index,
+    lut_size_for_budget,
+    reorder_to_doj,
+    reorder_to_jod,
+    shard_bounds,
+)
+
+
+def test_default_lut_size_is_reference_default():
+    assert DEFAULT_LUT_SIZE == orc.REFERENCE_DEFAULT_LUT_SIZE == 32768
+
+
+def test_schedule_invariants():  # test_kernels.py:417-425
+    with pytest.raises(ValueError, match="tile_out == lane_y"):
+        TileSchedule(tile_in=8, tile_out=8, lane_x=4, lane_y=16, g_x=1, g_y=1, d_in=8, d_out=8)
+    with pytest.raises(ValueError, match="g_x"):
+        TileSchedule(tile_in=8, tile_out=8, lane_x=4, lane_y=8, g_x=3, g_y=1, d_in=8, d_out=8)
+    s = TileSchedule.for_dims(100, 70, tile_in=16, tile_out=32)
+    assert s.g_x == 7 and s.g_y == 3
+    with pytest.raises(ValueError):
+        TileSchedule.for_dims(0, 4)
+
+
+def test_layout_index_maps_and_reorder_roundtrip():  # tensor.py:67-90
+    d_in, d_out, deg = 5, 3, 4
+    k = deg + 1
+    jod = torch.arange(d_in * d_out * k, dtype=torch.float32)
+    c = CoeffTensor(d_in, d_out, deg, Layout.JOD, jod)
+    doj = reorder_to_doj(c)
+    flat = doj.data.reshape(-1)
+    for j in range(d_in):
+        for o in range(d_out):
+            for kk in range(k):
+                assert flat[doj_index(d_in, d_out, kk, o, j)] == jod[jod_index(d_out, deg, j, o, kk)]
+    back = reorder_to_jod(doj)
+    assert torch.equal(back.data.reshape(-1), jod)
+    with pytest.raises(ValueError, match="expects JOD"):
+        reorder_to_doj(doj)
+    with pytest.raises(ValueError, match="expected"):
+        CoeffTensor(2, 2, 1, Layout.JOD, torch.zeros(7))
+
+
+def test_interp_bound_matches_oracle():
+    for d, n in ((8, 1024), (3, 512), (15, 16384), (24, 32768)):
+        assert np.array_equal(interp_error_bound(d, n), orc.interp_error_bound(d, n))
+
+
+def test_lut_size_for_budget():
+    for d in (3, 5, 8, 15):
+        n = lut_size_for_budget(d, 1e-4)
+        assert interp_error_bound(d, n).max() <= 1e-4
+        assert n == 2 or interp_error_bound(d, n // 2).max() > 1e-4
+
+
+def test_shard_bounds_partition():
+    for gb, w in ((262144, 8), (1000, 3), (5, 8)):
+        covered = []
+        for r in range(w):
+            a, b = shard_bounds(gb, r, w)
+            covered.extend(range(a, b))
+        assert covered == list(range(gb))
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
+
+
+def test_layer_init_matches_reference_init_params():  # model.py:72-83
+    layer = ChebyKANLayer(6, 4, 3, seed=123)
+    rng = np.random.default_rng(123)
+    s = 1.0 / np.sqrt(6 * 4)
+    want = rng.uniform(-s, s, size=6 * 4 * 4).reshape(6, 4, 4).astype(np.float32)
+    assert np.array_equal(layer.cheby_coeffs.detach().numpy(), want)
+    assert torch.count_nonzero(layer.bias) == 0
+    assert tuple(layer.coeff_doj.shape) == (4, 4, 6)
+    with pytest.raises(ValueError):
+        ChebyKANLayer(0, 4, 3)
+
+
+def test_layer_refuses_cpu_tensors():
+    layer = ChebyKANLayer(4, 2, 2)
+    with pytest.raises(ValueError, match="CUDA"):
+        layer(torch.zeros(3, 4))
