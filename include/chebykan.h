@@ -113,6 +113,18 @@ CK_API int ck_backward(const float* x, const float* dy, int64_t batch, int d_in,
 CK_API int ck_merge(const float* partials, int num_partials, int64_t stride, int64_t n, float* out,
              int accumulate, void* stream);
 
+/* --- Diagnostics --------------------------------------------------------------
+ * ck_launch_count: kernels this library has launched in the process.
+ * ck_timing_enable(1): bracket every launch with CUDA events on its stream;
+ * ck_timing_collect waits for them and returns the summed device time (ms)
+ * and launch count per kernel class, then clears the record.  Classes:
+ * 0 GEMM forward, 1 GEMM input-grad, 2 GEMM coeff-grad, 3 expand,
+ * 4 expand (transposed), 5 dx combine, 6 split, 7 reduce/merge/fill, 8 lut. */
+#define CK_NUM_KERNEL_CLASSES 9
+CK_API long long ck_launch_count(void);
+CK_API int ck_timing_enable(int on);
+CK_API int ck_timing_collect(double* ms_per_class, long long* launches_per_class, int n_classes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,7 +44,29 @@ SIGNATURES = {
     "ck_backward": (_c_int, [_c_p, _c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_p, _c_p, _c_p,
                              _c_p, _c_size, _c_p]),
     "ck_merge": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_int, _c_p]),
+    "ck_launch_count": (ctypes.c_longlong, []),
+    "ck_timing_enable": (_c_int, [_c_int]),
+    "ck_timing_collect": (_c_int, [_c_dp, ctypes.POINTER(ctypes.c_longlong), _c_int]),
 }
+
+KERNEL_CLASSES = ("gemm_fwd", "gemm_dx", "gemm_dc", "expand", "expand_t", "dx_combine", "split", "reduce", "lut")
+
+
+def launch_count() -> int:
+    return int(lib().ck_launch_count())
+
+
+def timing_enable(on: bool) -> None:
+    lib().ck_timing_enable(1 if on else 0)
+
+
+def timing_collect() -> dict:
+    """{class: (ms, launches)} since the last collect (waits for the events)."""
+    n = len(KERNEL_CLASSES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_longlong * n)()
+    check(lib().ck_timing_collect(ms, cnt, n), "ck_timing_collect")
+    return {KERNEL_CLASSES[i]: (ms[i], int(cnt[i])) for i in range(n)}
 
 _lib = None
 _lock = threading.Lock()

@@ -1,7 +1,10 @@
 // extern "C" entry points (include/chebykan.h): argument validation with
 // the reference's error wording, workspace carving, and the orchestration of
 // the forward / backward kernels on the caller's stream.
+#include <atomic>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "ck_common.cuh"
 #include "ck_internal.h"
@@ -102,6 +105,48 @@ int check_dims(int64_t batch, int d_in, int d_out, const ck_lut* lut) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Launch counter and optional per-class device timers.
+
+namespace {
+std::atomic<long long> g_launches{0};
+std::atomic<int> g_timing{0};
+std::mutex g_timing_mu;
+struct TimedLaunch {
+  int cls;
+  cudaEvent_t a, b;
+};
+std::vector<TimedLaunch> g_pending;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+LaunchScope::LaunchScope(int cls, cudaStream_t stream) : cls_(cls), stream_(stream) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_timing.load(std::memory_order_relaxed)) {
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    cudaEvent_t a = take_event();
+    cudaEvent_t b = take_event();
+    cudaEventRecord(a, stream_);
+    g_pending.push_back({cls_, a, b});
+    ev_ = b;
+  }
+}
+
+LaunchScope::~LaunchScope() {
+  if (ev_) cudaEventRecord(static_cast<cudaEvent_t>(ev_), stream_);
+}
+
 void set_error(const std::string& msg) { g_error = msg; }
 const char* last_error() { return g_error.c_str(); }
 
@@ -121,6 +166,44 @@ int num_sms() {
 }  // namespace ck
 
 using ck::kOk;
+
+extern "C" long long ck_launch_count(void) { return ck::g_launches.load(); }
+
+extern "C" int ck_timing_enable(int on) {
+  ck::g_timing.store(on ? 1 : 0);
+  return kOk;
+}
+
+extern "C" int ck_timing_collect(double* ms_per_class, long long* launches_per_class, int n_classes) {
+  CK_CHECK(n_classes >= 0, "ck_timing_collect: bad class count");
+  std::vector<ck::TimedLaunch> pending;
+  {
+    std::lock_guard<std::mutex> lk(ck::g_timing_mu);
+    pending.swap(ck::g_pending);
+  }
+  for (int c = 0; c < n_classes; ++c) {
+    if (ms_per_class) ms_per_class[c] = 0.0;
+    if (launches_per_class) launches_per_class[c] = 0;
+  }
+  int rc = kOk;
+  for (auto& t : pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(t.b) != cudaSuccess || cudaEventElapsedTime(&ms, t.a, t.b) != cudaSuccess) {
+      ck::set_error("ck_timing_collect: event query failed");
+      rc = ck::kCudaError;
+    }
+    if (t.cls >= 0 && t.cls < n_classes) {
+      if (ms_per_class) ms_per_class[t.cls] += ms;
+      if (launches_per_class) launches_per_class[t.cls] += 1;
+    }
+  }
+  std::lock_guard<std::mutex> lk(ck::g_timing_mu);
+  for (auto& t : pending) {
+    ck::g_event_pool.push_back(t.a);
+    ck::g_event_pool.push_back(t.b);
+  }
+  return rc;
+}
 
 extern "C" int ck_version(void) { return 1 * 10000 + 0 * 100 + 0; }
 
@@ -279,6 +362,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       gx.out_z_stride = rows * I;
       gx.split_ws = split_ws;
       gx.split_ws_elems = W.split_elems;
+      gx.kclass = ck::kKGemmDx;
       CK_TRY(ck::gemm_bf16x3(gx, s));
       CK_TRY(ck::launch_dx_combine(g, rows * I, xc, rows, d_in, lut, include_tanh_jacobian, dx + r0 * I, s));
     }
@@ -298,6 +382,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       gc.accumulate = ci > 0 ? 1 : 0;  // ascending chunk order: reproducible
       gc.split_ws = split_ws;
       gc.split_ws_elems = W.split_elems;
+      gc.kclass = ck::kKGemmDc;
       CK_TRY(ck::gemm_bf16x3(gc, s));
     }
   }

@@ -212,6 +212,7 @@ int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut,
   const LutView v = view(lut);
   const size_t tab = sizeof(float) * v.N * v.K * (slopes ? 2 : 1);
   const int blocks = grid_for(n, 8);
+  LaunchScope scope(kKExpand, s);
   if (tab <= static_cast<size_t>(kSmemLutMax)) {
     CK_CUDA(cudaFuncSetAttribute(expand_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
@@ -232,6 +233,7 @@ int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* l
   const int blocks = grid_for(rows * ((cols + 1) / 2), 8);
   auto* h = reinterpret_cast<uint32_t*>(hi);
   auto* l = reinterpret_cast<uint32_t*>(lo);
+  LaunchScope scope(kKExpand, s);
   if (tab <= static_cast<size_t>(kSmemLutMax)) {
     CK_CUDA(cudaFuncSetAttribute(expand_planes_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
@@ -252,6 +254,7 @@ int launch_expand_planes_t(const float* x, int64_t rows, int cols, const ck_lut*
   const int64_t tiles = ceil_div(rows, kTR) * ceil_div(cols, kTC);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 4;
   const int blocks = static_cast<int>(tiles < cap ? tiles : cap);
+  LaunchScope scope(kKExpandT, s);
   if (tab <= static_cast<size_t>(kSmemLutMax)) {
     CK_CUDA(cudaFuncSetAttribute(expand_planes_t_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
@@ -270,6 +273,7 @@ int launch_dx_combine(const float* g, int64_t g_plane, const float* x, int64_t r
   const LutView v = view(lut);
   const size_t tab = sizeof(float) * v.N * v.K;
   const int blocks = grid_for(n, 8);
+  LaunchScope scope(kKDxCombine, s);
   if (tab <= static_cast<size_t>(kSmemLutMax)) {
     CK_CUDA(cudaFuncSetAttribute(dx_combine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));

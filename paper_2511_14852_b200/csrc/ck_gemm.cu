@@ -276,6 +276,7 @@ int launch(const GemmProblem& p, int splits, int r_chunks, float* out, long long
   }
   dim3 grid(static_cast<unsigned>(ceil_div(k.N, BN)), static_cast<unsigned>(ceil_div(k.M, kBM)),
             static_cast<unsigned>(p.nz * splits));
+  LaunchScope scope(p.kclass, s);
   gemm_bf16x3_kernel<BN, STAGES><<<grid, kThreads, C::kSmemBytes, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, k);
   CK_CUDA(cudaGetLastError());
   return kOk;

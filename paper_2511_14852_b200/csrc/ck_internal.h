@@ -21,6 +21,33 @@ struct ck_lut {
 
 namespace ck {
 
+// Kernel classes for the launch counter / device timers (ck_timing_*).
+enum KClass : int {
+  kKGemmFwd = 0,
+  kKGemmDx = 1,
+  kKGemmDc = 2,
+  kKExpand = 3,
+  kKExpandT = 4,
+  kKDxCombine = 5,
+  kKSplit = 6,
+  kKReduce = 7,
+  kKLut = 8,
+  kKNumClasses = 9,
+};
+
+// RAII: counts one launch of class `cls` and, when timing is enabled,
+// brackets it with CUDA events on `stream`.
+class LaunchScope {
+ public:
+  LaunchScope(int cls, cudaStream_t stream);
+  ~LaunchScope();
+
+ private:
+  int cls_;
+  cudaStream_t stream_;
+  void* ev_ = nullptr;
+};
+
 // Rows processed per internal chunk by ck_forward / ck_backward (bounds the
 // workspace; chunks are processed in ascending order on one stream, so the
 // accumulated dC is bit-reproducible).
@@ -105,6 +132,7 @@ struct GemmProblem {
   int accumulate;      // out += result
   float* split_ws;     // workspace for split-R partials (nullable -> no split)
   int64_t split_ws_elems;
+  int kclass = kKGemmFwd;  // timing / counting class
 };
 int gemm_bf16x3(const GemmProblem& p, cudaStream_t s);
 // Workspace (floats) the split-R path may want for this problem shape.

@@ -100,6 +100,7 @@ extern "C" int ck_lut_build(int degree, int lut_size, int device, ck_lut** out) 
   CK_TRY(ck::lut_alloc(degree, lut_size, device, &l));
   const int threads = 256;
   const int blocks = static_cast<int>(ck::ceil_div(lut_size, threads));
+  ck::LaunchScope scope(ck::kKLut, nullptr);
   ck::lut_build_kernel<<<blocks, threads>>>(degree, lut_size, l->step, l->values64, l->values_pm,
                                             l->slopes_pm);
   cudaError_t e = cudaGetLastError();

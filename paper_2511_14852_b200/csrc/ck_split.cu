@@ -166,6 +166,7 @@ int launch_split_rows(const float* in, int64_t nz, int64_t rows, int64_t cols, i
                       __nv_bfloat16* lo, int64_t ld, int64_t out_zs, cudaStream_t s) {
   if (nz * rows * cols == 0) return kOk;
   CK_CHECK(ld % 2 == 0 && out_zs % 2 == 0, "split_rows: pitch must be even");
+  LaunchScope scope(kKSplit, s);
   split_rows_kernel<<<blocks_for(nz * rows * ((cols + 1) / 2)), kThreads, 0, s>>>(
       in, nz, rows, cols, in_zs, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, out_zs);
   CK_CUDA(cudaGetLastError());
@@ -177,6 +178,7 @@ int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t co
   if (nz * rows * cols == 0) return kOk;
   const int64_t tiles = nz * ceil_div(rows, 32) * ceil_div(cols, 32);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  LaunchScope scope(kKSplit, s);
   split_transpose_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s>>>(in, nz, rows, cols, in_zs,
                                                                                          hi, lo, ld, out_zs);
   CK_CUDA(cudaGetLastError());
@@ -185,6 +187,7 @@ int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t co
 
 int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s) {
   if (rows == 0) return kOk;
+  LaunchScope scope(kKReduce, s);
   row_sum_kernel<<<blocks_for(rows * 32), kThreads, 0, s>>>(in, rows, cols, out);
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -193,6 +196,7 @@ int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cuda
 int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part, int slots, cudaStream_t s) {
   if (cols == 0) return kOk;
   const int64_t chunk = ceil_div(rows > 0 ? rows : 1, slots);
+  LaunchScope scope(kKReduce, s);
   col_partial_kernel<<<blocks_for(slots * cols), kThreads, 0, s>>>(in, rows, cols, chunk, part, slots);
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -200,6 +204,7 @@ int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part
 
 int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s) {
   if (cols == 0) return kOk;
+  LaunchScope scope(kKReduce, s);
   col_finish_kernel<<<blocks_for(cols), kThreads, 0, s>>>(part, slots, cols, out);
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -207,6 +212,7 @@ int launch_col_finish(const double* part, int slots, int64_t cols, float* out, c
 
 int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate, cudaStream_t s) {
   if (n == 0) return kOk;
+  LaunchScope scope(kKReduce, s);
   merge_kernel<<<blocks_for(ceil_div(n, 4)), kThreads, 0, s>>>(partials, S, stride, n, out, accumulate);
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -214,6 +220,7 @@ int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float*
 
 int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s) {
   if (rows * cols == 0) return kOk;
+  LaunchScope scope(kKReduce, s);
   fill_rows_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, a, b);
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -221,6 +228,7 @@ int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, con
 
 int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s) {
   if (rows * cols == 0) return kOk;
+  LaunchScope scope(kKReduce, s);
   add_rows_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, a, b);
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -228,6 +236,7 @@ int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, cons
 
 int launch_broadcast_cols(float* out, int64_t rows, int64_t cols, const float* v, cudaStream_t s) {
   if (rows * cols == 0) return kOk;
+  LaunchScope scope(kKReduce, s);
   broadcast_cols_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, v);
   CK_CUDA(cudaGetLastError());
   return kOk;
