@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the fused ChebyKAN layer on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c1] [--sweep]
+
+Default workload (BASELINE.json configs[4], "C4"): data-parallel ChebyKAN
+training 4096->4096, degree 8, LUT N=32768, global batch 262144 rows sharded
+contiguously over the ranks (strong scaling; at N=1 one GPU runs all rows).
+One step = forward + backward (dC, db, dX) + allreduce of dC/db (N>1) +
+Adam update (+ the coefficient re-split the next forward needs), all on
+synthetic data of the named shapes with random-init weights.
+
+One JSON line on rank 0: ``value`` = training samples/s of the whole job,
+device-timed (CUDA events, barrier + synchronize on both sides, max over
+ranks), inputs resident in HBM (each rank's x shard is 4.3 GB at N=1, far
+larger than the 126 MB L2, so no flush is needed).  ``e2e`` repeats the step
+through the public module API with the step's x/dy copied from pinned host
+memory and the loss read back every step.  ``roofline`` is the dominant
+kernel (the tcgen05 BF16x3 GEMM family) timed live by the library's CUDA
+event timers inside the timed region.  ``cpu_baseline`` is the oracle port
+of the reference's CPU path on a bounded row sample (rank 0, N=1 only).
+
+``--impl reference`` times the reference's CPU algorithm (oracle port; the
+Python reference itself cannot travel to the GPU box) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "c4": dict(name="C4 DP ChebyKAN training 4096->4096 d8, global batch 262144", d_in=4096, d_out=4096,
+               degree=8, global_batch=262144, lut_size=32768),
+    "c1": dict(name="C1 ChebyKAN layer 4096->4096 d8, batch 16384 per GPU", d_in=4096, d_out=4096, degree=8,
+               global_batch=16384, lut_size=32768, weak=True),
+}
+METRIC = "ChebyKAN training (fwd+bwd+dC allreduce+Adam) samples/s"
+CPU_SAMPLE_ROWS = 128      # oracle rows timed for cpu_baseline (~10-20 s of CPU work)
+REF_STEP_ROWS = 64         # oracle rows per --impl reference step
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]),
+                    bf16_sus=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), source="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="fallback (B200_PROFILING.md)")
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md recipe)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = pathlib.Path(f"/tmp/ck_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f.lower() == "active"})
+        loaded = [r[0] for r in rows if r[0] > 500] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = test infrastructure, used here only as the baseline)
+
+def cpu_reference_time(rows: int, wl: dict, reps: int = 1, warmup: int = 0):
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import chebykan_oracle as orc
+
+    threads = os.cpu_count() or 1
+    x, c_jod, dy = orc.bench_inputs(rows, wl["d_in"], wl["d_out"], wl["degree"], seed=3)
+    vals, slopes, _ = orc.build_table(wl["degree"], wl["lut_size"])
+    c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
+    times = []
+    with threadpool_limits(1):  # BLAS single-threaded, tile tasks across all cores (best at large shapes)
+        for i in range(warmup + reps):
+            t0 = time.perf_counter()
+            orc.layer_forward(x, c_doj, vals, threads=threads)
+            orc.layer_backward(x, c_doj, dy, vals, slopes, threads=threads)
+            if i >= warmup:
+                times.append(time.perf_counter() - t0)
+    return times, threads
+
+
+def run_reference_arm(args, wl):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    times, threads = cpu_reference_time(REF_STEP_ROWS, wl, reps=args.steps, warmup=args.warmup)
+    t = statistics.mean(times)
+    value = REF_STEP_ROWS / t
+    sample = (f"{REF_STEP_ROWS} rows of {wl['d_in']}->{wl['d_out']} d{wl['degree']} N={wl['lut_size']} fwd+bwd per "
+              f"step; oracle port of polykan fused_forward/backward_fused (LUT mode, f64 NumPy), "
+              f"{threads} tile-task threads, BLAS 1 thread")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "global_batch": wl["global_batch"], "d_in": wl["d_in"],
+                   "d_out": wl["d_out"], "degree": wl["degree"], "lut_size": wl["lut_size"],
+                   "parallelism": "host threads", "sample_rows_per_step": REF_STEP_ROWS},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_14852_b200 as ck
+    from paper_2511_14852_b200 import _lib
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("NCCL_ALGO", "Ring")  # fixed reduction order -> reproducible dC
+        dist.init_process_group("nccl", device_id=dev)
+    if _lib.lib().ck_device_supported(local) != 1:
+        raise SystemExit(f"device {torch.cuda.get_device_name(local)} is not sm_100 (B200)")
+
+    I, O, d = wl["d_in"], wl["d_out"], wl["degree"]
+    if wl.get("weak"):
+        gb = wl["global_batch"] * world
+        a, b = rank * wl["global_batch"], (rank + 1) * wl["global_batch"]
+    else:
+        gb = wl["global_batch"]
+        a, b = ck.shard_bounds(gb, rank, world)
+    rows = b - a
+
+    torch.manual_seed(1234)  # identical synthetic weights on every rank
+    layer = ck.ChebyKANLayer(I, O, d, lut_size=wl["lut_size"]).to(dev)
+    opt = torch.optim.Adam(layer.parameters(), lr=1e-4, fused=True)
+    reducer = ck.GradientAllreducer(ck.chebykan_parameters(layer)) if world > 1 else None
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    x = (torch.rand(rows, I, device=dev, generator=gen) * 3.0 - 1.5).requires_grad_(True)
+    dy = torch.randn(rows, O, device=dev, generator=gen)
+
+    def step(xin, dyin, want_loss=False):
+        xin.grad = None
+        y = layer(xin)
+        loss = (y.detach() * dyin).sum() if want_loss else None  # L = sum(y * dy) -> dL/dy = dy
+        y.backward(dyin)
+        if reducer is not None:
+            reducer()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(ms):
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(x, dy)
+    barrier()
+
+    # ---- timed region: training steps, device-resident inputs -----------
+    clocks = ClockSampler(local) if local == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    _lib.timing_collect()
+    _lib.timing_enable(True)
+    launches0 = _lib.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step(x, dy)
+    ev1.record()
+    barrier()
+    launches = _lib.launch_count() - launches0
+    _lib.timing_enable(False)
+    kt = _lib.timing_collect()
+    clk = clocks.stop() if clocks else None
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms / args.steps
+    value = gb / (ms_step / 1e3)
+
+    # ---- forward-only throughput (inference), same shard ---------------
+    with torch.no_grad():
+        xs = x.detach()
+        for _ in range(2):
+            layer(xs)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            layer(xs)
+        f1.record()
+        barrier()
+        fwd_ms = max_over_ranks(f0.elapsed_time(f1)) / args.steps
+    fwd_value = gb / (fwd_ms / 1e3)
+
+    # ---- end to end: pinned host inputs copied in, loss read back -------
+    x_h = torch.empty((rows, I), dtype=torch.float32, pin_memory=True)
+    dy_h = torch.empty((rows, O), dtype=torch.float32, pin_memory=True)
+    x_h.copy_(x.detach())
+    dy_h.copy_(dy)
+    xd = torch.empty((rows, I), device=dev, requires_grad=True)
+    dyd = torch.empty((rows, O), device=dev)
+    barrier()
+    e2e_steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        with torch.no_grad():
+            xd.copy_(x_h, non_blocking=True)
+            dyd.copy_(dy_h, non_blocking=True)
+        loss = step(xd, dyd, want_loss=True)
+        float(loss.item())  # D2H of the step's result
+    e1.record()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    e2e_wall = (time.perf_counter() - t0) / e2e_steps
+    e2e_value = gb / (e2e_ms / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    flops = ck.count_flops(rows, I, O, d)
+    gemm_alg = 3 * 2 * rows * I * O * d * args.steps  # fwd + dX + dC GEMMs executed per step (k=0 folded)
+    gemm_ms = sum(kt[c][0] for c in ("gemm_fwd", "gemm_dx", "gemm_dc"))
+    gemm_tf = gemm_alg / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    peak_eff = peaks["bf16_sus"] / 3.0
+    total_kernel_ms = sum(v[0] for v in kt.values())
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("gemm_bf16x3_bytes_per_launch")
+        except (ValueError, OSError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if wl.get("weak") else "strong", "vs_baseline": None,
+        "dtype": "fp32 I/O, bf16x3 split tensor-core products, fp32 accumulate", "data": "synthetic",
+        "config": {"workload": wl["name"], "global_batch": gb, "rows_per_gpu": rows, "d_in": I, "d_out": O,
+                   "degree": d, "lut_size": wl["lut_size"], "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (x shard >> 126 MB), no flush"},
+        "fwd": {"value": fwd_value, "unit": "samples/s", "ms_per_step": fwd_ms},
+        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": 4 * rows * (I + O),
+                "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms, "wall_ms_per_step": e2e_wall * 1e3,
+                "path": "ChebyKANLayer forward/backward + Adam, inputs from pinned host"},
+        "gpu_launches": launches,
+        "roofline": {
+            "bound": "tensor", "kernel": "gemm_bf16x3 (tcgen05 fwd + dX + dC, BF16x3)",
+            "achieved": gemm_tf, "peak": peak_eff, "unit": "TFLOP/s", "frac": gemm_tf / peak_eff,
+            "traffic": traffic,
+            "peak_basis": f"{peaks['source']} bf16 sustained {peaks['bf16_sus']} TF/s / 3 (3 bf16 MMAs per "
+                          "algorithmic fp32 MMA)",
+            "algorithmic_flops_per_step": 3 * 2 * rows * I * O * d,
+            "gemm_share_of_kernel_time": gemm_ms / total_kernel_ms if total_kernel_ms else None,
+        },
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
+        "kernel_launches_per_step": {k: v[1] / args.steps for k, v in kt.items() if v[1]},
+        "train_alg_tflops_per_gpu": flops["train"] / (ms_step / 1e3) / 1e12,
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        times, threads = cpu_reference_time(CPU_SAMPLE_ROWS, wl)
+        line["cpu_baseline"] = {
+            "value": CPU_SAMPLE_ROWS / times[0], "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"{CPU_SAMPLE_ROWS} rows of the same layer (fwd+bwd, no optimizer), oracle port of polykan "
+                      f"LUT-mode fused_forward/backward_fused, f64 NumPy, {threads} threads, BLAS 1 thread"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_sweep(args):
+    """C1 sweep: I=O in 256..4096 x degree in {3,4,5,8}, batch 16384, fwd and fwd+bwd (1 GPU)."""
+    import torch
+
+    import paper_2511_14852_b200 as ck
+    from paper_2511_14852_b200.kernels import PreparedCoeff, backward_raw, forward_raw
+
+    dev = torch.device("cuda", 0)
+    peaks = load_peaks()
+    rows = []
+    for dim in (256, 512, 1024, 2048, 4096):
+        for deg in (3, 4, 5, 8):
+            b = 16384
+            x = torch.rand(b, dim, device=dev) * 3 - 1.5
+            c = (torch.rand(deg + 1, dim, dim, device=dev) * 2 - 1) / (dim * (deg + 1)) ** 0.5
+            dy = torch.randn(b, dim, device=dev)
+            lut = ck.lut_build(deg, 32768, device=dev)
+            prep = PreparedCoeff(c)
+            for _ in range(3):
+                forward_raw(x, prep, lut, None)
+                backward_raw(x, dy, prep, lut, True)
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+            for _ in range(args.steps):
+                forward_raw(x, prep, lut, None)
+            ev[1].record()
+            for _ in range(args.steps):
+                backward_raw(x, dy, prep, lut, True)
+            ev[2].record()
+            torch.cuda.synchronize()
+            f = ev[0].elapsed_time(ev[1]) / args.steps
+            bw = ev[1].elapsed_time(ev[2]) / args.steps
+            fl = ck.count_flops(b, dim, dim, deg)
+            peak = peaks["bf16"] / 3.0
+            r = {"d_in": dim, "d_out": dim, "degree": deg, "batch": b, "fwd_ms": f, "bwd_ms": bw,
+                 "fwd_samples_per_s": b / f * 1e3, "train_samples_per_s": b / (f + bw) * 1e3,
+                 "fwd_alg_tflops": fl["fwd"] / f / 1e9, "train_alg_tflops": fl["train"] / (f + bw) / 1e9,
+                 "fwd_frac_of_bf16x3_burst": fl["fwd"] / f / 1e9 / peak,
+                 "train_frac_of_bf16x3_burst": fl["train"] / (f + bw) / 1e9 / peak}
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            del x, c, dy, prep
+    out = ROOT / "gpurun_out" / "sweep.json"
+    out.parent.mkdir(exist_ok=True)
+    out.write_text(json.dumps(rows, indent=1))
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--sweep", action="store_true", help="run the C1 sweep table instead of the JSON line")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and not args.sweep:
+        args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+    elif args.sweep:
+        run_sweep(args)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()
