@@ -2,6 +2,7 @@
 // the reference's error wording, workspace carving, and the orchestration of
 // the forward / backward kernels on the caller's stream.
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -58,6 +59,7 @@ constexpr int kDbSlots = 32;
 
 struct BwdLayout {
   int64_t chunk, n_chunks, ldO, ldB;
+  bool fused_dx;
   size_t dy_hi, dy_lo, dyt_hi, dyt_lo, g, pt_hi, pt_lo, db_part, db_tmp, split, total;
   int64_t split_elems;
   BwdLayout(int64_t B, int I, int O, int K) {
@@ -69,7 +71,8 @@ struct BwdLayout {
     const int64_t d = K - 1;
     const size_t dy = align_up(sizeof(__nv_bfloat16) * chunk * ldO);
     const size_t dyt = align_up(sizeof(__nv_bfloat16) * O * ldB);
-    const size_t gb = align_up(sizeof(float) * d * chunk * I);
+    fused_dx = dx_tile_inputs(static_cast<int>(d)) > 0;
+    const size_t gb = fused_dx ? 0 : align_up(sizeof(float) * d * chunk * I);
     const size_t pt = align_up(sizeof(__nv_bfloat16) * d * I * ldB);
     const size_t dbp = align_up(sizeof(double) * n_chunks * kDbSlots * O);
     int64_t s1 = d > 0 ? gemm_split_ws_elems(chunk, I, static_cast<int>(d), O) : 0;
@@ -145,6 +148,18 @@ LaunchScope::LaunchScope(int cls, cudaStream_t stream) : cls_(cls), stream_(stre
 
 LaunchScope::~LaunchScope() {
   if (ev_) cudaEventRecord(static_cast<cudaEvent_t>(ev_), stream_);
+}
+
+int lut_source_override() {
+  static int v = [] {
+    const char* e = getenv("CK_LUT_SOURCE");
+    if (!e) return static_cast<int>(kLutAuto);
+    std::string s(e);
+    if (s == "smem") return static_cast<int>(kLutSmem);
+    if (s == "nodes") return static_cast<int>(kLutNodes);
+    return static_cast<int>(kLutAuto);
+  }();
+  return v;
 }
 
 void set_error(const std::string& msg) { g_error = msg; }
@@ -347,7 +362,22 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       if (dx) CK_CUDA(cudaMemsetAsync(dx + r0 * I, 0, sizeof(float) * rows * I, s));
       continue;
     }
-    if (dx) {
+    if (dx && W.fused_dx) {
+      // one GEMM: N tile = d features x n_i inputs, slope combine + Jacobian in the epilogue
+      CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
+      ck::DxEpilogue epi{xc, dx + r0 * I, ck::view(lut), include_tanh_jacobian, I, ck::dx_tile_inputs(d)};
+      ck::GemmProblem gx{};
+      gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
+      gx.b = {ck::at<__nv_bfloat16>(pv, P.djo_hi), ck::at<__nv_bfloat16>(pv, P.djo_lo), I, P.ldO, I * P.ldO, K};
+      gx.R = O;
+      gx.S = d;
+      gx.b_seg0 = 1;
+      gx.nz = 1;
+      gx.ldo = I;
+      gx.kclass = ck::kKGemmDx;
+      gx.dx = &epi;
+      CK_TRY(ck::gemm_bf16x3(gx, s));
+    } else if (dx) {
       CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
       ck::GemmProblem gx{};
       gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};

@@ -78,6 +78,20 @@ __device__ __forceinline__ void split_pack2(float a, float b, uint32_t& hi2, uin
   lo2 = *reinterpret_cast<uint32_t*>(&l);
 }
 
+// Exact cell choice (float64), lut.py:97-106: clip, pos = (t+1)*0.5*(N-1),
+// idx = min(trunc(pos), N-2), frac snapped to {0,1} within 1e-9.
+__device__ __forceinline__ void cell_f64(float xv, int n, int& idx, double& frac, double& t) {
+  t = tanh(static_cast<double>(xv));
+  const double tc = fmin(fmax(t, -1.0), 1.0);
+  const double pos = __dmul_rn(__dmul_rn(__dadd_rn(tc, 1.0), 0.5), static_cast<double>(n - 1));
+  long long i = static_cast<long long>(pos);
+  if (i > n - 2) i = n - 2;
+  idx = static_cast<int>(i);
+  frac = __dsub_rn(pos, static_cast<double>(idx));
+  if (frac < 1e-9) frac = 0.0;
+  if (frac > 1.0 - 1e-9) frac = 1.0;
+}
+
 // --- mbarrier --------------------------------------------------------------
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -189,6 +203,12 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
         "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
         "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
 }
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }

@@ -13,20 +13,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kSmemLutMax = 96 * 1024;  // stage tables up to this size in smem
-
-// Exact cell choice (float64), lut.py:97-106: clip, pos = (t+1)*0.5*(N-1),
-// idx = min(trunc(pos), N-2), frac snapped to {0,1} within 1e-9.
-__device__ __forceinline__ void cell_f64(float xv, int n, int& idx, double& frac, double& t) {
-  t = tanh(static_cast<double>(xv));
-  const double tc = fmin(fmax(t, -1.0), 1.0);
-  const double pos = __dmul_rn(__dmul_rn(__dadd_rn(tc, 1.0), 0.5), static_cast<double>(n - 1));
-  long long i = static_cast<long long>(pos);
-  if (i > n - 2) i = n - 2;
-  idx = static_cast<int>(i);
-  frac = __dsub_rn(pos, static_cast<double>(idx));
-  if (frac < 1e-9) frac = 0.0;
-  if (frac > 1.0 - 1e-9) frac = 1.0;
-}
+constexpr int kMaxK = 64;                // planes kernels: degree <= 63
 
 // Fast cell choice for value interpolation (float32).  frac is formed with
 // one rounding (fma of t*h against the exact h - idx), so the interpolated
@@ -80,8 +67,46 @@ __global__ void __launch_bounds__(kThreads) expand_f32_kernel(const float* __res
   }
 }
 
+// --- table columns ---------------------------------------------------------
+// Column source for the two table entries bracketing a cell.  kLutSmem reads
+// the float32 position-major table staged in shared memory; kLutNodes
+// recomputes T_k at the two grid nodes (exact float64 nodes, lut.py:83-84,
+// rounded to float32) by the recurrence T_{k+1} = 2x T_k - T_{k-1}
+// (basis.py:112-119) in float32 -- the same table entries to ~k^2 ulp, with
+// no memory traffic.  Both then interpolate v0 (1-f) + v1 f.
+__device__ __forceinline__ float grid_node_f(int i, int n, double step) {
+  return i >= n - 1 ? 1.0f : __double2float_rn(__dadd_rn(-1.0, __dmul_rn(step, static_cast<double>(i))));
+}
+
+template <int kSrc>
+struct Columns {
+  // Calls emit(k, value) for k = k0..K-1 in ascending order.
+  template <typename F>
+  __device__ __forceinline__ static void run(const float* tab, int K, int n, double step, int idx, float frac, int k0,
+                                             F&& emit) {
+    if constexpr (kSrc == kLutSmem) {
+      const float* v = tab + static_cast<int64_t>(idx) * K;
+      for (int k = k0; k < K; ++k) emit(k, lerp_ref(v[k], v[k + K], frac));
+    } else {
+      const float x0 = grid_node_f(idx, n, step), x1 = grid_node_f(idx + 1, n, step);
+      const float tx0 = 2.0f * x0, tx1 = 2.0f * x1;
+      float a_prev = 1.0f, a = x0, b_prev = 1.0f, b = x1;
+      if (k0 == 0) emit(0, 1.0f);
+      if (K > 1 && k0 <= 1) emit(1, lerp_ref(x0, x1, frac));
+      for (int k = 2; k < K; ++k) {
+        const float an = fmaf(tx0, a, -a_prev), bn = fmaf(tx1, b, -b_prev);
+        a_prev = a;
+        a = an;
+        b_prev = b;
+        b = bn;
+        if (k >= k0) emit(k, lerp_ref(a, b, frac));
+      }
+    }
+  }
+};
+
 // hi/lo planes [k-k0][r][ld], two columns per thread (packed bf16x2 stores).
-template <bool kSmem>
+template <int kSrc>
 __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __restrict__ x, int64_t rows,
                                                                  int cols, LutView lut, int k0,
                                                                  uint32_t* __restrict__ hi,
@@ -89,46 +114,79 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
                                                                  int64_t plane) {
   extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
-  const float* vt = stage_table<kSmem>(lut.values_pm, N * K, sm_tab);
+  const float* vt = kSrc == kLutSmem ? stage_table<true>(lut.values_pm, N * K, sm_tab) : nullptr;
   const int pairs = (cols + 1) >> 1;
   const int64_t n_items = rows * pairs;
+  const int64_t pl = plane >> 1;
   for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n_items;
        it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = it / pairs;
     const int c = static_cast<int>(it - r * pairs) * 2;
     const bool second = c + 1 < cols;
+    float2 xv;
+    if (second && ((cols & 1) == 0)) {
+      xv = *reinterpret_cast<const float2*>(x + r * cols + c);
+    } else {
+      xv.x = x[r * cols + c];
+      xv.y = second ? x[r * cols + c + 1] : 0.0f;
+    }
     int ia, ib;
     float fa, fb;
-    cell_f32(x[r * cols + c], N, ia, fa);
-    cell_f32(second ? x[r * cols + c + 1] : 0.0f, N, ib, fb);
-    const float* va = vt + static_cast<int64_t>(ia) * K;
-    const float* vb = vt + static_cast<int64_t>(ib) * K;
-    const int64_t o = (r * ld + c) >> 1;
-    for (int k = k0; k < K; ++k) {
-      const float a = lerp_ref(va[k], va[k + K], fa);
-      const float b = second ? lerp_ref(vb[k], vb[k + K], fb) : 0.0f;
+    cell_f32(xv.x, N, ia, fa);
+    cell_f32(xv.y, N, ib, fb);
+    uint32_t* h = hi + ((r * ld + c) >> 1);
+    uint32_t* l = lo + ((r * ld + c) >> 1);
+    auto put = [&](int k, float a, float b) {
       uint32_t h2, l2;
-      split_pack2(a, b, h2, l2);
-      const int64_t off = ((k - k0) * plane >> 1) + o;
-      hi[off] = h2;
-      lo[off] = l2;
+      split_pack2(a, second ? b : 0.0f, h2, l2);
+      h[(k - k0) * pl] = h2;
+      l[(k - k0) * pl] = l2;
+    };
+    if constexpr (kSrc == kLutSmem) {
+      const float* pa = vt + static_cast<int64_t>(ia) * K;
+      const float* pb = vt + static_cast<int64_t>(ib) * K;
+      for (int k = k0; k < K; ++k) put(k, lerp_ref(pa[k], pa[k + K], fa), lerp_ref(pb[k], pb[k + K], fb));
+    } else {
+      // both elements' recurrences advance together (no per-k arrays)
+      const float a0 = grid_node_f(ia, N, lut.step), a1 = grid_node_f(ia + 1, N, lut.step);
+      const float b0 = grid_node_f(ib, N, lut.step), b1 = grid_node_f(ib + 1, N, lut.step);
+      float pa0 = 1.0f, ca0 = a0, pa1 = 1.0f, ca1 = a1;
+      float pb0 = 1.0f, cb0 = b0, pb1 = 1.0f, cb1 = b1;
+      if (k0 == 0) put(0, 1.0f, 1.0f);
+      if (K > 1 && k0 <= 1) put(1, lerp_ref(a0, a1, fa), lerp_ref(b0, b1, fb));
+      for (int k = 2; k < K; ++k) {
+        float t;
+        t = fmaf(2.0f * a0, ca0, -pa0); pa0 = ca0; ca0 = t;
+        t = fmaf(2.0f * a1, ca1, -pa1); pa1 = ca1; ca1 = t;
+        t = fmaf(2.0f * b0, cb0, -pb0); pb0 = cb0; cb0 = t;
+        t = fmaf(2.0f * b1, cb1, -pb1); pb1 = cb1; cb1 = t;
+        if (k >= k0) put(k, lerp_ref(ca0, ca1, fa), lerp_ref(cb0, cb1, fb));
+      }
     }
   }
 }
 
-// Transposed hi/lo planes [k-k0][c][ldr] via a 64(r) x 32(c) smem tile.
-constexpr int kTR = 64, kTC = 32, kTP = kTR + 2;  // padded row (bf16) -> 33 words
-template <bool kSmem>
+// Transposed hi/lo planes [k-k0][c][ldr]: 64(r) x 32(c) tiles, every k of an
+// element produced at once, staged in smem per plane, written as full rows.
+constexpr int kTR = 64, kTC = 32, kTP = kTR + 2;  // padded row (bf16) -> 33 words, conflict-free
+template <int kSrc>
 __global__ void __launch_bounds__(kThreads) expand_planes_t_kernel(const float* __restrict__ x, int64_t rows,
                                                                    int cols, LutView lut, int k0,
                                                                    __nv_bfloat16* __restrict__ hi,
                                                                    __nv_bfloat16* __restrict__ lo,
                                                                    int64_t ldr, int64_t plane) {
-  extern __shared__ float sm_tab[];
-  __shared__ __align__(16) __nv_bfloat16 t_hi[kTC * kTP];
-  __shared__ __align__(16) __nv_bfloat16 t_lo[kTC * kTP];
+  extern __shared__ __align__(16) float sm_dyn[];
   const int K = lut.K, N = lut.N;
-  const float* vt = stage_table<kSmem>(lut.values_pm, N * K, sm_tab);
+  const int nk = K - k0;
+  const float* vt = nullptr;
+  __nv_bfloat16* t_hi;
+  if constexpr (kSrc == kLutSmem) {
+    vt = stage_table<true>(lut.values_pm, N * K, sm_dyn);
+    t_hi = reinterpret_cast<__nv_bfloat16*>(sm_dyn + ((N * K + 3) & ~3));
+  } else {
+    t_hi = reinterpret_cast<__nv_bfloat16*>(sm_dyn);
+  }
+  __nv_bfloat16* t_lo = t_hi + nk * kTC * kTP;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t r_tiles = ceil_div(rows, kTR);
   const int64_t c_tiles = ceil_div(cols, kTC);
@@ -136,40 +194,34 @@ __global__ void __launch_bounds__(kThreads) expand_planes_t_kernel(const float* 
     const int64_t r0 = (tile % r_tiles) * kTR;
     const int c0 = static_cast<int>(tile / r_tiles) * kTC;
     const int c = c0 + tx;
-    int idx[kTR / 8];
-    float fr[kTR / 8];
-    bool ok[kTR / 8];
-#pragma unroll
+#pragma unroll 2
     for (int j = 0; j < kTR / 8; ++j) {
-      const int64_t r = r0 + ty + 8 * j;
-      ok[j] = (r < rows) && (c < cols);
-      cell_f32(ok[j] ? x[r * cols + c] : 0.0f, N, idx[j], fr[j]);
-    }
-    for (int k = k0; k < K; ++k) {
-#pragma unroll
-      for (int j = 0; j < kTR / 8; ++j) {
-        const float* v = vt + static_cast<int64_t>(idx[j]) * K + k;
-        const float val = ok[j] ? lerp_ref(v[0], v[K], fr[j]) : 0.0f;
+      const int rr = ty + 8 * j;
+      const int64_t r = r0 + rr;
+      const bool ok = (r < rows) && (c < cols);
+      int idx;
+      float fr;
+      cell_f32(ok ? x[r * cols + c] : 0.0f, N, idx, fr);
+      Columns<kSrc>::run(vt, K, N, lut.step, idx, fr, k0, [&](int k, float v) {
         __nv_bfloat16 h, l;
-        split_bf16(val, h, l);
-        t_hi[tx * kTP + ty + 8 * j] = h;
-        t_lo[tx * kTP + ty + 8 * j] = l;
-      }
-      __syncthreads();
-      // each warp writes whole rows (fixed c) of 64 r-values = 32 words
-      for (int cc = ty; cc < kTC; cc += kThreads / 32) {
-        const int col = c0 + cc;
-        const int64_t r = r0 + 2 * tx;
-        if (col < cols && r < ldr) {
-          const int64_t off = (k - k0) * plane + static_cast<int64_t>(col) * ldr + r;
-          *reinterpret_cast<uint32_t*>(hi + off) =
-              *reinterpret_cast<const uint32_t*>(&t_hi[cc * kTP + 2 * tx]);
-          *reinterpret_cast<uint32_t*>(lo + off) =
-              *reinterpret_cast<const uint32_t*>(&t_lo[cc * kTP + 2 * tx]);
-        }
-      }
-      __syncthreads();
+        split_bf16(ok ? v : 0.0f, h, l);
+        t_hi[((k - k0) * kTC + tx) * kTP + rr] = h;
+        t_lo[((k - k0) * kTC + tx) * kTP + rr] = l;
+      });
     }
+    __syncthreads();
+    // each warp writes whole rows (fixed k, c) of 64 r-values = 32 words
+    for (int row = ty; row < nk * kTC; row += kThreads / 32) {
+      const int kk = row / kTC, cc = row % kTC;
+      const int col = c0 + cc;
+      const int64_t r = r0 + 2 * tx;
+      if (col < cols && r < ldr) {
+        const int64_t off = kk * plane + static_cast<int64_t>(col) * ldr + r;
+        *reinterpret_cast<uint32_t*>(hi + off) = *reinterpret_cast<const uint32_t*>(&t_hi[row * kTP + 2 * tx]);
+        *reinterpret_cast<uint32_t*>(lo + off) = *reinterpret_cast<const uint32_t*>(&t_lo[row * kTP + 2 * tx]);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -224,22 +276,32 @@ int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut,
   return kOk;
 }
 
+int pick_source(size_t table_bytes) {
+  const int o = lut_source_override();
+  if (o == kLutSmem && table_bytes <= static_cast<size_t>(kSmemLutMax)) return kLutSmem;
+  if (o == kLutNodes) return kLutNodes;
+  // default: recompute columns (no gathers, no bank conflicts); measured
+  // faster than the smem table on B200 for every table size we support
+  return kLutNodes;
+}
+
 int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
                          __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t plane, cudaStream_t s) {
   if (rows == 0 || cols == 0 || k0 >= lut->n_feat) return kOk;
   CK_CHECK(ld % 2 == 0 && plane % 2 == 0, "expand_planes: pitch must be even");
+  CK_CHECK(lut->n_feat <= kMaxK, "expand_planes: degree must be < 64");
   const LutView v = view(lut);
   const size_t tab = sizeof(float) * v.N * v.K;
   const int blocks = grid_for(rows * ((cols + 1) / 2), 8);
   auto* h = reinterpret_cast<uint32_t*>(hi);
   auto* l = reinterpret_cast<uint32_t*>(lo);
   LaunchScope scope(kKExpand, s);
-  if (tab <= static_cast<size_t>(kSmemLutMax)) {
-    CK_CUDA(cudaFuncSetAttribute(expand_planes_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (pick_source(tab) == kLutSmem) {
+    CK_CUDA(cudaFuncSetAttribute(expand_planes_kernel<kLutSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
-    expand_planes_kernel<true><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
+    expand_planes_kernel<kLutSmem><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
   } else {
-    expand_planes_kernel<false><<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
+    expand_planes_kernel<kLutNodes><<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
   }
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -251,16 +313,23 @@ int launch_expand_planes_t(const float* x, int64_t rows, int cols, const ck_lut*
   CK_CHECK(ldr % 2 == 0 && plane % 2 == 0, "expand_planes_t: pitch must be even");
   const LutView v = view(lut);
   const size_t tab = sizeof(float) * v.N * v.K;
+  const size_t tiles_bytes = 2 * sizeof(__nv_bfloat16) * static_cast<size_t>(v.K - k0) * kTC * kTP;
+  const int src = pick_source(tab + tiles_bytes);
+  const size_t smem = (src == kLutSmem ? ((tab + 15) & ~size_t(15)) : 0) + tiles_bytes;
+  CK_CHECK(smem <= 200 * 1024, "expand_planes_t: degree too large for the transpose tile");
   const int64_t tiles = ceil_div(rows, kTR) * ceil_div(cols, kTC);
-  const int64_t cap = static_cast<int64_t>(num_sms()) * 4;
+  const int per_sm = smem > 100 * 1024 ? 1 : (smem > 64 * 1024 ? 2 : 3);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
   const int blocks = static_cast<int>(tiles < cap ? tiles : cap);
   LaunchScope scope(kKExpandT, s);
-  if (tab <= static_cast<size_t>(kSmemLutMax)) {
-    CK_CUDA(cudaFuncSetAttribute(expand_planes_t_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(tab)));
-    expand_planes_t_kernel<true><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
+  if (src == kLutSmem) {
+    CK_CUDA(cudaFuncSetAttribute(expand_planes_t_kernel<kLutSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    expand_planes_t_kernel<kLutSmem><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
   } else {
-    expand_planes_t_kernel<false><<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
+    CK_CUDA(cudaFuncSetAttribute(expand_planes_t_kernel<kLutNodes>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    expand_planes_t_kernel<kLutNodes><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
   }
   CK_CUDA(cudaGetLastError());
   return kOk;

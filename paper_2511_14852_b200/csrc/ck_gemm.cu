@@ -40,10 +40,23 @@ struct Cfg {
   static_assert(kSmemBytes <= 232448, "smem budget");
 };
 
+constexpr int kEpiStore = 0;  // out (+)= acc (+ bias)
+constexpr int kEpiDx = 1;     // dx = J * sum_k slope_k * acc_k (stacked B)
+
 struct KArgs {
   int M, N;
   int S;
   int a_seg0, a_seg_z, b_seg0, b_seg_z;
+  int n_tile;      // output columns per CTA (BN, or n_i for the dx path)
+  int n_mma;       // MMA N (BN, or d * n_i)
+  int b_boxes;     // TMA boxes stacked along N per stage (1, or d)
+  uint32_t stage_tx;
+  // dx epilogue
+  const float* x;
+  float* dx;
+  const float* slopes_pm;
+  int lutK, lutN;
+  int jacobian;
   int splits;      // R splits per z
   int r_chunks;    // ceil(R / kBK)
   float* out;
@@ -53,7 +66,7 @@ struct KArgs {
   int accumulate;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                        const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
@@ -67,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
+  const int n0 = blockIdx.x * p.n_tile, m0 = blockIdx.y * kBM;
   const int z = blockIdx.z / p.splits, split = blockIdx.z % p.splits;
   const int c_begin = static_cast<int>(static_cast<long long>(split) * p.r_chunks / p.splits);
   const int c_end = static_cast<int>(static_cast<long long>(split + 1) * p.r_chunks / p.splits);
@@ -104,17 +117,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r0 = (c_begin + it % per_seg) * kBK;
         const int aseg = p.a_seg0 + s + p.a_seg_z * z;
         const int bseg = p.b_seg0 + s + p.b_seg_z * z;
-        mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+        mbar_arrive_expect_tx(&full[stage], p.stage_tx);
         tma_load_3d(st, &tm_a_hi, &full[stage], r0, m0, aseg);
         tma_load_3d(st + C::kABytes, &tm_a_lo, &full[stage], r0, m0, aseg);
-        tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, n0, bseg);
-        tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, n0, bseg);
+        if (EPI == kEpiDx) {
+          // N tile = d stacked boxes of n_i rows (feature k = bseg + j)
+          const uint32_t box_bytes = static_cast<uint32_t>(p.n_tile) * kRowBytes;
+          for (int j = 0; j < p.b_boxes; ++j) {
+            tma_load_3d(st + 2 * C::kABytes + j * box_bytes, &tm_b_hi, &full[stage], r0, n0, bseg + j);
+            tma_load_3d(st + 2 * C::kABytes + C::kBBytes + j * box_bytes, &tm_b_lo, &full[stage], r0, n0, bseg + j);
+          }
+        } else {
+          tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, n0, bseg);
+          tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, n0, bseg);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = umma_idesc_bf16_f32(kBM, BN);
+      const uint32_t idesc = umma_idesc_bf16_f32(kBM, p.n_mma);
       for (int it = 0; it < iters; ++it) {
         const int stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
@@ -139,6 +161,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       umma_commit(tmem_full);
     }
+  } else if (warp >= 4 && EPI == kEpiDx) {
+    // ---------------- fused dX epilogue ----------------
+    // TMEM column (k-1)*n_i + i holds G_k[row][i0+i] = sum_o dy[row][o] C[k][o][i0+i]
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    const bool row_ok = row < p.M;
+    const int n_i = p.n_tile, d = p.b_boxes, K = p.lutK;
+    const float* xr = p.x + static_cast<long long>(row) * p.ldo;
+    float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
+    const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+    for (int ib = 0; ib < n_i; ib += 8) {
+      int idx[8];
+      double tt[8];
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = n0 + ib + e;
+        const bool ok = row_ok && i < p.N;
+        double fr;
+        cell_f64(ok ? xr[i] : 0.0f, p.lutN, idx[e], fr, tt[e]);
+        acc[e] = 0.0f;
+      }
+#pragma unroll 1
+      for (int kb = 0; kb < d; kb += 4) {
+        uint32_t r[4][8];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (kb + kk < d) tmem_ld_32x32b_x8(tbase + (kb + kk) * n_i + ib, r[kk]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          if (kb + kk < d) {
+            const int k = kb + kk + 1;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              acc[e] = fmaf(__ldg(p.slopes_pm + static_cast<long long>(idx[e]) * K + k), __uint_as_float(r[kk][e]),
+                            acc[e]);
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = n0 + ib + e;
+        if (row_ok && i < p.N) {
+          double v = static_cast<double>(acc[e]);
+          if (p.jacobian) v *= 1.0 - tt[e] * tt[e];
+          dxr[i] = static_cast<float>(v);
+        }
+      }
+    }
+    tc_fence_before();
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     mbar_wait(tmem_full, 0);
@@ -242,19 +318,34 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   return kOk;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI>
 int launch(const GemmProblem& p, int splits, int r_chunks, float* out, long long out_split_stride, int accumulate,
            cudaStream_t s) {
   using C = Cfg<BN, STAGES>;
+  const int n_tile = EPI == kEpiDx ? p.dx->n_i : BN;
+  const int b_boxes = EPI == kEpiDx ? p.S : 1;
+  const int n_mma = n_tile * b_boxes;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM));
   CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM));
-  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, BN));
-  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, BN));
+  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile));
+  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile));
   KArgs k{};
+  k.n_tile = n_tile;
+  k.n_mma = n_mma;
+  k.b_boxes = b_boxes;
+  k.stage_tx = static_cast<uint32_t>(2 * C::kABytes + 2 * n_mma * kRowBytes);
+  if (EPI == kEpiDx) {
+    k.x = p.dx->x;
+    k.dx = p.dx->dx;
+    k.slopes_pm = p.dx->lut.slopes_pm;
+    k.lutK = p.dx->lut.K;
+    k.lutN = p.dx->lut.N;
+    k.jacobian = p.dx->jacobian;
+  }
   k.M = static_cast<int>(p.a.rows);
   k.N = static_cast<int>(p.b.rows);
-  k.S = p.S;
+  k.S = EPI == kEpiDx ? 1 : p.S;
   k.a_seg0 = p.a_seg0;
   k.a_seg_z = p.a_seg_z;
   k.b_seg0 = p.b_seg0;
@@ -270,14 +361,14 @@ int launch(const GemmProblem& p, int splits, int r_chunks, float* out, long long
   k.accumulate = accumulate;
   static bool attr_set = false;
   if (!attr_set) {
-    CK_CUDA(cudaFuncSetAttribute(gemm_bf16x3_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK_CUDA(cudaFuncSetAttribute(gemm_bf16x3_kernel<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::kSmemBytes));
     attr_set = true;
   }
-  dim3 grid(static_cast<unsigned>(ceil_div(k.N, BN)), static_cast<unsigned>(ceil_div(k.M, kBM)),
+  dim3 grid(static_cast<unsigned>(ceil_div(k.N, n_tile)), static_cast<unsigned>(ceil_div(k.M, kBM)),
             static_cast<unsigned>(p.nz * splits));
   LaunchScope scope(p.kclass, s);
-  gemm_bf16x3_kernel<BN, STAGES><<<grid, kThreads, C::kSmemBytes, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, k);
+  gemm_bf16x3_kernel<BN, STAGES, EPI><<<grid, kThreads, C::kSmemBytes, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, k);
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -304,8 +395,21 @@ int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R) {
   return splits > 1 ? static_cast<int64_t>(splits) * nz * M * N : 0;
 }
 
+int dx_tile_inputs(int d) {
+  if (d < 1) return 0;
+  for (int n_i = (256 / d) / 8 * 8; n_i >= 8; n_i -= 8)
+    if ((d * n_i) % 16 == 0 && d * n_i <= 256) return n_i;
+  return 0;
+}
+
 int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   CK_CHECK(p.S >= 1 && p.nz >= 1 && p.R >= 1, "gemm: empty reduction");
+  if (p.dx != nullptr) {
+    // fused dX: B = d stacked boxes (S = d features), N = cols of dx
+    CK_CHECK(p.nz == 1 && p.dx->n_i == dx_tile_inputs(p.S), "gemm: bad fused-dx configuration");
+    const int r_chunks = static_cast<int>(ceil_div(p.R, kBK));
+    return launch<256, 2, kEpiDx>(p, 1, r_chunks, nullptr, 0, 0, s);
+  }
   CK_CHECK(p.a.rows >= 1 && p.b.rows >= 1, "gemm: empty output");
   CK_CHECK(p.a.rows < (1ll << 31) && p.b.rows < (1ll << 31), "gemm: extent too large");
   const int bn = pick_bn(p.b.rows);
@@ -330,9 +434,9 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   // partial slot layout: [split][z][M][N]; the kernel offsets by split first
   int rc;
   if (bn == 128) {
-    rc = launch<128, 3>(q, splits, r_chunks, out, split_stride, acc, s);
+    rc = launch<128, 3, kEpiStore>(q, splits, r_chunks, out, split_stride, acc, s);
   } else {
-    rc = launch<256, 2>(q, splits, r_chunks, out, split_stride, acc, s);
+    rc = launch<256, 2, kEpiStore>(q, splits, r_chunks, out, split_stride, acc, s);
   }
   if (rc != kOk) return rc;
   if (splits > 1) {

@@ -59,8 +59,18 @@ struct LutView {
   const float* slopes_pm;
   int K;
   int N;
+  double step;
 };
-inline LutView view(const ck_lut* l) { return LutView{l->values_pm, l->slopes_pm, l->n_feat, l->lut_size}; }
+inline LutView view(const ck_lut* l) {
+  return LutView{l->values_pm, l->slopes_pm, l->n_feat, l->lut_size, l->step};
+}
+
+// How the expansion kernels obtain the two table columns bracketing a cell:
+// a shared-memory copy of the table, or recomputed on the fly from the grid
+// nodes by the Chebyshev recurrence (no table traffic at all).  kAuto picks
+// smem when the table is small, else the recurrence.
+enum LutSource : int { kLutAuto = 0, kLutSmem = 1, kLutNodes = 2 };
+int lut_source_override();  // CK_LUT_SOURCE=smem|nodes (experiments), else kLutAuto
 
 // --- expansion (ck_expand.cu) ---------------------------------------------
 // phi[r][c][k] (f32) and optional slopes[r][c][k] for every k.
@@ -119,6 +129,20 @@ struct GemmOperand {
   int64_t seg_stride;  // elements between segments
   int64_t segs;        // number of segments addressable
 };
+// Fused input-gradient epilogue (kernels.py:430-444): the GEMM's N tile
+// stacks d features x n_i inputs; the epilogue folds the d accumulators
+// with the cell slopes and the tanh Jacobian straight into dx.
+struct DxEpilogue {
+  const float* x;      // [M][cols] chunk of the layer input
+  float* dx;           // [M][cols]
+  LutView lut;
+  int jacobian;
+  int64_t cols;        // I
+  int n_i;             // inputs per N tile; the MMA N is d * n_i
+};
+// n_i for degree d, or 0 when the stacked layout does not fit one MMA.
+int dx_tile_inputs(int d);
+
 struct GemmProblem {
   GemmOperand a, b;
   int64_t R;          // reduction extent per segment
@@ -133,6 +157,7 @@ struct GemmProblem {
   float* split_ws;     // workspace for split-R partials (nullable -> no split)
   int64_t split_ws_elems;
   int kclass = kKGemmFwd;  // timing / counting class
+  const DxEpilogue* dx = nullptr;  // non-null: stacked-B fused dX path
 };
 int gemm_bf16x3(const GemmProblem& p, cudaStream_t s);
 // Workspace (floats) the split-R path may want for this problem shape.

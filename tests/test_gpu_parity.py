@@ -111,7 +111,8 @@ def test_module_autograd_matches_reference_golden(path):
 
 @pytest.mark.parametrize("shape", [(512, 1024, 1024, 8, 32768), (300, 257, 130, 3, 512),
                                    (1024, 64, 64, 4, 4096), (2048, 512, 512, 5, 1024),
-                                   (257, 96, 1, 5, 1024), (64, 257, 512, 15, 16384)])
+                                   (257, 96, 1, 5, 1024), (64, 257, 512, 15, 16384),
+                                   (128, 64, 48, 17, 2048), (96, 40, 300, 24, 32768)])
 def test_random_shapes_vs_oracle(shape):
     b, i, o, d, n = shape
     x, c_jod, dy = orc.bench_inputs(b, i, o, d, seed=b + i + o)
