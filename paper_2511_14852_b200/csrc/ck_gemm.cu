@@ -16,7 +16,9 @@
 // barrier (MMA -> epilogue).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "ck_common.cuh"
 #include "ck_internal.h"
@@ -25,16 +27,17 @@ namespace ck {
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kBK = 64;           // one 128-byte swizzle row of bf16
-constexpr int kRowBytes = kBK * 2;
 constexpr int kThreads = 256;
 
-template <int BN, int STAGES>
+// BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
+// or 32 (64-byte rows, SWIZZLE_64B, twice the stages for the same smem).
+template <int BN, int BK, int STAGES>
 struct Cfg {
+  static constexpr int kRowBytes = BK * 2;
   static constexpr int kABytes = kBM * kRowBytes;   // one of hi / lo
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
-  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   static constexpr int kBarrierBytes = 256;
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarrierBytes + 1024;
   static_assert(kSmemBytes <= 232448, "smem budget");
@@ -59,6 +62,7 @@ struct KArgs {
   int jacobian;
   int splits;      // R splits per z
   int r_chunks;    // ceil(R / kBK)
+  int n_tiles, m_tiles, total_tiles;
   float* out;
   long long ldo, out_z_stride, out_split_stride;
   const float* bias0;
@@ -66,26 +70,44 @@ struct KArgs {
   int accumulate;
 };
 
-template <int BN, int STAGES, int EPI>
+// Tile decode shared by all roles (persistent static schedule: CTA c takes
+// tiles c, c + grid, ...; n fastest so co-resident CTAs share A rows in L2).
+struct TileCoord {
+  int n0, m0, z, split, c_begin, per_seg, iters;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t) {
+  TileCoord c;
+  const int nt = p.n_tiles, mt = p.m_tiles;
+  c.n0 = (t % nt) * p.n_tile;
+  c.m0 = ((t / nt) % mt) * kBM;
+  const int zs = t / (nt * mt);
+  c.z = zs / p.splits;
+  c.split = zs % p.splits;
+  c.c_begin = static_cast<int>(static_cast<long long>(c.split) * p.r_chunks / p.splits);
+  const int c_end = static_cast<int>(static_cast<long long>(c.split + 1) * p.r_chunks / p.splits);
+  c.per_seg = c_end - c.c_begin;
+  c.iters = p.S * c.per_seg;
+  return c;
+}
+
+template <int BN, int BK, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                        const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                        const KArgs p) {
-  using C = Cfg<BN, STAGES>;
+  using C = Cfg<BN, BK, STAGES>;
+  constexpr int kRowBytes = C::kRowBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;  // [2] accumulator ready (MMA -> epilogue)
+  uint64_t* tempty = tfull + 2;      // [2] accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * p.n_tile, m0 = blockIdx.y * kBM;
-  const int z = blockIdx.z / p.splits, split = blockIdx.z % p.splits;
-  const int c_begin = static_cast<int>(static_cast<long long>(split) * p.r_chunks / p.splits);
-  const int c_end = static_cast<int>(static_cast<long long>(split + 1) * p.r_chunks / p.splits);
-  const int per_seg = c_end - c_begin;
-  const int iters = p.S * per_seg;
+  const int total = p.total_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a_hi);
@@ -96,7 +118,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
@@ -108,28 +133,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      for (int it = 0; it < iters; ++it) {
-        const int stage = it % STAGES;
-        const uint32_t phase = (it / STAGES) & 1;
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* st = smem + stage * C::kStageBytes;
-        const int s = it / per_seg;
-        const int r0 = (c_begin + it % per_seg) * kBK;
-        const int aseg = p.a_seg0 + s + p.a_seg_z * z;
-        const int bseg = p.b_seg0 + s + p.b_seg_z * z;
-        mbar_arrive_expect_tx(&full[stage], p.stage_tx);
-        tma_load_3d(st, &tm_a_hi, &full[stage], r0, m0, aseg);
-        tma_load_3d(st + C::kABytes, &tm_a_lo, &full[stage], r0, m0, aseg);
-        if (EPI == kEpiDx) {
-          // N tile = d stacked boxes of n_i rows (feature k = bseg + j)
-          const uint32_t box_bytes = static_cast<uint32_t>(p.n_tile) * kRowBytes;
-          for (int j = 0; j < p.b_boxes; ++j) {
-            tma_load_3d(st + 2 * C::kABytes + j * box_bytes, &tm_b_hi, &full[stage], r0, n0, bseg + j);
-            tma_load_3d(st + 2 * C::kABytes + C::kBBytes + j * box_bytes, &tm_b_lo, &full[stage], r0, n0, bseg + j);
+      uint32_t g = 0;  // global k-iteration counter (smem ring position)
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord tc = decode_tile(p, t);
+        for (int it = 0; it < tc.iters; ++it, ++g) {
+          const int stage = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * C::kStageBytes;
+          const int s = it / tc.per_seg;
+          const int r0 = (tc.c_begin + it % tc.per_seg) * BK;
+          const int aseg = p.a_seg0 + s + p.a_seg_z * tc.z;
+          const int bseg = p.b_seg0 + s + p.b_seg_z * tc.z;
+          mbar_arrive_expect_tx(&full[stage], p.stage_tx);
+          tma_load_3d(st, &tm_a_hi, &full[stage], r0, tc.m0, aseg);
+          tma_load_3d(st + C::kABytes, &tm_a_lo, &full[stage], r0, tc.m0, aseg);
+          if (EPI == kEpiDx) {
+            // N tile = d stacked boxes of n_i rows (feature k = bseg + j)
+            const uint32_t box_bytes = static_cast<uint32_t>(p.n_tile) * kRowBytes;
+            for (int j = 0; j < p.b_boxes; ++j) {
+              tma_load_3d(st + 2 * C::kABytes + j * box_bytes, &tm_b_hi, &full[stage], r0, tc.n0, bseg + j);
+              tma_load_3d(st + 2 * C::kABytes + C::kBBytes + j * box_bytes, &tm_b_lo, &full[stage], r0, tc.n0,
+                          bseg + j);
+            }
+          } else {
+            tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, tc.n0, bseg);
+            tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, tc.n0, bseg);
           }
-        } else {
-          tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, n0, bseg);
-          tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, n0, bseg);
         }
       }
     }
@@ -137,139 +167,148 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
       const uint32_t idesc = umma_idesc_bf16_f32(kBM, p.n_mma);
-      for (int it = 0; it < iters; ++it) {
-        const int stage = it % STAGES;
-        const uint32_t phase = (it / STAGES) & 1;
-        mbar_wait(&full[stage], phase);
+      uint32_t g = 0, lt = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+        const TileCoord tc = decode_tile(p, t);
+        const uint32_t acc = lt & 1, use = lt >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);  // epilogue has drained this buffer
         tc_fence_after();
-        const uint32_t a_hi = smem_u32(smem + stage * C::kStageBytes);
-        const uint32_t a_lo = a_hi + C::kABytes;
-        const uint32_t b_hi = a_hi + 2 * C::kABytes;
-        const uint32_t b_lo = b_hi + C::kBBytes;
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int it = 0; it < tc.iters; ++it, ++g) {
+          const int stage = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_hi = smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t a_lo = a_hi + C::kABytes;
+          const uint32_t b_hi = a_hi + 2 * C::kABytes;
+          const uint32_t b_lo = b_hi + C::kBBytes;
 #pragma unroll
-        for (int kk = 0; kk < kBK / 16; ++kk) {
-          const uint32_t off = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
-          const uint64_t dah = umma_desc_kmajor<kRowBytes>(a_hi + off);
-          const uint64_t dal = umma_desc_kmajor<kRowBytes>(a_lo + off);
-          const uint64_t dbh = umma_desc_kmajor<kRowBytes>(b_hi + off);
-          const uint64_t dbl = umma_desc_kmajor<kRowBytes>(b_lo + off);
-          umma_bf16(tmem_base, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
-          umma_bf16(tmem_base, dah, dbl, idesc, 1u);
-          umma_bf16(tmem_base, dal, dbh, idesc, 1u);
-        }
-        umma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
-      }
-      umma_commit(tmem_full);
-    }
-  } else if (warp >= 4 && EPI == kEpiDx) {
-    // ---------------- fused dX epilogue ----------------
-    // TMEM column (k-1)*n_i + i holds G_k[row][i0+i] = sum_o dy[row][o] C[k][o][i0+i]
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    const bool row_ok = row < p.M;
-    const int n_i = p.n_tile, d = p.b_boxes, K = p.lutK;
-    const float* xr = p.x + static_cast<long long>(row) * p.ldo;
-    float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
-    const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-#pragma unroll 1
-    for (int ib = 0; ib < n_i; ib += 8) {
-      int idx[8];
-      double tt[8];
-      float acc[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int i = n0 + ib + e;
-        const bool ok = row_ok && i < p.N;
-        double fr;
-        cell_f64(ok ? xr[i] : 0.0f, p.lutN, idx[e], fr, tt[e]);
-        acc[e] = 0.0f;
-      }
-#pragma unroll 1
-      for (int kb = 0; kb < d; kb += 4) {
-        uint32_t r[4][8];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          if (kb + kk < d) tmem_ld_32x32b_x8(tbase + (kb + kk) * n_i + ib, r[kk]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          if (kb + kk < d) {
-            const int k = kb + kk + 1;
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              acc[e] = fmaf(__ldg(p.slopes_pm + static_cast<long long>(idx[e]) * K + k), __uint_as_float(r[kk][e]),
-                            acc[e]);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint32_t off = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
+            const uint64_t dah = umma_desc_kmajor<kRowBytes>(a_hi + off);
+            const uint64_t dal = umma_desc_kmajor<kRowBytes>(a_lo + off);
+            const uint64_t dbh = umma_desc_kmajor<kRowBytes>(b_hi + off);
+            const uint64_t dbl = umma_desc_kmajor<kRowBytes>(b_lo + off);
+            umma_bf16(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+            umma_bf16(d_tmem, dah, dbl, idesc, 1u);
+            umma_bf16(d_tmem, dal, dbh, idesc, 1u);
           }
+          umma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
         }
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int i = n0 + ib + e;
-        if (row_ok && i < p.N) {
-          double v = static_cast<double>(acc[e]);
-          if (p.jacobian) v *= 1.0 - tt[e] * tt[e];
-          dxr[i] = static_cast<float>(v);
-        }
+        umma_commit(&tfull[acc]);
       }
     }
-    tc_fence_before();
   } else if (warp >= 4) {
-    // ---------------- epilogue ----------------
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    float* out = p.out + static_cast<long long>(z) * p.out_z_stride +
-                 static_cast<long long>(split) * p.out_split_stride;
-    const bool row_ok = row < p.M;
-    float* orow = out + static_cast<long long>(row) * p.ldo;
-    const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      const TileCoord tc = decode_tile(p, t);
+      const uint32_t acc = lt & 1, use = lt >> 1;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const int row = tc.m0 + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      if constexpr (EPI == kEpiDx) {
+        // ------------- fused dX epilogue -------------
+        // TMEM column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i]
+        const int n_i = p.n_tile, d = p.b_boxes, K = p.lutK;
+        const float* xr = p.x + static_cast<long long>(row) * p.ldo;
+        float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c, r);
-      tmem_ld_wait();
-      const int nb = n0 + c;
-      if (!row_ok || nb >= p.N) continue;
-      float v[32];
+        for (int ib = 0; ib < n_i; ib += 8) {
+          int idx[8];
+          double tt[8];
+          float sacc[8];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-      if (vec && nb + 32 <= p.N) {
+          for (int e = 0; e < 8; ++e) {
+            const int i = tc.n0 + ib + e;
+            const bool ok = row_ok && i < p.N;
+            double fr;
+            cell_f64(ok ? xr[i] : 0.0f, p.lutN, idx[e], fr, tt[e]);
+            sacc[e] = 0.0f;
+          }
+#pragma unroll 1
+          for (int kb = 0; kb < d; kb += 4) {
+            uint32_t r[4][8];
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          if (p.bias0) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias0 + nb + j));
-            o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+            for (int kk = 0; kk < 4; ++kk)
+              if (kb + kk < d) tmem_ld_32x32b_x8(tbase + (kb + kk) * n_i + ib, r[kk]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if (kb + kk < d) {
+                const int k = kb + kk + 1;
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  sacc[e] = fmaf(__ldg(p.slopes_pm + static_cast<long long>(idx[e]) * K + k),
+                                 __uint_as_float(r[kk][e]), sacc[e]);
+              }
+            }
           }
-          if (p.bias1) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias1 + nb + j));
-            o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int i = tc.n0 + ib + e;
+            if (row_ok && i < p.N) {
+              double v = static_cast<double>(sacc[e]);
+              if (p.jacobian) v *= 1.0 - tt[e] * tt[e];
+              dxr[i] = static_cast<float>(v);
+            }
           }
-          float4* dst = reinterpret_cast<float4*>(orow + nb + j);
-          if (p.accumulate) {
-            const float4 prev = *dst;
-            o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
-          }
-          *dst = o;
         }
       } else {
+        // ------------- store epilogue -------------
+        float* out = p.out + static_cast<long long>(tc.z) * p.out_z_stride +
+                     static_cast<long long>(tc.split) * p.out_split_stride;
+        float* orow = out + static_cast<long long>(row) * p.ldo;
+        const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + c, r);
+          tmem_ld_wait();
+          const int nb = tc.n0 + c;
+          if (!row_ok || nb >= p.N) continue;
+          if (vec && nb + 32 <= p.N) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = nb + j;
-          if (n < p.N) {
-            float o = v[j];
-            if (p.bias0) o += p.bias0[n];
-            if (p.bias1) o += p.bias1[n];
-            if (p.accumulate) o += orow[n];
-            orow[n] = o;
+            for (int j = 0; j < 32; j += 4) {
+              float4 o = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                     __uint_as_float(r[j + 3]));
+              if (p.bias0) {
+                const float4 bv = __ldg(reinterpret_cast<const float4*>(p.bias0 + nb + j));
+                o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
+              }
+              if (p.bias1) {
+                const float4 bv = __ldg(reinterpret_cast<const float4*>(p.bias1 + nb + j));
+                o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
+              }
+              float4* dst = reinterpret_cast<float4*>(orow + nb + j);
+              if (p.accumulate) {
+                const float4 prev = *dst;
+                o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
+              }
+              *dst = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = nb + j;
+              if (n < p.N) {
+                float o = __uint_as_float(r[j]);
+                if (p.bias0) o += p.bias0[n];
+                if (p.bias1) o += p.bias1[n];
+                if (p.accumulate) o += orow[n];
+                orow[n] = o;
+              }
+            }
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 2) {
@@ -296,7 +335,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t rows, int64_t segs, int64_t ld,
-             int64_t seg_stride, int box_rows) {
+             int64_t seg_stride, int box_rows, int bk) {
   auto encode = get_encode();
   if (!encode) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -306,10 +345,10 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   CK_CHECK(ld % 8 == 0 && seg_stride % 8 == 0, "gemm operand pitch must be a multiple of 8 elements");
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(segs)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 2), static_cast<cuuint64_t>(seg_stride * 2)};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(bk), static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(base), dims, strides, box,
-                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed with code " + std::to_string(static_cast<int>(r)));
@@ -318,18 +357,20 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   return kOk;
 }
 
-template <int BN, int STAGES, int EPI>
-int launch(const GemmProblem& p, int splits, int r_chunks, float* out, long long out_split_stride, int accumulate,
+template <int BN, int BK, int STAGES, int EPI>
+int launch(const GemmProblem& p, int splits, float* out, long long out_split_stride, int accumulate,
            cudaStream_t s) {
-  using C = Cfg<BN, STAGES>;
+  using C = Cfg<BN, BK, STAGES>;
+  constexpr int kRowBytes = C::kRowBytes;
+  const int r_chunks = static_cast<int>(ceil_div(p.R, BK));
   const int n_tile = EPI == kEpiDx ? p.dx->n_i : BN;
   const int b_boxes = EPI == kEpiDx ? p.S : 1;
   const int n_mma = n_tile * b_boxes;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
-  CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM));
-  CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM));
-  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile));
-  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile));
+  CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
+  CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
+  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile, BK));
+  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile, BK));
   KArgs k{};
   k.n_tile = n_tile;
   k.n_mma = n_mma;
@@ -361,24 +402,37 @@ int launch(const GemmProblem& p, int splits, int r_chunks, float* out, long long
   k.accumulate = accumulate;
   static bool attr_set = false;
   if (!attr_set) {
-    CK_CUDA(cudaFuncSetAttribute(gemm_bf16x3_kernel<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK_CUDA(cudaFuncSetAttribute(gemm_bf16x3_kernel<BN, BK, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::kSmemBytes));
     attr_set = true;
   }
-  dim3 grid(static_cast<unsigned>(ceil_div(k.N, n_tile)), static_cast<unsigned>(ceil_div(k.M, kBM)),
-            static_cast<unsigned>(p.nz * splits));
+  k.n_tiles = static_cast<int>(ceil_div(k.N, n_tile));
+  k.m_tiles = static_cast<int>(ceil_div(k.M, kBM));
+  const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles * p.nz * splits;
+  CK_CHECK(total < (1ll << 31), "gemm: too many tiles");
+  k.total_tiles = static_cast<int>(total);
+  const int sms = num_sms();
+  dim3 grid(static_cast<unsigned>(total < sms ? total : sms));
   LaunchScope scope(p.kclass, s);
-  gemm_bf16x3_kernel<BN, STAGES, EPI><<<grid, kThreads, C::kSmemBytes, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, k);
+  gemm_bf16x3_kernel<BN, BK, STAGES, EPI><<<grid, kThreads, C::kSmemBytes, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, k);
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
 
+int gemm_bk() {
+  static int bk = [] {
+    const char* e = getenv("CK_GEMM_BK");
+    return (e && std::string(e) == "64") ? 64 : 32;
+  }();
+  return bk;
+}
+
 int choose_splits(int64_t M, int64_t N, int nz, int64_t R, int bn) {
   const int64_t tiles = ceil_div(M, kBM) * ceil_div(N, bn) * nz;
-  const int64_t chunks = ceil_div(R, kBK);
+  const int64_t chunks = ceil_div(R, 64);
   const int64_t sms = num_sms();
   if (tiles >= sms) return 1;
-  // enough CTAs for ~2 waves, but keep >= 8 K-chunks per split
+  // enough CTAs for ~2 waves, but keep >= 8 64-wide chunks per split
   int64_t splits = ceil_div(2 * sms, tiles);
   const int64_t max_splits = chunks / 8 > 1 ? chunks / 8 : 1;
   if (splits > max_splits) splits = max_splits;
@@ -407,13 +461,12 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   if (p.dx != nullptr) {
     // fused dX: B = d stacked boxes (S = d features), N = cols of dx
     CK_CHECK(p.nz == 1 && p.dx->n_i == dx_tile_inputs(p.S), "gemm: bad fused-dx configuration");
-    const int r_chunks = static_cast<int>(ceil_div(p.R, kBK));
-    return launch<256, 2, kEpiDx>(p, 1, r_chunks, nullptr, 0, 0, s);
+    if (gemm_bk() == 64) return launch<256, 64, 2, kEpiDx>(p, 1, nullptr, 0, 0, s);
+    return launch<256, 32, 4, kEpiDx>(p, 1, nullptr, 0, 0, s);
   }
   CK_CHECK(p.a.rows >= 1 && p.b.rows >= 1, "gemm: empty output");
   CK_CHECK(p.a.rows < (1ll << 31) && p.b.rows < (1ll << 31), "gemm: extent too large");
   const int bn = pick_bn(p.b.rows);
-  const int r_chunks = static_cast<int>(ceil_div(p.R, kBK));
   int splits = choose_splits(p.a.rows, p.b.rows, p.nz, p.R, bn);
   const int64_t need = static_cast<int64_t>(splits) * p.nz * p.a.rows * p.b.rows;
   if (splits > 1 && (p.split_ws == nullptr || p.split_ws_elems < need)) splits = 1;
@@ -433,10 +486,13 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   GemmProblem q = p;
   // partial slot layout: [split][z][M][N]; the kernel offsets by split first
   int rc;
+  const bool bk64 = gemm_bk() == 64;
   if (bn == 128) {
-    rc = launch<128, 3, kEpiStore>(q, splits, r_chunks, out, split_stride, acc, s);
+    rc = bk64 ? launch<128, 64, 3, kEpiStore>(q, splits, out, split_stride, acc, s)
+              : launch<128, 32, 6, kEpiStore>(q, splits, out, split_stride, acc, s);
   } else {
-    rc = launch<256, 2, kEpiStore>(q, splits, r_chunks, out, split_stride, acc, s);
+    rc = bk64 ? launch<256, 64, 2, kEpiStore>(q, splits, out, split_stride, acc, s)
+              : launch<256, 32, 4, kEpiStore>(q, splits, out, split_stride, acc, s);
   }
   if (rc != kOk) return rc;
   if (splits > 1) {
