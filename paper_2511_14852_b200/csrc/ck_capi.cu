@@ -18,21 +18,28 @@ thread_local std::string g_error;
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-// Opaque coefficient-prep buffer: bf16 hi/lo DOJ [K][O][ldI], DJO [K][I][ldO],
-// and c0sum[O] = sum_i C[0][o][i].
+// Opaque coefficient-prep buffer: bf16 hi/lo DOJ [K][O][ldI] (forward B
+// operand); the input-gradient B operand, either "stacked" -- rows
+// (i-tile, k, i) so one TMA box feeds a d x n_i N tile -- or plain DJO
+// [K][I][ldO] when the degree is too large to stack; and c0sum[O].
 struct PrepLayout {
   int64_t ldI, ldO;
-  size_t doj_hi, doj_lo, djo_hi, djo_lo, c0sum, total;
+  int n_i;             // inputs per stacked tile (0: DJO layout)
+  int64_t dxb_rows;    // rows of the input-gradient operand
+  size_t doj_hi, doj_lo, dxb_hi, dxb_lo, c0sum, total;
   PrepLayout(int I, int O, int K) {
     ldI = round_up(I, 8);
     ldO = round_up(O, 8);
+    const int d = K - 1;
+    n_i = dx_tile_inputs(d);
+    dxb_rows = n_i > 0 ? ceil_div(I, n_i) * d * n_i : static_cast<int64_t>(K) * I;
     const size_t doj = align_up(sizeof(__nv_bfloat16) * K * O * ldI);
-    const size_t djo = align_up(sizeof(__nv_bfloat16) * K * I * ldO);
+    const size_t dxb = align_up(sizeof(__nv_bfloat16) * dxb_rows * ldO);
     doj_hi = 0;
     doj_lo = doj_hi + doj;
-    djo_hi = doj_lo + doj;
-    djo_lo = djo_hi + djo;
-    c0sum = djo_lo + djo;
+    dxb_hi = doj_lo + doj;
+    dxb_lo = dxb_hi + dxb;
+    c0sum = dxb_lo + dxb;
     total = c0sum + align_up(sizeof(float) * O);
   }
 };
@@ -255,9 +262,15 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
   // DOJ copies: rows (k,o), unit stride in i
   CK_TRY(ck::launch_split_rows(coeff_doj, 1, K * O, I, 0, ck::at<__nv_bfloat16>(prep, L.doj_hi),
                                ck::at<__nv_bfloat16>(prep, L.doj_lo), L.ldI, 0, s));
-  // DJO copies: per k, transpose [O][I] -> [I][O]
-  CK_TRY(ck::launch_split_transpose(coeff_doj, K, O, I, O * I, ck::at<__nv_bfloat16>(prep, L.djo_hi),
-                                    ck::at<__nv_bfloat16>(prep, L.djo_lo), L.ldO, I * L.ldO, s));
+  if (L.n_i > 0) {
+    // stacked input-gradient operand (k = 1..d), padded inputs zeroed
+    CK_TRY(ck::launch_split_transpose_stacked(coeff_doj, K, O, I, L.n_i, ck::at<__nv_bfloat16>(prep, L.dxb_hi),
+                                              ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, s));
+  } else {
+    // DJO copies: per k, transpose [O][I] -> [I][O]
+    CK_TRY(ck::launch_split_transpose(coeff_doj, K, O, I, O * I, ck::at<__nv_bfloat16>(prep, L.dxb_hi),
+                                      ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, I * L.ldO, s));
+  }
   // k = 0 term: T_0 == 1 so its contribution is the per-output constant
   CK_TRY(ck::launch_row_sum(coeff_doj, O, I, ck::at<float>(prep, L.c0sum), s));
   return kOk;
@@ -365,13 +378,13 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
     if (dx && W.fused_dx) {
       // one GEMM: N tile = d features x n_i inputs, slope combine + Jacobian in the epilogue
       CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
-      ck::DxEpilogue epi{xc, dx + r0 * I, ck::view(lut), include_tanh_jacobian, I, ck::dx_tile_inputs(d)};
+      ck::DxEpilogue epi{xc, dx + r0 * I, ck::view(lut), include_tanh_jacobian, I, P.n_i};
       ck::GemmProblem gx{};
       gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
-      gx.b = {ck::at<__nv_bfloat16>(pv, P.djo_hi), ck::at<__nv_bfloat16>(pv, P.djo_lo), I, P.ldO, I * P.ldO, K};
+      gx.b = {ck::at<__nv_bfloat16>(pv, P.dxb_hi), ck::at<__nv_bfloat16>(pv, P.dxb_lo), P.dxb_rows, P.ldO,
+              P.dxb_rows * P.ldO, 1};
       gx.R = O;
       gx.S = d;
-      gx.b_seg0 = 1;
       gx.nz = 1;
       gx.ldo = I;
       gx.kclass = ck::kKGemmDx;
@@ -381,7 +394,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
       ck::GemmProblem gx{};
       gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
-      gx.b = {ck::at<__nv_bfloat16>(pv, P.djo_hi), ck::at<__nv_bfloat16>(pv, P.djo_lo), I, P.ldO, I * P.ldO, K};
+      gx.b = {ck::at<__nv_bfloat16>(pv, P.dxb_hi), ck::at<__nv_bfloat16>(pv, P.dxb_lo), I, P.ldO, I * P.ldO, K};
       gx.R = O;
       gx.S = 1;
       gx.b_seg0 = 1;   // z = k - 1

@@ -27,7 +27,8 @@ namespace ck {
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
 
 // BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
 // or 32 (64-byte rows, SWIZZLE_64B, twice the stages for the same smem).
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -149,13 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_3d(st, &tm_a_hi, &full[stage], r0, tc.m0, aseg);
           tma_load_3d(st + C::kABytes, &tm_a_lo, &full[stage], r0, tc.m0, aseg);
           if (EPI == kEpiDx) {
-            // N tile = d stacked boxes of n_i rows (feature k = bseg + j)
-            const uint32_t box_bytes = static_cast<uint32_t>(p.n_tile) * kRowBytes;
-            for (int j = 0; j < p.b_boxes; ++j) {
-              tma_load_3d(st + 2 * C::kABytes + j * box_bytes, &tm_b_hi, &full[stage], r0, tc.n0, bseg + j);
-              tma_load_3d(st + 2 * C::kABytes + C::kBBytes + j * box_bytes, &tm_b_lo, &full[stage], r0, tc.n0,
-                          bseg + j);
-            }
+            // stacked operand: the whole d x n_i N tile is one box of n_mma rows
+            const int brow = (tc.n0 / p.n_tile) * p.n_mma;
+            tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, brow, 0);
+            tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, brow, 0);
           } else {
             tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, tc.n0, bseg);
             tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, tc.n0, bseg);
@@ -200,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int h = (warp - 4) >> 2;   // which half of the tile's columns
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const TileCoord tc = decode_tile(p, t);
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* xr = p.x + static_cast<long long>(row) * p.ldo;
         float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
 #pragma unroll 1
-        for (int ib = 0; ib < n_i; ib += 8) {
+        for (int ib = 8 * h; ib < n_i; ib += 16) {
           int idx[8];
           double tt[8];
           float sacc[8];
@@ -264,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* orow = out + static_cast<long long>(row) * p.ldo;
         const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = h * (BN / 2); c < (h + 1) * (BN / 2); c += 32) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tbase + c, r);
           tmem_ld_wait();
@@ -369,8 +368,9 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
   CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
-  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile, BK));
-  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, n_tile, BK));
+  const int b_box = EPI == kEpiDx ? n_mma : n_tile;
+  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK));
+  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK));
   KArgs k{};
   k.n_tile = n_tile;
   k.n_mma = n_mma;
@@ -385,7 +385,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
     k.jacobian = p.dx->jacobian;
   }
   k.M = static_cast<int>(p.a.rows);
-  k.N = static_cast<int>(p.b.rows);
+  k.N = static_cast<int>(EPI == kEpiDx ? p.dx->cols : p.b.rows);
   k.S = EPI == kEpiDx ? 1 : p.S;
   k.a_seg0 = p.a_seg0;
   k.a_seg_z = p.a_seg_z;

@@ -97,6 +97,11 @@ int launch_split_rows(const float* in, int64_t nz, int64_t rows, int64_t cols, i
 int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t cols, int64_t in_z_stride,
                            __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t out_z_stride,
                            cudaStream_t s);
+// Stacked input-gradient operand from DOJ fp32 [K][O][I]: row
+// (i / n_i) * d * n_i + (k-1) * n_i + i % n_i holds C[k][:, i] (k = 1..d,
+// d = K-1) as bf16 hi/lo with pitch ld; rows of padded inputs are zero.
+int launch_split_transpose_stacked(const float* c_doj, int64_t K, int64_t O, int64_t I, int n_i, __nv_bfloat16* hi,
+                                   __nv_bfloat16* lo, int64_t ld, cudaStream_t s);
 // out[r] = sum_c in[r][c]  (float64 accumulation in a fixed order)
 int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s);
 // part[slot][c] = sum over rows of in[rows][cols]  (float64, fixed order)

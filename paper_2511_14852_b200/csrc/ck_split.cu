@@ -67,6 +67,40 @@ __global__ void split_transpose_kernel(const float* __restrict__ in, int64_t nz,
   }
 }
 
+// Stacked transpose: input tile 32 (o) x 32 (i) of plane k (>= 1); output
+// row (i / n_i) * d * n_i + (k-1) * n_i + i % n_i, column o.
+__global__ void split_transpose_stacked_kernel(const float* __restrict__ c, int64_t K, int64_t O, int64_t I, int n_i,
+                                               __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
+                                               int64_t ld) {
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t d = K - 1;
+  const int64_t i_pad = ceil_div(I, n_i) * n_i;
+  const int64_t ot = ceil_div(O, 32), it_ = ceil_div(i_pad, 32);
+  for (int64_t t = blockIdx.x; t < d * ot * it_; t += gridDim.x) {
+    const int64_t k = 1 + t / (ot * it_);
+    const int64_t rem = t % (ot * it_);
+    const int64_t o0 = (rem / it_) * 32, i0 = (rem % it_) * 32;
+    const float* src = c + k * O * I;
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t o = o0 + j, i = i0 + tx;
+      tile[j][tx] = (o < O && i < I) ? src[o * I + i] : 0.0f;
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t i = i0 + j, o = o0 + tx;
+      if (i < i_pad && o < ld) {
+        __nv_bfloat16 h, l;
+        split_bf16(tile[tx][j], h, l);
+        const int64_t row = (i / n_i) * d * n_i + (k - 1) * n_i + i % n_i;
+        hi[row * ld + o] = h;
+        lo[row * ld + o] = l;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // one warp per row, float64 lane partials combined by a fixed shuffle tree
 __global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -181,6 +215,19 @@ int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t co
   LaunchScope scope(kKSplit, s);
   split_transpose_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s>>>(in, nz, rows, cols, in_zs,
                                                                                          hi, lo, ld, out_zs);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_split_transpose_stacked(const float* c_doj, int64_t K, int64_t O, int64_t I, int n_i, __nv_bfloat16* hi,
+                                   __nv_bfloat16* lo, int64_t ld, cudaStream_t s) {
+  if (K < 2 || O == 0 || I == 0) return kOk;
+  const int64_t i_pad = ceil_div(I, n_i) * n_i;
+  const int64_t tiles = (K - 1) * ceil_div(O, 32) * ceil_div(i_pad, 32);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  LaunchScope scope(kKSplit, s);
+  split_transpose_stacked_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s>>>(c_doj, K, O, I, n_i,
+                                                                                                 hi, lo, ld);
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
