@@ -194,6 +194,12 @@ __global__ void __launch_bounds__(kThreads) expand_planes_t_kernel(const float* 
     const int64_t r0 = (tile % r_tiles) * kTR;
     const int c0 = static_cast<int>(tile / r_tiles) * kTC;
     const int c = c0 + tx;
+    float xv[kTR / 8];
+#pragma unroll
+    for (int j = 0; j < kTR / 8; ++j) {  // all loads in flight before any math
+      const int64_t r = r0 + ty + 8 * j;
+      xv[j] = (r < rows && c < cols) ? __ldg(x + r * cols + c) : 0.0f;
+    }
 #pragma unroll 2
     for (int j = 0; j < kTR / 8; ++j) {
       const int rr = ty + 8 * j;
@@ -201,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) expand_planes_t_kernel(const float* 
       const bool ok = (r < rows) && (c < cols);
       int idx;
       float fr;
-      cell_f32(ok ? x[r * cols + c] : 0.0f, N, idx, fr);
+      cell_f32(xv[j], N, idx, fr);
       Columns<kSrc>::run(vt, K, N, lut.step, idx, fr, k0, [&](int k, float v) {
         __nv_bfloat16 h, l;
         split_bf16(ok ? v : 0.0f, h, l);

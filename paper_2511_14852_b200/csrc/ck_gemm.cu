@@ -29,6 +29,7 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
+constexpr int kMaxDFused = 16;       // fused dX epilogue: degree <= 16
 
 // BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
 // or 32 (64-byte rows, SWIZZLE_64B, twice the stages for the same smem).
@@ -60,6 +61,8 @@ struct KArgs {
   float* dx;
   const float* slopes_pm;
   int lutK, lutN;
+  double step;
+  float guard;
   int jacobian;
   int splits;      // R splits per z
   int r_chunks;    // ceil(R / kBK)
@@ -215,46 +218,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_i = p.n_tile, d = p.b_boxes, K = p.lutK;
         const float* xr = p.x + static_cast<long long>(row) * p.ldo;
         float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
+        // columns interleaved between the two warps of this lane quarter;
+        // x of the next column is prefetched to hide its load latency
+        const double hN = 0.5 * static_cast<double>(p.lutN - 1);
+        float xnext = (row_ok && tc.n0 + h < p.N && h < n_i) ? xr[tc.n0 + h] : 0.0f;
 #pragma unroll 1
-        for (int ib = 8 * h; ib < n_i; ib += 16) {
-          int idx[8];
-          double tt[8];
-          float sacc[8];
+        for (int col = h; col < n_i; col += 2) {
+          const int i = tc.n0 + col;
+          const bool ok = row_ok && i < p.N;
+          const float xv = xnext;
+          xnext = (row_ok && i + 2 < p.N && col + 2 < n_i) ? xr[i + 2] : 0.0f;
+          uint32_t r[kMaxDFused];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int i = tc.n0 + ib + e;
-            const bool ok = row_ok && i < p.N;
-            double fr;
-            cell_f64(ok ? xr[i] : 0.0f, p.lutN, idx[e], fr, tt[e]);
-            sacc[e] = 0.0f;
-          }
-#pragma unroll 1
-          for (int kb = 0; kb < d; kb += 4) {
-            uint32_t r[4][8];
+          for (int kk = 0; kk < kMaxDFused; ++kk)
+            if (kk < d) tmem_ld_32x32b_x1(tbase + kk * n_i + col, r[kk]);
+          float t;
+          const int idx = cell_guarded(ok ? xv : 0.0f, p.lutN, p.guard, t);
+          // slopes of cell idx from the two grid nodes (float64 recurrence)
+          const double x0 = __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx)));
+          const double x1 = idx + 1 >= p.lutN - 1 ? 1.0 : __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx + 1)));
+          const double tx0 = 2.0 * x0, tx1 = 2.0 * x1;
+          double pa = 1.0, ca = x0, pb = 1.0, cb = x1;
+          tmem_ld_wait();
+          float acc = __double2float_rn((x1 - x0) * hN) * __uint_as_float(r[0]);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              if (kb + kk < d) tmem_ld_32x32b_x8(tbase + (kb + kk) * n_i + ib, r[kk]);
-            tmem_ld_wait();
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              if (kb + kk < d) {
-                const int k = kb + kk + 1;
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  sacc[e] = fmaf(__ldg(p.slopes_pm + static_cast<long long>(idx[e]) * K + k),
-                                 __uint_as_float(r[kk][e]), sacc[e]);
-              }
+          for (int kk = 1; kk < kMaxDFused; ++kk) {
+            if (kk < d) {
+              const double na = fma(tx0, ca, -pa), nb = fma(tx1, cb, -pb);
+              pa = ca;
+              ca = na;
+              pb = cb;
+              cb = nb;
+              acc = fmaf(__double2float_rn((cb - ca) * hN), __uint_as_float(r[kk]), acc);
             }
           }
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int i = tc.n0 + ib + e;
-            if (row_ok && i < p.N) {
-              double v = static_cast<double>(sacc[e]);
-              if (p.jacobian) v *= 1.0 - tt[e] * tt[e];
-              dxr[i] = static_cast<float>(v);
-            }
-          }
+          if (ok) dxr[i] = p.jacobian ? acc * (1.0f - t * t) : acc;
         }
       } else {
         // ------------- store epilogue -------------
@@ -382,6 +380,10 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
     k.slopes_pm = p.dx->lut.slopes_pm;
     k.lutK = p.dx->lut.K;
     k.lutN = p.dx->lut.N;
+    k.step = p.dx->lut.step;
+    // float32 position error <= (3e-7 tanhf + ulp) * (N-1)/2; recompute in
+    // float64 inside that band
+    k.guard = fminf(0.5f, fmaxf(1e-3f, 4e-7f * static_cast<float>(p.dx->lut.N)));
     k.jacobian = p.dx->jacobian;
   }
   k.M = static_cast<int>(p.a.rows);
@@ -450,7 +452,7 @@ int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R) {
 }
 
 int dx_tile_inputs(int d) {
-  if (d < 1) return 0;
+  if (d < 1 || d > kMaxDFused) return 0;
   for (int n_i = (256 / d) / 8 * 8; n_i >= 8; n_i -= 8)
     if ((d * n_i) % 16 == 0 && d * n_i <= 256) return n_i;
   return 0;
