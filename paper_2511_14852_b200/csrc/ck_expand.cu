@@ -105,7 +105,132 @@ struct Columns {
   }
 };
 
-// hi/lo planes [k-k0][r][ld], two columns per thread (packed bf16x2 stores).
+// Planes for features k = 1..D of two elements (a, b), fully unrolled:
+// out[k-1] packs (value_a, value_b) as bf16x2 hi / lo words.
+template <int kSrc, int D>
+__device__ __forceinline__ void pair_planes(const float* vt, int K, int n, double step, int ia, float fa, int ib,
+                                            float fb, uint32_t (&hw)[D], uint32_t (&lw)[D]) {
+  if constexpr (kSrc == kLutSmem) {
+    const float* pa = vt + static_cast<int64_t>(ia) * K;
+    const float* pb = vt + static_cast<int64_t>(ib) * K;
+#pragma unroll
+    for (int k = 1; k <= D; ++k)
+      split_pack2(lerp_ref(pa[k], pa[k + K], fa), lerp_ref(pb[k], pb[k + K], fb), hw[k - 1], lw[k - 1]);
+  } else {
+    const float a0 = grid_node_f(ia, n, step), a1 = grid_node_f(ia + 1, n, step);
+    const float b0 = grid_node_f(ib, n, step), b1 = grid_node_f(ib + 1, n, step);
+    const float ta0 = 2.0f * a0, ta1 = 2.0f * a1, tb0 = 2.0f * b0, tb1 = 2.0f * b1;
+    float pa0 = 1.0f, ca0 = a0, pa1 = 1.0f, ca1 = a1, pb0 = 1.0f, cb0 = b0, pb1 = 1.0f, cb1 = b1;
+    split_pack2(lerp_ref(a0, a1, fa), lerp_ref(b0, b1, fb), hw[0], lw[0]);
+#pragma unroll
+    for (int k = 2; k <= D; ++k) {
+      float t;
+      t = fmaf(ta0, ca0, -pa0); pa0 = ca0; ca0 = t;
+      t = fmaf(ta1, ca1, -pa1); pa1 = ca1; ca1 = t;
+      t = fmaf(tb0, cb0, -pb0); pb0 = cb0; cb0 = t;
+      t = fmaf(tb1, cb1, -pb1); pb1 = cb1; cb1 = t;
+      split_pack2(lerp_ref(ca0, ca1, fa), lerp_ref(cb0, cb1, fb), hw[k - 1], lw[k - 1]);
+    }
+  }
+}
+
+// Split planes k = 1..D.  TRANSPOSED = false: hi/lo [k-1][r][ld], the pair is
+// two adjacent columns of one row.  TRANSPOSED = true: hi/lo [k-1][c][ld], the
+// pair is two adjacent rows of one column (a warp covers 64 rows of a column:
+// one 128-byte store per plane, no smem staging; the x reads of neighbouring
+// columns hit the same L1 sectors because a CTA walks a 64 x 32 tile).
+template <int kSrc, int D, bool TRANSPOSED>
+__global__ void __launch_bounds__(kThreads) expand_pairs_kernel(const float* __restrict__ x, int64_t rows, int cols,
+                                                                LutView lut, uint32_t* __restrict__ hi,
+                                                                uint32_t* __restrict__ lo, int64_t ld,
+                                                                int64_t plane) {
+  extern __shared__ float sm_tab[];
+  const int K = lut.K, N = lut.N;
+  const float* vt = kSrc == kLutSmem ? stage_table<true>(lut.values_pm, N * K, sm_tab) : nullptr;
+  const int64_t pl = plane >> 1;  // plane stride in words
+  int64_t n_items;
+  if (TRANSPOSED) {
+    n_items = ceil_div(rows, 64) * ceil_div(cols, 32) * kThreads;  // tiles of 64 rows x 32 cols
+  } else {
+    n_items = rows * ((cols + 1) >> 1);
+  }
+  for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n_items;
+       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r;
+    int c;
+    bool first, second;
+    float xa, xb;
+    int64_t word;
+    if (TRANSPOSED) {
+      const int64_t tile = it / kThreads;
+      const int tid = static_cast<int>(it % kThreads);
+      const int64_t r_tiles = ceil_div(rows, 64);
+      const int lane = tid & 31, w = tid >> 5;  // warp w: columns w, w+8, w+16, w+24
+      r = (tile % r_tiles) * 64 + 2 * lane;
+      const int c_base = static_cast<int>(tile / r_tiles) * 32;
+      // 8 warps x 4 columns each -> handled by 4 passes below
+      for (int pass = 0; pass < 4; ++pass) {
+        c = c_base + w + 8 * pass;
+        if (c >= cols) break;
+        first = r < rows;
+        second = r + 1 < rows;
+        if (r >= ld) break;
+        xa = first ? __ldg(x + r * cols + c) : 0.0f;
+        xb = second ? __ldg(x + (r + 1) * cols + c) : 0.0f;
+        int ia, ib;
+        float fa, fb;
+        cell_f32(xa, N, ia, fa);
+        cell_f32(xb, N, ib, fb);
+        uint32_t hw[D], lw[D];
+        pair_planes<kSrc, D>(vt, K, N, lut.step, ia, fa, ib, fb, hw, lw);
+        word = (static_cast<int64_t>(c) * ld + r) >> 1;
+        uint32_t* hp = hi + word;
+        uint32_t* lp = lo + word;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const uint32_t mh = first ? (second ? hw[k] : (hw[k] & 0xffffu)) : 0u;
+          const uint32_t ml = first ? (second ? lw[k] : (lw[k] & 0xffffu)) : 0u;
+          *hp = mh;
+          *lp = ml;
+          hp += pl;
+          lp += pl;
+        }
+      }
+    } else {
+      const int pairs = (cols + 1) >> 1;
+      r = it / pairs;
+      c = static_cast<int>(it - r * pairs) * 2;
+      second = c + 1 < cols;
+      if (second && ((cols & 1) == 0)) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(x + r * cols + c));
+        xa = v.x;
+        xb = v.y;
+      } else {
+        xa = __ldg(x + r * cols + c);
+        xb = second ? __ldg(x + r * cols + c + 1) : 0.0f;
+      }
+      int ia, ib;
+      float fa, fb;
+      cell_f32(xa, N, ia, fa);
+      cell_f32(xb, N, ib, fb);
+      uint32_t hw[D], lw[D];
+      pair_planes<kSrc, D>(vt, K, N, lut.step, ia, fa, ib, fb, hw, lw);
+      word = (r * ld + c) >> 1;
+      uint32_t* hp = hi + word;
+      uint32_t* lp = lo + word;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        *hp = second ? hw[k] : (hw[k] & 0xffffu);
+        *lp = second ? lw[k] : (lw[k] & 0xffffu);
+        hp += pl;
+        lp += pl;
+      }
+    }
+  }
+}
+
+// Generic (any degree) fallbacks: hi/lo planes [k-k0][r][ld], two columns
+// per thread.
 template <int kSrc>
 __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __restrict__ x, int64_t rows,
                                                                  int cols, LutView lut, int k0,
@@ -123,111 +248,53 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
     const int64_t r = it / pairs;
     const int c = static_cast<int>(it - r * pairs) * 2;
     const bool second = c + 1 < cols;
-    float2 xv;
-    if (second && ((cols & 1) == 0)) {
-      xv = *reinterpret_cast<const float2*>(x + r * cols + c);
-    } else {
-      xv.x = x[r * cols + c];
-      xv.y = second ? x[r * cols + c + 1] : 0.0f;
-    }
+    const float xa = x[r * cols + c];
+    const float xb = second ? x[r * cols + c + 1] : 0.0f;
     int ia, ib;
     float fa, fb;
-    cell_f32(xv.x, N, ia, fa);
-    cell_f32(xv.y, N, ib, fb);
+    cell_f32(xa, N, ia, fa);
+    cell_f32(xb, N, ib, fb);
     uint32_t* h = hi + ((r * ld + c) >> 1);
     uint32_t* l = lo + ((r * ld + c) >> 1);
-    auto put = [&](int k, float a, float b) {
+    Columns<kSrc>::run(vt, K, N, lut.step, ia, fa, k0, [&](int k, float v) {
+      float vb2 = 0.0f;
+      if (second) {
+        // second element: recompute through the same source (rare generic path)
+        Columns<kSrc>::run(vt, K, N, lut.step, ib, fb, k, [&](int kk, float w) {
+          if (kk == k) vb2 = w;
+        });
+      }
       uint32_t h2, l2;
-      split_pack2(a, second ? b : 0.0f, h2, l2);
+      split_pack2(v, vb2, h2, l2);
       h[(k - k0) * pl] = h2;
       l[(k - k0) * pl] = l2;
-    };
-    if constexpr (kSrc == kLutSmem) {
-      const float* pa = vt + static_cast<int64_t>(ia) * K;
-      const float* pb = vt + static_cast<int64_t>(ib) * K;
-      for (int k = k0; k < K; ++k) put(k, lerp_ref(pa[k], pa[k + K], fa), lerp_ref(pb[k], pb[k + K], fb));
-    } else {
-      // both elements' recurrences advance together (no per-k arrays)
-      const float a0 = grid_node_f(ia, N, lut.step), a1 = grid_node_f(ia + 1, N, lut.step);
-      const float b0 = grid_node_f(ib, N, lut.step), b1 = grid_node_f(ib + 1, N, lut.step);
-      float pa0 = 1.0f, ca0 = a0, pa1 = 1.0f, ca1 = a1;
-      float pb0 = 1.0f, cb0 = b0, pb1 = 1.0f, cb1 = b1;
-      if (k0 == 0) put(0, 1.0f, 1.0f);
-      if (K > 1 && k0 <= 1) put(1, lerp_ref(a0, a1, fa), lerp_ref(b0, b1, fb));
-      for (int k = 2; k < K; ++k) {
-        float t;
-        t = fmaf(2.0f * a0, ca0, -pa0); pa0 = ca0; ca0 = t;
-        t = fmaf(2.0f * a1, ca1, -pa1); pa1 = ca1; ca1 = t;
-        t = fmaf(2.0f * b0, cb0, -pb0); pb0 = cb0; cb0 = t;
-        t = fmaf(2.0f * b1, cb1, -pb1); pb1 = cb1; cb1 = t;
-        if (k >= k0) put(k, lerp_ref(ca0, ca1, fa), lerp_ref(cb0, cb1, fb));
-      }
-    }
+    });
   }
 }
 
-// Transposed hi/lo planes [k-k0][c][ldr]: 64(r) x 32(c) tiles, every k of an
-// element produced at once, staged in smem per plane, written as full rows.
-constexpr int kTR = 64, kTC = 32, kTP = kTR + 2;  // padded row (bf16) -> 33 words, conflict-free
+// Transposed generic fallback: hi/lo [k-k0][c][ldr], one element per thread.
 template <int kSrc>
 __global__ void __launch_bounds__(kThreads) expand_planes_t_kernel(const float* __restrict__ x, int64_t rows,
                                                                    int cols, LutView lut, int k0,
                                                                    __nv_bfloat16* __restrict__ hi,
                                                                    __nv_bfloat16* __restrict__ lo,
                                                                    int64_t ldr, int64_t plane) {
-  extern __shared__ __align__(16) float sm_dyn[];
+  extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
-  const int nk = K - k0;
-  const float* vt = nullptr;
-  __nv_bfloat16* t_hi;
-  if constexpr (kSrc == kLutSmem) {
-    vt = stage_table<true>(lut.values_pm, N * K, sm_dyn);
-    t_hi = reinterpret_cast<__nv_bfloat16*>(sm_dyn + ((N * K + 3) & ~3));
-  } else {
-    t_hi = reinterpret_cast<__nv_bfloat16*>(sm_dyn);
-  }
-  __nv_bfloat16* t_lo = t_hi + nk * kTC * kTP;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t r_tiles = ceil_div(rows, kTR);
-  const int64_t c_tiles = ceil_div(cols, kTC);
-  for (int64_t tile = blockIdx.x; tile < r_tiles * c_tiles; tile += gridDim.x) {
-    const int64_t r0 = (tile % r_tiles) * kTR;
-    const int c0 = static_cast<int>(tile / r_tiles) * kTC;
-    const int c = c0 + tx;
-    float xv[kTR / 8];
-#pragma unroll
-    for (int j = 0; j < kTR / 8; ++j) {  // all loads in flight before any math
-      const int64_t r = r0 + ty + 8 * j;
-      xv[j] = (r < rows && c < cols) ? __ldg(x + r * cols + c) : 0.0f;
-    }
-#pragma unroll 2
-    for (int j = 0; j < kTR / 8; ++j) {
-      const int rr = ty + 8 * j;
-      const int64_t r = r0 + rr;
-      const bool ok = (r < rows) && (c < cols);
-      int idx;
-      float fr;
-      cell_f32(xv[j], N, idx, fr);
-      Columns<kSrc>::run(vt, K, N, lut.step, idx, fr, k0, [&](int k, float v) {
-        __nv_bfloat16 h, l;
-        split_bf16(ok ? v : 0.0f, h, l);
-        t_hi[((k - k0) * kTC + tx) * kTP + rr] = h;
-        t_lo[((k - k0) * kTC + tx) * kTP + rr] = l;
-      });
-    }
-    __syncthreads();
-    // each warp writes whole rows (fixed k, c) of 64 r-values = 32 words
-    for (int row = ty; row < nk * kTC; row += kThreads / 32) {
-      const int kk = row / kTC, cc = row % kTC;
-      const int col = c0 + cc;
-      const int64_t r = r0 + 2 * tx;
-      if (col < cols && r < ldr) {
-        const int64_t off = kk * plane + static_cast<int64_t>(col) * ldr + r;
-        *reinterpret_cast<uint32_t*>(hi + off) = *reinterpret_cast<const uint32_t*>(&t_hi[row * kTP + 2 * tx]);
-        *reinterpret_cast<uint32_t*>(lo + off) = *reinterpret_cast<const uint32_t*>(&t_lo[row * kTP + 2 * tx]);
-      }
-    }
-    __syncthreads();
+  const float* vt = kSrc == kLutSmem ? stage_table<true>(lut.values_pm, N * K, sm_tab) : nullptr;
+  const int64_t n_items = rows * cols;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_items;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / rows, r = e - c * rows;  // consecutive threads: consecutive rows
+    int idx;
+    float fr;
+    cell_f32(x[r * cols + c], N, idx, fr);
+    Columns<kSrc>::run(vt, K, N, lut.step, idx, fr, k0, [&](int k, float v) {
+      __nv_bfloat16 h, l;
+      split_bf16(v, h, l);
+      hi[(k - k0) * plane + c * ldr + r] = h;
+      lo[(k - k0) * plane + c * ldr + r] = l;
+    });
   }
 }
 
@@ -282,12 +349,35 @@ int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut,
   return kOk;
 }
 
+
+template <int kSrc, bool T>
+int launch_pairs(int d, const float* x, int64_t rows, int cols, const LutView& v, uint32_t* h, uint32_t* l,
+                 int64_t ld, int64_t plane, size_t tab, int blocks, cudaStream_t s) {
+  const size_t smem = kSrc == kLutSmem ? tab : 0;
+#define CK_PAIRS_CASE(D)                                                                                      \
+  case D:                                                                                                     \
+    if (smem) {                                                                                               \
+      CK_CUDA(cudaFuncSetAttribute(expand_pairs_kernel<kSrc, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   static_cast<int>(smem)));                                                  \
+    }                                                                                                         \
+    expand_pairs_kernel<kSrc, D, T><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, h, l, ld, plane);        \
+    break;
+  switch (d) {
+    CK_PAIRS_CASE(1) CK_PAIRS_CASE(2) CK_PAIRS_CASE(3) CK_PAIRS_CASE(4) CK_PAIRS_CASE(5) CK_PAIRS_CASE(6)
+    CK_PAIRS_CASE(7) CK_PAIRS_CASE(8) CK_PAIRS_CASE(9) CK_PAIRS_CASE(10) CK_PAIRS_CASE(11) CK_PAIRS_CASE(12)
+    CK_PAIRS_CASE(13) CK_PAIRS_CASE(14) CK_PAIRS_CASE(15) CK_PAIRS_CASE(16)
+    default:
+      return kUnsupported;
+  }
+#undef CK_PAIRS_CASE
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
 int pick_source(size_t table_bytes) {
   const int o = lut_source_override();
   if (o == kLutSmem && table_bytes <= static_cast<size_t>(kSmemLutMax)) return kLutSmem;
-  if (o == kLutNodes) return kLutNodes;
-  // default: recompute columns (no gathers, no bank conflicts); measured
-  // faster than the smem table on B200 for every table size we support
+  // default: recompute columns (no gathers, no bank conflicts)
   return kLutNodes;
 }
 
@@ -295,14 +385,20 @@ int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* l
                          __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t plane, cudaStream_t s) {
   if (rows == 0 || cols == 0 || k0 >= lut->n_feat) return kOk;
   CK_CHECK(ld % 2 == 0 && plane % 2 == 0, "expand_planes: pitch must be even");
-  CK_CHECK(lut->n_feat <= kMaxK, "expand_planes: degree must be < 64");
   const LutView v = view(lut);
   const size_t tab = sizeof(float) * v.N * v.K;
+  const int src = pick_source(tab);
   const int blocks = grid_for(rows * ((cols + 1) / 2), 8);
   auto* h = reinterpret_cast<uint32_t*>(hi);
   auto* l = reinterpret_cast<uint32_t*>(lo);
   LaunchScope scope(kKExpand, s);
-  if (pick_source(tab) == kLutSmem) {
+  if (k0 == 1) {
+    const int d = v.K - 1;
+    const int rc = src == kLutSmem ? launch_pairs<kLutSmem, false>(d, x, rows, cols, v, h, l, ld, plane, tab, blocks, s)
+                                   : launch_pairs<kLutNodes, false>(d, x, rows, cols, v, h, l, ld, plane, tab, blocks, s);
+    if (rc != kUnsupported) return rc;
+  }
+  if (src == kLutSmem) {
     CK_CUDA(cudaFuncSetAttribute(expand_planes_kernel<kLutSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
     expand_planes_kernel<kLutSmem><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
@@ -319,23 +415,25 @@ int launch_expand_planes_t(const float* x, int64_t rows, int cols, const ck_lut*
   CK_CHECK(ldr % 2 == 0 && plane % 2 == 0, "expand_planes_t: pitch must be even");
   const LutView v = view(lut);
   const size_t tab = sizeof(float) * v.N * v.K;
-  const size_t tiles_bytes = 2 * sizeof(__nv_bfloat16) * static_cast<size_t>(v.K - k0) * kTC * kTP;
-  const int src = pick_source(tab + tiles_bytes);
-  const size_t smem = (src == kLutSmem ? ((tab + 15) & ~size_t(15)) : 0) + tiles_bytes;
-  CK_CHECK(smem <= 200 * 1024, "expand_planes_t: degree too large for the transpose tile");
-  const int64_t tiles = ceil_div(rows, kTR) * ceil_div(cols, kTC);
-  const int per_sm = smem > 100 * 1024 ? 1 : (smem > 64 * 1024 ? 2 : 3);
-  const int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
-  const int blocks = static_cast<int>(tiles < cap ? tiles : cap);
+  const int src = pick_source(tab);
   LaunchScope scope(kKExpandT, s);
+  if (k0 == 1) {
+    const int64_t items = ceil_div(rows, 64) * ceil_div(cols, 32) * kThreads;
+    const int blocks = grid_for(items, 8);
+    auto* h = reinterpret_cast<uint32_t*>(hi);
+    auto* l = reinterpret_cast<uint32_t*>(lo);
+    const int d = v.K - 1;
+    const int rc = src == kLutSmem ? launch_pairs<kLutSmem, true>(d, x, rows, cols, v, h, l, ldr, plane, tab, blocks, s)
+                                   : launch_pairs<kLutNodes, true>(d, x, rows, cols, v, h, l, ldr, plane, tab, blocks, s);
+    if (rc != kUnsupported) return rc;
+  }
+  const int blocks = grid_for(rows * cols, 8);
   if (src == kLutSmem) {
     CK_CUDA(cudaFuncSetAttribute(expand_planes_t_kernel<kLutSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    expand_planes_t_kernel<kLutSmem><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
+                                 static_cast<int>(tab)));
+    expand_planes_t_kernel<kLutSmem><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
   } else {
-    CK_CUDA(cudaFuncSetAttribute(expand_planes_t_kernel<kLutNodes>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    expand_planes_t_kernel<kLutNodes><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
+    expand_planes_t_kernel<kLutNodes><<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
   }
   CK_CUDA(cudaGetLastError());
   return kOk;
