@@ -95,6 +95,73 @@ __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t) {
   return c;
 }
 
+// Fused dX epilogue for one 128-row tile, degree D (compile time): TMEM
+// column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
+// Each thread owns one row; the two warps of a TMEM lane quarter take
+// alternate 4-column blocks.  Per element: exact cell (guarded fp32 tanh),
+// cell slopes from the two grid nodes (float64 recurrence), fold, Jacobian.
+template <int D>
+__device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
+  const int n_i = p.n_tile;
+  const float* xr = p.x + static_cast<long long>(row) * p.ldo;
+  float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
+  const double hN = 0.5 * static_cast<double>(p.lutN - 1);
+  const bool vec = ((p.ldo & 3) == 0);
+#pragma unroll 1
+  for (int cb = 4 * h; cb < n_i; cb += 8) {
+    uint32_t r[D][4];
+#pragma unroll
+    for (int k = 0; k < D; ++k) tmem_ld_32x32b_x4(tbase + k * n_i + cb, r[k]);
+    const int i0 = n0 + cb;
+    float xv[4];
+    if (vec && row_ok && i0 + 4 <= p.N) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + i0);
+      xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
+    }
+    int idx[4];
+    float t[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) idx[e] = cell_guarded(xv[e], p.lutN, p.guard, t[e]);
+    float acc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double x0 = __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx[e])));
+      const double x1 =
+          idx[e] + 1 >= p.lutN - 1 ? 1.0 : __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx[e] + 1)));
+      const double tx0 = 2.0 * x0, tx1 = 2.0 * x1;
+      double pa = 1.0, ca = x0, pb = 1.0, cb1 = x1;
+      float sl[D];
+      sl[0] = __double2float_rn((x1 - x0) * hN);
+#pragma unroll
+      for (int k = 1; k < D; ++k) {
+        const double na = fma(tx0, ca, -pa), nb = fma(tx1, cb1, -pb);
+        pa = ca;
+        ca = na;
+        pb = cb1;
+        cb1 = nb;
+        sl[k] = __double2float_rn((cb1 - ca) * hN);
+      }
+      acc[e] = 0.0f;
+      if (e == 0) tmem_ld_wait();
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc[e] = fmaf(sl[k], __uint_as_float(r[k][e]), acc[e]);
+      if (p.jacobian) acc[e] *= 1.0f - t[e] * t[e];
+    }
+    if (row_ok) {
+      if (vec && i0 + 4 <= p.N) {
+        *reinterpret_cast<float4*>(dxr + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (i0 + e < p.N) dxr[i0 + e] = acc[e];
+      }
+    }
+  }
+}
+
 template <int BN, int BK, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
@@ -213,46 +280,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = tc.m0 + q * 32 + lane;
       const bool row_ok = row < p.M;
       if constexpr (EPI == kEpiDx) {
-        // ------------- fused dX epilogue -------------
-        // TMEM column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i]
-        const int n_i = p.n_tile, d = p.b_boxes, K = p.lutK;
-        const float* xr = p.x + static_cast<long long>(row) * p.ldo;
-        float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
-        // columns interleaved between the two warps of this lane quarter;
-        // x of the next column is prefetched to hide its load latency
-        const double hN = 0.5 * static_cast<double>(p.lutN - 1);
-        float xnext = (row_ok && tc.n0 + h < p.N && h < n_i) ? xr[tc.n0 + h] : 0.0f;
-#pragma unroll 1
-        for (int col = h; col < n_i; col += 2) {
-          const int i = tc.n0 + col;
-          const bool ok = row_ok && i < p.N;
-          const float xv = xnext;
-          xnext = (row_ok && i + 2 < p.N && col + 2 < n_i) ? xr[i + 2] : 0.0f;
-          uint32_t r[kMaxDFused];
-#pragma unroll
-          for (int kk = 0; kk < kMaxDFused; ++kk)
-            if (kk < d) tmem_ld_32x32b_x1(tbase + kk * n_i + col, r[kk]);
-          float t;
-          const int idx = cell_guarded(ok ? xv : 0.0f, p.lutN, p.guard, t);
-          // slopes of cell idx from the two grid nodes (float64 recurrence)
-          const double x0 = __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx)));
-          const double x1 = idx + 1 >= p.lutN - 1 ? 1.0 : __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx + 1)));
-          const double tx0 = 2.0 * x0, tx1 = 2.0 * x1;
-          double pa = 1.0, ca = x0, pb = 1.0, cb = x1;
-          tmem_ld_wait();
-          float acc = __double2float_rn((x1 - x0) * hN) * __uint_as_float(r[0]);
-#pragma unroll
-          for (int kk = 1; kk < kMaxDFused; ++kk) {
-            if (kk < d) {
-              const double na = fma(tx0, ca, -pa), nb = fma(tx1, cb, -pb);
-              pa = ca;
-              ca = na;
-              pb = cb;
-              cb = nb;
-              acc = fmaf(__double2float_rn((cb - ca) * hN), __uint_as_float(r[kk]), acc);
-            }
-          }
-          if (ok) dxr[i] = p.jacobian ? acc * (1.0f - t * t) : acc;
+        // ------------- fused dX epilogue (degree-specialized) -------------
+        switch (p.b_boxes) {
+#define CK_DX_CASE(D) \
+  case D:             \
+    dx_epilogue<D>(p, tbase, tc.n0, row, row_ok, h); \
+    break;
+          CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
+          CK_DX_CASE(8) CK_DX_CASE(9) CK_DX_CASE(10) CK_DX_CASE(11) CK_DX_CASE(12) CK_DX_CASE(13)
+          CK_DX_CASE(14) CK_DX_CASE(15) CK_DX_CASE(16)
+#undef CK_DX_CASE
+          default:
+            break;
         }
       } else {
         // ------------- store epilogue -------------
