@@ -33,11 +33,13 @@ constexpr int kMaxDFused = 16;       // fused dX epilogue: degree <= 16
 
 // BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
 // or 32 (64-byte rows, SWIZZLE_64B, twice the stages for the same smem).
-template <int BN, int BK, int STAGES>
+// CG = CTA group: 1 (one SM per 128 x BN tile) or 2 (an SM pair per 256 x BN
+// tile; each CTA stages its 128 rows of A and half of the B rows).
+template <int BN, int BK, int STAGES, int CG = 1>
 struct Cfg {
   static constexpr int kRowBytes = BK * 2;
   static constexpr int kABytes = kBM * kRowBytes;   // one of hi / lo
-  static constexpr int kBBytes = BN * kRowBytes;
+  static constexpr int kBBytes = (BN / CG) * kRowBytes;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   static constexpr int kBarrierBytes = 256;
@@ -80,11 +82,11 @@ struct TileCoord {
   int n0, m0, z, split, c_begin, per_seg, iters;
 };
 
-__device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t) {
+__device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_tile_rows) {
   TileCoord c;
   const int nt = p.n_tiles, mt = p.m_tiles;
   c.n0 = (t % nt) * p.n_tile;
-  c.m0 = ((t / nt) % mt) * kBM;
+  c.m0 = ((t / nt) % mt) * m_tile_rows;
   const int zs = t / (nt * mt);
   c.z = zs / p.splits;
   c.split = zs % p.splits;
@@ -162,12 +164,12 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
   }
 }
 
-template <int BN, int BK, int STAGES, int EPI>
+template <int BN, int BK, int STAGES, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                        const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                        const KArgs p) {
-  using C = Cfg<BN, BK, STAGES>;
+  using C = Cfg<BN, BK, STAGES, CG>;
   constexpr int kRowBytes = C::kRowBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -179,6 +181,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.total_tiles;
+  // persistent schedule over work units (a CTA, or a CTA pair for CG = 2)
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;
+  const int row_off = static_cast<int>(rank) * kBM;  // this CTA's rows inside a pair tile
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a_hi);
@@ -191,13 +198,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], CG * kEpiWarps);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 2) {
+    if constexpr (CG == 2) {
+      tmem_alloc_pair(tmem_slot, C::kTmemCols);
+    } else {
+      tmem_alloc(tmem_slot, C::kTmemCols);
+    }
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    cluster_sync();  // barriers of both CTAs initialised before any remote signal
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -205,8 +222,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       uint32_t g = 0;  // global k-iteration counter (smem ring position)
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = decode_tile(p, t);
+      const int b_half = p.n_mma / CG;  // B rows this CTA stages
+      for (int t = unit; t < total; t += n_units) {
+        const TileCoord tc = decode_tile(p, t, kBM * CG);
         for (int it = 0; it < tc.iters; ++it, ++g) {
           const int stage = g % STAGES;
           const uint32_t phase = (g / STAGES) & 1;
@@ -216,28 +234,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int r0 = (tc.c_begin + it % tc.per_seg) * BK;
           const int aseg = p.a_seg0 + s + p.a_seg_z * tc.z;
           const int bseg = p.b_seg0 + s + p.b_seg_z * tc.z;
-          mbar_arrive_expect_tx(&full[stage], p.stage_tx);
-          tma_load_3d(st, &tm_a_hi, &full[stage], r0, tc.m0, aseg);
-          tma_load_3d(st + C::kABytes, &tm_a_lo, &full[stage], r0, tc.m0, aseg);
+          const int arow = tc.m0 + row_off;
+          int brow, bz;
           if (EPI == kEpiDx) {
-            // stacked operand: the whole d x n_i N tile is one box of n_mma rows
-            const int brow = (tc.n0 / p.n_tile) * p.n_mma;
-            tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, brow, 0);
-            tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, brow, 0);
+            // stacked operand: the d x n_i N tile is one box of n_mma rows (per pair)
+            brow = (tc.n0 / p.n_tile) * p.n_mma + static_cast<int>(rank) * b_half;
+            bz = 0;
           } else {
-            tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, tc.n0, bseg);
-            tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, tc.n0, bseg);
+            brow = tc.n0 + static_cast<int>(rank) * b_half;
+            bz = bseg;
+          }
+          if constexpr (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], p.stage_tx);  // bytes of both CTAs
+            tma_load_3d_pair(st, &tm_a_hi, &full[stage], r0, arow, aseg);
+            tma_load_3d_pair(st + C::kABytes, &tm_a_lo, &full[stage], r0, arow, aseg);
+            tma_load_3d_pair(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, brow, bz);
+            tma_load_3d_pair(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, brow, bz);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], p.stage_tx);
+            tma_load_3d(st, &tm_a_hi, &full[stage], r0, arow, aseg);
+            tma_load_3d(st + C::kABytes, &tm_a_lo, &full[stage], r0, arow, aseg);
+            tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, brow, bz);
+            tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, brow, bz);
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      const uint32_t idesc = umma_idesc_bf16_f32(kBM, p.n_mma);
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA of a pair) ----------------
+      const uint32_t idesc = umma_idesc_bf16_f32(kBM * CG, p.n_mma);
       uint32_t g = 0, lt = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-        const TileCoord tc = decode_tile(p, t);
+      for (int t = unit; t < total; t += n_units, ++lt) {
+        const TileCoord tc = decode_tile(p, t, kBM * CG);
         const uint32_t acc = lt & 1, use = lt >> 1;
         mbar_wait(&tempty[acc], (use & 1) ^ 1);  // epilogue has drained this buffer
         tc_fence_after();
@@ -258,26 +287,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dal = umma_desc_kmajor<kRowBytes>(a_lo + off);
             const uint64_t dbh = umma_desc_kmajor<kRowBytes>(b_hi + off);
             const uint64_t dbl = umma_desc_kmajor<kRowBytes>(b_lo + off);
-            umma_bf16(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
-            umma_bf16(d_tmem, dah, dbl, idesc, 1u);
-            umma_bf16(d_tmem, dal, dbh, idesc, 1u);
+            if constexpr (CG == 2) {
+              umma_bf16_pair(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+              umma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);
+              umma_bf16_pair(d_tmem, dal, dbh, idesc, 1u);
+            } else {
+              umma_bf16(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+              umma_bf16(d_tmem, dah, dbl, idesc, 1u);
+              umma_bf16(d_tmem, dal, dbh, idesc, 1u);
+            }
           }
-          umma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+          // frees the smem slot (in both CTAs) once these MMAs retire
+          if constexpr (CG == 2) {
+            umma_commit_pair(&empty[stage]);
+          } else {
+            umma_commit(&empty[stage]);
+          }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (CG == 2) {
+          umma_commit_pair(&tfull[acc]);
+        } else {
+          umma_commit(&tfull[acc]);
+        }
       }
     }
   } else if (warp >= 4) {
     const int q = warp & 3;          // TMEM lane quarter this warp may access
     const int h = (warp - 4) >> 2;   // which half of the tile's columns
     uint32_t lt = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-      const TileCoord tc = decode_tile(p, t);
+    for (int t = unit; t < total; t += n_units, ++lt) {
+      const TileCoord tc = decode_tile(p, t, kBM * CG);
       const uint32_t acc = lt & 1, use = lt >> 1;
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      const int row = tc.m0 + q * 32 + lane;
+      const int row = tc.m0 + row_off + q * 32 + lane;
       const bool row_ok = row < p.M;
       if constexpr (EPI == kEpiDx) {
         // ------------- fused dX epilogue (degree-specialized) -------------
@@ -343,13 +387,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) {
+          mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits on it
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
+      }
     }
   }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, C::kTmemCols);
+  __syncwarp();  // reconverge the role warps before the aligned barriers
+  if constexpr (CG == 2) {
+    tc_fence_before();
+    cluster_sync();  // no CTA leaves while its peer may still signal it
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc_pair(tmem_base, C::kTmemCols);
+    }
+  } else {
+    __syncthreads();
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc(tmem_base, C::kTmemCols);
+    }
   }
 }
 
@@ -393,26 +453,28 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   return kOk;
 }
 
-template <int BN, int BK, int STAGES, int EPI>
+template <int BN, int BK, int STAGES, int EPI, int CG>
 int launch(const GemmProblem& p, int splits, float* out, long long out_split_stride, int accumulate,
            cudaStream_t s) {
-  using C = Cfg<BN, BK, STAGES>;
+  using C = Cfg<BN, BK, STAGES, CG>;
   constexpr int kRowBytes = C::kRowBytes;
   const int r_chunks = static_cast<int>(ceil_div(p.R, BK));
   const int n_tile = EPI == kEpiDx ? p.dx->n_i : BN;
   const int b_boxes = EPI == kEpiDx ? p.S : 1;
   const int n_mma = n_tile * b_boxes;
+  CK_CHECK(n_mma % (8 * CG) == 0 && n_mma <= BN, "gemm: bad MMA N");
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
   CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
-  const int b_box = EPI == kEpiDx ? n_mma : n_tile;
+  const int b_box = n_mma / CG;  // each CTA of a pair stages half of the B rows
   CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK));
   CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK));
   KArgs k{};
   k.n_tile = n_tile;
   k.n_mma = n_mma;
   k.b_boxes = b_boxes;
-  k.stage_tx = static_cast<uint32_t>(2 * C::kABytes + 2 * n_mma * kRowBytes);
+  // bytes landing on the (leader's) full barrier per stage: A and B of all CTAs
+  k.stage_tx = static_cast<uint32_t>(CG * 2 * C::kABytes + 2 * n_mma * kRowBytes);
   if (EPI == kEpiDx) {
     k.x = p.dx->x;
     k.dx = p.dx->dx;
@@ -441,31 +503,51 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.bias0 = splits == 1 ? p.bias0 : nullptr;
   k.bias1 = splits == 1 ? p.bias1 : nullptr;
   k.accumulate = accumulate;
+  auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    CK_CUDA(cudaFuncSetAttribute(gemm_bf16x3_kernel<BN, BK, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 C::kSmemBytes));
+    CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     attr_set = true;
   }
   k.n_tiles = static_cast<int>(ceil_div(k.N, n_tile));
-  k.m_tiles = static_cast<int>(ceil_div(k.M, kBM));
+  k.m_tiles = static_cast<int>(ceil_div(k.M, kBM * CG));
   const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles * p.nz * splits;
   CK_CHECK(total < (1ll << 31), "gemm: too many tiles");
   k.total_tiles = static_cast<int>(total);
-  const int sms = num_sms();
-  dim3 grid(static_cast<unsigned>(total < sms ? total : sms));
+  const int units_max = num_sms() / CG;
+  const int units = static_cast<int>(total < units_max ? total : units_max);
   LaunchScope scope(p.kclass, s);
-  gemm_bf16x3_kernel<BN, BK, STAGES, EPI><<<grid, kThreads, C::kSmemBytes, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, k);
-  CK_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(units * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CG == 2 ? 1 : 0;
+  CK_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta_hi, ta_lo, tb_hi, tb_lo, k));
   return kOk;
 }
 
 int gemm_bk() {
   static int bk = [] {
     const char* e = getenv("CK_GEMM_BK");
-    return (e && std::string(e) == "64") ? 64 : 32;
+    return (e && std::string(e) == "32") ? 32 : 64;
   }();
   return bk;
+}
+
+// CTA group for the GEMMs: 2 (SM pairs, default) or 1 (CK_GEMM_CG=1).
+int gemm_cg() {
+  static int cg = [] {
+    const char* e = getenv("CK_GEMM_CG");
+    return (e && std::string(e) == "1") ? 1 : 2;
+  }();
+  return cg;
 }
 
 int choose_splits(int64_t M, int64_t N, int nz, int64_t R, int bn) {
@@ -502,8 +584,12 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   if (p.dx != nullptr) {
     // fused dX: B = d stacked boxes (S = d features), N = cols of dx
     CK_CHECK(p.nz == 1 && p.dx->n_i == dx_tile_inputs(p.S), "gemm: bad fused-dx configuration");
-    if (gemm_bk() == 64) return launch<256, 64, 2, kEpiDx>(p, 1, nullptr, 0, 0, s);
-    return launch<256, 32, 4, kEpiDx>(p, 1, nullptr, 0, 0, s);
+    const bool bk64 = gemm_bk() == 64;
+    if (gemm_cg() == 2)
+      return bk64 ? launch<256, 64, 3, kEpiDx, 2>(p, 1, nullptr, 0, 0, s)
+                  : launch<256, 32, 6, kEpiDx, 2>(p, 1, nullptr, 0, 0, s);
+    return bk64 ? launch<256, 64, 2, kEpiDx, 1>(p, 1, nullptr, 0, 0, s)
+                : launch<256, 32, 4, kEpiDx, 1>(p, 1, nullptr, 0, 0, s);
   }
   CK_CHECK(p.a.rows >= 1 && p.b.rows >= 1, "gemm: empty output");
   CK_CHECK(p.a.rows < (1ll << 31) && p.b.rows < (1ll << 31), "gemm: extent too large");
@@ -529,11 +615,14 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   int rc;
   const bool bk64 = gemm_bk() == 64;
   if (bn == 128) {
-    rc = bk64 ? launch<128, 64, 3, kEpiStore>(q, splits, out, split_stride, acc, s)
-              : launch<128, 32, 6, kEpiStore>(q, splits, out, split_stride, acc, s);
+    rc = bk64 ? launch<128, 64, 3, kEpiStore, 1>(q, splits, out, split_stride, acc, s)
+              : launch<128, 32, 6, kEpiStore, 1>(q, splits, out, split_stride, acc, s);
+  } else if (gemm_cg() == 2) {
+    rc = bk64 ? launch<256, 64, 3, kEpiStore, 2>(q, splits, out, split_stride, acc, s)
+              : launch<256, 32, 6, kEpiStore, 2>(q, splits, out, split_stride, acc, s);
   } else {
-    rc = bk64 ? launch<256, 64, 2, kEpiStore>(q, splits, out, split_stride, acc, s)
-              : launch<256, 32, 4, kEpiStore>(q, splits, out, split_stride, acc, s);
+    rc = bk64 ? launch<256, 64, 2, kEpiStore, 1>(q, splits, out, split_stride, acc, s)
+              : launch<256, 32, 4, kEpiStore, 1>(q, splits, out, split_stride, acc, s);
   }
   if (rc != kOk) return rc;
   if (splits > 1) {
