@@ -82,12 +82,23 @@ struct TileCoord {
   int n0, m0, z, split, c_begin, per_seg, iters;
 };
 
+// Grouped rasterisation: consecutive tiles walk kGroupM m-tiles for one n,
+// then the next n, so a wave of ~74-148 co-resident units covers a compact
+// (kGroupM x ~wave/kGroupM) block and both operands are reused from L2.
+constexpr int kGroupM = 8;
+
 __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_tile_rows) {
   TileCoord c;
   const int nt = p.n_tiles, mt = p.m_tiles;
-  c.n0 = (t % nt) * p.n_tile;
-  c.m0 = ((t / nt) % mt) * m_tile_rows;
-  const int zs = t / (nt * mt);
+  const int per_z = nt * mt;
+  const int zs = t / per_z;
+  const int r = t - zs * per_z;
+  const int group = r / (kGroupM * nt);
+  const int first_m = group * kGroupM;
+  const int gm = min(kGroupM, mt - first_m);  // last group may be short
+  const int rr = r - group * kGroupM * nt;
+  c.m0 = (first_m + rr % gm) * m_tile_rows;
+  c.n0 = (rr / gm) * p.n_tile;
   c.z = zs / p.splits;
   c.split = zs % p.splits;
   c.c_begin = static_cast<int>(static_cast<long long>(c.split) * p.r_chunks / p.splits);

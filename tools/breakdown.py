@@ -27,11 +27,17 @@ for _ in range(reps):
     forward_raw(x, prep, lut, None)
     backward_raw(x, dy, prep, lut, True)
 torch.cuda.synchronize()
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    clk = pynvml.nvmlDeviceGetClockInfo(pynvml.nvmlDeviceGetHandleByIndex(0), pynvml.NVML_CLOCK_SM)
+except Exception:
+    clk = -1
 _lib.timing_enable(False)
 kt = _lib.timing_collect()
 fl = 2 * b * i * o * d
 tot = sum(v[0] for v in kt.values()) / reps
-print(f"B={b} {i}->{o} d{d} N={n}: total kernel {tot:.3f} ms/step")
+print(f"B={b} {i}->{o} d{d} N={n}: total kernel {tot:.3f} ms/step  (sm clock at end {clk} MHz)")
 for k, (ms, cnt) in kt.items():
     if cnt:
         extra = f"  {fl / (ms / reps) / 1e9:7.1f} TF/s alg" if k.startswith("gemm") else ""
