@@ -74,8 +74,11 @@ __global__ void __launch_bounds__(kThreads) expand_f32_kernel(const float* __res
 // rounded to float32) by the recurrence T_{k+1} = 2x T_k - T_{k-1}
 // (basis.py:112-119) in float32 -- the same table entries to ~k^2 ulp, with
 // no memory traffic.  Both then interpolate v0 (1-f) + v1 f.
-__device__ __forceinline__ float grid_node_f(int i, int n, double step) {
-  return i >= n - 1 ? 1.0f : __double2float_rn(__dadd_rn(-1.0, __dmul_rn(step, static_cast<double>(i))));
+// Grid node -1 + i*step (lut.py:82-84) rounded to float32: (2i - (N-1)) / (N-1)
+// with an exact integer numerator and one correctly rounded fp32 division
+// (the FP64 pipe is too narrow on B200 to spend it here).
+__device__ __forceinline__ float grid_node_f(int i, int n, double /*step*/) {
+  return i >= n - 1 ? 1.0f : __fdiv_rn(static_cast<float>(2 * i - (n - 1)), static_cast<float>(n - 1));
 }
 
 template <int kSrc>

@@ -112,13 +112,16 @@ __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_ti
 // column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
 // Each thread owns one row; the two warps of a TMEM lane quarter take
 // alternate 4-column blocks.  Per element: exact cell (guarded fp32 tanh),
-// cell slopes from the two grid nodes (float64 recurrence), fold, Jacobian.
+// the cell's float32 slopes gathered from the position-major slope table
+// (exact reference values, L2-resident; all gathers of a block in flight
+// together), fold with the d accumulators, Jacobian.  (Recomputing the
+// slopes by a float64 recurrence was measured FP64-pipe bound on B200.)
 template <int D>
 __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
-  const int n_i = p.n_tile;
+  constexpr int KC = D < 8 ? D : 8;  // slope gathers in flight per element
+  const int n_i = p.n_tile, K = p.lutK;
   const float* xr = p.x + static_cast<long long>(row) * p.ldo;
   float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
-  const double hN = 0.5 * static_cast<double>(p.lutN - 1);
   const bool vec = ((p.ldo & 3) == 0);
 #pragma unroll 1
   for (int cb = 4 * h; cb < n_i; cb += 8) {
@@ -134,34 +137,30 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
 #pragma unroll
       for (int e = 0; e < 4; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
     }
-    int idx[4];
-    float t[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) idx[e] = cell_guarded(xv[e], p.lutN, p.guard, t[e]);
-    float acc[4];
+    const float* srow[4];
+    float t[4], acc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const double x0 = __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx[e])));
-      const double x1 =
-          idx[e] + 1 >= p.lutN - 1 ? 1.0 : __dadd_rn(-1.0, __dmul_rn(p.step, static_cast<double>(idx[e] + 1)));
-      const double tx0 = 2.0 * x0, tx1 = 2.0 * x1;
-      double pa = 1.0, ca = x0, pb = 1.0, cb1 = x1;
-      float sl[D];
-      sl[0] = __double2float_rn((x1 - x0) * hN);
-#pragma unroll
-      for (int k = 1; k < D; ++k) {
-        const double na = fma(tx0, ca, -pa), nb = fma(tx1, cb1, -pb);
-        pa = ca;
-        ca = na;
-        pb = cb1;
-        cb1 = nb;
-        sl[k] = __double2float_rn((cb1 - ca) * hN);
-      }
+      srow[e] = p.slopes_pm + static_cast<long long>(cell_guarded(xv[e], p.lutN, p.guard, t[e])) * K + 1;
       acc[e] = 0.0f;
-      if (e == 0) tmem_ld_wait();
+    }
 #pragma unroll
-      for (int k = 0; k < D; ++k) acc[e] = fmaf(sl[k], __uint_as_float(r[k][e]), acc[e]);
-      if (p.jacobian) acc[e] *= 1.0f - t[e] * t[e];
+    for (int kc = 0; kc < D; kc += KC) {
+      float sl[4][KC];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int k = 0; k < KC; ++k) sl[e][k] = (kc + k < D) ? __ldg(srow[e] + kc + k) : 0.0f;
+      if (kc == 0) tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int k = 0; k < KC; ++k)
+          if (kc + k < D) acc[e] = fmaf(sl[e][k], __uint_as_float(r[kc + k][e]), acc[e]);
+    }
+    if (p.jacobian) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] *= 1.0f - t[e] * t[e];
     }
     if (row_ok) {
       if (vec && i0 + 4 <= p.N) {
