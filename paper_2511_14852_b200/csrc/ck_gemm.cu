@@ -62,6 +62,7 @@ struct KArgs {
   const float* x;
   float* dx;
   const float* slopes_pm;
+  const float* dxrows;
   int lutK, lutN;
   double step;
   float guard;
@@ -111,63 +112,77 @@ __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_ti
 // Fused dX epilogue for one 128-row tile, degree D (compile time): TMEM
 // column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
 // Each thread owns one row; the two warps of a TMEM lane quarter take
-// alternate 4-column blocks.  Per element: exact cell (guarded fp32 tanh),
-// the cell's float32 slopes gathered from the position-major slope table
-// (exact reference values, L2-resident; all gathers of a block in flight
-// together), fold with the d accumulators, Jacobian.  (Recomputing the
-// slopes by a float64 recurrence was measured FP64-pipe bound on B200.)
+// alternate 4-column blocks.  Per element: float32 tanh gives a candidate
+// cell; its dx row {lower boundary, slopes} and the next row's boundary are
+// gathered together (L2-resident table), and the rare element outside
+// [b_i, b_{i+1}) re-gathers the neighbouring row -- the exact reference cell
+// without any float64 work; then fold with the d accumulators and apply the
+// Jacobian.
 template <int D>
 __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
-  constexpr int KC = D < 8 ? D : 8;  // slope gathers in flight per element
-  const int n_i = p.n_tile, K = p.lutK;
+  constexpr int K = D + 1;          // dx row stride (= LUT features)
+  constexpr int W = D <= 8 ? 4 : 2;  // columns per block (register budget)
+  const int n_i = p.n_tile, N = p.lutN;
   const float* xr = p.x + static_cast<long long>(row) * p.ldo;
   float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
   const bool vec = ((p.ldo & 3) == 0);
+  const float hN = 0.5f * static_cast<float>(N - 1);
 #pragma unroll 1
-  for (int cb = 4 * h; cb < n_i; cb += 8) {
-    uint32_t r[D][4];
+  for (int cb = W * h; cb < n_i; cb += 2 * W) {
+    uint32_t r[D][W];
 #pragma unroll
-    for (int k = 0; k < D; ++k) tmem_ld_32x32b_x4(tbase + k * n_i + cb, r[k]);
+    for (int k = 0; k < D; ++k) {
+      if constexpr (W == 4) {
+        tmem_ld_32x32b_x4(tbase + k * n_i + cb, r[k]);
+      } else {
+        tmem_ld_32x32b_x2(tbase + k * n_i + cb, r[k]);
+      }
+    }
     const int i0 = n0 + cb;
-    float xv[4];
-    if (vec && row_ok && i0 + 4 <= p.N) {
+    float xv[W];
+    if (W == 4 && vec && row_ok && i0 + 4 <= p.N) {
       const float4 v = *reinterpret_cast<const float4*>(xr + i0);
-      xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+      xv[0] = v.x; xv[1] = v.y; xv[W - 2] = v.z; xv[W - 1] = v.w;
     } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
+      for (int e = 0; e < W; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
     }
-    const float* srow[4];
-    float t[4], acc[4];
+    float t[W], acc[W];
+    float sl[W][D + 2];  // [0] = b_idx, [1..D] = slopes, [D+1] = b_{idx+1}
+    const float* rp[W];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      srow[e] = p.slopes_pm + static_cast<long long>(cell_guarded(xv[e], p.lutN, p.guard, t[e])) * K + 1;
-      acc[e] = 0.0f;
+    for (int e = 0; e < W; ++e) {
+      float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
+      t[e] = tt;
+      const int c = min(static_cast<int>(fmaf(tt, hN, hN)), N - 2);
+      rp[e] = p.dxrows + static_cast<long long>(c) * K;
+#pragma unroll
+      for (int j = 0; j <= K; ++j) sl[e][j] = __ldg(rp[e] + j);  // row c and the next boundary
     }
 #pragma unroll
-    for (int kc = 0; kc < D; kc += KC) {
-      float sl[4][KC];
+    for (int e = 0; e < W; ++e) {
+      // exact reference cell: b_idx <= x < b_{idx+1}; at most one step off
+      const bool lo = xv[e] < sl[e][0], hi = !(xv[e] < sl[e][K]);
+      if (lo || hi) {
+        rp[e] += lo ? -K : K;
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-#pragma unroll
-        for (int k = 0; k < KC; ++k) sl[e][k] = (kc + k < D) ? __ldg(srow[e] + kc + k) : 0.0f;
-      if (kc == 0) tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-#pragma unroll
-        for (int k = 0; k < KC; ++k)
-          if (kc + k < D) acc[e] = fmaf(sl[e][k], __uint_as_float(r[kc + k][e]), acc[e]);
+        for (int j = 0; j <= K; ++j) sl[e][j] = __ldg(rp[e] + j);
+      }
     }
-    if (p.jacobian) {
+    tmem_ld_wait();
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[e] *= 1.0f - t[e] * t[e];
+    for (int e = 0; e < W; ++e) {
+      float a = 0.0f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) a = fmaf(sl[e][k + 1], __uint_as_float(r[k][e]), a);
+      acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
     }
     if (row_ok) {
-      if (vec && i0 + 4 <= p.N) {
-        *reinterpret_cast<float4*>(dxr + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if (W == 4 && vec && i0 + 4 <= p.N) {
+        *reinterpret_cast<float4*>(dxr + i0) = make_float4(acc[0], acc[1], acc[W - 2], acc[W - 1]);
       } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
+        for (int e = 0; e < W; ++e)
           if (i0 + e < p.N) dxr[i0 + e] = acc[e];
       }
     }
@@ -489,6 +504,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
     k.x = p.dx->x;
     k.dx = p.dx->dx;
     k.slopes_pm = p.dx->lut.slopes_pm;
+    k.dxrows = p.dx->lut.dxrows;
     k.lutK = p.dx->lut.K;
     k.lutN = p.dx->lut.N;
     k.step = p.dx->lut.step;

@@ -17,6 +17,11 @@ struct ck_lut {
   double* values64 = nullptr;  // [K][N]   float64 build-precision table (validation)
   float* values_pm = nullptr;  // [N][K]   float32, position-major (gather rows idx, idx+1)
   float* slopes_pm = nullptr;  // [N-1][K] float32 cell slopes, position-major
+  // [N][K] input-gradient rows: [0] = smallest float32 x whose reference
+  // (float64) cell is >= i (-inf for i = 0, +inf sentinel row N-1), [1..d] =
+  // the cell's float32 slopes.  Lets kernels pick the exact reference cell
+  // with float32 compares only.
+  float* dxrows = nullptr;
 };
 
 namespace ck {
@@ -57,12 +62,13 @@ constexpr int64_t kChunkRows = 32768;
 struct LutView {
   const float* values_pm;
   const float* slopes_pm;
+  const float* dxrows;
   int K;
   int N;
   double step;
 };
 inline LutView view(const ck_lut* l) {
-  return LutView{l->values_pm, l->slopes_pm, l->n_feat, l->lut_size, l->step};
+  return LutView{l->values_pm, l->slopes_pm, l->dxrows, l->n_feat, l->lut_size, l->step};
 }
 
 // How the expansion kernels obtain the two table columns bracketing a cell:

@@ -1,5 +1,6 @@
 // Device-side LUT construction: T_k on a uniform grid, float64 build
 // precision, bit-identical to the reference's lut_build (lut.py:76-94).
+#include <cfloat>
 #include <cstring>
 #include <vector>
 
@@ -49,6 +50,41 @@ __global__ void lut_build_kernel(int degree, int n, double step, double* __restr
   }
 }
 
+// Reference cell of float32 input x (lut.py:97-106 after kernels.py:288).
+__device__ __forceinline__ int ref_cell(float x, int n) {
+  int idx;
+  double fr, t;
+  cell_f64(x, n, idx, fr, t);
+  return idx;
+}
+
+// dxrows[i] = {boundary_i, slope_1..slope_d of cell i}; boundary_i is the
+// smallest float32 x with ref_cell(x) >= i, found from atanh(node_i) by
+// stepping one float32 ulp at a time (ref_cell is monotone in x).
+__global__ void lut_dxrows_kernel(int K, int n, double step, const float* __restrict__ s_pm,
+                                  float* __restrict__ rows) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float b;
+  if (i == 0) {
+    b = -INFINITY;
+  } else if (i >= n - 1) {
+    b = INFINITY;  // cell n-1 is never selected (idx = min(., n-2))
+  } else {
+    const double node = __dadd_rn(-1.0, __dmul_rn(step, static_cast<double>(i)));
+    float x = __double2float_rn(atanh(node));
+    if (isinf(x)) x = copysignf(FLT_MAX, x);
+    int guard = 0;
+    while (ref_cell(x, n) >= i && guard++ < 4096) x = nextafterf(x, -INFINITY);
+    guard = 0;
+    while (ref_cell(x, n) < i && guard++ < 4096) x = nextafterf(x, INFINITY);
+    b = x;
+  }
+  rows[static_cast<int64_t>(i) * K] = b;
+  for (int k = 1; k < K; ++k)
+    rows[static_cast<int64_t>(i) * K + k] = i < n - 1 ? s_pm[static_cast<int64_t>(i) * K + k] : 0.0f;
+}
+
 __global__ void lut_pack_kernel(int K, int n, const double* __restrict__ v64, const float* __restrict__ s_fm,
                                 float* __restrict__ v_pm, float* __restrict__ s_pm) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -76,6 +112,7 @@ int lut_alloc(int degree, int lut_size, int device, ck_lut** out) {
   cudaError_t e = cudaMalloc(&l->values64, kn * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&l->values_pm, kn * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&l->slopes_pm, kn * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&l->dxrows, kn * sizeof(float));
   if (e != cudaSuccess) {
     ck_lut_destroy(l);
     set_error(std::string("ck_lut: cudaMalloc failed: ") + cudaGetErrorString(e));
@@ -103,6 +140,7 @@ extern "C" int ck_lut_build(int degree, int lut_size, int device, ck_lut** out) 
   ck::LaunchScope scope(ck::kKLut, nullptr);
   ck::lut_build_kernel<<<blocks, threads>>>(degree, lut_size, l->step, l->values64, l->values_pm,
                                             l->slopes_pm);
+  ck::lut_dxrows_kernel<<<blocks, threads>>>(l->n_feat, lut_size, l->step, l->slopes_pm, l->dxrows);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -129,6 +167,8 @@ extern "C" int ck_lut_create(int degree, int lut_size, const double* values_host
     const int threads = 256;
     ck::lut_pack_kernel<<<static_cast<int>(ck::ceil_div(lut_size, threads)), threads>>>(
         l->n_feat, lut_size, l->values64, s_fm, l->values_pm, l->slopes_pm);
+    ck::lut_dxrows_kernel<<<static_cast<int>(ck::ceil_div(lut_size, threads)), threads>>>(
+        l->n_feat, lut_size, l->step, l->slopes_pm, l->dxrows);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
@@ -147,6 +187,7 @@ extern "C" void ck_lut_destroy(ck_lut* l) {
   if (l->values64) cudaFree(l->values64);
   if (l->values_pm) cudaFree(l->values_pm);
   if (l->slopes_pm) cudaFree(l->slopes_pm);
+  if (l->dxrows) cudaFree(l->dxrows);
   delete l;
 }
 

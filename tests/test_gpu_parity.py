@@ -180,3 +180,28 @@ def test_hand_examples():
     assert torch.count_nonzero(dx) == 0
     for j in range(3):
         assert torch.equal(cg.data[0, :, j], dy.sum(0))
+
+
+@pytest.mark.parametrize("n", [1024, 32768])
+def test_dx_cells_exact_at_cell_edges(n):
+    # Inputs placed within a few float32 ulps of cell edges (where a float32
+    # tanh would pick the neighbouring cell): the fused dX must
+    # still use the reference's float64 cell, so no element may show the
+    # ~1e-3 relative error a wrong (piecewise-constant) slope produces.
+    b, i, o, d = 64, 256, 64, 8
+    rng = np.random.default_rng(n)
+    step = 2.0 / (n - 1)
+    cells = rng.integers(1, n - 1, size=(b, i))
+    x = np.arctanh(-1.0 + cells * step).astype(np.float32)
+    ulps = rng.integers(-3, 4, size=(b, i)).astype(np.float32)
+    x = (x + ulps * np.spacing(x)).astype(np.float32)
+    _, c_jod, dy = orc.bench_inputs(b, i, o, d, seed=3)
+    vals, slopes, _ = orc.build_table(d, n)
+    c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
+    _, want_dx, _ = orc.layer_backward(x, c_doj, dy, vals, slopes)
+    table = ck.lut_build(d, n, device=_dev())
+    c = ck.CoeffTensor(i, o, d, ck.Layout.DOJ, _t(c_doj.astype(np.float32)))
+    _, dx = ck.backward_fused(_t(x), c, _t(dy), table)
+    got = dx.cpu().numpy().astype(np.float64)
+    rel = np.abs(got - want_dx) / np.maximum(np.abs(want_dx), 1e-3 * np.abs(want_dx).max())
+    assert rel.max() <= 1e-4, (rel.max(), int((rel > 1e-4).sum()))
