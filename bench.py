@@ -43,8 +43,13 @@ WORKLOADS = {
                degree=8, global_batch=262144, lut_size=32768),
     "c1": dict(name="C1 ChebyKAN layer 4096->4096 d8, batch 16384 per GPU", d_in=4096, d_out=4096, degree=8,
                global_batch=16384, lut_size=32768, weak=True),
+    "c2": dict(name="C2 tabular ChebyKAN net [64->512->512->1] d5, MSE, batch 16384", layers=[64, 512, 512, 1],
+               degree=5, global_batch=16384, lut_size=32768),
+    "c3": dict(name="C3 speech ChebyKAN FFN [257->512->512->257] d15, MSE, 64x500 frames", layers=[257, 512, 512, 257],
+               degree=15, global_batch=32000, lut_size=32768),
 }
 METRIC = "ChebyKAN training (fwd+bwd+dC allreduce+Adam) samples/s"
+METRIC_NET = "ChebyKAN net training (fwd+bwd+allreduce+Adam) samples/s"
 CPU_SAMPLE_ROWS = 128      # oracle rows timed for cpu_baseline (~10-20 s of CPU work)
 REF_STEP_ROWS = 64         # oracle rows per --impl reference step
 
@@ -115,23 +120,35 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU legs (oracle = test infrastructure, used here only as the baseline)
 
+def layer_dims(wl):
+    if "layers" in wl:
+        return list(zip(wl["layers"][:-1], wl["layers"][1:]))
+    return [(wl["d_in"], wl["d_out"])]
+
+
 def cpu_reference_time(rows: int, wl: dict, reps: int = 1, warmup: int = 0):
+    """Oracle port of the reference's fused_forward/backward_fused over the
+    workload's layers (a net's layers run back to back, forward then backward)."""
     import numpy as np
     from threadpoolctl import threadpool_limits
 
     from oracle import chebykan_oracle as orc
 
     threads = os.cpu_count() or 1
-    x, c_jod, dy = orc.bench_inputs(rows, wl["d_in"], wl["d_out"], wl["degree"], seed=3)
     vals, slopes, _ = orc.build_table(wl["degree"], wl["lut_size"])
-    c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
+    layers = []
+    for li, (i, o) in enumerate(layer_dims(wl)):
+        x, c_jod, dy = orc.bench_inputs(rows, i, o, wl["degree"], seed=3 + li)
+        layers.append((x, orc.jod_to_doj(c_jod.astype(np.float64)), dy))
     times = []
     with threadpool_limits(1):  # BLAS single-threaded, tile tasks across all cores (best at large shapes)
-        for i in range(warmup + reps):
+        for it in range(warmup + reps):
             t0 = time.perf_counter()
-            orc.layer_forward(x, c_doj, vals, threads=threads)
-            orc.layer_backward(x, c_doj, dy, vals, slopes, threads=threads)
-            if i >= warmup:
+            for x, c_doj, _ in layers:
+                orc.layer_forward(x, c_doj, vals, threads=threads)
+            for x, c_doj, dy in reversed(layers):
+                orc.layer_backward(x, c_doj, dy, vals, slopes, threads=threads)
+            if it >= warmup:
                 times.append(time.perf_counter() - t0)
     return times, threads
 
@@ -143,15 +160,15 @@ def run_reference_arm(args, wl):
     times, threads = cpu_reference_time(REF_STEP_ROWS, wl, reps=args.steps, warmup=args.warmup)
     t = statistics.mean(times)
     value = REF_STEP_ROWS / t
-    sample = (f"{REF_STEP_ROWS} rows of {wl['d_in']}->{wl['d_out']} d{wl['degree']} N={wl['lut_size']} fwd+bwd per "
+    sample = (f"{REF_STEP_ROWS} rows of {layer_dims(wl)} d{wl['degree']} N={wl['lut_size']} fwd+bwd per "
               f"step; oracle port of polykan fused_forward/backward_fused (LUT mode, f64 NumPy), "
               f"{threads} tile-task threads, BLAS 1 thread")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["name"], "global_batch": wl["global_batch"], "d_in": wl["d_in"],
-                   "d_out": wl["d_out"], "degree": wl["degree"], "lut_size": wl["lut_size"],
+        "config": {"workload": wl["name"], "global_batch": wl["global_batch"], "layers": layer_dims(wl),
+                   "degree": wl["degree"], "lut_size": wl["lut_size"],
                    "parallelism": "host threads", "sample_rows_per_step": REF_STEP_ROWS},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -180,7 +197,10 @@ def run_ours(args, wl):
     if _lib.lib().ck_device_supported(local) != 1:
         raise SystemExit(f"device {torch.cuda.get_device_name(local)} is not sm_100 (B200)")
 
-    I, O, d = wl["d_in"], wl["d_out"], wl["degree"]
+    d = wl["degree"]
+    dims = layer_dims(wl)
+    is_net = "layers" in wl
+    I, O = dims[0][0], dims[-1][1]
     if wl.get("weak"):
         gb = wl["global_batch"] * world
         a, b = rank * wl["global_batch"], (rank + 1) * wl["global_batch"]
@@ -190,19 +210,35 @@ def run_ours(args, wl):
     rows = b - a
 
     torch.manual_seed(1234)  # identical synthetic weights on every rank
-    layer = ck.ChebyKANLayer(I, O, d, lut_size=wl["lut_size"]).to(dev)
-    opt = torch.optim.Adam(layer.parameters(), lr=1e-4, fused=True)
-    reducer = ck.GradientAllreducer(ck.chebykan_parameters(layer)) if world > 1 else None
+    layers = [ck.ChebyKANLayer(i, o, d, lut_size=wl["lut_size"]) for i, o in dims]
+    model = (torch.nn.Sequential(*layers) if is_net else layers[0]).to(dev)
+    opt = torch.optim.Adam(model.parameters(), lr=1e-4, fused=True)
+    reducer = ck.GradientAllreducer(ck.chebykan_parameters(model)) if world > 1 else None
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
-    x = (torch.rand(rows, I, device=dev, generator=gen) * 3.0 - 1.5).requires_grad_(True)
-    dy = torch.randn(rows, O, device=dev, generator=gen)
+    if is_net:
+        # tabular / spectrogram-like features ~ N(0,1); regression target
+        x = torch.randn(rows, I, device=dev, generator=gen)
+        if O == 1:
+            dy = torch.sin(x).sum(dim=1, keepdim=True) / 8 + 0.01 * torch.randn(rows, 1, device=dev, generator=gen)
+        else:
+            dy = torch.randn(rows, O, device=dev, generator=gen)
+    else:
+        x = (torch.rand(rows, I, device=dev, generator=gen) * 3.0 - 1.5).requires_grad_(True)
+        dy = torch.randn(rows, O, device=dev, generator=gen)
 
     def step(xin, dyin, want_loss=False):
-        xin.grad = None
-        y = layer(xin)
-        loss = (y.detach() * dyin).sum() if want_loss else None  # L = sum(y * dy) -> dL/dy = dy
-        y.backward(dyin)
+        """One training step; dyin is dL/dy (layer workloads) or the regression target (nets)."""
+        if xin.requires_grad:
+            xin.grad = None
+        y = model(xin)
+        if is_net:
+            loss = torch.nn.functional.mse_loss(y, dyin)
+            loss.backward()
+            loss = loss.detach() if want_loss else None
+        else:
+            loss = (y.detach() * dyin).sum() if want_loss else None  # L = sum(y * dy) -> dL/dy = dy
+            y.backward(dyin)
         if reducer is not None:
             reducer()
         opt.step()
@@ -252,12 +288,12 @@ def run_ours(args, wl):
     with torch.no_grad():
         xs = x.detach()
         for _ in range(2):
-            layer(xs)
+            model(xs)
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(args.steps):
-            layer(xs)
+            model(xs)
         f1.record()
         barrier()
         fwd_ms = max_over_ranks(f0.elapsed_time(f1)) / args.steps
@@ -296,10 +332,15 @@ def run_ours(args, wl):
                 dyb[k][: hi - lo].copy_(dy_h[lo:hi], non_blocking=True)
                 ready[k].record(copy_stream)
             cur.wait_event(ready[k])
-            xin = xb[k][: hi - lo].detach().requires_grad_(True)
-            y = layer(xin)
-            loss += (y.detach() * dyb[k][: hi - lo]).sum()
-            y.backward(dyb[k][: hi - lo])
+            xin = xb[k][: hi - lo].detach().requires_grad_(not is_net)
+            y = model(xin)
+            if is_net:
+                part = torch.nn.functional.mse_loss(y, dyb[k][: hi - lo], reduction="sum") / rows
+                part.backward()
+                loss += part.detach()
+            else:
+                loss += (y.detach() * dyb[k][: hi - lo]).sum()
+                y.backward(dyb[k][: hi - lo])
             free[k].record(cur)
         if reducer is not None:
             reducer()
@@ -327,8 +368,15 @@ def run_ours(args, wl):
         return
 
     peaks = load_peaks()
-    flops = ck.count_flops(rows, I, O, d)
-    gemm_alg = 3 * 2 * rows * I * O * d * args.steps  # fwd + dX + dC GEMMs executed per step (k=0 folded)
+    # algorithmic flops; executed GEMM flops use d planes (k=0 folded)
+    # and skip dX of a net's first layer (its input needs no gradient)
+    train_flops, step_gemm = 0, 0
+    for li, (i, o) in enumerate(dims):
+        f = ck.count_flops(rows, i, o, d)
+        need_dx = not (is_net and li == 0)
+        train_flops += f["fwd"] + 2 * rows * i * o * (d + 1) + (2 * rows * i * o * d if need_dx else 0)
+        step_gemm += 2 * rows * i * o * d * (3 if need_dx else 2)
+    gemm_alg = step_gemm * args.steps
     gemm_ms = sum(kt[c][0] for c in ("gemm_fwd", "gemm_dx", "gemm_dc"))
     gemm_tf = gemm_alg / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     peak_eff = peaks["bf16_sus"] / 3.0
@@ -341,13 +389,14 @@ def run_ours(args, wl):
         except (ValueError, OSError):
             traffic = None
     line = {
-        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC_NET if is_net else METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if wl.get("weak") else "strong", "vs_baseline": None,
         "dtype": "fp32 I/O, bf16x3 split tensor-core products, fp32 accumulate", "data": "synthetic",
-        "config": {"workload": wl["name"], "global_batch": gb, "rows_per_gpu": rows, "d_in": I, "d_out": O,
+        "config": {"workload": wl["name"], "global_batch": gb, "rows_per_gpu": rows, "layers": dims,
                    "degree": d, "lut_size": wl["lut_size"], "parallelism": f"dp{world}",
-                   "l2": "inputs larger than L2 (x shard >> 126 MB), no flush"},
+                   "l2": ("inputs larger than L2 (x shard >> 126 MB), no flush" if rows * I * 4 > 126e6 else
+                          "working set below L2 size; steps run back to back (no flush)")},
         "fwd": {"value": fwd_value, "unit": "samples/s", "ms_per_step": fwd_ms},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": 4 * rows * (I + O),
                 "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms, "wall_ms_per_step": e2e_wall * 1e3,
@@ -360,12 +409,12 @@ def run_ours(args, wl):
             "traffic": traffic,
             "peak_basis": f"{peaks['source']} bf16 sustained {peaks['bf16_sus']} TF/s / 3 (3 bf16 MMAs per "
                           "algorithmic fp32 MMA)",
-            "algorithmic_flops_per_step": 3 * 2 * rows * I * O * d,
+            "algorithmic_flops_per_step": step_gemm,
             "gemm_share_of_kernel_time": gemm_ms / total_kernel_ms if total_kernel_ms else None,
         },
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
         "kernel_launches_per_step": {k: v[1] / args.steps for k, v in kt.items() if v[1]},
-        "train_alg_tflops_per_gpu": flops["train"] / (ms_step / 1e3) / 1e12,
+        "train_alg_tflops_per_gpu": train_flops / (ms_step / 1e3) / 1e12,
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:

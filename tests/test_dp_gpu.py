@@ -1,0 +1,75 @@
+"""Data-parallel numerics on the GPU: two ranks (gloo, both on cuda:0 -- this
+sandbox has one device and NCCL refuses two ranks per GPU) each run the fused
+layer on their contiguous shard and allreduce [dC, db]; the reduced gradients
+must equal the single-process full-batch gradients."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _grads(layer, x, dy):
+    layer.zero_grad(set_to_none=True)
+    xx = x.clone().requires_grad_(True)
+    layer(xx).backward(dy)
+    return layer.coeff_doj.grad.clone(), layer.bias.grad.clone(), xx.grad.clone()
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2511_14852_b200 as ck
+
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(0)
+    layer = ck.ChebyKANLayer(96, 80, 5, lut_size=4096, seed=3).to(dev)
+    g = torch.Generator().manual_seed(7)
+    B = 1000
+    x = (torch.rand(B, 96, generator=g) * 3 - 1.5).to(dev)
+    dy = torch.randn(B, 80, generator=g).to(dev)
+    lo, hi = ck.shard_bounds(B, rank, world)
+    dc, db, dx = _grads(layer, x[lo:hi], dy[lo:hi])
+    red = ck.GradientAllreducer(ck.chebykan_parameters(layer))
+    red()
+    q.put((rank, layer.coeff_doj.grad.cpu().numpy(), layer.bias.grad.cpu().numpy(), dx.cpu().numpy(), lo, hi))
+    dist.destroy_process_group()
+
+
+def test_dp_two_ranks_match_full_batch():
+    import paper_2511_14852_b200 as ck
+    from oracle import chebykan_oracle as orc
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dev = torch.device("cuda", 0)
+    layer = ck.ChebyKANLayer(96, 80, 5, lut_size=4096, seed=3).to(dev)
+    g = torch.Generator().manual_seed(7)
+    x = (torch.rand(1000, 96, generator=g) * 3 - 1.5).to(dev)
+    dy = torch.randn(1000, 80, generator=g).to(dev)
+    dc, db, dx = _grads(layer, x, dy)
+    for r in (0, 1):
+        rdc, rdb, rdx, lo, hi = res[r]
+        assert orc.normwise_err(rdc, dc.cpu().numpy()) <= 1e-5
+        assert orc.normwise_err(rdb, db.cpu().numpy()) <= 1e-6
+        assert orc.normwise_err(rdx, dx[lo:hi].cpu().numpy()) <= 1e-6
+    assert np.array_equal(res[0][0], res[1][0])  # identical reduced gradients on both ranks
