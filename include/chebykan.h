@@ -88,10 +88,15 @@ CK_API int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int n_f
 
 /* --- Forward: replaces fused_forward (kernels.py:351-371) ------------------
  * y[b][o] = sum_i sum_k T_k(tanh x[b][i]) C[k][o][i] + bias[o]
- * x [B][I], y [B][O]; bias nullable.  Workspace: ck_forward_workspace_bytes. */
+ * x [B][I], y [B][O]; bias nullable.  Workspace: ck_forward_workspace_bytes.
+ * basis_cache (nullable, ck_basis_cache_bytes): when given, the forward keeps
+ * the expanded basis planes there and ck_backward reuses them (the backward of
+ * the same x then skips the expansion). */
 CK_API size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
+CK_API size_t ck_basis_cache_bytes(int64_t batch, int d_in, int n_feat);
 CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
-               const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream);
+               const float* bias, float* y, void* workspace, size_t workspace_bytes, void* basis_cache,
+               size_t basis_cache_bytes, void* stream);
 
 /* --- Backward: replaces backward_fused (kernels.py:374-447) plus the bias
  * gradient of Layer.backward (model.py:147) --------------------------------
@@ -104,7 +109,8 @@ CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const 
 CK_API size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
                 const void* prep, int include_tanh_jacobian, float* dx, float* dc_doj, float* db,
-                void* workspace, size_t workspace_bytes, void* stream);
+                void* workspace, size_t workspace_bytes, const void* basis_cache, size_t basis_cache_bytes,
+                void* stream);
 
 /* --- Deterministic merge: replaces combine's ordered fold (kernels.py:321-348)
  * and the ordered x-grad merge (kernels.py:438-442) as a standalone op.

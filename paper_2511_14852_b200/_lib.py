@@ -39,10 +39,12 @@ SIGNATURES = {
     "ck_coeff_prep_bytes": (_c_size, [_c_int, _c_int, _c_int]),
     "ck_coeff_prepare": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_p, _c_size, _c_p]),
     "ck_forward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
-    "ck_forward": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "ck_basis_cache_bytes": (_c_size, [_c_i64, _c_int, _c_int]),
+    "ck_forward": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p, _c_size,
+                            _c_p]),
     "ck_backward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
     "ck_backward": (_c_int, [_c_p, _c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_p, _c_p, _c_p,
-                             _c_p, _c_size, _c_p]),
+                             _c_p, _c_size, _c_p, _c_size, _c_p]),
     "ck_merge": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_int, _c_p]),
     "ck_launch_count": (ctypes.c_longlong, []),
     "ck_timing_enable": (_c_int, [_c_int]),

@@ -44,20 +44,38 @@ struct PrepLayout {
   }
 };
 
-struct FwdLayout {
-  int64_t chunk, ldI;
-  size_t hi, lo, split, total;
-  int64_t split_elems;
-  FwdLayout(int64_t B, int I, int O, int K) {
+// Basis planes of one chunk: Φ_k hi/lo for k = 1..d, [d][chunk][ldI] bf16.
+// The forward writes them; the backward's dC GEMM reads them as its MN-major
+// B operand.  With a caller-provided cache the planes of every chunk persist
+// from forward to backward (no re-expansion); else they live in workspace.
+struct BasisLayout {
+  int64_t chunk, n_chunks, ldI, plane;
+  size_t half, per_chunk, total;
+  BasisLayout(int64_t B, int I, int K) {
     chunk = B < kChunkRows ? B : kChunkRows;
     if (chunk < 1) chunk = 1;
+    n_chunks = ceil_div(B > 0 ? B : 1, chunk);
     ldI = round_up(I, 8);
+    plane = chunk * ldI;
     const int d = K - 1;
-    const size_t planes = align_up(sizeof(__nv_bfloat16) * (d > 0 ? d : 0) * chunk * ldI);
+    half = align_up(sizeof(__nv_bfloat16) * (d > 0 ? d : 0) * plane);
+    per_chunk = 2 * half;
+    total = per_chunk * n_chunks + kAlign;
+  }
+};
+
+struct FwdLayout {
+  int64_t chunk, ldI;
+  size_t planes, split, total;
+  int64_t split_elems;
+  FwdLayout(int64_t B, int I, int O, int K) {
+    const BasisLayout L(B, I, K);
+    chunk = L.chunk;
+    ldI = L.ldI;
+    const int d = K - 1;
+    planes = 0;
     split_elems = d > 0 ? gemm_split_ws_elems(chunk, O, 1, I) : 0;
-    hi = 0;
-    lo = planes;
-    split = lo + planes;
+    split = planes + L.per_chunk;
     total = split + align_up(sizeof(float) * split_elems) + kAlign;
   }
 };
@@ -65,34 +83,28 @@ struct FwdLayout {
 constexpr int kDbSlots = 32;
 
 struct BwdLayout {
-  int64_t chunk, n_chunks, ldO, ldB;
+  int64_t chunk, n_chunks, ldO;
   bool fused_dx;
-  size_t dy_hi, dy_lo, dyt_hi, dyt_lo, g, pt_hi, pt_lo, db_part, db_tmp, split, total;
+  size_t dy_hi, dy_lo, g, planes, db_part, db_tmp, split, total;
   int64_t split_elems;
   BwdLayout(int64_t B, int I, int O, int K) {
-    chunk = B < kChunkRows ? B : kChunkRows;
-    if (chunk < 1) chunk = 1;
-    n_chunks = ceil_div(B > 0 ? B : 1, chunk);
+    const BasisLayout L(B, I, K);
+    chunk = L.chunk;
+    n_chunks = L.n_chunks;
     ldO = round_up(O, 8);
-    ldB = round_up(chunk, 8);
     const int64_t d = K - 1;
     const size_t dy = align_up(sizeof(__nv_bfloat16) * chunk * ldO);
-    const size_t dyt = align_up(sizeof(__nv_bfloat16) * O * ldB);
     fused_dx = dx_tile_inputs(static_cast<int>(d)) > 0;
     const size_t gb = fused_dx ? 0 : align_up(sizeof(float) * d * chunk * I);
-    const size_t pt = align_up(sizeof(__nv_bfloat16) * d * I * ldB);
     const size_t dbp = align_up(sizeof(double) * n_chunks * kDbSlots * O);
     int64_t s1 = d > 0 ? gemm_split_ws_elems(chunk, I, static_cast<int>(d), O) : 0;
     int64_t s2 = d > 0 ? gemm_split_ws_elems(O, I, static_cast<int>(d), chunk) : 0;
     split_elems = s1 > s2 ? s1 : s2;
     dy_hi = 0;
     dy_lo = dy_hi + dy;
-    dyt_hi = dy_lo + dy;
-    dyt_lo = dyt_hi + dyt;
-    g = dyt_lo + dyt;
-    pt_hi = g + gb;
-    pt_lo = pt_hi + pt;
-    db_part = pt_lo + pt;
+    g = dy_lo + dy;
+    planes = g + gb;  // basis planes when no cache is given
+    db_part = planes + L.per_chunk;
     db_tmp = db_part + dbp;
     split = db_tmp + align_up(sizeof(float) * O);
     total = split + align_up(sizeof(float) * split_elems) + kAlign;
@@ -281,14 +293,25 @@ extern "C" size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out,
   return ck::FwdLayout(batch, d_in, d_out, n_feat).total;
 }
 
+extern "C" size_t ck_basis_cache_bytes(int64_t batch, int d_in, int n_feat) {
+  if (d_in < 1 || n_feat < 1 || batch < 0) return 0;
+  return ck::BasisLayout(batch, d_in, n_feat).total;
+}
+
 extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
-                          const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream) {
+                          const float* bias, float* y, void* workspace, size_t workspace_bytes, void* basis_cache,
+                          size_t basis_cache_bytes, void* stream) {
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
   CK_CHECK(x != nullptr && y != nullptr && prep != nullptr, "ck_forward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
   const ck::FwdLayout W(batch, d_in, d_out, K);
+  const ck::BasisLayout L(batch, d_in, K);
   if (workspace_bytes < W.total) {
     ck::set_error("forward workspace too small: need " + std::to_string(W.total) + " bytes");
+    return ck::kWorkspace;
+  }
+  if (basis_cache != nullptr && basis_cache_bytes < L.total) {
+    ck::set_error("basis cache too small: need " + std::to_string(L.total) + " bytes");
     return ck::kWorkspace;
   }
   if (batch == 0) return kOk;
@@ -296,19 +319,21 @@ extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, co
   const ck::PrepLayout P(d_in, d_out, K);
   void* pv = const_cast<void*>(prep);
   const float* c0sum = ck::at<float>(pv, P.c0sum);
-  auto* phi_hi = ck::at<__nv_bfloat16>(workspace, W.hi);
-  auto* phi_lo = ck::at<__nv_bfloat16>(workspace, W.lo);
-  for (int64_t r0 = 0; r0 < batch; r0 += W.chunk) {
+  int64_t ci = 0;
+  for (int64_t r0 = 0; r0 < batch; r0 += W.chunk, ++ci) {
     const int64_t rows = batch - r0 < W.chunk ? batch - r0 : W.chunk;
     float* yc = y + r0 * d_out;
     if (d == 0) {
       CK_TRY(ck::launch_fill_rows(yc, rows, d_out, bias, c0sum, s));
       continue;
     }
-    const int64_t plane = W.chunk * W.ldI;
-    CK_TRY(ck::launch_expand_planes(x + r0 * d_in, rows, d_in, lut, 1, phi_hi, phi_lo, W.ldI, plane, s));
+    // planes: this chunk's slot of the cache, or the workspace
+    auto* phi_hi = basis_cache ? ck::at<__nv_bfloat16>(basis_cache, ci * L.per_chunk)
+                               : ck::at<__nv_bfloat16>(workspace, W.planes);
+    auto* phi_lo = phi_hi + L.half / sizeof(__nv_bfloat16);
+    CK_TRY(ck::launch_expand_planes(x + r0 * d_in, rows, d_in, lut, 1, phi_hi, phi_lo, L.ldI, L.plane, s));
     ck::GemmProblem g{};
-    g.a = {phi_hi, phi_lo, rows, W.ldI, plane, d};
+    g.a = {phi_hi, phi_lo, rows, L.ldI, L.plane, d};
     g.b = {ck::at<__nv_bfloat16>(pv, P.doj_hi), ck::at<__nv_bfloat16>(pv, P.doj_lo), d_out, P.ldI,
            static_cast<int64_t>(d_out) * P.ldI, K};
     g.R = d_in;
@@ -335,13 +360,19 @@ extern "C" size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out
 
 extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
                            const void* prep, int include_tanh_jacobian, float* dx, float* dc_doj, float* db,
-                           void* workspace, size_t workspace_bytes, void* stream) {
+                           void* workspace, size_t workspace_bytes, const void* basis_cache,
+                           size_t basis_cache_bytes, void* stream) {
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
   CK_CHECK(x != nullptr && dy != nullptr && prep != nullptr, "ck_backward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
   const ck::BwdLayout W(batch, d_in, d_out, K);
+  const ck::BasisLayout L(batch, d_in, K);
   if (workspace_bytes < W.total) {
     ck::set_error("backward workspace too small: need " + std::to_string(W.total) + " bytes");
+    return ck::kWorkspace;
+  }
+  if (basis_cache != nullptr && basis_cache_bytes < L.total) {
+    ck::set_error("basis cache too small: need " + std::to_string(L.total) + " bytes");
     return ck::kWorkspace;
   }
   auto s = static_cast<cudaStream_t>(stream);
@@ -355,11 +386,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
   void* pv = const_cast<void*>(prep);
   auto* dy_hi = ck::at<__nv_bfloat16>(workspace, W.dy_hi);
   auto* dy_lo = ck::at<__nv_bfloat16>(workspace, W.dy_lo);
-  auto* dyt_hi = ck::at<__nv_bfloat16>(workspace, W.dyt_hi);
-  auto* dyt_lo = ck::at<__nv_bfloat16>(workspace, W.dyt_lo);
   float* g = ck::at<float>(workspace, W.g);
-  auto* pt_hi = ck::at<__nv_bfloat16>(workspace, W.pt_hi);
-  auto* pt_lo = ck::at<__nv_bfloat16>(workspace, W.pt_lo);
   double* db_part = ck::at<double>(workspace, W.db_part);
   float* split_ws = ck::at<float>(workspace, W.split);
   // db is needed for dC_0 as well; keep a private copy when the caller skips it
@@ -375,9 +402,10 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       if (dx) CK_CUDA(cudaMemsetAsync(dx + r0 * I, 0, sizeof(float) * rows * I, s));
       continue;
     }
+    // dy hi/lo [rows][ldO]: K-major A of the dX GEMM and MN-major A of the dC GEMM
+    if (dx || dc_doj) CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
     if (dx && W.fused_dx) {
       // one GEMM: N tile = d features x n_i inputs, slope combine + Jacobian in the epilogue
-      CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
       ck::DxEpilogue epi{xc, dx + r0 * I, ck::view(lut), include_tanh_jacobian, I, P.n_i};
       ck::GemmProblem gx{};
       gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
@@ -391,7 +419,6 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       gx.dx = &epi;
       CK_TRY(ck::gemm_bf16x3(gx, s));
     } else if (dx) {
-      CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
       ck::GemmProblem gx{};
       gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
       gx.b = {ck::at<__nv_bfloat16>(pv, P.dxb_hi), ck::at<__nv_bfloat16>(pv, P.dxb_lo), I, P.ldO, I * P.ldO, K};
@@ -410,11 +437,20 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       CK_TRY(ck::launch_dx_combine(g, rows * I, xc, rows, d_in, lut, include_tanh_jacobian, dx + r0 * I, s));
     }
     if (dc_doj) {
-      CK_TRY(ck::launch_split_transpose(dyc, 1, rows, O, 0, dyt_hi, dyt_lo, W.ldB, 0, s));
-      CK_TRY(ck::launch_expand_planes_t(xc, rows, d_in, lut, 1, pt_hi, pt_lo, W.ldB, I * W.ldB, s));
+      const __nv_bfloat16* ph;
+      if (basis_cache != nullptr) {
+        ph = ck::at<__nv_bfloat16>(const_cast<void*>(basis_cache), ci * L.per_chunk);  // from the forward
+      } else {
+        auto* w = ck::at<__nv_bfloat16>(workspace, W.planes);
+        CK_TRY(ck::launch_expand_planes(xc, rows, d_in, lut, 1, w, w + L.half / sizeof(__nv_bfloat16), L.ldI,
+                                        L.plane, s));
+        ph = w;
+      }
+      const __nv_bfloat16* pl = ph + L.half / sizeof(__nv_bfloat16);
+      // dC_k[o][i] = sum_b dy[b][o] Φ_k[b][i]: both operands MN-major (batch = K)
       ck::GemmProblem gc{};
-      gc.a = {dyt_hi, dyt_lo, O, W.ldB, O * W.ldB, 1};
-      gc.b = {pt_hi, pt_lo, I, W.ldB, I * W.ldB, d};
+      gc.a = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
+      gc.b = {ph, pl, I, L.ldI, L.plane, d, 1};
       gc.R = rows;
       gc.S = 1;
       gc.b_seg_z = 1;  // plane z holds k = z + 1

@@ -351,11 +351,29 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr) {
   return d;
 }
 
-// Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major.
-__host__ __device__ constexpr uint32_t umma_idesc_bf16_f32(int m, int n) {
+// UMMA descriptor for an MN-major operand tile staged by TMA with
+// SWIZZLE_128B boxes of 64 (MN) x K rows: each 64-element MN slab is a
+// column of 1 KB core groups (8 K-rows x 128 B); slabs are `slab_bytes`
+// apart (LBO) and K-groups 1024 B apart (SBO).  A K-advance of 16 rows is a
+// start-address offset of 2048 B.
+__device__ __forceinline__ uint64_t umma_desc_mnmajor(uint32_t smem_addr, uint32_t slab_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((slab_bytes >> 4) & 0x3FFFu) << 16;  // LBO: next MN slab
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;                   // SBO: next 8-row K group
+  d |= 1ull << 46;
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, A=B=bf16, D=f32; a_mn / b_mn select
+// MN-major operands (bits 15 / 16), else K-major.
+__host__ __device__ constexpr uint32_t umma_idesc_bf16_f32(int m, int n, int a_mn = 0, int b_mn = 0) {
   return (1u << 4)                            // D format f32
          | (1u << 7)                          // A format bf16
          | (1u << 10)                         // B format bf16
+         | (static_cast<uint32_t>(a_mn & 1) << 15)
+         | (static_cast<uint32_t>(b_mn & 1) << 16)
          | (static_cast<uint32_t>(n >> 3) << 17)
          | (static_cast<uint32_t>(m >> 4) << 24);
 }

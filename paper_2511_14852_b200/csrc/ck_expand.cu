@@ -137,97 +137,51 @@ __device__ __forceinline__ void pair_planes(const float* vt, int K, int n, doubl
   }
 }
 
-// Split planes k = 1..D.  TRANSPOSED = false: hi/lo [k-1][r][ld], the pair is
-// two adjacent columns of one row.  TRANSPOSED = true: hi/lo [k-1][c][ld], the
-// pair is two adjacent rows of one column (a warp covers 64 rows of a column:
-// one 128-byte store per plane, no smem staging; the x reads of neighbouring
-// columns hit the same L1 sectors because a CTA walks a 64 x 32 tile).
-template <int kSrc, int D, bool TRANSPOSED>
-__global__ void __launch_bounds__(kThreads) expand_pairs_kernel(const float* __restrict__ x, int64_t rows, int cols,
-                                                                LutView lut, uint32_t* __restrict__ hi,
-                                                                uint32_t* __restrict__ lo, int64_t ld,
-                                                                int64_t plane) {
+// Split planes k = 1..D, hi/lo [k-1][r][ld]: each thread expands 4 adjacent
+// columns of one row (two bf16x2 pairs) and writes one 8-byte word per plane
+// for hi and lo (a warp stores 256 contiguous bytes per plane).
+template <int kSrc, int D>
+__global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __restrict__ x, int64_t rows, int cols,
+                                                                LutView lut, uint2* __restrict__ hi,
+                                                                uint2* __restrict__ lo, int64_t ld, int64_t plane) {
   extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
   const float* vt = kSrc == kLutSmem ? stage_table<true>(lut.values_pm, N * K, sm_tab) : nullptr;
-  const int64_t pl = plane >> 1;  // plane stride in words
-  int64_t n_items;
-  if (TRANSPOSED) {
-    n_items = ceil_div(rows, 64) * ceil_div(cols, 32) * kThreads;  // tiles of 64 rows x 32 cols
-  } else {
-    n_items = rows * ((cols + 1) >> 1);
-  }
+  const int64_t pq = plane >> 2;  // plane stride in 8-byte words
+  const int quads = (cols + 3) >> 2;
+  const int64_t n_items = rows * quads;
+  const bool vec = (cols & 3) == 0;
   for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n_items;
        it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t r;
-    int c;
-    bool first, second;
-    float xa, xb;
-    int64_t word;
-    if (TRANSPOSED) {
-      const int64_t tile = it / kThreads;
-      const int tid = static_cast<int>(it % kThreads);
-      const int64_t r_tiles = ceil_div(rows, 64);
-      const int lane = tid & 31, w = tid >> 5;  // warp w: columns w, w+8, w+16, w+24
-      r = (tile % r_tiles) * 64 + 2 * lane;
-      const int c_base = static_cast<int>(tile / r_tiles) * 32;
-      // 8 warps x 4 columns each -> handled by 4 passes below
-      for (int pass = 0; pass < 4; ++pass) {
-        c = c_base + w + 8 * pass;
-        if (c >= cols) break;
-        first = r < rows;
-        second = r + 1 < rows;
-        if (r >= ld) break;
-        xa = first ? __ldg(x + r * cols + c) : 0.0f;
-        xb = second ? __ldg(x + (r + 1) * cols + c) : 0.0f;
-        int ia, ib;
-        float fa, fb;
-        cell_f32(xa, N, ia, fa);
-        cell_f32(xb, N, ib, fb);
-        uint32_t hw[D], lw[D];
-        pair_planes<kSrc, D>(vt, K, N, lut.step, ia, fa, ib, fb, hw, lw);
-        word = (static_cast<int64_t>(c) * ld + r) >> 1;
-        uint32_t* hp = hi + word;
-        uint32_t* lp = lo + word;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          const uint32_t mh = first ? (second ? hw[k] : (hw[k] & 0xffffu)) : 0u;
-          const uint32_t ml = first ? (second ? lw[k] : (lw[k] & 0xffffu)) : 0u;
-          *hp = mh;
-          *lp = ml;
-          hp += pl;
-          lp += pl;
-        }
-      }
+    const int64_t r = it / quads;
+    const int c = static_cast<int>(it - r * quads) * 4;
+    const float* xr = x + r * cols + c;
+    float xv[4];
+    if (vec) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xr));
+      xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
     } else {
-      const int pairs = (cols + 1) >> 1;
-      r = it / pairs;
-      c = static_cast<int>(it - r * pairs) * 2;
-      second = c + 1 < cols;
-      if (second && ((cols & 1) == 0)) {
-        const float2 v = __ldg(reinterpret_cast<const float2*>(x + r * cols + c));
-        xa = v.x;
-        xb = v.y;
-      } else {
-        xa = __ldg(x + r * cols + c);
-        xb = second ? __ldg(x + r * cols + c + 1) : 0.0f;
-      }
-      int ia, ib;
-      float fa, fb;
-      cell_f32(xa, N, ia, fa);
-      cell_f32(xb, N, ib, fb);
-      uint32_t hw[D], lw[D];
-      pair_planes<kSrc, D>(vt, K, N, lut.step, ia, fa, ib, fb, hw, lw);
-      word = (r * ld + c) >> 1;
-      uint32_t* hp = hi + word;
-      uint32_t* lp = lo + word;
 #pragma unroll
-      for (int k = 0; k < D; ++k) {
-        *hp = second ? hw[k] : (hw[k] & 0xffffu);
-        *lp = second ? lw[k] : (lw[k] & 0xffffu);
-        hp += pl;
-        lp += pl;
-      }
+      for (int e = 0; e < 4; ++e) xv[e] = c + e < cols ? __ldg(xr + e) : 0.0f;
+    }
+    int id[4];
+    float fr[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cell_f32(xv[e], N, id[e], fr[e]);
+    uint32_t h0[D], l0[D], h1[D], l1[D];
+    pair_planes<kSrc, D>(vt, K, N, lut.step, id[0], fr[0], id[1], fr[1], h0, l0);
+    pair_planes<kSrc, D>(vt, K, N, lut.step, id[2], fr[2], id[3], fr[3], h1, l1);
+    // padded columns (c+e >= cols) are written as zeros inside [cols, ld)
+    const uint32_t m0 = c + 1 < cols ? 0xffffffffu : (c < cols ? 0xffffu : 0u);
+    const uint32_t m1 = c + 3 < cols ? 0xffffffffu : (c + 2 < cols ? 0xffffu : 0u);
+    uint2* hp = hi + ((r * ld + c) >> 2);
+    uint2* lp = lo + ((r * ld + c) >> 2);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      *hp = make_uint2(h0[k] & m0, h1[k] & m1);
+      *lp = make_uint2(l0[k] & m0, l1[k] & m1);
+      hp += pq;
+      lp += pq;
     }
   }
 }
@@ -271,32 +225,6 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
       split_pack2(v, vb2, h2, l2);
       h[(k - k0) * pl] = h2;
       l[(k - k0) * pl] = l2;
-    });
-  }
-}
-
-// Transposed generic fallback: hi/lo [k-k0][c][ldr], one element per thread.
-template <int kSrc>
-__global__ void __launch_bounds__(kThreads) expand_planes_t_kernel(const float* __restrict__ x, int64_t rows,
-                                                                   int cols, LutView lut, int k0,
-                                                                   __nv_bfloat16* __restrict__ hi,
-                                                                   __nv_bfloat16* __restrict__ lo,
-                                                                   int64_t ldr, int64_t plane) {
-  extern __shared__ float sm_tab[];
-  const int K = lut.K, N = lut.N;
-  const float* vt = kSrc == kLutSmem ? stage_table<true>(lut.values_pm, N * K, sm_tab) : nullptr;
-  const int64_t n_items = rows * cols;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_items;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t c = e / rows, r = e - c * rows;  // consecutive threads: consecutive rows
-    int idx;
-    float fr;
-    cell_f32(x[r * cols + c], N, idx, fr);
-    Columns<kSrc>::run(vt, K, N, lut.step, idx, fr, k0, [&](int k, float v) {
-      __nv_bfloat16 h, l;
-      split_bf16(v, h, l);
-      hi[(k - k0) * plane + c * ldr + r] = h;
-      lo[(k - k0) * plane + c * ldr + r] = l;
     });
   }
 }
@@ -353,26 +281,26 @@ int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut,
 }
 
 
-template <int kSrc, bool T>
-int launch_pairs(int d, const float* x, int64_t rows, int cols, const LutView& v, uint32_t* h, uint32_t* l,
-                 int64_t ld, int64_t plane, size_t tab, int blocks, cudaStream_t s) {
+template <int kSrc>
+int launch_quads(int d, const float* x, int64_t rows, int cols, const LutView& v, uint2* h, uint2* l, int64_t ld,
+                 int64_t plane, size_t tab, int blocks, cudaStream_t s) {
   const size_t smem = kSrc == kLutSmem ? tab : 0;
-#define CK_PAIRS_CASE(D)                                                                                      \
-  case D:                                                                                                     \
-    if (smem) {                                                                                               \
-      CK_CUDA(cudaFuncSetAttribute(expand_pairs_kernel<kSrc, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   static_cast<int>(smem)));                                                  \
-    }                                                                                                         \
-    expand_pairs_kernel<kSrc, D, T><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, h, l, ld, plane);        \
+#define CK_QUADS_CASE(D)                                                                                     \
+  case D:                                                                                                    \
+    if (smem) {                                                                                              \
+      CK_CUDA(cudaFuncSetAttribute(expand_quads_kernel<kSrc, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   static_cast<int>(smem)));                                                 \
+    }                                                                                                        \
+    expand_quads_kernel<kSrc, D><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, h, l, ld, plane);          \
     break;
   switch (d) {
-    CK_PAIRS_CASE(1) CK_PAIRS_CASE(2) CK_PAIRS_CASE(3) CK_PAIRS_CASE(4) CK_PAIRS_CASE(5) CK_PAIRS_CASE(6)
-    CK_PAIRS_CASE(7) CK_PAIRS_CASE(8) CK_PAIRS_CASE(9) CK_PAIRS_CASE(10) CK_PAIRS_CASE(11) CK_PAIRS_CASE(12)
-    CK_PAIRS_CASE(13) CK_PAIRS_CASE(14) CK_PAIRS_CASE(15) CK_PAIRS_CASE(16)
+    CK_QUADS_CASE(1) CK_QUADS_CASE(2) CK_QUADS_CASE(3) CK_QUADS_CASE(4) CK_QUADS_CASE(5) CK_QUADS_CASE(6)
+    CK_QUADS_CASE(7) CK_QUADS_CASE(8) CK_QUADS_CASE(9) CK_QUADS_CASE(10) CK_QUADS_CASE(11) CK_QUADS_CASE(12)
+    CK_QUADS_CASE(13) CK_QUADS_CASE(14) CK_QUADS_CASE(15) CK_QUADS_CASE(16)
     default:
       return kUnsupported;
   }
-#undef CK_PAIRS_CASE
+#undef CK_QUADS_CASE
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -391,52 +319,25 @@ int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* l
   const LutView v = view(lut);
   const size_t tab = sizeof(float) * v.N * v.K;
   const int src = pick_source(tab);
-  const int blocks = grid_for(rows * ((cols + 1) / 2), 8);
   auto* h = reinterpret_cast<uint32_t*>(hi);
   auto* l = reinterpret_cast<uint32_t*>(lo);
   LaunchScope scope(kKExpand, s);
-  if (k0 == 1) {
+  if (k0 == 1 && ld % 4 == 0 && plane % 4 == 0) {
     const int d = v.K - 1;
-    const int rc = src == kLutSmem ? launch_pairs<kLutSmem, false>(d, x, rows, cols, v, h, l, ld, plane, tab, blocks, s)
-                                   : launch_pairs<kLutNodes, false>(d, x, rows, cols, v, h, l, ld, plane, tab, blocks, s);
+    const int qb = grid_for(rows * ((cols + 3) / 4), 8);
+    auto* h8 = reinterpret_cast<uint2*>(hi);
+    auto* l8 = reinterpret_cast<uint2*>(lo);
+    const int rc = src == kLutSmem ? launch_quads<kLutSmem>(d, x, rows, cols, v, h8, l8, ld, plane, tab, qb, s)
+                                   : launch_quads<kLutNodes>(d, x, rows, cols, v, h8, l8, ld, plane, tab, qb, s);
     if (rc != kUnsupported) return rc;
   }
+  const int blocks = grid_for(rows * ((cols + 1) / 2), 8);
   if (src == kLutSmem) {
     CK_CUDA(cudaFuncSetAttribute(expand_planes_kernel<kLutSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
     expand_planes_kernel<kLutSmem><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
   } else {
     expand_planes_kernel<kLutNodes><<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
-  }
-  CK_CUDA(cudaGetLastError());
-  return kOk;
-}
-
-int launch_expand_planes_t(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
-                           __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ldr, int64_t plane, cudaStream_t s) {
-  if (rows == 0 || cols == 0 || k0 >= lut->n_feat) return kOk;
-  CK_CHECK(ldr % 2 == 0 && plane % 2 == 0, "expand_planes_t: pitch must be even");
-  const LutView v = view(lut);
-  const size_t tab = sizeof(float) * v.N * v.K;
-  const int src = pick_source(tab);
-  LaunchScope scope(kKExpandT, s);
-  if (k0 == 1) {
-    const int64_t items = ceil_div(rows, 64) * ceil_div(cols, 32) * kThreads;
-    const int blocks = grid_for(items, 8);
-    auto* h = reinterpret_cast<uint32_t*>(hi);
-    auto* l = reinterpret_cast<uint32_t*>(lo);
-    const int d = v.K - 1;
-    const int rc = src == kLutSmem ? launch_pairs<kLutSmem, true>(d, x, rows, cols, v, h, l, ldr, plane, tab, blocks, s)
-                                   : launch_pairs<kLutNodes, true>(d, x, rows, cols, v, h, l, ldr, plane, tab, blocks, s);
-    if (rc != kUnsupported) return rc;
-  }
-  const int blocks = grid_for(rows * cols, 8);
-  if (src == kLutSmem) {
-    CK_CUDA(cudaFuncSetAttribute(expand_planes_t_kernel<kLutSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(tab)));
-    expand_planes_t_kernel<kLutSmem><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
-  } else {
-    expand_planes_t_kernel<kLutNodes><<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, hi, lo, ldr, plane);
   }
   CK_CUDA(cudaGetLastError());
   return kOk;

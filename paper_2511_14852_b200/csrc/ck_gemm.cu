@@ -189,7 +189,7 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
   }
 }
 
-template <int BN, int BK, int STAGES, int EPI, int CG>
+template <int BN, int BK, int STAGES, int EPI, int CG, int AMN, int BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                        const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
@@ -271,16 +271,36 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if constexpr (CG == 2) {
             if (leader) mbar_arrive_expect_tx(&full[stage], p.stage_tx);  // bytes of both CTAs
-            tma_load_3d_pair(st, &tm_a_hi, &full[stage], r0, arow, aseg);
-            tma_load_3d_pair(st + C::kABytes, &tm_a_lo, &full[stage], r0, arow, aseg);
-            tma_load_3d_pair(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, brow, bz);
-            tma_load_3d_pair(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, brow, bz);
           } else {
             mbar_arrive_expect_tx(&full[stage], p.stage_tx);
-            tma_load_3d(st, &tm_a_hi, &full[stage], r0, arow, aseg);
-            tma_load_3d(st + C::kABytes, &tm_a_lo, &full[stage], r0, arow, aseg);
-            tma_load_3d(st + 2 * C::kABytes, &tm_b_hi, &full[stage], r0, brow, bz);
-            tma_load_3d(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, &full[stage], r0, brow, bz);
+          }
+          // A: 128 rows of this CTA; B: b_half rows.  MN-major operands come
+          // as 64-wide MN slabs (8 KB each for BK = 64).
+          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, int c2) {
+            if constexpr (CG == 2) {
+              tma_load_3d_pair(dst, map, &full[stage], c0, c1, c2);
+            } else {
+              tma_load_3d(dst, map, &full[stage], c0, c1, c2);
+            }
+          };
+          if constexpr (AMN) {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j) {
+              load(st + j * 64 * kRowBytes, &tm_a_hi, arow + 64 * j, r0, aseg);
+              load(st + C::kABytes + j * 64 * kRowBytes, &tm_a_lo, arow + 64 * j, r0, aseg);
+            }
+          } else {
+            load(st, &tm_a_hi, r0, arow, aseg);
+            load(st + C::kABytes, &tm_a_lo, r0, arow, aseg);
+          }
+          if constexpr (BMN) {
+            for (int j = 0; j < b_half / 64; ++j) {
+              load(st + 2 * C::kABytes + j * 64 * kRowBytes, &tm_b_hi, brow + 64 * j, r0, bz);
+              load(st + 2 * C::kABytes + C::kBBytes + j * 64 * kRowBytes, &tm_b_lo, brow + 64 * j, r0, bz);
+            }
+          } else {
+            load(st + 2 * C::kABytes, &tm_b_hi, r0, brow, bz);
+            load(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, r0, brow, bz);
           }
         }
       }
@@ -288,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader CTA of a pair) ----------------
-      const uint32_t idesc = umma_idesc_bf16_f32(kBM * CG, p.n_mma);
+      const uint32_t idesc = umma_idesc_bf16_f32(kBM * CG, p.n_mma, AMN, BMN);
       uint32_t g = 0, lt = 0;
       for (int t = unit; t < total; t += n_units, ++lt) {
         const TileCoord tc = decode_tile(p, t, kBM * CG);
@@ -307,11 +327,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b_lo = b_hi + C::kBBytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t off = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
-            const uint64_t dah = umma_desc_kmajor<kRowBytes>(a_hi + off);
-            const uint64_t dal = umma_desc_kmajor<kRowBytes>(a_lo + off);
-            const uint64_t dbh = umma_desc_kmajor<kRowBytes>(b_hi + off);
-            const uint64_t dbl = umma_desc_kmajor<kRowBytes>(b_lo + off);
+            // K-major: 16 bf16 = 32 bytes along the swizzled row;
+            // MN-major: 16 K-rows = 2 core groups = 2048 bytes
+            constexpr uint32_t kSlab = 64 * kRowBytes;
+            uint64_t dah, dal, dbh, dbl;
+            if constexpr (AMN) {
+              dah = umma_desc_mnmajor(a_hi + kk * 2048, kSlab);
+              dal = umma_desc_mnmajor(a_lo + kk * 2048, kSlab);
+            } else {
+              dah = umma_desc_kmajor<kRowBytes>(a_hi + kk * 32);
+              dal = umma_desc_kmajor<kRowBytes>(a_lo + kk * 32);
+            }
+            if constexpr (BMN) {
+              dbh = umma_desc_mnmajor(b_hi + kk * 2048, kSlab);
+              dbl = umma_desc_mnmajor(b_lo + kk * 2048, kSlab);
+            } else {
+              dbh = umma_desc_kmajor<kRowBytes>(b_hi + kk * 32);
+              dbl = umma_desc_kmajor<kRowBytes>(b_lo + kk * 32);
+            }
             if constexpr (CG == 2) {
               umma_bf16_pair(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
               umma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);
@@ -456,7 +489,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t rows, int64_t segs, int64_t ld,
-             int64_t seg_stride, int box_rows, int bk) {
+             int64_t seg_stride, int box_rows, int bk, int mn_major = 0) {
   auto encode = get_encode();
   if (!encode) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -464,9 +497,13 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   }
   CK_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, "gemm operand not 16-byte aligned");
   CK_CHECK(ld % 8 == 0 && seg_stride % 8 == 0, "gemm operand pitch must be a multiple of 8 elements");
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(segs)};
+  // K-major: dims (K, rows, segs), box (bk, box_rows).  MN-major: dims
+  // (rows, K, segs), box (64 MN elements = one 128-byte swizzle row, bk K-rows).
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(mn_major ? rows : R), static_cast<cuuint64_t>(mn_major ? R : rows),
+                        static_cast<cuuint64_t>(segs)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 2), static_cast<cuuint64_t>(seg_stride * 2)};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(bk), static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(mn_major ? 64 : bk), static_cast<cuuint32_t>(mn_major ? bk : box_rows),
+                       1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(base), dims, strides, box,
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -478,9 +515,10 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   return kOk;
 }
 
-template <int BN, int BK, int STAGES, int EPI, int CG>
+template <int BN, int BK, int STAGES, int EPI, int CG, int AMN = 0, int BMN = 0>
 int launch(const GemmProblem& p, int splits, float* out, long long out_split_stride, int accumulate,
            cudaStream_t s) {
+  static_assert(!(AMN || BMN) || BK == 64, "MN-major operands use 128-byte (BK = 64) K slabs");
   using C = Cfg<BN, BK, STAGES, CG>;
   constexpr int kRowBytes = C::kRowBytes;
   const int r_chunks = static_cast<int>(ceil_div(p.R, BK));
@@ -489,11 +527,13 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   const int n_mma = n_tile * b_boxes;
   CK_CHECK(n_mma % (8 * CG) == 0 && n_mma <= BN, "gemm: bad MMA N");
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
-  CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
-  CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK));
+  CK_CHECK(p.a.mn_major == AMN && p.b.mn_major == BMN, "gemm: operand majorness mismatch");
+  CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK, AMN));
+  CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK, AMN));
   const int b_box = n_mma / CG;  // each CTA of a pair stages half of the B rows
-  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK));
-  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK));
+  CK_CHECK(!BMN || b_box % 64 == 0, "gemm: MN-major B tile must be a multiple of 64 rows");
+  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK, BMN));
+  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK, BMN));
   KArgs k{};
   k.n_tile = n_tile;
   k.n_mma = n_mma;
@@ -529,7 +569,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.bias0 = splits == 1 ? p.bias0 : nullptr;
   k.bias1 = splits == 1 ? p.bias1 : nullptr;
   k.accumulate = accumulate;
-  auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG>;
+  auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN>;
   static bool attr_set = false;
   if (!attr_set) {
     CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
@@ -640,7 +680,16 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   // partial slot layout: [split][z][M][N]; the kernel offsets by split first
   int rc;
   const bool bk64 = gemm_bk() == 64;
-  if (bn == 128) {
+  if (p.a.mn_major || p.b.mn_major) {
+    CK_CHECK(p.a.mn_major && p.b.mn_major, "gemm: mixed-majorness store GEMM not instantiated");
+    if (bn == 128) {
+      rc = launch<128, 64, 3, kEpiStore, 1, 1, 1>(q, splits, out, split_stride, acc, s);
+    } else if (gemm_cg() == 2) {
+      rc = launch<256, 64, 3, kEpiStore, 2, 1, 1>(q, splits, out, split_stride, acc, s);
+    } else {
+      rc = launch<256, 64, 2, kEpiStore, 1, 1, 1>(q, splits, out, split_stride, acc, s);
+    }
+  } else if (bn == 128) {
     rc = bk64 ? launch<128, 64, 3, kEpiStore, 1>(q, splits, out, split_stride, acc, s)
               : launch<128, 32, 6, kEpiStore, 1>(q, splits, out, split_stride, acc, s);
   } else if (gemm_cg() == 2) {

@@ -86,10 +86,6 @@ int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut,
 int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
                          __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t plane_stride,
                          cudaStream_t s);
-// Transposed split planes hi/lo [nk][cols][ldr] (element (r,c) at [k][c][r]).
-int launch_expand_planes_t(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
-                           __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ldr, int64_t plane_stride,
-                           cudaStream_t s);
 // dx[r][c] = J * sum_{k>=1} slope_k(cell(tanh x)) * g[k-1][r][c]
 int launch_dx_combine(const float* g, int64_t g_plane_stride, const float* x, int64_t rows, int cols,
                       const ck_lut* lut, int jacobian, float* dx, cudaStream_t s);
@@ -136,9 +132,10 @@ struct GemmOperand {
   const __nv_bfloat16* hi;
   const __nv_bfloat16* lo;
   int64_t rows;        // M (for A) or N (for B)
-  int64_t ld;          // row pitch in elements
+  int64_t ld;          // pitch in elements between consecutive rows (K-major) or K-rows (MN-major)
   int64_t seg_stride;  // elements between segments
   int64_t segs;        // number of segments addressable
+  int mn_major = 0;    // 1: stored [K][MN] (M/N contiguous), e.g. dy [B][O] as the dC A operand
 };
 // Fused input-gradient epilogue (kernels.py:430-444): the GEMM's N tile
 // stacks d features x n_i inputs; the epilogue folds the d accumulators

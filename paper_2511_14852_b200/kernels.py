@@ -130,21 +130,36 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
-def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut: LutTable, bias: torch.Tensor | None) -> torch.Tensor:
-    """y = fused layer forward on prepared coefficients (x fp32 contiguous [B, I])."""
+def basis_cache_bytes(batch: int, d_in: int, n_feat: int) -> int:
+    """Bytes of the forward->backward basis cache (bf16 hi/lo planes, k >= 1)."""
+    return int(_lib.lib().ck_basis_cache_bytes(batch, d_in, n_feat))
+
+
+def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut: LutTable, bias: torch.Tensor | None,
+                cache: torch.Tensor | None = None) -> torch.Tensor:
+    """y = fused layer forward on prepared coefficients (x fp32 contiguous [B, I]).
+
+    ``cache`` (uint8, >= basis_cache_bytes): keep the expanded basis for the
+    backward of the same x.
+    """
     b = x.shape[0]
     y = torch.empty((b, prep.d_out), dtype=torch.float32, device=x.device)
     lb = _lib.lib()
     ws = _workspace(lb.ck_forward_workspace_bytes(b, prep.d_in, prep.d_out, prep.n_feat), x.device)
     rc = lb.ck_forward(x.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(), _lib.ptr(bias),
-                       y.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle(x.device))
+                       y.data_ptr(), ws.data_ptr(), ws.numel(), _lib.ptr(cache), 0 if cache is None else cache.numel(),
+                       _lib.stream_handle(x.device))
     _lib.check(rc, "ck_forward")
     return y
 
 
 def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut: LutTable, jacobian: bool,
-                 want_dx: bool = True, want_dc: bool = True, want_db: bool = True):
-    """(dC DOJ, dX, db) on prepared coefficients; unrequested outputs are None."""
+                 want_dx: bool = True, want_dc: bool = True, want_db: bool = True,
+                 cache: torch.Tensor | None = None):
+    """(dC DOJ, dX, db) on prepared coefficients; unrequested outputs are None.
+
+    ``cache``: the basis cache filled by forward_raw on the same x (optional).
+    """
     b = x.shape[0]
     dev = x.device
     dx = torch.empty((b, prep.d_in), dtype=torch.float32, device=dev) if want_dx else None
@@ -154,7 +169,7 @@ def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut: Lu
     ws = _workspace(lb.ck_backward_workspace_bytes(b, prep.d_in, prep.d_out, prep.n_feat), dev)
     rc = lb.ck_backward(x.data_ptr(), dy.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(),
                         1 if jacobian else 0, _lib.ptr(dx), _lib.ptr(dc), _lib.ptr(db), ws.data_ptr(), ws.numel(),
-                        _lib.stream_handle(dev))
+                        _lib.ptr(cache), 0 if cache is None else cache.numel(), _lib.stream_handle(dev))
     _lib.check(rc, "ck_backward")
     return dc, dx, db
 

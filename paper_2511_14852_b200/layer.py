@@ -15,17 +15,18 @@ import numpy as np
 import torch
 from torch import nn
 
-from .kernels import PreparedCoeff, backward_raw, forward_raw
+from .kernels import PreparedCoeff, backward_raw, basis_cache_bytes, forward_raw
 from .lut import DEFAULT_LUT_SIZE, LutTable, lut_build
 
 
 class _LayerState:
     """Per-module LUT and coefficient-prep cache (not a parameter)."""
 
-    def __init__(self, degree: int, lut_size: int, jacobian: bool):
+    def __init__(self, degree: int, lut_size: int, jacobian: bool, cache_basis="auto"):
         self.degree = degree
         self.lut_size = lut_size
         self.jacobian = jacobian
+        self.cache_basis = cache_basis
         self._luts: dict[int, LutTable] = {}
         self._prep: PreparedCoeff | None = None
 
@@ -58,9 +59,16 @@ class ChebyKANFunction(torch.autograd.Function):
         x = x.to(torch.float32).contiguous()
         lut = state.lut(x.device)
         prep = state.prepared(coeff_doj)
-        y = forward_raw(x, prep, lut, None if bias is None else bias.detach())
+        cache = None
+        if ctx.needs_input_grad[1] and state.cache_basis:
+            # keep the expanded basis for dC (saves the backward's re-expansion)
+            nbytes = basis_cache_bytes(x.shape[0], prep.d_in, prep.n_feat)
+            if state.cache_basis is True or nbytes <= 0.35 * torch.cuda.mem_get_info(x.device)[0]:
+                cache = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+        y = forward_raw(x, prep, lut, None if bias is None else bias.detach(), cache)
         ctx.save_for_backward(x, coeff_doj)
         ctx.state = state
+        ctx.cache = cache
         ctx.has_bias = bias is not None
         return y
 
@@ -72,7 +80,8 @@ class ChebyKANFunction(torch.autograd.Function):
         need_x, need_c, need_b = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
         prep = state.prepared(coeff_doj)
         dc, dx, db = backward_raw(x, dy, prep, state.lut(x.device), state.jacobian, want_dx=need_x,
-                                  want_dc=need_c, want_db=need_b and ctx.has_bias)
+                                  want_dc=need_c, want_db=need_b and ctx.has_bias, cache=ctx.cache)
+        ctx.cache = None
         return dx, dc, db, None
 
 
@@ -87,11 +96,14 @@ class ChebyKANLayer(nn.Module):
     include_tanh_jacobian : KernelMode flag (kernels.py:35-44)
     seed : when given, coefficients are drawn exactly as init_params
         (numpy default_rng(seed).uniform(-s, s) in JOD order, model.py:72-83)
+    cache_basis : keep the forward's expanded basis (bf16 hi/lo planes,
+        4*B*I*degree bytes) for the coefficient-gradient GEMM: "auto" when it
+        fits in 35 % of free device memory, True, or False (re-expand)
     """
 
     def __init__(self, input_dim: int, output_dim: int, degree: int, bias: bool = True,
                  lut_size: int = DEFAULT_LUT_SIZE, include_tanh_jacobian: bool = True, seed: int | None = None,
-                 device=None):
+                 device=None, cache_basis="auto"):
         super().__init__()
         if input_dim < 1 or output_dim < 1:
             raise ValueError("layer dimensions must be >= 1")
@@ -102,7 +114,7 @@ class ChebyKANLayer(nn.Module):
         k = self.degree + 1
         self.coeff_doj = nn.Parameter(torch.empty((k, self.output_dim, self.input_dim), device=device))
         self.bias = nn.Parameter(torch.zeros(self.output_dim, device=device)) if bias else None
-        self._state = _LayerState(self.degree, self.lut_size, include_tanh_jacobian)
+        self._state = _LayerState(self.degree, self.lut_size, include_tanh_jacobian, cache_basis)
         self.reset_parameters(seed)
 
     @property

@@ -48,7 +48,7 @@ def test_version_and_sizes_are_host_only():
 
 def test_forward_without_lut_is_a_value_error():
     lib = _lib.lib()
-    rc = lib.ck_forward(None, 4, 8, 8, None, None, None, None, None, 0, None)
+    rc = lib.ck_forward(None, 4, 8, 8, None, None, None, None, None, 0, None, 0, None)
     assert rc == _lib.CK_INVALID_ARGUMENT
     assert "LUT mode requires a LutTable" in _lib.last_error()
     with pytest.raises(ValueError, match="LUT mode requires a LutTable"):
