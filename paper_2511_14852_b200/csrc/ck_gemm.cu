@@ -70,6 +70,7 @@ struct KArgs {
   int splits;      // R splits per z
   int r_chunks;    // ceil(R / kBK)
   int n_tiles, m_tiles, total_tiles;
+  int group_m;     // rasterisation group (m-tiles walked per n)
   float* out;
   long long ldo, out_z_stride, out_split_stride;
   const float* bias0;
@@ -86,18 +87,16 @@ struct TileCoord {
 // Grouped rasterisation: consecutive tiles walk kGroupM m-tiles for one n,
 // then the next n, so a wave of ~74-148 co-resident units covers a compact
 // (kGroupM x ~wave/kGroupM) block and both operands are reused from L2.
-constexpr int kGroupM = 8;
-
 __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_tile_rows) {
   TileCoord c;
-  const int nt = p.n_tiles, mt = p.m_tiles;
+  const int nt = p.n_tiles, mt = p.m_tiles, G = p.group_m;
   const int per_z = nt * mt;
   const int zs = t / per_z;
   const int r = t - zs * per_z;
-  const int group = r / (kGroupM * nt);
-  const int first_m = group * kGroupM;
-  const int gm = min(kGroupM, mt - first_m);  // last group may be short
-  const int rr = r - group * kGroupM * nt;
+  const int group = r / (G * nt);
+  const int first_m = group * G;
+  const int gm = min(G, mt - first_m);  // last group may be short
+  const int rr = r - group * G * nt;
   c.m0 = (first_m + rr % gm) * m_tile_rows;
   c.n0 = (rr / gm) * p.n_tile;
   c.z = zs / p.splits;
@@ -515,6 +514,8 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   return kOk;
 }
 
+int gemm_group();
+
 template <int BN, int BK, int STAGES, int EPI, int CG, int AMN = 0, int BMN = 0>
 int launch(const GemmProblem& p, int splits, float* out, long long out_split_stride, int accumulate,
            cudaStream_t s) {
@@ -575,6 +576,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
     CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     attr_set = true;
   }
+  k.group_m = gemm_group();
   k.n_tiles = static_cast<int>(ceil_div(k.N, n_tile));
   k.m_tiles = static_cast<int>(ceil_div(k.M, kBM * CG));
   const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles * p.nz * splits;
@@ -605,6 +607,16 @@ int gemm_bk() {
     return (e && std::string(e) == "32") ? 32 : 64;
   }();
   return bk;
+}
+
+// Rasterisation group size (m-tiles per group; CK_GEMM_GROUP overrides).
+int gemm_group() {
+  static int g = [] {
+    const char* e = getenv("CK_GEMM_GROUP");
+    const int v = e ? atoi(e) : 8;
+    return v >= 1 && v <= 1024 ? v : 8;
+  }();
+  return g;
 }
 
 // CTA group for the GEMMs: 2 (SM pairs, default) or 1 (CK_GEMM_CG=1).
