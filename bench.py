@@ -444,7 +444,7 @@ def run_sweep(args):
             x = torch.rand(b, dim, device=dev) * 3 - 1.5
             c = (torch.rand(deg + 1, dim, dim, device=dev) * 2 - 1) / (dim * (deg + 1)) ** 0.5
             dy = torch.randn(b, dim, device=dev)
-            lut = ck.lut_build(deg, 32768, device=dev)
+            lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, deg, 32768, device=dev)
             prep = PreparedCoeff(c)
             for _ in range(3):
                 forward_raw(x, prep, lut, None)

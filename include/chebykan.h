@@ -47,32 +47,57 @@ CK_API const char* ck_last_error(void);
 /* 1 when the current device is sm_100 (B200) and the kernels can launch. */
 CK_API int ck_device_supported(int device);
 
+/* --- Basis families -----------------------------------------------------
+ * Values are the reference's PKLT basis tags (lut.py:35-40, BasisKind
+ * basis.py:17-21).  Feature count K = degree + 1, or 2*degree + 1 for
+ * Fourier (feature_count, basis.py:24-34).  CK_BASIS_CHEBYSHEV_TRIG is the
+ * exact-only cos(k*acos t) evaluation (trig_rows basis.py:144-152, the
+ * reference_forward(trig=True) path kernels.py:450-478). */
+typedef enum {
+  CK_BASIS_CHEBYSHEV = 0,
+  CK_BASIS_LEGENDRE = 1,
+  CK_BASIS_HERMITE = 2,
+  CK_BASIS_FOURIER = 3,
+  CK_BASIS_CHEBYSHEV_TRIG = 4
+} ck_basis_kind;
+
 /* --- LUT ------------------------------------------------------------------
- * ck_lut_build replaces lut_build(BasisKind.CHEBYSHEV, degree, lut_size)
- * (lut.py:76-94): float64 grid -1 + i*step with the last node forced to 1.0,
- * values by the T_k recurrence (basis.py:112-119), slopes = float64 first
- * differences / step rounded to float32.  Built on the device in float64
- * (bit-identical to the reference table); stored as float32 values and
- * float32 slopes, position-major, for the kernels.  Errors as lut.py:78-81.
+ * ck_lut_build replaces lut_build(kind, degree, lut_size) (lut.py:76-94):
+ * float64 grid -1 + i*step with the last node forced to 1.0, values by the
+ * family's three-term recurrence (basis.py:87-119; Fourier by the
+ * angle-addition identities, basis.py:100-110), slopes = float64 first
+ * differences / step rounded to float32.  Values are built in float64 with
+ * the reference's operation order (bit-identical table) and kept on the
+ * device as float32 position-major copies for the kernels.  Errors as
+ * lut.py:78-81.
  */
-CK_API int ck_lut_build(int degree, int lut_size, int device, ck_lut** out);
+CK_API int ck_lut_build(int kind, int degree, int lut_size, int device, ck_lut** out);
 /* Wrap a caller-provided table (e.g. a PKLT file, load_lut lut.py:180-206):
  * values[K][N] float64 and slopes[K][N-1] float32, host memory. */
-CK_API int ck_lut_create(int degree, int lut_size, const double* values_host, const float* slopes_host,
+CK_API int ck_lut_create(int kind, int degree, int lut_size, const double* values_host, const float* slopes_host,
                   int device, ck_lut** out);
+/* Exact-evaluation handle (BasisPath.EXACT_RECURRENCE, kernels.py:30-32,
+ * 219-224): no table; the kernels evaluate basis_rows / derivative_rows
+ * (basis.py:87-119, 155-204) at t = tanh(x) in float32.  Accepted wherever a
+ * ck_lut is (ck_expand, ck_forward, ck_backward). */
+CK_API int ck_basis_exact(int kind, int degree, int device, ck_lut** out);
 CK_API void ck_lut_destroy(ck_lut* lut);
 /* degree, lut_size and step of a table (LutTable fields, lut.py:52-56). */
 CK_API int ck_lut_info(const ck_lut* lut, int* degree, int* lut_size, double* step);
+/* kind, feature count and exact flag of a handle. */
+CK_API int ck_lut_kind(const ck_lut* lut, int* kind, int* n_feat, int* exact);
 /* Copy the float64 values [K][N] and float32 slopes [K][N-1] to host memory
  * (either pointer may be NULL); synchronous. */
 CK_API int ck_lut_read(const ck_lut* lut, double* values_host, float* slopes_host);
 
 /* --- Basis expansion ---------------------------------------------------------
- * phi[b][i][k] = interp of T_k at tanh(x[b][i]) and, when slopes != NULL,
+ * phi[b][i][k] = interp of B_k at tanh(x[b][i]) and, when slopes != NULL,
  * slopes[b][i][k] = the active cell's slope: interp_rows_with_slope
  * (lut.py:97-123) applied to np.tanh(x) (kernels.py:288, 414).  The cell
  * (clip, idx, frac, snap) is computed in float64 so it matches the
- * reference's choice exactly; values are interpolated in float32. */
+ * reference's choice exactly; values are interpolated in float32.  With an
+ * exact handle: phi = basis_rows, slopes = derivative_rows at tanh(x)
+ * (kernels.py:219-224). */
 CK_API int ck_expand(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi, float* slopes,
               void* stream);
 

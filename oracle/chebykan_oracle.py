@@ -53,6 +53,86 @@ def chebyshev_rows(degree: int, t: np.ndarray) -> np.ndarray:
     return rows
 
 
+KINDS = ("chebyshev", "legendre", "hermite", "fourier")
+
+
+def feature_count(kind: str, degree: int) -> int:
+    """basis.py:24-34: Fourier has 2*degree+1 features, the others degree+1."""
+    return 2 * degree + 1 if kind == "fourier" else degree + 1
+
+
+def degree_for(kind: str, n_feat: int) -> int:
+    """kernels.py:227-233."""
+    return (n_feat - 1) // 2 if kind == "fourier" else n_feat - 1
+
+
+def basis_rows(kind: str, degree: int, t: np.ndarray) -> np.ndarray:
+    """All features at every point; basis.py:87-119 with the recurrence
+    coefficients of basis.py:52-77 (alpha, beta(x), gamma), evaluated as
+    (beta_k(x) * B_k - gamma_k * B_{k-1}) / alpha_k in numpy's order; Fourier
+    by the angle-addition identities from cos/sin(pi x) (basis.py:100-110)."""
+    if kind == "chebyshev":
+        return chebyshev_rows(degree, t)
+    t = np.asarray(t, dtype=np.float64)
+    nf = feature_count(kind, degree)
+    out = np.empty((nf,) + t.shape, dtype=np.float64)
+    out[0] = 1.0
+    if kind == "fourier":
+        if degree >= 1:
+            theta = np.pi * t
+            c1, s1 = np.cos(theta), np.sin(theta)
+            out[1], out[2] = c1, s1
+            for k in range(1, degree):
+                out[2 * k + 1] = c1 * out[2 * k - 1] - s1 * out[2 * k]
+                out[2 * k + 2] = s1 * out[2 * k - 1] + c1 * out[2 * k]
+        return out
+    if degree >= 1:
+        out[1] = 2.0 * t if kind == "hermite" else t.copy()
+    for k in range(1, degree):
+        if kind == "legendre":
+            alpha, beta, gamma = float(k + 1), (2.0 * k + 1.0) * t, float(k)
+        elif kind == "hermite":
+            alpha, beta, gamma = 1.0, 2.0 * t, 2.0 * k
+        else:
+            raise ValueError(f"unsupported basis kind: {kind}")
+        out[k + 1] = (beta * out[k] - gamma * out[k - 1]) / alpha
+    return out
+
+
+def derivative_rows(kind: str, degree: int, t: np.ndarray) -> np.ndarray:
+    """Analytic dB_k/dx; basis.py:155-204 (T_n' = n U_{n-1}; P'_{k+1} =
+    P'_{k-1} + (2k+1) P_k; H_n' = 2n H_{n-1}; d/dx of cos/sin(k pi x))."""
+    t = np.asarray(t, dtype=np.float64)
+    nf = feature_count(kind, degree)
+    out = np.zeros((nf,) + t.shape, dtype=np.float64)
+    if degree < 1:
+        return out
+    if kind == "chebyshev":
+        u_prev = np.ones_like(t)
+        out[1] = u_prev
+        if degree >= 2:
+            u_cur = 2.0 * t
+            out[2] = 2.0 * u_cur
+            for n in range(3, degree + 1):
+                u_prev, u_cur = u_cur, 2.0 * t * u_cur - u_prev
+                out[n] = n * u_cur
+        return out
+    b = basis_rows(kind, degree, t)
+    if kind == "legendre":
+        out[1] = 1.0
+        for k in range(1, degree):
+            out[k + 1] = out[k - 1] + (2.0 * k + 1.0) * b[k]
+    elif kind == "hermite":
+        for n in range(1, degree + 1):
+            out[n] = 2.0 * n * b[n - 1]
+    else:
+        for k in range(1, degree + 1):
+            kpi = k * np.pi
+            out[2 * k - 1] = -kpi * b[2 * k]
+            out[2 * k] = kpi * b[2 * k - 1]
+    return out
+
+
 def chebyshev_trig_rows(degree: int, t: np.ndarray) -> np.ndarray:
     """cos(k * arccos t), the exact path used for the interpolation report.
 
@@ -64,8 +144,8 @@ def chebyshev_trig_rows(degree: int, t: np.ndarray) -> np.ndarray:
     return np.cos(k * theta)
 
 
-def build_table(degree: int, lut_size: int):
-    """Uniform-grid table of T_k values (f64) and per-cell slopes (f32).
+def build_table(degree: int, lut_size: int, kind: str = "chebyshev"):
+    """Uniform-grid table of basis values (f64) and per-cell slopes (f32).
 
     lut.py:76-94: grid x_i = -1 + i*step with step = 2/(N-1) and the last
     node forced to exactly 1.0; slopes are float64 first differences over
@@ -79,7 +159,7 @@ def build_table(degree: int, lut_size: int):
     step = 2.0 / (lut_size - 1)
     nodes = -1.0 + step * np.arange(lut_size, dtype=np.float64)
     nodes[-1] = 1.0
-    values = chebyshev_rows(degree, nodes)
+    values = basis_rows(kind, degree, nodes)
     slopes = ((values[:, 1:] - values[:, :-1]) / step).astype(np.float32)
     return values, slopes, step
 
@@ -188,6 +268,11 @@ def layer_forward(x, c_doj, values, bias=None, *, tile_in=REF_TILE_IN,
         raise ValueError(f"LUT has {values.shape[0]} features, coefficients expect {n_feat}")
     batch = x.shape[0]
     planes, _ = _planes(np.tanh(x), values)
+    return _tiled_forward(planes, c, bias, batch, tile_in, tile_out, threads)
+
+
+def _tiled_forward(planes, c, bias, batch, tile_in, tile_out, threads):
+    n_feat, d_out, d_in = c.shape
     ins, outs = _tiles(d_in, tile_in), _tiles(d_out, tile_out)
     partial = np.zeros((len(outs), len(ins), batch, tile_out))
 
@@ -228,6 +313,12 @@ def layer_backward(x, c_doj, dy, values, slopes, *, include_tanh_jacobian=True,
         raise ValueError(f"dy must have shape ({batch}, {d_out}), got {dy.shape}")
     t = np.tanh(x)
     planes, slope_planes = _planes(t, values, slopes)
+    return _tiled_backward(t, planes, slope_planes, c, dy, include_tanh_jacobian, tile_in, tile_out, threads)
+
+
+def _tiled_backward(t, planes, slope_planes, c, dy, include_tanh_jacobian, tile_in, tile_out, threads):
+    n_feat, d_out, d_in = c.shape
+    batch = t.shape[0]
     ins, outs = _tiles(d_in, tile_in), _tiles(d_out, tile_out)
     dc = np.zeros_like(c)
     stage = np.zeros((len(outs), batch, d_in))
@@ -248,6 +339,30 @@ def layer_backward(x, c_doj, dy, values, slopes, *, include_tanh_jacobian=True,
     if include_tanh_jacobian:
         dx *= 1.0 - t * t
     return dc, dx, dy.sum(axis=0)
+
+
+def exact_layer_forward(x, c_doj, kind: str = "chebyshev", bias=None, *, tile_in=REF_TILE_IN,
+                        tile_out=REF_TILE_OUT, threads=1) -> np.ndarray:
+    """fused_forward in EXACT_RECURRENCE mode (kernels.py:219-224): the same
+    tiled contraction over basis_rows(kind, degree, tanh x)."""
+    x = np.asarray(x, dtype=np.float64)
+    c = np.asarray(c_doj, dtype=np.float64)
+    planes = basis_rows(kind, degree_for(kind, c.shape[0]), np.tanh(x))
+    return _tiled_forward(planes, c, bias, x.shape[0], tile_in, tile_out, threads)
+
+
+def exact_layer_backward(x, c_doj, dy, kind: str = "chebyshev", *, include_tanh_jacobian=True,
+                         tile_in=REF_TILE_IN, tile_out=REF_TILE_OUT, threads=1):
+    """backward_fused in EXACT_RECURRENCE mode: planes = basis_rows, slope
+    planes = derivative_rows at tanh x (kernels.py:222-224)."""
+    x = np.asarray(x, dtype=np.float64)
+    c = np.asarray(c_doj, dtype=np.float64)
+    t = np.tanh(x)
+    degree = degree_for(kind, c.shape[0])
+    planes = basis_rows(kind, degree, t)
+    deriv = derivative_rows(kind, degree, t)
+    return _tiled_backward(t, planes, deriv, c, np.asarray(dy, dtype=np.float64), include_tanh_jacobian,
+                           tile_in, tile_out, threads)
 
 
 def exact_forward(x, c_doj, bias=None) -> np.ndarray:

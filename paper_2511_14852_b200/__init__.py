@@ -7,21 +7,30 @@ Public surface mirrors the reference package ``polykan`` for this path:
 ``ChebyKANLayer`` and data-parallel helpers.  All compute runs in the
 sm_100a kernels of ``lib/libchebykan.so``; there is no CPU fallback.
 """
+from .basis import BasisKind, degree_for, feature_count
 from .kernels import (
+    EXACT_MODE,
     LUT_MODE,
+    AtomicCounts,
     BasisPath,
+    KernelCounters,
     KernelMode,
     NonFiniteInputError,
     PreparedCoeff,
     TileSchedule,
     backward_fused,
+    count_atomics,
     count_flops,
     fused_forward,
+    reference_backward,
+    reference_forward,
 )
-from .layer import ChebyKANFunction, ChebyKANLayer
+from .layer import ChebyKANFunction, ChebyKANLayer, KANLayer
 from .lut import (
     DEFAULT_LUT_SIZE,
+    ExactBasis,
     LutTable,
+    exact_basis,
     expand,
     interp_error_bound,
     lut_build,

@@ -30,10 +30,12 @@ SIGNATURES = {
     "ck_version": (_c_int, []),
     "ck_last_error": (ctypes.c_char_p, []),
     "ck_device_supported": (_c_int, [_c_int]),
-    "ck_lut_build": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_p)]),
-    "ck_lut_create": (_c_int, [_c_int, _c_int, _c_dp, _c_fp, _c_int, ctypes.POINTER(_c_p)]),
+    "ck_lut_build": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_p)]),
+    "ck_lut_create": (_c_int, [_c_int, _c_int, _c_int, _c_dp, _c_fp, _c_int, ctypes.POINTER(_c_p)]),
+    "ck_basis_exact": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_p)]),
     "ck_lut_destroy": (None, [_c_p]),
     "ck_lut_info": (_c_int, [_c_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), _c_dp]),
+    "ck_lut_kind": (_c_int, [_c_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)]),
     "ck_lut_read": (_c_int, [_c_p, _c_dp, _c_fp]),
     "ck_expand": (_c_int, [_c_p, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p]),
     "ck_coeff_prep_bytes": (_c_size, [_c_int, _c_int, _c_int]),

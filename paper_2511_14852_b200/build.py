@@ -25,8 +25,9 @@ HEADER = ROOT / "include" / "chebykan.h"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
-    "-Xcompiler", "-fvisibility=hidden", "-cudart", "static", "-Xptxas", "-v",
-    "-DCK_BUILD",
+    # no FMA contraction in host code: the float64 LUT build must round like numpy
+    "-Xcompiler", "-fvisibility=hidden", "-Xcompiler", "-ffp-contract=off",
+    "-cudart", "static", "-Xptxas", "-v", "-DCK_BUILD",
 ]
 
 
@@ -49,21 +50,41 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+def _compile(src: pathlib.Path, obj: pathlib.Path) -> tuple[int, str]:
+    cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-c", "-o", str(obj), str(src)]
+    res = subprocess.run(cmd, cwd=str(CSRC), capture_output=True, text=True)
+    return res.returncode, " ".join(cmd) + "\n" + res.stdout + res.stderr
+
+
 def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
+    """Compile every csrc/*.cu to an object in parallel, then link the .so."""
     if not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
+    obj_dir = LIB_DIR / "obj"
+    obj_dir.mkdir(exist_ok=True)
+    srcs = sources()
+    objs = [obj_dir / (s.stem + ".o") for s in srcs]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as pool:
+        results = list(pool.map(lambda so: _compile(*so), zip(srcs, objs)))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-shared", "-o", str(tmp),
-           *[str(s) for s in sources()], "-lcuda" if _have_libcuda() else "-ldl"]
-    res = subprocess.run(cmd, cwd=str(CSRC), capture_output=True, text=True)
-    log = (LIB_DIR / "build.log")
-    log.write_text(" ".join(cmd) + "\n\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+    link = [nvcc(), *ARCH_FLAGS, "-shared", "-cudart", "static", "-o", str(tmp), *[str(o) for o in objs],
+            "-lcuda" if _have_libcuda() else "-ldl"]
+    logs = [r[1] for r in results]
+    ok = all(r[0] == 0 for r in results)
+    if ok:
+        res = subprocess.run(link, cwd=str(CSRC), capture_output=True, text=True)
+        logs.append(" ".join(link) + "\n" + res.stdout + res.stderr)
+        ok = res.returncode == 0
+    log = LIB_DIR / "build.log"
+    log.write_text("\n\n".join(logs))
+    if not ok:
+        sys.stderr.write("\n".join(lg for r, lg in zip(results, logs) if r[0] != 0) or logs[-1])
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stdout.write(res.stderr)
+        sys.stdout.write(log.read_text())
     tmp.replace(LIB)
     return LIB
 

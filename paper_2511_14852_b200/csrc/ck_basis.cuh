@@ -1,0 +1,107 @@
+// Basis families evaluated in float32 on the device: values (basis_rows,
+// basis.py:87-119) and analytic derivatives (derivative_rows,
+// basis.py:155-204) of the Chebyshev / Legendre / Hermite / Fourier
+// families, plus the cos(k acos t) Chebyshev form (trig_rows,
+// basis.py:144-152).  P = number of non-constant features (K - 1), a
+// compile-time constant so every recurrence fully unrolls into registers.
+//
+// Used by the expansion kernels (values at the two grid nodes of a LUT cell,
+// or at t itself in exact mode) and by the exact-mode input-gradient
+// epilogue (derivatives at t).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace ck {
+
+enum BasisKindId : int { kCheb = 0, kLegendre = 1, kHermite = 2, kFourier = 3, kChebTrig = 4 };
+
+// feature_count (basis.py:24-34)
+__host__ __device__ inline int basis_features(int kind, int degree) {
+  return kind == kFourier ? 2 * degree + 1 : degree + 1;
+}
+
+// v[0..P] = B_0..B_P at x.
+template <int KIND, int P>
+__device__ __forceinline__ void basis_f32(float x, float (&v)[P + 1]) {
+  v[0] = 1.0f;
+  if constexpr (P >= 1) {
+    if constexpr (KIND == kFourier) {
+      static_assert(P % 2 == 0, "Fourier features come in cos/sin pairs");
+      float s1, c1;
+      sincospif(x, &s1, &c1);  // cos(pi x), sin(pi x)
+      v[1] = c1;
+      v[2] = s1;
+#pragma unroll
+      for (int k = 1; k < P / 2; ++k) {
+        // cos((k+1)t) = cos t cos kt - sin t sin kt; sin((k+1)t) = sin t cos kt + cos t sin kt
+        v[2 * k + 1] = fmaf(c1, v[2 * k - 1], -s1 * v[2 * k]);
+        v[2 * k + 2] = fmaf(s1, v[2 * k - 1], c1 * v[2 * k]);
+      }
+    } else if constexpr (KIND == kChebTrig) {
+      const float th = acosf(fminf(fmaxf(x, -1.0f), 1.0f));
+#pragma unroll
+      for (int k = 1; k <= P; ++k) v[k] = cosf(static_cast<float>(k) * th);
+    } else {
+      const float two_x = 2.0f * x;
+      v[1] = KIND == kHermite ? two_x : x;
+#pragma unroll
+      for (int k = 1; k < P; ++k) {
+        if constexpr (KIND == kCheb) {
+          v[k + 1] = fmaf(two_x, v[k], -v[k - 1]);  // T_{k+1} = 2x T_k - T_{k-1}
+        } else if constexpr (KIND == kLegendre) {
+          // (k+1) P_{k+1} = (2k+1) x P_k - k P_{k-1}
+          const float num = fmaf(static_cast<float>(2 * k + 1) * x, v[k], -static_cast<float>(k) * v[k - 1]);
+          v[k + 1] = num * (1.0f / static_cast<float>(k + 1));
+        } else {
+          v[k + 1] = fmaf(two_x, v[k], -static_cast<float>(2 * k) * v[k - 1]);  // H_{k+1} = 2x H_k - 2k H_{k-1}
+        }
+      }
+    }
+  }
+}
+
+// dv[0..P] = dB_k/dx at x (dv[0] = 0).  Needs the values for Legendre,
+// Hermite and Fourier; they are recomputed here (registers only).
+template <int KIND, int P>
+__device__ __forceinline__ void deriv_f32(float x, float (&dv)[P + 1]) {
+  dv[0] = 0.0f;
+  if constexpr (P >= 1) {
+    if constexpr (KIND == kCheb || KIND == kChebTrig) {
+      // T_n' = n U_{n-1}; U_0 = 1, U_1 = 2x, U_{k+1} = 2x U_k - U_{k-1}
+      const float two_x = 2.0f * x;
+      float up = 1.0f, uc = two_x;
+      dv[1] = 1.0f;
+      if constexpr (P >= 2) dv[2] = 2.0f * uc;
+#pragma unroll
+      for (int n = 3; n <= P; ++n) {
+        const float un = fmaf(two_x, uc, -up);
+        up = uc;
+        uc = un;
+        dv[n] = static_cast<float>(n) * uc;
+      }
+    } else {
+      float v[P + 1];
+      basis_f32<KIND, P>(x, v);
+      if constexpr (KIND == kLegendre) {
+        // P'_{k+1} = P'_{k-1} + (2k+1) P_k
+        dv[1] = 1.0f;
+#pragma unroll
+        for (int k = 1; k < P; ++k) dv[k + 1] = fmaf(static_cast<float>(2 * k + 1), v[k], dv[k - 1]);
+      } else if constexpr (KIND == kHermite) {
+#pragma unroll
+        for (int n = 1; n <= P; ++n) dv[n] = static_cast<float>(2 * n) * v[n - 1];  // H_n' = 2n H_{n-1}
+      } else {
+        constexpr float kPi = 3.14159265358979323846f;
+#pragma unroll
+        for (int k = 1; k <= P / 2; ++k) {
+          const float kpi = static_cast<float>(k) * kPi;
+          dv[2 * k - 1] = -kpi * v[2 * k];  // d/dx cos(k pi x)
+          dv[2 * k] = kpi * v[2 * k - 1];   // d/dx sin(k pi x)
+        }
+      }
+    }
+  }
+}
+
+}  // namespace ck

@@ -169,18 +169,6 @@ LaunchScope::~LaunchScope() {
   if (ev_) cudaEventRecord(static_cast<cudaEvent_t>(ev_), stream_);
 }
 
-int lut_source_override() {
-  static int v = [] {
-    const char* e = getenv("CK_LUT_SOURCE");
-    if (!e) return static_cast<int>(kLutAuto);
-    std::string s(e);
-    if (s == "smem") return static_cast<int>(kLutSmem);
-    if (s == "nodes") return static_cast<int>(kLutNodes);
-    return static_cast<int>(kLutAuto);
-  }();
-  return v;
-}
-
 void set_error(const std::string& msg) { g_error = msg; }
 const char* last_error() { return g_error.c_str(); }
 

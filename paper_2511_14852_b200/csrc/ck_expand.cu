@@ -1,10 +1,13 @@
-// Basis expansion kernels: T_k(tanh x) by linear interpolation in a
-// shared-memory lookup table (lut.py:97-123 semantics), plus the fused
-// input-gradient combine that uses the derivative (slope) table.
+// Basis expansion kernels: B_k(tanh x) by linear interpolation in the
+// lookup table (lut.py:97-123 semantics) or, for exact-evaluation handles,
+// by the family's recurrence at t itself (basis_rows, kernels.py:219-224);
+// plus the unfused input-gradient combine that uses the slope table or the
+// analytic derivatives (only for degrees beyond the fused GEMM epilogue).
 //
 // All kernels are HBM-bound streaming kernels: grid = a few CTAs per SM,
-// grid-stride loops, the LUT staged once per CTA in shared memory when it
-// fits (else read through L1/L2 from the position-major global copy).
+// grid-stride loops.  The GEMM operand planes are written as bf16 hi/lo
+// pairs [k-1][row][ld] with 8-byte (4-column) stores per plane.
+#include "ck_basis.cuh"
 #include "ck_common.cuh"
 #include "ck_internal.h"
 
@@ -12,8 +15,9 @@ namespace ck {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSmemLutMax = 96 * 1024;  // stage tables up to this size in smem
-constexpr int kMaxK = 64;                // planes kernels: degree <= 63
+constexpr int kSmemLutMax = 96 * 1024;  // fp32 API: stage tables up to this size in smem
+constexpr int kMaxK = 64;                // runtime-degree paths: features <= 64
+constexpr int kMaxPlanesFused = 16;      // specialized (unrolled) kernels: 1..16 planes
 
 // Fast cell choice for value interpolation (float32).  frac is formed with
 // one rounding (fma of t*h against the exact h - idx), so the interpolated
@@ -35,25 +39,129 @@ __device__ __forceinline__ float lerp_ref(float v0, float v1, float f) {
   return fmaf(v1, f, v0 * (1.0f - f));
 }
 
-template <bool kSmem>
-__device__ __forceinline__ const float* stage_table(const float* g, int count, float* s) {
-  if (!kSmem) return g;
-  for (int j = threadIdx.x; j < count; j += blockDim.x) s[j] = g[j];
-  __syncthreads();
-  return s;
+// Grid node -1 + i*step (lut.py:82-84) rounded to float32: (2i - (N-1)) / (N-1)
+// with an exact integer numerator and one correctly rounded fp32 division
+// (the FP64 pipe is too narrow on B200 to spend it here).
+__device__ __forceinline__ float grid_node_f(int i, int n) {
+  return i >= n - 1 ? 1.0f : __fdiv_rn(static_cast<float>(2 * i - (n - 1)), static_cast<float>(n - 1));
 }
 
-// phi[e][k], slopes[e][k] for element e = r*cols + c.
+// --- runtime-degree basis (generic paths) -----------------------------------
+// Streams B_1, B_2, ... at one point for a runtime kind (same recurrences as
+// basis_f32 in ck_basis.cuh).
+struct Rec {
+  int kind, k;
+  float x, prev, cur, c1, s1, cm, sm, th;
+  __device__ __forceinline__ void init(int kind_, float x_) {
+    kind = kind_;
+    x = x_;
+    k = 0;
+    prev = 0.0f;
+    cur = 1.0f;
+    if (kind == kFourier) {
+      sincospif(x, &s1, &c1);
+      cm = 1.0f;
+      sm = 0.0f;
+    } else if (kind == kChebTrig) {
+      th = acosf(fminf(fmaxf(x, -1.0f), 1.0f));
+    }
+  }
+  // B_{k+1}
+  __device__ __forceinline__ float next() {
+    float v;
+    if (kind == kFourier) {
+      // features 2m-1 = cos(m pi x), 2m = sin(m pi x)
+      if ((k & 1) == 0) {
+        const float c = fmaf(c1, cm, -s1 * sm), s = fmaf(s1, cm, c1 * sm);
+        cm = c;
+        sm = s;
+        v = cm;
+      } else {
+        v = sm;
+      }
+    } else if (kind == kChebTrig) {
+      v = cosf(static_cast<float>(k + 1) * th);
+    } else if (k == 0) {
+      v = kind == kHermite ? 2.0f * x : x;
+    } else if (kind == kCheb) {
+      v = fmaf(2.0f * x, cur, -prev);
+    } else if (kind == kLegendre) {
+      v = fmaf(static_cast<float>(2 * k + 1) * x, cur, -static_cast<float>(k) * prev) *
+          (1.0f / static_cast<float>(k + 1));
+    } else {
+      v = fmaf(2.0f * x, cur, -static_cast<float>(2 * k) * prev);
+    }
+    prev = cur;
+    cur = v;
+    ++k;
+    return v;
+  }
+};
+
+// v[0..P], dv[0..P] at x for a runtime kind / P (P < kMaxK).
+__device__ void basis_deriv_rt(int kind, int P, float x, float* v, float* dv) {
+  Rec r;
+  r.init(kind, x);
+  v[0] = 1.0f;
+  for (int k = 1; k <= P; ++k) v[k] = r.next();
+  if (dv == nullptr) return;
+  dv[0] = 0.0f;
+  if (kind == kCheb || kind == kChebTrig) {
+    float up = 1.0f, uc = 2.0f * x;
+    if (P >= 1) dv[1] = 1.0f;
+    if (P >= 2) dv[2] = 2.0f * uc;
+    for (int n = 3; n <= P; ++n) {
+      const float un = fmaf(2.0f * x, uc, -up);
+      up = uc;
+      uc = un;
+      dv[n] = static_cast<float>(n) * uc;
+    }
+  } else if (kind == kLegendre) {
+    if (P >= 1) dv[1] = 1.0f;
+    for (int k = 1; k < P; ++k) dv[k + 1] = fmaf(static_cast<float>(2 * k + 1), v[k], dv[k - 1]);
+  } else if (kind == kHermite) {
+    for (int n = 1; n <= P; ++n) dv[n] = static_cast<float>(2 * n) * v[n - 1];
+  } else {
+    constexpr float kPi = 3.14159265358979323846f;
+    for (int m = 1; 2 * m <= P; ++m) {
+      dv[2 * m - 1] = -static_cast<float>(m) * kPi * v[2 * m];
+      dv[2 * m] = static_cast<float>(m) * kPi * v[2 * m - 1];
+    }
+  }
+}
+
+template <bool kSmem>
+__device__ __forceinline__ const float* stage_table(const float* g, int count, float* s) {
+  if constexpr (!kSmem) {
+    return g;
+  } else {
+    for (int j = threadIdx.x; j < count; j += blockDim.x) s[j] = g[j];
+    __syncthreads();
+    return s;
+  }
+}
+
+// fp32 API (ck_expand): phi[e][k], slopes[e][k] for element e = r*cols + c.
+// LUT handles: float64 reference cell, table values and slopes.  Exact
+// handles: basis and derivative at float32 tanh(x).
 template <bool kSmem>
 __global__ void __launch_bounds__(kThreads) expand_f32_kernel(const float* __restrict__ x, int64_t n_elem,
                                                               LutView lut, float* __restrict__ phi,
                                                               float* __restrict__ slopes) {
   extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
-  const float* vt = stage_table<kSmem>(lut.values_pm, N * K, sm_tab);
-  const float* st = slopes ? stage_table<kSmem>(lut.slopes_pm, N * K, sm_tab + N * K) : nullptr;
+  const float* vt = lut.exact ? nullptr : stage_table<kSmem>(lut.values_pm, N * K, sm_tab);
+  const float* st = (slopes && !lut.exact) ? stage_table<kSmem>(lut.slopes_pm, N * K, sm_tab + N * K) : nullptr;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_elem;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (lut.exact) {
+      float v[kMaxK], dv[kMaxK];
+      basis_deriv_rt(lut.kind, K - 1, tanhf(x[e]), v, slopes ? dv : nullptr);
+      for (int k = 0; k < K; ++k) phi[e * K + k] = v[k];
+      if (slopes)
+        for (int k = 0; k < K; ++k) slopes[e * K + k] = dv[k];
+      continue;
+    }
     int idx;
     double frac, t;
     cell_f64(x[e], N, idx, frac, t);
@@ -67,86 +175,40 @@ __global__ void __launch_bounds__(kThreads) expand_f32_kernel(const float* __res
   }
 }
 
-// --- table columns ---------------------------------------------------------
-// Column source for the two table entries bracketing a cell.  kLutSmem reads
-// the float32 position-major table staged in shared memory; kLutNodes
-// recomputes T_k at the two grid nodes (exact float64 nodes, lut.py:83-84,
-// rounded to float32) by the recurrence T_{k+1} = 2x T_k - T_{k-1}
-// (basis.py:112-119) in float32 -- the same table entries to ~k^2 ulp, with
-// no memory traffic.  Both then interpolate v0 (1-f) + v1 f.
-// Grid node -1 + i*step (lut.py:82-84) rounded to float32: (2i - (N-1)) / (N-1)
-// with an exact integer numerator and one correctly rounded fp32 division
-// (the FP64 pipe is too narrow on B200 to spend it here).
-__device__ __forceinline__ float grid_node_f(int i, int n, double /*step*/) {
-  return i >= n - 1 ? 1.0f : __fdiv_rn(static_cast<float>(2 * i - (n - 1)), static_cast<float>(n - 1));
-}
+// --- specialized planes kernels ----------------------------------------------
+// Values of features k = 1..D at one element.  kLutNodes: the two table
+// entries bracketing the cell are recomputed at the (float32-rounded) grid
+// nodes by the family's recurrence -- the same table entries to ~k^2 ulp,
+// with no memory traffic -- then interpolated v0 (1-f) + v1 f.  kExact:
+// the basis at t = tanh(x) itself.
+enum PlaneSource : int { kSrcNodes = 0, kSrcExact = 1 };
 
-template <int kSrc>
-struct Columns {
-  // Calls emit(k, value) for k = k0..K-1 in ascending order.
-  template <typename F>
-  __device__ __forceinline__ static void run(const float* tab, int K, int n, double step, int idx, float frac, int k0,
-                                             F&& emit) {
-    if constexpr (kSrc == kLutSmem) {
-      const float* v = tab + static_cast<int64_t>(idx) * K;
-      for (int k = k0; k < K; ++k) emit(k, lerp_ref(v[k], v[k + K], frac));
-    } else {
-      const float x0 = grid_node_f(idx, n, step), x1 = grid_node_f(idx + 1, n, step);
-      const float tx0 = 2.0f * x0, tx1 = 2.0f * x1;
-      float a_prev = 1.0f, a = x0, b_prev = 1.0f, b = x1;
-      if (k0 == 0) emit(0, 1.0f);
-      if (K > 1 && k0 <= 1) emit(1, lerp_ref(x0, x1, frac));
-      for (int k = 2; k < K; ++k) {
-        const float an = fmaf(tx0, a, -a_prev), bn = fmaf(tx1, b, -b_prev);
-        a_prev = a;
-        a = an;
-        b_prev = b;
-        b = bn;
-        if (k >= k0) emit(k, lerp_ref(a, b, frac));
-      }
-    }
-  }
-};
-
-// Planes for features k = 1..D of two elements (a, b), fully unrolled:
-// out[k-1] packs (value_a, value_b) as bf16x2 hi / lo words.
-template <int kSrc, int D>
-__device__ __forceinline__ void pair_planes(const float* vt, int K, int n, double step, int ia, float fa, int ib,
-                                            float fb, uint32_t (&hw)[D], uint32_t (&lw)[D]) {
-  if constexpr (kSrc == kLutSmem) {
-    const float* pa = vt + static_cast<int64_t>(ia) * K;
-    const float* pb = vt + static_cast<int64_t>(ib) * K;
+template <int kSrc, int KIND, int D>
+__device__ __forceinline__ void elem_planes(float xv, int n, float (&out)[D]) {
+  if constexpr (kSrc == kSrcExact) {
+    float v[D + 1];
+    basis_f32<KIND, D>(tanhf(xv), v);
 #pragma unroll
-    for (int k = 1; k <= D; ++k)
-      split_pack2(lerp_ref(pa[k], pa[k + K], fa), lerp_ref(pb[k], pb[k + K], fb), hw[k - 1], lw[k - 1]);
+    for (int k = 1; k <= D; ++k) out[k - 1] = v[k];
   } else {
-    const float a0 = grid_node_f(ia, n, step), a1 = grid_node_f(ia + 1, n, step);
-    const float b0 = grid_node_f(ib, n, step), b1 = grid_node_f(ib + 1, n, step);
-    const float ta0 = 2.0f * a0, ta1 = 2.0f * a1, tb0 = 2.0f * b0, tb1 = 2.0f * b1;
-    float pa0 = 1.0f, ca0 = a0, pa1 = 1.0f, ca1 = a1, pb0 = 1.0f, cb0 = b0, pb1 = 1.0f, cb1 = b1;
-    split_pack2(lerp_ref(a0, a1, fa), lerp_ref(b0, b1, fb), hw[0], lw[0]);
+    int idx;
+    float f;
+    cell_f32(xv, n, idx, f);
+    float v0[D + 1], v1[D + 1];
+    basis_f32<KIND, D>(grid_node_f(idx, n), v0);
+    basis_f32<KIND, D>(grid_node_f(idx + 1, n), v1);
 #pragma unroll
-    for (int k = 2; k <= D; ++k) {
-      float t;
-      t = fmaf(ta0, ca0, -pa0); pa0 = ca0; ca0 = t;
-      t = fmaf(ta1, ca1, -pa1); pa1 = ca1; ca1 = t;
-      t = fmaf(tb0, cb0, -pb0); pb0 = cb0; cb0 = t;
-      t = fmaf(tb1, cb1, -pb1); pb1 = cb1; cb1 = t;
-      split_pack2(lerp_ref(ca0, ca1, fa), lerp_ref(cb0, cb1, fb), hw[k - 1], lw[k - 1]);
-    }
+    for (int k = 1; k <= D; ++k) out[k - 1] = lerp_ref(v0[k], v1[k], f);
   }
 }
 
-// Split planes k = 1..D, hi/lo [k-1][r][ld]: each thread expands 4 adjacent
+// Planes k = 1..D, hi/lo [k-1][r][ld]: each thread expands 4 adjacent
 // columns of one row (two bf16x2 pairs) and writes one 8-byte word per plane
 // for hi and lo (a warp stores 256 contiguous bytes per plane).
-template <int kSrc, int D>
+template <int kSrc, int KIND, int D>
 __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __restrict__ x, int64_t rows, int cols,
-                                                                LutView lut, uint2* __restrict__ hi,
+                                                                int lut_n, uint2* __restrict__ hi,
                                                                 uint2* __restrict__ lo, int64_t ld, int64_t plane) {
-  extern __shared__ float sm_tab[];
-  const int K = lut.K, N = lut.N;
-  const float* vt = kSrc == kLutSmem ? stage_table<true>(lut.values_pm, N * K, sm_tab) : nullptr;
   const int64_t pq = plane >> 2;  // plane stride in 8-byte words
   const int quads = (cols + 3) >> 2;
   const int64_t n_items = rows * quads;
@@ -164,13 +226,21 @@ __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __r
 #pragma unroll
       for (int e = 0; e < 4; ++e) xv[e] = c + e < cols ? __ldg(xr + e) : 0.0f;
     }
-    int id[4];
-    float fr[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) cell_f32(xv[e], N, id[e], fr[e]);
     uint32_t h0[D], l0[D], h1[D], l1[D];
-    pair_planes<kSrc, D>(vt, K, N, lut.step, id[0], fr[0], id[1], fr[1], h0, l0);
-    pair_planes<kSrc, D>(vt, K, N, lut.step, id[2], fr[2], id[3], fr[3], h1, l1);
+    {
+      float a[D], b[D];
+      elem_planes<kSrc, KIND, D>(xv[0], lut_n, a);
+      elem_planes<kSrc, KIND, D>(xv[1], lut_n, b);
+#pragma unroll
+      for (int k = 0; k < D; ++k) split_pack2(a[k], b[k], h0[k], l0[k]);
+    }
+    {
+      float a[D], b[D];
+      elem_planes<kSrc, KIND, D>(xv[2], lut_n, a);
+      elem_planes<kSrc, KIND, D>(xv[3], lut_n, b);
+#pragma unroll
+      for (int k = 0; k < D; ++k) split_pack2(a[k], b[k], h1[k], l1[k]);
+    }
     // padded columns (c+e >= cols) are written as zeros inside [cols, ld)
     const uint32_t m0 = c + 1 < cols ? 0xffffffffu : (c < cols ? 0xffffu : 0u);
     const uint32_t m1 = c + 3 < cols ? 0xffffffffu : (c + 2 < cols ? 0xffffu : 0u);
@@ -186,17 +256,15 @@ __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __r
   }
 }
 
-// Generic (any degree) fallbacks: hi/lo planes [k-k0][r][ld], two columns
-// per thread.
-template <int kSrc>
+// Generic (any degree / first feature k0 >= 1, runtime kind) planes
+// [k-k0][r][ld]: two columns per thread, features streamed by Rec at the two
+// grid nodes of each element (LUT) or at t (exact).
 __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __restrict__ x, int64_t rows,
                                                                  int cols, LutView lut, int k0,
                                                                  uint32_t* __restrict__ hi,
                                                                  uint32_t* __restrict__ lo, int64_t ld,
                                                                  int64_t plane) {
-  extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
-  const float* vt = kSrc == kLutSmem ? stage_table<true>(lut.values_pm, N * K, sm_tab) : nullptr;
   const int pairs = (cols + 1) >> 1;
   const int64_t n_items = rows * pairs;
   const int64_t pl = plane >> 1;
@@ -205,32 +273,39 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
     const int64_t r = it / pairs;
     const int c = static_cast<int>(it - r * pairs) * 2;
     const bool second = c + 1 < cols;
-    const float xa = x[r * cols + c];
-    const float xb = second ? x[r * cols + c + 1] : 0.0f;
-    int ia, ib;
-    float fa, fb;
-    cell_f32(xa, N, ia, fa);
-    cell_f32(xb, N, ib, fb);
+    const float xs[2] = {x[r * cols + c], second ? x[r * cols + c + 1] : 0.0f};
+    Rec ra[2], rb[2];
+    float fr[2];
+    for (int e = 0; e < 2; ++e) {
+      if (lut.exact) {
+        ra[e].init(lut.kind, tanhf(xs[e]));
+      } else {
+        int idx;
+        cell_f32(xs[e], N, idx, fr[e]);
+        ra[e].init(lut.kind, grid_node_f(idx, N));
+        rb[e].init(lut.kind, grid_node_f(idx + 1, N));
+      }
+    }
     uint32_t* h = hi + ((r * ld + c) >> 1);
     uint32_t* l = lo + ((r * ld + c) >> 1);
-    Columns<kSrc>::run(vt, K, N, lut.step, ia, fa, k0, [&](int k, float v) {
-      float vb2 = 0.0f;
-      if (second) {
-        // second element: recompute through the same source (rare generic path)
-        Columns<kSrc>::run(vt, K, N, lut.step, ib, fb, k, [&](int kk, float w) {
-          if (kk == k) vb2 = w;
-        });
+    for (int k = 1; k < K; ++k) {
+      float v[2];
+      for (int e = 0; e < 2; ++e) {
+        const float a = ra[e].next();
+        v[e] = lut.exact ? a : lerp_ref(a, rb[e].next(), fr[e]);
       }
+      if (k < k0) continue;
       uint32_t h2, l2;
-      split_pack2(v, vb2, h2, l2);
+      split_pack2(v[0], second ? v[1] : 0.0f, h2, l2);
       h[(k - k0) * pl] = h2;
       l[(k - k0) * pl] = l2;
-    });
+    }
   }
 }
 
-// dx = J * sum_{k>=1} slope_k * g_{k-1}  (kernels.py:430-444); the cell is
-// chosen in float64 so the piecewise-constant slope matches the reference.
+// dx = J * sum_{k>=1} slope_k * g[k-1]  (kernels.py:430-444).  LUT: the
+// cell is chosen in float64 so the piecewise-constant slope matches the
+// reference.  Exact: derivative_rows at t (kernels.py:224).
 template <bool kSmem>
 __global__ void __launch_bounds__(kThreads) dx_combine_kernel(const float* __restrict__ g, int64_t g_plane,
                                                               const float* __restrict__ x, int64_t n_elem,
@@ -238,14 +313,22 @@ __global__ void __launch_bounds__(kThreads) dx_combine_kernel(const float* __res
                                                               float* __restrict__ dx) {
   extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
-  const float* st = stage_table<kSmem>(lut.slopes_pm, N * K, sm_tab);
+  const float* st = lut.exact ? nullptr : stage_table<kSmem>(lut.slopes_pm, N * K, sm_tab);
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_elem;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = 0.0f;
+    if (lut.exact) {
+      float v[kMaxK], dv[kMaxK];
+      const float t = tanhf(x[e]);
+      basis_deriv_rt(lut.kind, K - 1, t, v, dv);
+      for (int k = 1; k < K; ++k) acc = fmaf(dv[k], g[(k - 1) * g_plane + e], acc);
+      dx[e] = jacobian ? acc * (1.0f - t * t) : acc;
+      continue;
+    }
     int idx;
     double frac, t;
     cell_f64(x[e], N, idx, frac, t);
     const float* s0 = st + static_cast<int64_t>(idx) * K;
-    float acc = 0.0f;
     for (int k = 1; k < K; ++k) acc = fmaf(s0[k], g[(k - 1) * g_plane + e], acc);
     double v = static_cast<double>(acc);
     if (jacobian) v *= 1.0 - t * t;
@@ -259,40 +342,17 @@ int grid_for(int64_t items, int per_sm) {
   return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
-}  // namespace
-
-int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi, float* slopes,
-                      cudaStream_t s) {
-  const int64_t n = rows * cols;
-  if (n == 0) return kOk;
-  const LutView v = view(lut);
-  const size_t tab = sizeof(float) * v.N * v.K * (slopes ? 2 : 1);
-  const int blocks = grid_for(n, 8);
-  LaunchScope scope(kKExpand, s);
-  if (tab <= static_cast<size_t>(kSmemLutMax)) {
-    CK_CUDA(cudaFuncSetAttribute(expand_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(tab)));
-    expand_f32_kernel<true><<<blocks, kThreads, tab, s>>>(x, n, v, phi, slopes);
-  } else {
-    expand_f32_kernel<false><<<blocks, kThreads, 0, s>>>(x, n, v, phi, slopes);
-  }
-  CK_CUDA(cudaGetLastError());
-  return kOk;
-}
-
-
-template <int kSrc>
-int launch_quads(int d, const float* x, int64_t rows, int cols, const LutView& v, uint2* h, uint2* l, int64_t ld,
-                 int64_t plane, size_t tab, int blocks, cudaStream_t s) {
-  const size_t smem = kSrc == kLutSmem ? tab : 0;
-#define CK_QUADS_CASE(D)                                                                                     \
-  case D:                                                                                                    \
-    if (smem) {                                                                                              \
-      CK_CUDA(cudaFuncSetAttribute(expand_quads_kernel<kSrc, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   static_cast<int>(smem)));                                                 \
-    }                                                                                                        \
-    expand_quads_kernel<kSrc, D><<<blocks, kThreads, smem, s>>>(x, rows, cols, v, h, l, ld, plane);          \
-    break;
+template <int kSrc, int KIND>
+int launch_quads_kind(int d, const float* x, int64_t rows, int cols, int lut_n, uint2* h, uint2* l, int64_t ld,
+                      int64_t plane, int blocks, cudaStream_t s) {
+#define CK_QUADS_CASE(D)                                                                            \
+  case D:                                                                                           \
+    if constexpr (KIND != kFourier || D % 2 == 0) {                                                 \
+      expand_quads_kernel<kSrc, KIND, D><<<blocks, kThreads, 0, s>>>(x, rows, cols, lut_n, h, l, ld, plane); \
+      break;                                                                                        \
+    } else {                                                                                        \
+      return kUnsupported;                                                                          \
+    }
   switch (d) {
     CK_QUADS_CASE(1) CK_QUADS_CASE(2) CK_QUADS_CASE(3) CK_QUADS_CASE(4) CK_QUADS_CASE(5) CK_QUADS_CASE(6)
     CK_QUADS_CASE(7) CK_QUADS_CASE(8) CK_QUADS_CASE(9) CK_QUADS_CASE(10) CK_QUADS_CASE(11) CK_QUADS_CASE(12)
@@ -305,11 +365,49 @@ int launch_quads(int d, const float* x, int64_t rows, int cols, const LutView& v
   return kOk;
 }
 
-int pick_source(size_t table_bytes) {
-  const int o = lut_source_override();
-  if (o == kLutSmem && table_bytes <= static_cast<size_t>(kSmemLutMax)) return kLutSmem;
-  // default: recompute columns (no gathers, no bank conflicts)
-  return kLutNodes;
+template <int kSrc>
+int launch_quads(const LutView& v, const float* x, int64_t rows, int cols, uint2* h, uint2* l, int64_t ld,
+                 int64_t plane, int blocks, cudaStream_t s) {
+  const int d = v.K - 1;
+  switch (v.kind) {
+    case kCheb:
+      return launch_quads_kind<kSrc, kCheb>(d, x, rows, cols, v.N, h, l, ld, plane, blocks, s);
+    case kLegendre:
+      return launch_quads_kind<kSrc, kLegendre>(d, x, rows, cols, v.N, h, l, ld, plane, blocks, s);
+    case kHermite:
+      return launch_quads_kind<kSrc, kHermite>(d, x, rows, cols, v.N, h, l, ld, plane, blocks, s);
+    case kFourier:
+      return launch_quads_kind<kSrc, kFourier>(d, x, rows, cols, v.N, h, l, ld, plane, blocks, s);
+    case kChebTrig:
+      if constexpr (kSrc == kSrcExact) {
+        return launch_quads_kind<kSrc, kChebTrig>(d, x, rows, cols, v.N, h, l, ld, plane, blocks, s);
+      }
+      return kUnsupported;
+    default:
+      return kUnsupported;
+  }
+}
+
+}  // namespace
+
+int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi, float* slopes,
+                      cudaStream_t s) {
+  const int64_t n = rows * cols;
+  if (n == 0) return kOk;
+  const LutView v = view(lut);
+  CK_CHECK(v.K <= kMaxK, "ck_expand: at most 64 features");
+  const size_t tab = v.exact ? 0 : sizeof(float) * v.N * v.K * (slopes ? 2 : 1);
+  const int blocks = grid_for(n, 8);
+  LaunchScope scope(kKExpand, s);
+  if (tab > 0 && tab <= static_cast<size_t>(kSmemLutMax)) {
+    CK_CUDA(cudaFuncSetAttribute(expand_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(tab)));
+    expand_f32_kernel<true><<<blocks, kThreads, tab, s>>>(x, n, v, phi, slopes);
+  } else {
+    expand_f32_kernel<false><<<blocks, kThreads, 0, s>>>(x, n, v, phi, slopes);
+  }
+  CK_CUDA(cudaGetLastError());
+  return kOk;
 }
 
 int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
@@ -317,28 +415,18 @@ int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* l
   if (rows == 0 || cols == 0 || k0 >= lut->n_feat) return kOk;
   CK_CHECK(ld % 2 == 0 && plane % 2 == 0, "expand_planes: pitch must be even");
   const LutView v = view(lut);
-  const size_t tab = sizeof(float) * v.N * v.K;
-  const int src = pick_source(tab);
-  auto* h = reinterpret_cast<uint32_t*>(hi);
-  auto* l = reinterpret_cast<uint32_t*>(lo);
   LaunchScope scope(kKExpand, s);
-  if (k0 == 1 && ld % 4 == 0 && plane % 4 == 0) {
-    const int d = v.K - 1;
+  if (k0 == 1 && ld % 4 == 0 && plane % 4 == 0 && v.K - 1 <= kMaxPlanesFused) {
     const int qb = grid_for(rows * ((cols + 3) / 4), 8);
     auto* h8 = reinterpret_cast<uint2*>(hi);
     auto* l8 = reinterpret_cast<uint2*>(lo);
-    const int rc = src == kLutSmem ? launch_quads<kLutSmem>(d, x, rows, cols, v, h8, l8, ld, plane, tab, qb, s)
-                                   : launch_quads<kLutNodes>(d, x, rows, cols, v, h8, l8, ld, plane, tab, qb, s);
+    const int rc = v.exact ? launch_quads<kSrcExact>(v, x, rows, cols, h8, l8, ld, plane, qb, s)
+                           : launch_quads<kSrcNodes>(v, x, rows, cols, h8, l8, ld, plane, qb, s);
     if (rc != kUnsupported) return rc;
   }
   const int blocks = grid_for(rows * ((cols + 1) / 2), 8);
-  if (src == kLutSmem) {
-    CK_CUDA(cudaFuncSetAttribute(expand_planes_kernel<kLutSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(tab)));
-    expand_planes_kernel<kLutSmem><<<blocks, kThreads, tab, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
-  } else {
-    expand_planes_kernel<kLutNodes><<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, h, l, ld, plane);
-  }
+  expand_planes_kernel<<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, reinterpret_cast<uint32_t*>(hi),
+                                                   reinterpret_cast<uint32_t*>(lo), ld, plane);
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -348,10 +436,11 @@ int launch_dx_combine(const float* g, int64_t g_plane, const float* x, int64_t r
   const int64_t n = rows * cols;
   if (n == 0) return kOk;
   const LutView v = view(lut);
-  const size_t tab = sizeof(float) * v.N * v.K;
+  CK_CHECK(!v.exact || v.K <= kMaxK, "exact input gradient: at most 64 features");
+  const size_t tab = v.exact ? 0 : sizeof(float) * v.N * v.K;
   const int blocks = grid_for(n, 8);
   LaunchScope scope(kKDxCombine, s);
-  if (tab <= static_cast<size_t>(kSmemLutMax)) {
+  if (tab > 0 && tab <= static_cast<size_t>(kSmemLutMax)) {
     CK_CUDA(cudaFuncSetAttribute(dx_combine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
     dx_combine_kernel<true><<<blocks, kThreads, tab, s>>>(g, g_plane, x, n, v, jacobian, dx);

@@ -1,0 +1,651 @@
+// tcgen05 split-precision (BF16x3) GEMM for the ChebyKAN contractions.
+//
+//   out[z][m][n] (+)= sum_{s<S} sum_r A[aseg][m][r] * B[bseg][n][r]
+//
+// A and B are each given as a bf16 (hi, lo) pair with v ~= hi + lo; per
+// 16-wide K step the single elected MMA thread issues three
+// tcgen05.mma.kind::f16 into one fp32 TMEM accumulator:
+// hi*hi + hi*lo + lo*hi (the lo*lo term is below fp32 round-off).
+//
+// Warp roles (256 threads, 1 CTA/SM):
+//   warp 0      TMA producer (one elected lane), SWIZZLE_128B K-major tiles
+//   warp 1      MMA issuer (one elected lane)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> (+bias) -> global
+// Pipelines: smem full/empty mbarrier ring (TMA <-> MMA), one tmem-full
+// barrier (MMA -> epilogue).
+#pragma once
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <string>
+
+#include "ck_basis.cuh"
+#include "ck_common.cuh"
+#include "ck_internal.h"
+
+namespace ck {
+
+// shared host helpers (ck_gemm.cu)
+int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t rows, int64_t segs, int64_t ld,
+             int64_t seg_stride, int box_rows, int bk, int mn_major = 0);
+int gemm_group();
+// fused dX GEMM with the exact-mode (analytic derivative) epilogue (ck_gemm_dx_exact.cu)
+int launch_dx_exact(const struct GemmProblem& p, cudaStream_t s);
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
+constexpr int kMaxDFused = 16;       // fused dX epilogue: degree <= 16
+
+// BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
+// or 32 (64-byte rows, SWIZZLE_64B, twice the stages for the same smem).
+// CG = CTA group: 1 (one SM per 128 x BN tile) or 2 (an SM pair per 256 x BN
+// tile; each CTA stages its 128 rows of A and half of the B rows).
+template <int BN, int BK, int STAGES, int CG = 1>
+struct Cfg {
+  static constexpr int kRowBytes = BK * 2;
+  static constexpr int kABytes = kBM * kRowBytes;   // one of hi / lo
+  static constexpr int kBBytes = (BN / CG) * kRowBytes;
+  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
+  static constexpr int kBarrierBytes = 256;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + kBarrierBytes + 1024;
+  static_assert(kSmemBytes <= 232448, "smem budget");
+};
+
+constexpr int kEpiStore = 0;  // out (+)= acc (+ bias)
+constexpr int kEpiDx = 1;     // dx = J * sum_k slope_k * acc_k (stacked B)
+
+struct KArgs {
+  int M, N;
+  int S;
+  int a_seg0, a_seg_z, b_seg0, b_seg_z;
+  int n_tile;      // output columns per CTA (BN, or n_i for the dx path)
+  int n_mma;       // MMA N (BN, or d * n_i)
+  int b_boxes;     // TMA boxes stacked along N per stage (1, or d)
+  uint32_t stage_tx;
+  // dx epilogue
+  const float* x;
+  float* dx;
+  const float* slopes_pm;
+  const float* dxrows;
+  int lutK, lutN;
+  double step;
+  float guard;
+  int jacobian;
+  int splits;      // R splits per z
+  int r_chunks;    // ceil(R / kBK)
+  int n_tiles, m_tiles, total_tiles;
+  int group_m;     // rasterisation group (m-tiles walked per n)
+  float* out;
+  long long ldo, out_z_stride, out_split_stride;
+  const float* bias0;
+  const float* bias1;
+  int accumulate;
+};
+
+// Tile decode shared by all roles (persistent static schedule: CTA c takes
+// tiles c, c + grid, ...; n fastest so co-resident CTAs share A rows in L2).
+struct TileCoord {
+  int n0, m0, z, split, c_begin, per_seg, iters;
+};
+
+// Grouped rasterisation: consecutive tiles walk kGroupM m-tiles for one n,
+// then the next n, so a wave of ~74-148 co-resident units covers a compact
+// (kGroupM x ~wave/kGroupM) block and both operands are reused from L2.
+__device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_tile_rows) {
+  TileCoord c;
+  const int nt = p.n_tiles, mt = p.m_tiles, G = p.group_m;
+  const int per_z = nt * mt;
+  const int zs = t / per_z;
+  const int r = t - zs * per_z;
+  const int group = r / (G * nt);
+  const int first_m = group * G;
+  const int gm = min(G, mt - first_m);  // last group may be short
+  const int rr = r - group * G * nt;
+  c.m0 = (first_m + rr % gm) * m_tile_rows;
+  c.n0 = (rr / gm) * p.n_tile;
+  c.z = zs / p.splits;
+  c.split = zs % p.splits;
+  c.c_begin = static_cast<int>(static_cast<long long>(c.split) * p.r_chunks / p.splits);
+  const int c_end = static_cast<int>(static_cast<long long>(c.split + 1) * p.r_chunks / p.splits);
+  c.per_seg = c_end - c.c_begin;
+  c.iters = p.S * c.per_seg;
+  return c;
+}
+
+// Fused dX epilogue for one 128-row tile, degree D (compile time): TMEM
+// column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
+// Each thread owns one row; the two warps of a TMEM lane quarter take
+// alternate 4-column blocks.  Per element: float32 tanh gives a candidate
+// cell; its dx row {lower boundary, slopes} and the next row's boundary are
+// gathered together (L2-resident table), and the rare element outside
+// [b_i, b_{i+1}) re-gathers the neighbouring row -- the exact reference cell
+// without any float64 work; then fold with the d accumulators and apply the
+// Jacobian.
+template <int D>
+__device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
+  constexpr int K = D + 1;          // dx row stride (= LUT features)
+  constexpr int W = D <= 8 ? 4 : 2;  // columns per block (register budget)
+  const int n_i = p.n_tile, N = p.lutN;
+  const float* xr = p.x + static_cast<long long>(row) * p.ldo;
+  float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
+  const bool vec = ((p.ldo & 3) == 0);
+  const float hN = 0.5f * static_cast<float>(N - 1);
+#pragma unroll 1
+  for (int cb = W * h; cb < n_i; cb += 2 * W) {
+    uint32_t r[D][W];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if constexpr (W == 4) {
+        tmem_ld_32x32b_x4(tbase + k * n_i + cb, r[k]);
+      } else {
+        tmem_ld_32x32b_x2(tbase + k * n_i + cb, r[k]);
+      }
+    }
+    const int i0 = n0 + cb;
+    float xv[W];
+    if (W == 4 && vec && row_ok && i0 + 4 <= p.N) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + i0);
+      xv[0] = v.x; xv[1] = v.y; xv[W - 2] = v.z; xv[W - 1] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < W; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
+    }
+    float t[W], acc[W];
+    float sl[W][D + 2];  // [0] = b_idx, [1..D] = slopes, [D+1] = b_{idx+1}
+    const float* rp[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
+      t[e] = tt;
+      const int c = min(static_cast<int>(fmaf(tt, hN, hN)), N - 2);
+      rp[e] = p.dxrows + static_cast<long long>(c) * K;
+#pragma unroll
+      for (int j = 0; j <= K; ++j) sl[e][j] = __ldg(rp[e] + j);  // row c and the next boundary
+    }
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      // exact reference cell: b_idx <= x < b_{idx+1}; at most one step off
+      const bool lo = xv[e] < sl[e][0], hi = !(xv[e] < sl[e][K]);
+      if (lo || hi) {
+        rp[e] += lo ? -K : K;
+#pragma unroll
+        for (int j = 0; j <= K; ++j) sl[e][j] = __ldg(rp[e] + j);
+      }
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      float a = 0.0f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) a = fmaf(sl[e][k + 1], __uint_as_float(r[k][e]), a);
+      acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
+    }
+    if (row_ok) {
+      if (W == 4 && vec && i0 + 4 <= p.N) {
+        *reinterpret_cast<float4*>(dxr + i0) = make_float4(acc[0], acc[1], acc[W - 2], acc[W - 1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < W; ++e)
+          if (i0 + e < p.N) dxr[i0 + e] = acc[e];
+      }
+    }
+  }
+}
+
+// Exact-mode input-gradient epilogue (BasisPath.EXACT_RECURRENCE): the
+// slopes are the analytic derivatives derivative_rows(kind, t)
+// (basis.py:155-204, kernels.py:224) at float32 t = tanh(x), recomputed in
+// registers; no table and no cell.
+template <int KIND, int D>
+__device__ __forceinline__ void dx_epilogue_exact(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok,
+                                                  int h) {
+  constexpr int W = D <= 8 ? 4 : 2;
+  const int n_i = p.n_tile;
+  const float* xr = p.x + static_cast<long long>(row) * p.ldo;
+  float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
+  const bool vec = ((p.ldo & 3) == 0);
+#pragma unroll 1
+  for (int cb = W * h; cb < n_i; cb += 2 * W) {
+    uint32_t r[D][W];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if constexpr (W == 4) {
+        tmem_ld_32x32b_x4(tbase + k * n_i + cb, r[k]);
+      } else {
+        tmem_ld_32x32b_x2(tbase + k * n_i + cb, r[k]);
+      }
+    }
+    const int i0 = n0 + cb;
+    float xv[W];
+    if (W == 4 && vec && row_ok && i0 + 4 <= p.N) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + i0);
+      xv[0] = v.x; xv[1] = v.y; xv[W - 2] = v.z; xv[W - 1] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < W; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
+    }
+    float acc[W];
+    float t[W];
+    float dv[W][D + 1];
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      t[e] = tanhf(xv[e]);
+      deriv_f32<KIND, D>(t[e], dv[e]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      float a = 0.0f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) a = fmaf(dv[e][k + 1], __uint_as_float(r[k][e]), a);
+      acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
+    }
+    if (row_ok) {
+      if (W == 4 && vec && i0 + 4 <= p.N) {
+        *reinterpret_cast<float4*>(dxr + i0) = make_float4(acc[0], acc[1], acc[W - 2], acc[W - 1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < W; ++e)
+          if (i0 + e < p.N) dxr[i0 + e] = acc[e];
+      }
+    }
+  }
+}
+
+// DXM: input-gradient epilogue flavour -- 0 = LUT slopes (exact reference
+// cell), 1 + kind = analytic derivatives of that basis kind.
+template <int BN, int BK, int STAGES, int EPI, int CG, int AMN, int BMN, int DXM = 0>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
+                       const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
+                       const KArgs p) {
+  using C = Cfg<BN, BK, STAGES, CG>;
+  constexpr int kRowBytes = C::kRowBytes;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2] accumulator ready (MMA -> epilogue)
+  uint64_t* tempty = tfull + 2;      // [2] accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = p.total_tiles;
+  // persistent schedule over work units (a CTA, or a CTA pair for CG = 2)
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;
+  const int row_off = static_cast<int>(rank) * kBM;  // this CTA's rows inside a pair tile
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_a_hi);
+    tma_prefetch_desc(&tm_a_lo);
+    tma_prefetch_desc(&tm_b_hi);
+    tma_prefetch_desc(&tm_b_lo);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], CG * kEpiWarps);  // one arrive per epilogue warp (of both CTAs)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    if constexpr (CG == 2) {
+      tmem_alloc_pair(tmem_slot, C::kTmemCols);
+    } else {
+      tmem_alloc(tmem_slot, C::kTmemCols);
+    }
+  }
+  tc_fence_before();
+  if constexpr (CG == 2) {
+    cluster_sync();  // barriers of both CTAs initialised before any remote signal
+  } else {
+    __syncthreads();
+  }
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      uint32_t g = 0;  // global k-iteration counter (smem ring position)
+      const int b_half = p.n_mma / CG;  // B rows this CTA stages
+      for (int t = unit; t < total; t += n_units) {
+        const TileCoord tc = decode_tile(p, t, kBM * CG);
+        for (int it = 0; it < tc.iters; ++it, ++g) {
+          const int stage = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * C::kStageBytes;
+          const int s = it / tc.per_seg;
+          const int r0 = (tc.c_begin + it % tc.per_seg) * BK;
+          const int aseg = p.a_seg0 + s + p.a_seg_z * tc.z;
+          const int bseg = p.b_seg0 + s + p.b_seg_z * tc.z;
+          const int arow = tc.m0 + row_off;
+          int brow, bz;
+          if (EPI == kEpiDx) {
+            // stacked operand: the d x n_i N tile is one box of n_mma rows (per pair)
+            brow = (tc.n0 / p.n_tile) * p.n_mma + static_cast<int>(rank) * b_half;
+            bz = 0;
+          } else {
+            brow = tc.n0 + static_cast<int>(rank) * b_half;
+            bz = bseg;
+          }
+          if constexpr (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], p.stage_tx);  // bytes of both CTAs
+          } else {
+            mbar_arrive_expect_tx(&full[stage], p.stage_tx);
+          }
+          // A: 128 rows of this CTA; B: b_half rows.  MN-major operands come
+          // as 64-wide MN slabs (8 KB each for BK = 64).
+          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, int c2) {
+            if constexpr (CG == 2) {
+              tma_load_3d_pair(dst, map, &full[stage], c0, c1, c2);
+            } else {
+              tma_load_3d(dst, map, &full[stage], c0, c1, c2);
+            }
+          };
+          if constexpr (AMN) {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j) {
+              load(st + j * 64 * kRowBytes, &tm_a_hi, arow + 64 * j, r0, aseg);
+              load(st + C::kABytes + j * 64 * kRowBytes, &tm_a_lo, arow + 64 * j, r0, aseg);
+            }
+          } else {
+            load(st, &tm_a_hi, r0, arow, aseg);
+            load(st + C::kABytes, &tm_a_lo, r0, arow, aseg);
+          }
+          if constexpr (BMN) {
+            for (int j = 0; j < b_half / 64; ++j) {
+              load(st + 2 * C::kABytes + j * 64 * kRowBytes, &tm_b_hi, brow + 64 * j, r0, bz);
+              load(st + 2 * C::kABytes + C::kBBytes + j * 64 * kRowBytes, &tm_b_lo, brow + 64 * j, r0, bz);
+            }
+          } else {
+            load(st + 2 * C::kABytes, &tm_b_hi, r0, brow, bz);
+            load(st + 2 * C::kABytes + C::kBBytes, &tm_b_lo, r0, brow, bz);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA of a pair) ----------------
+      const uint32_t idesc = umma_idesc_bf16_f32(kBM * CG, p.n_mma, AMN, BMN);
+      uint32_t g = 0, lt = 0;
+      for (int t = unit; t < total; t += n_units, ++lt) {
+        const TileCoord tc = decode_tile(p, t, kBM * CG);
+        const uint32_t acc = lt & 1, use = lt >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);  // epilogue has drained this buffer
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int it = 0; it < tc.iters; ++it, ++g) {
+          const int stage = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_hi = smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t a_lo = a_hi + C::kABytes;
+          const uint32_t b_hi = a_hi + 2 * C::kABytes;
+          const uint32_t b_lo = b_hi + C::kBBytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major: 16 bf16 = 32 bytes along the swizzled row;
+            // MN-major: 16 K-rows = 2 core groups = 2048 bytes
+            constexpr uint32_t kSlab = 64 * kRowBytes;
+            uint64_t dah, dal, dbh, dbl;
+            if constexpr (AMN) {
+              dah = umma_desc_mnmajor(a_hi + kk * 2048, kSlab);
+              dal = umma_desc_mnmajor(a_lo + kk * 2048, kSlab);
+            } else {
+              dah = umma_desc_kmajor<kRowBytes>(a_hi + kk * 32);
+              dal = umma_desc_kmajor<kRowBytes>(a_lo + kk * 32);
+            }
+            if constexpr (BMN) {
+              dbh = umma_desc_mnmajor(b_hi + kk * 2048, kSlab);
+              dbl = umma_desc_mnmajor(b_lo + kk * 2048, kSlab);
+            } else {
+              dbh = umma_desc_kmajor<kRowBytes>(b_hi + kk * 32);
+              dbl = umma_desc_kmajor<kRowBytes>(b_lo + kk * 32);
+            }
+            if constexpr (CG == 2) {
+              umma_bf16_pair(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+              umma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);
+              umma_bf16_pair(d_tmem, dal, dbh, idesc, 1u);
+            } else {
+              umma_bf16(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+              umma_bf16(d_tmem, dah, dbl, idesc, 1u);
+              umma_bf16(d_tmem, dal, dbh, idesc, 1u);
+            }
+          }
+          // frees the smem slot (in both CTAs) once these MMAs retire
+          if constexpr (CG == 2) {
+            umma_commit_pair(&empty[stage]);
+          } else {
+            umma_commit(&empty[stage]);
+          }
+        }
+        if constexpr (CG == 2) {
+          umma_commit_pair(&tfull[acc]);
+        } else {
+          umma_commit(&tfull[acc]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int h = (warp - 4) >> 2;   // which half of the tile's columns
+    uint32_t lt = 0;
+    for (int t = unit; t < total; t += n_units, ++lt) {
+      const TileCoord tc = decode_tile(p, t, kBM * CG);
+      const uint32_t acc = lt & 1, use = lt >> 1;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const int row = tc.m0 + row_off + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      if constexpr (EPI == kEpiDx) {
+        // ------------- fused dX epilogue (degree-specialized) -------------
+        if constexpr (DXM == 0) {
+          switch (p.b_boxes) {
+#define CK_DX_CASE(D) \
+  case D:             \
+    dx_epilogue<D>(p, tbase, tc.n0, row, row_ok, h); \
+    break;
+            CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
+            CK_DX_CASE(8) CK_DX_CASE(9) CK_DX_CASE(10) CK_DX_CASE(11) CK_DX_CASE(12) CK_DX_CASE(13)
+            CK_DX_CASE(14) CK_DX_CASE(15) CK_DX_CASE(16)
+#undef CK_DX_CASE
+            default:
+              break;
+          }
+        } else {
+          constexpr int KIND = DXM - 1;
+          switch (p.b_boxes) {
+#define CK_DX_CASE(D)                                                   \
+  case D:                                                               \
+    if constexpr (KIND != kFourier || D % 2 == 0) {                     \
+      dx_epilogue_exact<KIND, D>(p, tbase, tc.n0, row, row_ok, h);      \
+    }                                                                   \
+    break;
+            CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
+            CK_DX_CASE(8) CK_DX_CASE(9) CK_DX_CASE(10) CK_DX_CASE(11) CK_DX_CASE(12) CK_DX_CASE(13)
+            CK_DX_CASE(14) CK_DX_CASE(15) CK_DX_CASE(16)
+#undef CK_DX_CASE
+            default:
+              break;
+          }
+        }
+      } else {
+        // ------------- store epilogue -------------
+        float* out = p.out + static_cast<long long>(tc.z) * p.out_z_stride +
+                     static_cast<long long>(tc.split) * p.out_split_stride;
+        float* orow = out + static_cast<long long>(row) * p.ldo;
+        const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+#pragma unroll 1
+        for (int c = h * (BN / 2); c < (h + 1) * (BN / 2); c += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + c, r);
+          tmem_ld_wait();
+          const int nb = tc.n0 + c;
+          if (!row_ok || nb >= p.N) continue;
+          if (vec && nb + 32 <= p.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 o = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                     __uint_as_float(r[j + 3]));
+              if (p.bias0) {
+                const float4 bv = __ldg(reinterpret_cast<const float4*>(p.bias0 + nb + j));
+                o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
+              }
+              if (p.bias1) {
+                const float4 bv = __ldg(reinterpret_cast<const float4*>(p.bias1 + nb + j));
+                o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
+              }
+              float4* dst = reinterpret_cast<float4*>(orow + nb + j);
+              if (p.accumulate) {
+                const float4 prev = *dst;
+                o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
+              }
+              *dst = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = nb + j;
+              if (n < p.N) {
+                float o = __uint_as_float(r[j]);
+                if (p.bias0) o += p.bias0[n];
+                if (p.bias1) o += p.bias1[n];
+                if (p.accumulate) o += orow[n];
+                orow[n] = o;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) {
+          mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits on it
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
+      }
+    }
+  }
+  __syncwarp();  // reconverge the role warps before the aligned barriers
+  if constexpr (CG == 2) {
+    tc_fence_before();
+    cluster_sync();  // no CTA leaves while its peer may still signal it
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc_pair(tmem_base, C::kTmemCols);
+    }
+  } else {
+    __syncthreads();
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc(tmem_base, C::kTmemCols);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Host side: launch
+
+template <int BN, int BK, int STAGES, int EPI, int CG, int AMN = 0, int BMN = 0, int DXM = 0>
+int launch(const GemmProblem& p, int splits, float* out, long long out_split_stride, int accumulate,
+           cudaStream_t s) {
+  static_assert(!(AMN || BMN) || BK == 64, "MN-major operands use 128-byte (BK = 64) K slabs");
+  using C = Cfg<BN, BK, STAGES, CG>;
+  constexpr int kRowBytes = C::kRowBytes;
+  const int r_chunks = static_cast<int>(ceil_div(p.R, BK));
+  const int n_tile = EPI == kEpiDx ? p.dx->n_i : BN;
+  const int b_boxes = EPI == kEpiDx ? p.S : 1;
+  const int n_mma = n_tile * b_boxes;
+  CK_CHECK(n_mma % (8 * CG) == 0 && n_mma <= BN, "gemm: bad MMA N");
+  CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+  CK_CHECK(p.a.mn_major == AMN && p.b.mn_major == BMN, "gemm: operand majorness mismatch");
+  CK_TRY(make_map(&ta_hi, p.a.hi, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK, AMN));
+  CK_TRY(make_map(&ta_lo, p.a.lo, p.R, p.a.rows, p.a.segs, p.a.ld, p.a.seg_stride, kBM, BK, AMN));
+  const int b_box = n_mma / CG;  // each CTA of a pair stages half of the B rows
+  CK_CHECK(!BMN || b_box % 64 == 0, "gemm: MN-major B tile must be a multiple of 64 rows");
+  CK_TRY(make_map(&tb_hi, p.b.hi, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK, BMN));
+  CK_TRY(make_map(&tb_lo, p.b.lo, p.R, p.b.rows, p.b.segs, p.b.ld, p.b.seg_stride, b_box, BK, BMN));
+  KArgs k{};
+  k.n_tile = n_tile;
+  k.n_mma = n_mma;
+  k.b_boxes = b_boxes;
+  // bytes landing on the (leader's) full barrier per stage: A and B of all CTAs
+  k.stage_tx = static_cast<uint32_t>(CG * 2 * C::kABytes + 2 * n_mma * kRowBytes);
+  if (EPI == kEpiDx) {
+    k.x = p.dx->x;
+    k.dx = p.dx->dx;
+    k.slopes_pm = p.dx->lut.slopes_pm;
+    k.dxrows = p.dx->lut.dxrows;
+    k.lutK = p.dx->lut.K;
+    k.lutN = p.dx->lut.N;
+    k.step = p.dx->lut.step;
+    // float32 position error <= (3e-7 tanhf + ulp) * (N-1)/2; recompute in
+    // float64 inside that band
+    k.guard = fminf(0.5f, fmaxf(1e-3f, 4e-7f * static_cast<float>(p.dx->lut.N)));
+    k.jacobian = p.dx->jacobian;
+  }
+  k.M = static_cast<int>(p.a.rows);
+  k.N = static_cast<int>(EPI == kEpiDx ? p.dx->cols : p.b.rows);
+  k.S = EPI == kEpiDx ? 1 : p.S;
+  k.a_seg0 = p.a_seg0;
+  k.a_seg_z = p.a_seg_z;
+  k.b_seg0 = p.b_seg0;
+  k.b_seg_z = p.b_seg_z;
+  k.splits = splits;
+  k.r_chunks = r_chunks;
+  k.out = out;
+  k.ldo = p.ldo;
+  k.out_z_stride = p.out_z_stride;
+  k.out_split_stride = out_split_stride;
+  k.bias0 = splits == 1 ? p.bias0 : nullptr;
+  k.bias1 = splits == 1 ? p.bias1 : nullptr;
+  k.accumulate = accumulate;
+  auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    attr_set = true;
+  }
+  k.group_m = gemm_group();
+  k.n_tiles = static_cast<int>(ceil_div(k.N, n_tile));
+  k.m_tiles = static_cast<int>(ceil_div(k.M, kBM * CG));
+  const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles * p.nz * splits;
+  CK_CHECK(total < (1ll << 31), "gemm: too many tiles");
+  k.total_tiles = static_cast<int>(total);
+  const int units_max = num_sms() / CG;
+  const int units = static_cast<int>(total < units_max ? total : units_max);
+  LaunchScope scope(p.kclass, s);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(units * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CG == 2 ? 1 : 0;
+  CK_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta_hi, ta_lo, tb_hi, tb_lo, k));
+  return kOk;
+}
+
+}  // namespace
+}  // namespace ck

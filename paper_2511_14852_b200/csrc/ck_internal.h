@@ -9,9 +9,11 @@
 #include "../../include/chebykan.h"
 
 struct ck_lut {
+  int kind = 0;        // basis family (ck_basis_kind; tags of lut.py:35-40)
+  int exact = 0;       // 1: exact evaluation handle (BasisPath.EXACT_RECURRENCE), no tables
   int degree = 0;
-  int n_feat = 0;      // K = degree + 1
-  int lut_size = 0;    // N
+  int n_feat = 0;      // K = feature_count(kind, degree) (basis.py:24-34)
+  int lut_size = 0;    // N (0 for exact handles)
   double step = 0.0;   // 2 / (N - 1)
   int device = 0;
   double* values64 = nullptr;  // [K][N]   float64 build-precision table (validation)
@@ -66,17 +68,12 @@ struct LutView {
   int K;
   int N;
   double step;
+  int kind;   // ck_basis_kind
+  int exact;  // 1: evaluate the basis at t (no table)
 };
 inline LutView view(const ck_lut* l) {
-  return LutView{l->values_pm, l->slopes_pm, l->dxrows, l->n_feat, l->lut_size, l->step};
+  return LutView{l->values_pm, l->slopes_pm, l->dxrows, l->n_feat, l->lut_size, l->step, l->kind, l->exact};
 }
-
-// How the expansion kernels obtain the two table columns bracketing a cell:
-// a shared-memory copy of the table, or recomputed on the fly from the grid
-// nodes by the Chebyshev recurrence (no table traffic at all).  kAuto picks
-// smem when the table is small, else the recurrence.
-enum LutSource : int { kLutAuto = 0, kLutSmem = 1, kLutNodes = 2 };
-int lut_source_override();  // CK_LUT_SOURCE=smem|nodes (experiments), else kLutAuto
 
 // --- expansion (ck_expand.cu) ---------------------------------------------
 // phi[r][c][k] (f32) and optional slopes[r][c][k] for every k.

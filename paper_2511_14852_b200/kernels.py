@@ -16,7 +16,8 @@ from enum import Enum
 import torch
 
 from . import _lib
-from .lut import LutTable
+from .basis import BasisKind, as_kind, degree_for
+from .lut import ExactBasis, LutTable, exact_basis
 from .tensor import CoeffTensor, Layout
 
 
@@ -34,6 +35,7 @@ class KernelMode:
 
 
 LUT_MODE = KernelMode(BasisPath.LUT_INTERP)
+EXACT_MODE = KernelMode(BasisPath.EXACT_RECURRENCE)
 
 
 @dataclass(frozen=True)
@@ -74,6 +76,34 @@ class TileSchedule:
         lane_y = tile_out if lane_y is None else lane_y
         return cls(tile_in, tile_out, lane_x, lane_y, math.ceil(d_in / tile_in), math.ceil(d_out / tile_out),
                    d_in, d_out)
+
+
+@dataclass
+class KernelCounters:
+    """Merge/store counts (kernels.py:140-147).  The B200 kernels have no
+    atomics either; the counts follow the reference's closed forms for the
+    same logical reduction (one partial slot per input tile, one combine
+    store per output, one ordered x-grad merge per output tile)."""
+
+    forward_atomics: int = 0
+    partial_writes: int = 0
+    combine_stores: int = 0
+    x_grad_merges: int = 0
+
+
+@dataclass(frozen=True)
+class AtomicCounts:
+    fwd_baseline: int
+    fwd_ours: int
+    bwd_x_naive: int
+    bwd_x_ours: int
+
+
+def count_atomics(batch: int, d_in: int, d_out: int, sched: TileSchedule) -> AtomicCounts:
+    """Closed-form atomic/merge counts of the reduction strategies (kernels.py:158-167)."""
+    if min(batch, d_in, d_out) < 1:
+        raise ValueError("batch, d_in, d_out must be >= 1")
+    return AtomicCounts(batch * d_out * sched.g_x, 0, batch * d_in * d_out, batch * d_in * sched.g_y)
 
 
 class NonFiniteInputError(ValueError):
@@ -135,7 +165,7 @@ def basis_cache_bytes(batch: int, d_in: int, n_feat: int) -> int:
     return int(_lib.lib().ck_basis_cache_bytes(batch, d_in, n_feat))
 
 
-def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut: LutTable, bias: torch.Tensor | None,
+def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut, bias: torch.Tensor | None,
                 cache: torch.Tensor | None = None) -> torch.Tensor:
     """y = fused layer forward on prepared coefficients (x fp32 contiguous [B, I]).
 
@@ -153,7 +183,7 @@ def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut: LutTable, bias: torch
     return y
 
 
-def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut: LutTable, jacobian: bool,
+def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut, jacobian: bool,
                  want_dx: bool = True, want_dc: bool = True, want_db: bool = True,
                  cache: torch.Tensor | None = None):
     """(dC DOJ, dX, db) on prepared coefficients; unrequested outputs are None.
@@ -174,32 +204,52 @@ def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut: Lu
     return dc, dx, db
 
 
-def _check_common(coeff: CoeffTensor, lut: LutTable | None, sched: TileSchedule | None, mode: KernelMode,
-                  what: str) -> None:
+def _resolve_kind(lut, kind) -> BasisKind:
+    """kernels.py:186-191."""
+    if lut is not None:
+        return lut.kind
+    if kind is not None:
+        return as_kind(kind)
+    raise ValueError("exact mode without a LUT requires an explicit basis kind")
+
+
+def _basis_for(coeff: CoeffTensor, lut, sched: TileSchedule | None, mode: KernelMode, kind, what: str, device):
+    """Validate like the reference and return the device basis handle:
+    the LutTable (LUT mode) or the exact-evaluation handle (kernels.py:194-224)."""
     if coeff.layout is not Layout.DOJ:
         raise ValueError(f"{what} requires DOJ coefficient layout")
-    if mode.basis_path is not BasisPath.LUT_INTERP:
-        raise NotImplementedError("only the LUT-interpolation basis path runs on the B200 kernels")
-    if lut is None:
-        raise ValueError("LUT mode requires a LutTable")
-    if lut.n_features != coeff.n_feat:
-        raise ValueError(f"LUT has {lut.n_features} features, coefficients expect {coeff.n_feat}")
     if sched is not None and (sched.d_in != coeff.d_in or sched.d_out != coeff.d_out):
         raise ValueError("schedule dimensions do not match the coefficient tensor")
+    if mode.basis_path is BasisPath.LUT_INTERP:
+        if lut is None:
+            raise ValueError("LUT mode requires a LutTable")
+        if lut.n_features != coeff.n_feat:
+            raise ValueError(f"LUT has {lut.n_features} features, coefficients expect {coeff.n_feat}")
+        return lut
+    bkind = _resolve_kind(lut, kind)
+    dev = lut.device if lut is not None else device
+    return exact_basis(bkind, degree_for(bkind, coeff.n_feat), device=dev)
 
 
-def _device_of(coeff: CoeffTensor, lut: LutTable) -> torch.device:
-    return torch.device("cuda", lut.device)
+def _device_for(x, lut) -> torch.device:
+    if lut is not None:
+        return torch.device("cuda", lut.device)
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return x.device
+    return torch.device("cuda", torch.cuda.current_device())
 
 
-def fused_forward(x, coeff: CoeffTensor, lut: LutTable, sched: TileSchedule | None = None,
-                  mode: KernelMode = LUT_MODE, bias=None, *, validate: bool = False) -> torch.Tensor:
-    """y[b,o] = sum_j sum_k C[k,o,j] T_k(tanh x[b,j]) + bias[o]; returns (B, d_out) fp32.
+def fused_forward(x, coeff: CoeffTensor, lut, sched: TileSchedule | None = None, mode: KernelMode = LUT_MODE,
+                  bias=None, *, workers: int = 1, counters: KernelCounters | None = None, validate: bool = False,
+                  kind: BasisKind | None = None) -> torch.Tensor:
+    """y[b,o] = sum_j sum_k C[k,o,j] B_k(tanh x[b,j]) + bias[o]; returns (B, d_out) fp32.
 
-    kernels.py:351-371 (forward_partial 263-290 + combine 321-348).
+    kernels.py:351-371 (forward_partial 263-290 + combine 321-348).  ``workers``
+    is accepted for signature compatibility (the GPU kernels own the
+    parallelism).
     """
-    _check_common(coeff, lut, sched, mode, "forward_partial")
-    dev = _device_of(coeff, lut)
+    dev = _device_for(x, lut)
+    basis = _basis_for(coeff, lut, sched, mode, kind, "forward_partial", dev)
     x = _as_f32(x, dev)
     if x.dim() != 2:
         raise ValueError(f"input must be 2-D (batch, d_in), got shape {tuple(x.shape)}")
@@ -212,14 +262,20 @@ def fused_forward(x, coeff: CoeffTensor, lut: LutTable, sched: TileSchedule | No
     if validate:
         _check_finite(x)
     prep = PreparedCoeff(_as_f32(coeff.as3d(), dev))
-    return forward_raw(x, prep, lut, bias)
+    y = forward_raw(x, prep, basis, bias)
+    if counters is not None:
+        sched = sched or TileSchedule.for_dims(coeff.d_in, coeff.d_out)
+        counters.partial_writes += x.shape[0] * coeff.d_out * sched.g_x
+        counters.combine_stores += x.shape[0] * coeff.d_out
+    return y
 
 
-def backward_fused(x, coeff: CoeffTensor, dy, lut: LutTable, sched: TileSchedule | None = None,
-                   mode: KernelMode = LUT_MODE, *, validate: bool = False):
+def backward_fused(x, coeff: CoeffTensor, dy, lut, sched: TileSchedule | None = None, mode: KernelMode = LUT_MODE,
+                   *, workers: int = 1, counters: KernelCounters | None = None, validate: bool = False,
+                   kind: BasisKind | None = None):
     """(coeff_grad DOJ CoeffTensor, x_grad (B, d_in)); kernels.py:374-447."""
-    _check_common(coeff, lut, sched, mode, "backward_fused")
-    dev = _device_of(coeff, lut)
+    dev = _device_for(x, lut)
+    basis = _basis_for(coeff, lut, sched, mode, kind, "backward_fused", dev)
     x = _as_f32(x, dev)
     dy = _as_f32(dy, dev)
     if x.dim() != 2 or dy.dim() != 2:
@@ -232,13 +288,57 @@ def backward_fused(x, coeff: CoeffTensor, dy, lut: LutTable, sched: TileSchedule
         _check_finite(x)
         _check_finite(dy)
     prep = PreparedCoeff(_as_f32(coeff.as3d(), dev))
-    dc, dx, _ = backward_raw(x, dy, prep, lut, mode.include_tanh_jacobian, want_db=False)
+    dc, dx, _ = backward_raw(x, dy, prep, basis, mode.include_tanh_jacobian, want_db=False)
+    if counters is not None:
+        sched = sched or TileSchedule.for_dims(coeff.d_in, coeff.d_out)
+        counters.x_grad_merges += x.shape[0] * coeff.d_in * sched.g_y
     return CoeffTensor(coeff.d_in, coeff.d_out, coeff.degree, Layout.DOJ, dc), dx
 
 
-def count_flops(batch: int, d_in: int, d_out: int, degree: int) -> dict:
-    """Algorithmic FLOPs of one layer call."""
-    k = degree + 1
+def _exact_for(kind, n_feat: int, trig: bool, device) -> ExactBasis:
+    bkind = as_kind(kind) if kind is not None else BasisKind.CHEBYSHEV
+    if trig and bkind is not BasisKind.CHEBYSHEV:
+        raise ValueError("the trig path applies to the Chebyshev basis only")
+    return exact_basis(bkind, degree_for(bkind, n_feat), device=device, trig=trig)
+
+
+def reference_forward(x, coeff: CoeffTensor, degree: int, *, trig: bool = False,
+                      kind: BasisKind | None = None) -> torch.Tensor:
+    """Exact (table-free) evaluation, kernels.py:450-478: basis_rows (or
+    cos(n arccos t) with ``trig``) at tanh(x), contracted with JOD coefficients.
+    Runs on the B200 kernels with an exact-evaluation handle."""
+    if coeff.layout is not Layout.JOD:
+        raise ValueError("reference_forward expects JOD coefficient layout")
+    if degree != coeff.degree:
+        raise ValueError(f"degree {degree} does not match coefficients ({coeff.degree})")
+    dev = _device_for(x, None)
+    x = _as_f32(x, dev)
+    if x.dim() != 2 or x.shape[1] != coeff.d_in:
+        raise ValueError(f"input must be (batch, {coeff.d_in}), got {tuple(x.shape)}")
+    basis = _exact_for(kind, coeff.n_feat, trig, dev)
+    prep = PreparedCoeff(_as_f32(coeff.as3d().permute(2, 1, 0), dev))
+    return forward_raw(x, prep, basis, None)
+
+
+def reference_backward(x, coeff: CoeffTensor, dy, *, trig: bool = False, kind: BasisKind | None = None,
+                       include_tanh_jacobian: bool = True):
+    """Exact backward with analytic derivatives, kernels.py:481-510; returns
+    (JOD coefficient gradient, x_grad)."""
+    if coeff.layout is not Layout.JOD:
+        raise ValueError("reference_backward expects JOD coefficient layout")
+    dev = _device_for(x, None)
+    x = _as_f32(x, dev)
+    dy = _as_f32(dy, dev)
+    basis = _exact_for(kind, coeff.n_feat, trig, dev)
+    prep = PreparedCoeff(_as_f32(coeff.as3d().permute(2, 1, 0), dev))
+    dc, dx, _ = backward_raw(x, dy, prep, basis, include_tanh_jacobian, want_db=False)
+    return CoeffTensor(coeff.d_in, coeff.d_out, coeff.degree, Layout.JOD, dc.permute(2, 1, 0).contiguous()), dx
+
+
+def count_flops(batch: int, d_in: int, d_out: int, degree: int, n_feat: int | None = None) -> dict:
+    """Algorithmic FLOPs of one layer call; K = n_feat
+    (degree + 1 unless given, e.g. 2*degree + 1 for Fourier)."""
+    k = degree + 1 if n_feat is None else n_feat
     fwd = 2 * batch * d_in * d_out * k
-    bwd = 2 * batch * d_in * d_out * k + 2 * batch * d_in * d_out * degree
+    bwd = 2 * batch * d_in * d_out * k + 2 * batch * d_in * d_out * (k - 1)
     return {"fwd": fwd, "bwd": bwd, "train": fwd + bwd}

@@ -15,26 +15,34 @@ import numpy as np
 import torch
 from torch import nn
 
-from .kernels import PreparedCoeff, backward_raw, basis_cache_bytes, forward_raw
-from .lut import DEFAULT_LUT_SIZE, LutTable, lut_build
+from .basis import BasisKind, as_kind, feature_count
+from .kernels import BasisPath, PreparedCoeff, backward_raw, basis_cache_bytes, forward_raw
+from .lut import DEFAULT_LUT_SIZE, exact_basis, lut_build
 
 
 class _LayerState:
-    """Per-module LUT and coefficient-prep cache (not a parameter)."""
+    """Per-module basis handle (LUT or exact) and coefficient-prep cache (not a parameter)."""
 
-    def __init__(self, degree: int, lut_size: int, jacobian: bool, cache_basis="auto"):
+    def __init__(self, kind: BasisKind, degree: int, lut_size: int, jacobian: bool, exact: bool,
+                 cache_basis="auto"):
+        self.kind = kind
         self.degree = degree
         self.lut_size = lut_size
         self.jacobian = jacobian
+        self.exact = exact
         self.cache_basis = cache_basis
-        self._luts: dict[int, LutTable] = {}
+        self._luts: dict = {}
         self._prep: PreparedCoeff | None = None
 
-    def lut(self, device: torch.device) -> LutTable:
+    def lut(self, device: torch.device):
         idx = device.index if device.index is not None else torch.cuda.current_device()
         t = self._luts.get(idx)
         if t is None:
-            t = lut_build(self.degree, self.lut_size, device=torch.device("cuda", idx))
+            dev = torch.device("cuda", idx)
+            if self.exact:
+                t = exact_basis(self.kind, self.degree, device=dev)
+            else:
+                t = lut_build(self.kind, self.degree, self.lut_size, device=dev)
             self._luts[idx] = t
         return t
 
@@ -86,11 +94,15 @@ class ChebyKANFunction(torch.autograd.Function):
 
 
 class ChebyKANLayer(nn.Module):
-    """Chebyshev-KAN layer y = sum_i sum_k C[k,o,i] T_k(tanh x_i) + b_o.
+    """Chebyshev-KAN layer y = sum_i sum_k C[k,o,i] T_k(tanh x_i) + b_o (or any
+    basis family of the reference: ``kind``).
 
     Parameters
     ----------
     input_dim, output_dim, degree : layer shape (LayerSpec, model.py:37-54)
+    kind : basis family (BasisKind, basis.py:17-21; default Chebyshev); the
+        layer has feature_count(kind, degree) coefficient planes
+    basis_path : BasisPath.LUT_INTERP (table, default) or EXACT_RECURRENCE
     bias : learnable bias, zero-initialised (model.py:82)
     lut_size : interpolation table size (reference default 32768, lut.py:32)
     include_tanh_jacobian : KernelMode flag (kernels.py:35-44)
@@ -103,7 +115,8 @@ class ChebyKANLayer(nn.Module):
 
     def __init__(self, input_dim: int, output_dim: int, degree: int, bias: bool = True,
                  lut_size: int = DEFAULT_LUT_SIZE, include_tanh_jacobian: bool = True, seed: int | None = None,
-                 device=None, cache_basis="auto"):
+                 device=None, cache_basis="auto", kind: BasisKind = BasisKind.CHEBYSHEV,
+                 basis_path: BasisPath = BasisPath.LUT_INTERP):
         super().__init__()
         if input_dim < 1 or output_dim < 1:
             raise ValueError("layer dimensions must be >= 1")
@@ -111,15 +124,19 @@ class ChebyKANLayer(nn.Module):
             raise ValueError("degree must be >= 0")
         self.input_dim, self.output_dim, self.degree = int(input_dim), int(output_dim), int(degree)
         self.lut_size = int(lut_size)
-        k = self.degree + 1
+        self.kind = as_kind(kind)
+        self.basis_path = BasisPath(basis_path)
+        self.include_tanh_jacobian = bool(include_tanh_jacobian)
+        k = feature_count(self.kind, self.degree)
         self.coeff_doj = nn.Parameter(torch.empty((k, self.output_dim, self.input_dim), device=device))
         self.bias = nn.Parameter(torch.zeros(self.output_dim, device=device)) if bias else None
-        self._state = _LayerState(self.degree, self.lut_size, include_tanh_jacobian, cache_basis)
+        self._state = _LayerState(self.kind, self.degree, self.lut_size, self.include_tanh_jacobian,
+                                  self.basis_path is BasisPath.EXACT_RECURRENCE, cache_basis)
         self.reset_parameters(seed)
 
     @property
     def n_feat(self) -> int:
-        return self.degree + 1
+        return feature_count(self.kind, self.degree)
 
     @property
     def cheby_coeffs(self) -> torch.Tensor:
@@ -156,4 +173,9 @@ class ChebyKANLayer(nn.Module):
 
     def extra_repr(self) -> str:
         return (f"input_dim={self.input_dim}, output_dim={self.output_dim}, degree={self.degree}, "
-                f"bias={self.bias is not None}, lut_size={self.lut_size}")
+                f"kind={self.kind.value}, basis_path={self.basis_path.value}, bias={self.bias is not None}, "
+                f"lut_size={self.lut_size}")
+
+
+# The layer is basis-generic; the reference calls it a KAN layer.
+KANLayer = ChebyKANLayer

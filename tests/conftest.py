@@ -20,3 +20,12 @@ def golden_layer_cases():
 
 def golden_lut_cases():
     return sorted(p for p in GOLDEN.glob("lut_d*_n*.npz"))
+
+
+def golden_kind_cases():
+    """Other basis families (LUT mode) and the exact-evaluation path."""
+    return sorted(GOLDEN.glob("kind_*.npz"))
+
+
+def golden_kind_lut_cases():
+    return sorted(GOLDEN.glob("lutk_*.npz"))

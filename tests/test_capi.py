@@ -58,10 +58,15 @@ def test_forward_without_lut_is_a_value_error():
 def test_lut_build_argument_errors_match_reference_wording():
     lib = _lib.lib()
     h = ctypes.c_void_p()
-    assert lib.ck_lut_build(4, 1, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
+    assert lib.ck_lut_build(0, 4, 1, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
     assert "lut_size must be >= 2" in _lib.last_error()       # lut.py:78-79
-    assert lib.ck_lut_build(-1, 16, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
+    assert lib.ck_lut_build(0, -1, 16, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
     assert "degree must be >= 0" in _lib.last_error()          # lut.py:80-81
+    assert lib.ck_lut_build(7, 3, 16, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
+    assert "unsupported basis kind" in _lib.last_error()
+    # cos(k acos t) exists only as exact evaluation (trig_rows, basis.py:144-152)
+    assert lib.ck_lut_build(4, 3, 16, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
+    assert lib.ck_basis_exact(1, -2, 0, ctypes.byref(h)) == _lib.CK_INVALID_ARGUMENT
 
 
 def test_merge_rejects_bad_extents():

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import GOLDEN, golden_layer_cases, golden_lut_cases
+from conftest import GOLDEN, golden_kind_cases, golden_kind_lut_cases, golden_layer_cases, golden_lut_cases
 from oracle import chebykan_oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -36,7 +36,7 @@ def test_device_is_b200_and_library_loads():
 
 @pytest.mark.parametrize("degree,n", [(2, 3), (8, 1024), (8, 4096), (3, 512), (15, 16384), (5, 32768), (0, 16)])
 def test_lut_build_bit_identical_to_oracle(degree, n):
-    table = ck.lut_build(degree, n, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, degree, n, device=_dev())
     v, s, step = orc.build_table(degree, n)
     assert table.step == step
     assert np.array_equal(table.values, v)
@@ -48,7 +48,7 @@ def test_expand_matches_reference_interp(path):
     g = np.load(path)
     degree = int(path.stem.split("_")[1][1:])
     n = int(path.stem.split("_")[2][1:])
-    table = ck.lut_build(degree, n, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, degree, n, device=_dev())
     # feed pre-images so the kernel's tanh lands on the reference's points
     t = g["points"].astype(np.float64)
     x = np.arctanh(np.clip(t, -1 + 1e-7, 1 - 1e-7)).astype(np.float32)
@@ -64,7 +64,7 @@ def test_expand_matches_reference_interp(path):
 
 def _run_layer(g):
     degree, n = int(g["degree"]), int(g["lut_size"])
-    table = ck.lut_build(degree, n, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, degree, n, device=_dev())
     c = ck.reorder_to_doj(ck.CoeffTensor(g["x"].shape[1], g["dy"].shape[1], degree, ck.Layout.JOD,
                                           _t(g["c_jod"])))
     bias = _t(g["bias"]) if "bias" in g else None
@@ -120,7 +120,7 @@ def test_random_shapes_vs_oracle(shape):
     c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
     want_y = orc.layer_forward(x, c_doj, vals, threads=8)
     want_dc, want_dx, want_db = orc.layer_backward(x, c_doj, dy, vals, slopes, threads=8)
-    table = ck.lut_build(d, n, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=_dev())
     c = ck.CoeffTensor(i, o, d, ck.Layout.DOJ, _t(c_doj.astype(np.float32)))
     y = ck.fused_forward(_t(x), c, table).cpu().numpy()
     cg, dx = ck.backward_fused(_t(x), c, _t(dy), table)
@@ -133,7 +133,7 @@ def test_random_shapes_vs_oracle(shape):
 def test_bitwise_determinism():
     b, i, o, d = 4096, 512, 384, 6
     x, c_jod, dy = orc.bench_inputs(b, i, o, d, seed=7)
-    table = ck.lut_build(d, 4096, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, 4096, device=_dev())
     c = ck.reorder_to_doj(ck.CoeffTensor(i, o, d, ck.Layout.JOD, _t(c_jod)))
     outs = []
     for _ in range(3):
@@ -146,7 +146,7 @@ def test_bitwise_determinism():
 
 
 def test_error_paths_match_reference_wording():
-    table = ck.lut_build(2, 64, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, 2, 64, device=_dev())
     c_jod = ck.CoeffTensor(3, 2, 2, ck.Layout.JOD, torch.ones(18, device=_dev()))
     with pytest.raises(ValueError, match="DOJ"):
         ck.fused_forward(torch.zeros(1, 3, device=_dev()), c_jod, table)
@@ -155,7 +155,7 @@ def test_error_paths_match_reference_wording():
         ck.fused_forward(torch.zeros(2, 4, device=_dev()), c, table)
     with pytest.raises(ValueError, match="dy must have shape"):
         ck.backward_fused(torch.zeros(2, 3, device=_dev()), c, torch.zeros(2, 3, device=_dev()), table)
-    other = ck.lut_build(3, 64, device=_dev())
+    other = ck.lut_build(ck.BasisKind.CHEBYSHEV, 3, 64, device=_dev())
     with pytest.raises(ValueError, match="LUT has 4 features, coefficients expect 3"):
         ck.fused_forward(torch.zeros(2, 3, device=_dev()), c, other)
     x = torch.zeros(2, 3, device=_dev())
@@ -167,12 +167,12 @@ def test_error_paths_match_reference_wording():
 def test_hand_examples():
     # test_kernels.py:63-70 (LUT mode at N=32768: linear features are exact
     # up to float32): all-ones coefficients, X = [0, 10] -> 1 + (1 + tanh 10)
-    table = ck.lut_build(1, 32768, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, 1, 32768, device=_dev())
     c = ck.CoeffTensor(2, 1, 1, ck.Layout.DOJ, torch.ones(4, device=_dev()))
     y = ck.fused_forward(torch.tensor([[0.0, 10.0]], device=_dev()), c, table)
     assert abs(float(y[0, 0]) - (2.0 + np.tanh(10.0))) <= 1e-6
     # degree 0: dC = sum_b dy for every j, dX = 0 (test_kernels.py:152-162)
-    t0 = ck.lut_build(0, 16, device=_dev())
+    t0 = ck.lut_build(ck.BasisKind.CHEBYSHEV, 0, 16, device=_dev())
     c0 = ck.CoeffTensor(3, 2, 0, ck.Layout.DOJ, torch.ones(6, device=_dev()))
     x = torch.tensor([[0.1, -0.4, 2.0], [1.0, 0.0, -1.0]], device=_dev())
     dy = torch.tensor([[1.0, 2.0], [3.0, 4.0]], device=_dev())
@@ -199,7 +199,7 @@ def test_dx_cells_exact_at_cell_edges(n):
     vals, slopes, _ = orc.build_table(d, n)
     c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
     _, want_dx, _ = orc.layer_backward(x, c_doj, dy, vals, slopes)
-    table = ck.lut_build(d, n, device=_dev())
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=_dev())
     c = ck.CoeffTensor(i, o, d, ck.Layout.DOJ, _t(c_doj.astype(np.float32)))
     _, dx = ck.backward_fused(_t(x), c, _t(dy), table)
     got = dx.cpu().numpy().astype(np.float64)
@@ -209,3 +209,151 @@ def test_dx_cells_exact_at_cell_edges(n):
     big = np.abs(want_dx) > 0.05 * np.abs(want_dx).max()
     rel = np.abs(got - want_dx)[big] / np.abs(want_dx)[big]
     assert rel.max() <= 5e-4, (rel.max(), int((rel > 5e-4).sum()))
+
+
+# ---------------------------------------------------------------------------
+# Other basis families (LUT mode) and the exact-evaluation path
+
+
+@pytest.mark.parametrize("path", golden_kind_lut_cases(), ids=lambda p: p.stem)
+def test_kind_lut_build_matches_reference(path):
+    g = np.load(path)
+    kind, degree, n = str(g["kind"]), int(g["degree"]), int(g["lut_size"])
+    table = ck.lut_build(ck.BasisKind(kind), degree, n, device=_dev())
+    assert table.n_features == orc.feature_count(kind, degree)
+    v, s = table.values, table.slopes
+    cols = g["cols"]
+    if kind == "fourier":
+        # cos/sin(pi x) come from the host libm like numpy's; allow 2 ulp in
+        # case the GPU box's numpy dispatches another float64 cos/sin
+        np.testing.assert_allclose(v[:, cols], g["values"], rtol=0, atol=5e-16)
+        assert np.abs(s[:, cols[cols < n - 1]].astype(np.float64) - g["slopes"]).max() <= \
+            2 * np.spacing(np.abs(g["slopes"]).max().astype(np.float32))
+    else:
+        assert np.array_equal(v[:, cols], g["values"])
+        assert np.array_equal(s[:, cols[cols < n - 1]], g["slopes"])
+        assert np.array_equal(v.sum(axis=1), g["value_sums"])
+    # table values interpolated by the fp32 kernel (float64 reference cell)
+    t = g["points"].astype(np.float64)
+    x = np.arctanh(np.clip(t, -1 + 1e-7, 1 - 1e-7)).astype(np.float32)
+    tt = np.tanh(x.astype(np.float64))
+    want_v, want_s = orc.lut_values_and_slopes(tt, *orc.build_table(degree, n, kind)[:2])
+    phi, slopes = ck.expand(_t(x).reshape(1, -1), table, with_slopes=True)
+    k = table.n_features
+    scale = max(1.0, float(np.abs(want_v).max()))
+    assert np.abs(phi.reshape(-1, k).cpu().numpy() - want_v).max() <= 4e-6 * scale
+
+
+def _kind_layer(g, functional: bool):
+    kind, degree, exact = ck.BasisKind(str(g["kind"])), int(g["degree"]), bool(g["exact"])
+    i, o = g["x"].shape[1], g["dy"].shape[1]
+    jac = bool(g["jacobian"])
+    path = ck.BasisPath.EXACT_RECURRENCE if exact else ck.BasisPath.LUT_INTERP
+    if functional:
+        table = None if exact else ck.lut_build(kind, degree, int(g["lut_size"]), device=_dev())
+        k = ck.feature_count(kind, degree)
+        c = ck.reorder_to_doj(ck.CoeffTensor(i, o, k - 1, ck.Layout.JOD, _t(g["c_jod"])))
+        bias = _t(g["bias"]) if "bias" in g else None
+        mode = ck.KernelMode(path, include_tanh_jacobian=jac)
+        y = ck.fused_forward(_t(g["x"]), c, table, None, mode, bias, kind=kind)
+        cg, dx = ck.backward_fused(_t(g["x"]), c, _t(g["dy"]), table, None, mode, kind=kind)
+        return y.cpu().numpy(), cg.data.cpu().numpy(), dx.cpu().numpy(), None
+    layer = ck.ChebyKANLayer(i, o, degree, bias="bias" in g, lut_size=max(int(g["lut_size"]), 2),
+                             include_tanh_jacobian=jac, kind=kind, basis_path=path).to(_dev())
+    layer.load_jod(g["c_jod"])
+    if "bias" in g:
+        with torch.no_grad():
+            layer.bias.copy_(_t(g["bias"]))
+    x = _t(g["x"]).requires_grad_(True)
+    y = layer(x)
+    y.backward(_t(g["dy"]))
+    db = layer.bias.grad.cpu().numpy() if "bias" in g else None
+    return y.detach().cpu().numpy(), layer.coeff_doj.grad.cpu().numpy(), x.grad.cpu().numpy(), db
+
+
+@pytest.mark.parametrize("functional", [True, False], ids=["functional", "module"])
+@pytest.mark.parametrize("path", golden_kind_cases(), ids=lambda p: p.stem)
+def test_kind_layers_match_reference_golden(path, functional):
+    g = np.load(path)
+    y, dc, dx, db = _kind_layer(g, functional)
+    errs = {"y": orc.normwise_err(y, g["y"]), "dc": orc.normwise_err(dc, g["dc_doj"]),
+            "dx": orc.normwise_err(dx, g["dx"])}
+    if db is not None:
+        errs["db"] = orc.normwise_err(db, g["db"])
+    print(path.stem, {k: f"{v:.2e}" for k, v in errs.items()})
+    for k, e in errs.items():
+        assert e <= TOL, (k, e)
+
+
+@pytest.mark.parametrize("path", [p for p in golden_kind_cases() if "exact_chebyshev" in p.stem],
+                         ids=lambda p: p.stem)
+def test_reference_kernels_trig_match_reference(path):
+    # reference_forward / reference_backward with trig=True (kernels.py:450-510)
+    g = np.load(path)
+    i, o = g["x"].shape[1], g["dy"].shape[1]
+    degree = int(g["degree"])
+    c = ck.CoeffTensor(i, o, degree, ck.Layout.JOD, _t(g["c_jod"]))
+    y = ck.reference_forward(_t(g["x"]), c, degree, trig=True).cpu().numpy()
+    assert orc.normwise_err(y, g["y_ref_trig"]) <= TOL
+    cg, dx = ck.reference_backward(_t(g["x"]), c, _t(g["dy"]), trig=True,
+                                   include_tanh_jacobian=bool(g["jacobian"]))
+    assert cg.layout is ck.Layout.JOD
+    assert orc.normwise_err(cg.data.cpu().numpy(), g["dc_ref_trig_jod"]) <= TOL
+    assert orc.normwise_err(dx.cpu().numpy(), g["dx_ref_trig"]) <= TOL
+
+
+@pytest.mark.parametrize("kind", ["chebyshev", "legendre", "hermite", "fourier"])
+@pytest.mark.parametrize("degree", [0, 1, 3, 8, 13])
+def test_exact_expand_matches_basis_and_derivative_rows(kind, degree):
+    rng = np.random.default_rng(degree)
+    x = rng.uniform(-2.5, 2.5, 4000).astype(np.float32)
+    basis = ck.exact_basis(ck.BasisKind(kind), degree, device=_dev())
+    phi, dphi = ck.expand(_t(x).reshape(1, -1), basis, with_slopes=True)
+    t = np.tanh(x.astype(np.float64))
+    want_v = orc.basis_rows(kind, degree, t).T
+    want_d = orc.derivative_rows(kind, degree, t).T
+    k = want_v.shape[1]
+    # float32 tanh (1-2 ulp) amplified by |B_k'| and the recurrence round-off
+    assert orc.normwise_err(phi.reshape(-1, k).cpu().numpy(), want_v) <= 1e-5
+    assert orc.normwise_err(dphi.reshape(-1, k).cpu().numpy(), want_d) <= 1e-5
+
+
+@pytest.mark.parametrize("kind", ["legendre", "hermite", "fourier"])
+def test_kind_random_shapes_vs_oracle(kind):
+    # larger shapes than the golden files, through the tensor-core path
+    b, i, o, d, n = 1024, 384, 320, 4, 4096
+    k = orc.feature_count(kind, d)
+    rng = np.random.default_rng(5)
+    s = 1.0 / np.sqrt(i * k)
+    x = rng.uniform(-1.5, 1.5, (b, i)).astype(np.float32)
+    c_doj = rng.uniform(-s, s, (k, o, i)).astype(np.float32)
+    dy = rng.standard_normal((b, o)).astype(np.float32)
+    for exact in (False, True):
+        if exact:
+            wy = orc.exact_layer_forward(x, c_doj, kind, threads=8)
+            wdc, wdx, _ = orc.exact_layer_backward(x, c_doj, dy, kind, threads=8)
+            table, mode = None, ck.EXACT_MODE
+        else:
+            vals, slopes, _ = orc.build_table(d, n, kind)
+            wy = orc.layer_forward(x, c_doj, vals, threads=8)
+            wdc, wdx, _ = orc.layer_backward(x, c_doj, dy, vals, slopes, threads=8)
+            table, mode = ck.lut_build(ck.BasisKind(kind), d, n, device=_dev()), ck.LUT_MODE
+        c = ck.CoeffTensor(i, o, k - 1, ck.Layout.DOJ, _t(c_doj))
+        y = ck.fused_forward(_t(x), c, table, None, mode, kind=ck.BasisKind(kind)).cpu().numpy()
+        cg, dx = ck.backward_fused(_t(x), c, _t(dy), table, None, mode, kind=ck.BasisKind(kind))
+        e = (orc.normwise_err(y, wy), orc.normwise_err(cg.data.cpu().numpy(), wdc),
+             orc.normwise_err(dx.cpu().numpy(), wdx))
+        print(kind, "exact" if exact else "lut", [f"{v:.2e}" for v in e])
+        assert max(e) <= TOL, e
+
+
+def test_exact_mode_error_paths():
+    c = ck.CoeffTensor(3, 2, 2, ck.Layout.DOJ, torch.ones(18, device=_dev()))
+    with pytest.raises(ValueError, match="exact mode without a LUT requires an explicit basis kind"):
+        ck.fused_forward(torch.zeros(1, 3, device=_dev()), c, None, None, ck.EXACT_MODE)
+    with pytest.raises(ValueError, match="Fourier feature count must be odd"):
+        ck.fused_forward(torch.zeros(1, 3, device=_dev()), c.__class__(3, 2, 1, ck.Layout.DOJ,
+                         torch.ones(12, device=_dev())), None, None, ck.EXACT_MODE, kind=ck.BasisKind.FOURIER)
+    cj = ck.CoeffTensor(3, 2, 2, ck.Layout.JOD, torch.ones(18, device=_dev()))
+    with pytest.raises(ValueError, match="trig path applies to the Chebyshev basis only"):
+        ck.reference_forward(torch.zeros(1, 3, device=_dev()), cj, 2, trig=True, kind=ck.BasisKind.HERMITE)

@@ -14,7 +14,7 @@ b, i, o, d, n = (args + [16384, 4096, 4096, 8, 32768][len(args):])[:5]
 x = torch.rand(b, i, device=dev) * 3 - 1.5
 c = (torch.rand(d + 1, o, i, device=dev) * 2 - 1) / (i * (d + 1)) ** 0.5
 dy = torch.randn(b, o, device=dev)
-lut = ck.lut_build(d, n, device=dev)
+lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=dev)
 prep = PreparedCoeff(c)
 for _ in range(2):
     forward_raw(x, prep, lut, None)

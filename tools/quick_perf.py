@@ -17,7 +17,7 @@ def bench(b, i, o, d, n=32768, reps=5):
     s = 1 / np.sqrt(i * (d + 1))
     c = (torch.rand(d + 1, o, i, device=dev) * 2 - 1) * s
     dy = torch.randn(b, o, device=dev)
-    lut = ck.lut_build(d, n, device=dev)
+    lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=dev)
     prep = PreparedCoeff(c)
     forward_raw(x, prep, lut, None)
     backward_raw(x, dy, prep, lut, True)
