@@ -212,7 +212,7 @@ def run_ours(args, wl):
     torch.manual_seed(1234)  # identical synthetic weights on every rank
     layers = [ck.ChebyKANLayer(i, o, d, lut_size=wl["lut_size"]) for i, o in dims]
     model = (torch.nn.Sequential(*layers) if is_net else layers[0]).to(dev)
-    opt = torch.optim.Adam(model.parameters(), lr=1e-4, fused=True)
+    opt = ck.Adam(model.parameters(), lr=1e-4)  # ck_adam_step (reference adam_step rule)
     reducer = ck.GradientAllreducer(ck.chebykan_parameters(model)) if world > 1 else None
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
@@ -379,7 +379,12 @@ def run_ours(args, wl):
     gemm_alg = step_gemm * args.steps
     gemm_ms = sum(kt[c][0] for c in ("gemm_fwd", "gemm_dx", "gemm_dc"))
     gemm_tf = gemm_alg / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
-    peak_eff = peaks["bf16_sus"] / 3.0
+    # Denominator: the measured bf16 BURST figure / 3.  The kernel runs inside a
+    # long power-capped step, but the box-to-box clock under the 1 kW cap
+    # varies (1.1-1.35 GHz seen), so the pod's sustained figure (cuBLAS at the
+    # measuring pod's capped clock) can sit below what a cooler box reaches;
+    # the burst figure keeps frac <= 1 and is the conservative choice.
+    peak_eff = peaks["bf16"] / 3.0
     total_kernel_ms = sum(v[0] for v in kt.values())
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
@@ -407,8 +412,9 @@ def run_ours(args, wl):
             "bound": "tensor", "kernel": "gemm_bf16x3 (tcgen05 fwd + dX + dC, BF16x3)",
             "achieved": gemm_tf, "peak": peak_eff, "unit": "TFLOP/s", "frac": gemm_tf / peak_eff,
             "traffic": traffic,
-            "peak_basis": f"{peaks['source']} bf16 sustained {peaks['bf16_sus']} TF/s / 3 (3 bf16 MMAs per "
-                          "algorithmic fp32 MMA)",
+            "peak_basis": f"{peaks['source']} bf16 burst {peaks['bf16']} TF/s / 3 (3 bf16 MMAs per "
+                          f"algorithmic fp32 MMA); sustained {peaks['bf16_sus']} TF/s gives frac "
+                          f"{gemm_tf / (peaks['bf16_sus'] / 3.0):.3f}",
             "algorithmic_flops_per_step": step_gemm,
             "gemm_share_of_kernel_time": gemm_ms / total_kernel_ms if total_kernel_ms else None,
         },
@@ -462,12 +468,17 @@ def run_sweep(args):
             f = ev[0].elapsed_time(ev[1]) / args.steps
             bw = ev[1].elapsed_time(ev[2]) / args.steps
             fl = ck.count_flops(b, dim, dim, deg)
+            # executed GEMM flops: the T_0 == 1 folds remove one of the d+1
+            # planes from the forward and dC GEMMs
+            ex_f = 2 * b * dim * dim * deg
+            ex_t = 3 * ex_f
             peak = peaks["bf16"] / 3.0
             r = {"d_in": dim, "d_out": dim, "degree": deg, "batch": b, "fwd_ms": f, "bwd_ms": bw,
                  "fwd_samples_per_s": b / f * 1e3, "train_samples_per_s": b / (f + bw) * 1e3,
                  "fwd_alg_tflops": fl["fwd"] / f / 1e9, "train_alg_tflops": fl["train"] / (f + bw) / 1e9,
-                 "fwd_frac_of_bf16x3_burst": fl["fwd"] / f / 1e9 / peak,
-                 "train_frac_of_bf16x3_burst": fl["train"] / (f + bw) / 1e9 / peak}
+                 "fwd_exec_tflops": ex_f / f / 1e9, "train_exec_tflops": ex_t / (f + bw) / 1e9,
+                 "fwd_frac_of_bf16x3_burst": ex_f / f / 1e9 / peak,
+                 "train_frac_of_bf16x3_burst": ex_t / (f + bw) / 1e9 / peak}
             rows.append(r)
             print(json.dumps(r), flush=True)
             del x, c, dy, prep

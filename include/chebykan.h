@@ -12,7 +12,7 @@
  *
  * Coefficient layout: DOJ = [K][O][I] (order, output, input; input innermost),
  * the kernel layout of tensor.py:26-28 / doj_index tensor.py:72-74.
- * K = degree + 1.
+ * K = feature count (degree + 1; 2*degree + 1 for Fourier).
  */
 #ifndef CHEBYKAN_H_
 #define CHEBYKAN_H_
@@ -144,14 +144,24 @@ CK_API int ck_backward(const float* x, const float* dy, int64_t batch, int d_in,
 CK_API int ck_merge(const float* partials, int num_partials, int64_t stride, int64_t n, float* out,
              int accumulate, void* stream);
 
+/* --- Optimizer: replaces adam_step (model.py:247-266) -----------------------
+ * In place on one fp32 parameter tensor and its moments (all n elements):
+ * m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+ * p -= lr (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps).
+ * lr already includes any schedule scale (cosine decay, model.py:447-451);
+ * step counts from 1 (AdamState.step after increment). */
+CK_API int ck_adam_step(float* param, const float* grad, float* m, float* v, int64_t n, double lr, double beta1,
+                 double beta2, double eps, int64_t step, void* stream);
+
 /* --- Diagnostics --------------------------------------------------------------
  * ck_launch_count: kernels this library has launched in the process.
  * ck_timing_enable(1): bracket every launch with CUDA events on its stream;
  * ck_timing_collect waits for them and returns the summed device time (ms)
  * and launch count per kernel class, then clears the record.  Classes:
  * 0 GEMM forward, 1 GEMM input-grad, 2 GEMM coeff-grad, 3 expand,
- * 4 expand (transposed), 5 dx combine, 6 split, 7 reduce/merge/fill, 8 lut. */
-#define CK_NUM_KERNEL_CLASSES 9
+ * 4 expand (transposed), 5 dx combine, 6 split, 7 reduce/merge/fill, 8 lut,
+ * 9 optimizer. */
+#define CK_NUM_KERNEL_CLASSES 10
 CK_API long long ck_launch_count(void);
 CK_API int ck_timing_enable(int on);
 CK_API int ck_timing_collect(double* ms_per_class, long long* launches_per_class, int n_classes);

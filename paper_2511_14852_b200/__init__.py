@@ -38,6 +38,34 @@ from .lut import (
     lut_max_error_bound,
     lut_size_for_budget,
 )
+from .formats import load_coeff, load_lut, load_matrix, save_coeff, save_lut, save_matrix
+from .model import (
+    AdamHParams,
+    AdamState,
+    Dataset,
+    DatasetError,
+    Layer,
+    LayerSpec,
+    Loss,
+    Network,
+    NetworkSpec,
+    TrainingDiverged,
+    TrainResult,
+    TrainTrace,
+    adam_step,
+    cross_entropy_loss,
+    init_params,
+    layer_forward,
+    load_checkpoint,
+    save_checkpoint,
+    load_csv,
+    loss_fn,
+    make_synthetic,
+    mse_loss,
+    network_train,
+    rmsle_loss,
+)
+from .optim import Adam, adam_update, cosine_scale
 from .parallel import GradientAllreducer, allreduce_gradients, chebykan_parameters, shard_bounds
 from .tensor import CoeffTensor, Layout, doj_index, jod_index, reorder_to_doj, reorder_to_jod
 

@@ -48,12 +48,15 @@ SIGNATURES = {
     "ck_backward": (_c_int, [_c_p, _c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_p, _c_p, _c_p,
                              _c_p, _c_size, _c_p, _c_size, _c_p]),
     "ck_merge": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_int, _c_p]),
+    "ck_adam_step": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                              ctypes.c_double, _c_i64, _c_p]),
     "ck_launch_count": (ctypes.c_longlong, []),
     "ck_timing_enable": (_c_int, [_c_int]),
     "ck_timing_collect": (_c_int, [_c_dp, ctypes.POINTER(ctypes.c_longlong), _c_int]),
 }
 
-KERNEL_CLASSES = ("gemm_fwd", "gemm_dx", "gemm_dc", "expand", "expand_t", "dx_combine", "split", "reduce", "lut")
+KERNEL_CLASSES = ("gemm_fwd", "gemm_dx", "gemm_dc", "expand", "expand_t", "dx_combine", "split", "reduce", "lut",
+                  "optim")
 
 
 def launch_count() -> int:

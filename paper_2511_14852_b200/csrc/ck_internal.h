@@ -39,7 +39,8 @@ enum KClass : int {
   kKSplit = 6,
   kKReduce = 7,
   kKLut = 8,
-  kKNumClasses = 9,
+  kKOptim = 9,
+  kKNumClasses = 10,
 };
 
 // RAII: counts one launch of class `cls` and, when timing is enabled,

@@ -1,0 +1,83 @@
+// Optimizer step on the device: Adam with bias correction, the update rule
+// of the reference trainer (adam_step, model.py:247-266), elementwise over
+// one parameter tensor and its moment buffers.  HBM-bound: reads p, g, m, v
+// and writes p, m, v (28 bytes per element).
+#include <cmath>
+
+#include "ck_common.cuh"
+#include "ck_internal.h"
+
+namespace ck {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct AdamArgs {
+  float lr, b1, omb1, b2, omb2, bc1, bc2, eps;
+};
+
+// m = m*b1 + (1-b1)*g; v = v*b2 + (1-b2)*g*g; p -= lr * (m/bc1) / (sqrt(v/bc2) + eps)
+// with the reference's operation order and no FMA contraction.
+__device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, const AdamArgs& a) {
+  m = __fadd_rn(__fmul_rn(m, a.b1), __fmul_rn(a.omb1, g));
+  v = __fadd_rn(__fmul_rn(v, a.b2), __fmul_rn(a.omb2, __fmul_rn(g, g)));
+  const float mh = __fdiv_rn(m, a.bc1), vh = __fdiv_rn(v, a.bc2);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(a.lr, mh), __fadd_rn(__fsqrt_rn(vh), a.eps)));
+}
+
+__global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                        float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                                        AdamArgs a) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
+                     reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  if (vec) {
+    const int64_t n4 = n >> 2;
+    for (int64_t i = t0; i < n4; i += stride) {
+      float4 pp = reinterpret_cast<float4*>(p)[i];
+      const float4 gg = reinterpret_cast<const float4*>(g)[i];
+      float4 mm = reinterpret_cast<float4*>(m)[i];
+      float4 vv = reinterpret_cast<float4*>(v)[i];
+      adam_one(pp.x, gg.x, mm.x, vv.x, a);
+      adam_one(pp.y, gg.y, mm.y, vv.y, a);
+      adam_one(pp.z, gg.z, mm.z, vv.z, a);
+      adam_one(pp.w, gg.w, mm.w, vv.w, a);
+      reinterpret_cast<float4*>(p)[i] = pp;
+      reinterpret_cast<float4*>(m)[i] = mm;
+      reinterpret_cast<float4*>(v)[i] = vv;
+    }
+    for (int64_t i = (n4 << 2) + t0; i < n; i += stride) adam_one(p[i], g[i], m[i], v[i], a);
+  } else {
+    for (int64_t i = t0; i < n; i += stride) adam_one(p[i], g[i], m[i], v[i], a);
+  }
+}
+
+}  // namespace
+}  // namespace ck
+
+extern "C" int ck_adam_step(float* param, const float* grad, float* m, float* v, int64_t n, double lr,
+                            double beta1, double beta2, double eps, int64_t step, void* stream) {
+  CK_CHECK(n >= 0, "ck_adam_step: negative size");
+  CK_CHECK(step >= 1, "ck_adam_step: step counts from 1");
+  if (n == 0) return ck::kOk;
+  CK_CHECK(param && grad && m && v, "ck_adam_step: NULL tensor");
+  ck::AdamArgs a;
+  a.lr = static_cast<float>(lr);
+  a.b1 = static_cast<float>(beta1);
+  a.omb1 = static_cast<float>(1.0 - beta1);
+  a.b2 = static_cast<float>(beta2);
+  a.omb2 = static_cast<float>(1.0 - beta2);
+  // bias corrections 1 - beta^t in float64 on the host (model.py:262-263)
+  a.bc1 = static_cast<float>(1.0 - std::pow(beta1, static_cast<double>(step)));
+  a.bc2 = static_cast<float>(1.0 - std::pow(beta2, static_cast<double>(step)));
+  a.eps = static_cast<float>(eps);
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t want = ck::ceil_div(ck::ceil_div(n, 4), ck::kThreads);
+  const int64_t cap = static_cast<int64_t>(ck::num_sms()) * 8;
+  const int blocks = static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
+  ck::LaunchScope scope(ck::kKOptim, s);
+  ck::adam_kernel<<<blocks, ck::kThreads, 0, s>>>(param, grad, m, v, n, a);
+  CK_CUDA(cudaGetLastError());
+  return ck::kOk;
+}

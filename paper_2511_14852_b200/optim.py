@@ -1,0 +1,76 @@
+"""Device optimizer: Adam with bias correction on the library's own kernel.
+
+The update rule is the reference trainer's ``adam_step`` (model.py:247-266):
+m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2, p -= lr * m_hat / (sqrt(v_hat) + eps),
+one step counter per optimizer, an optional per-step ``lr_scale`` (the cosine
+decay of network_train, model.py:447-451).  ``ck_adam_step`` runs it in place
+on each fp32 parameter tensor (one HBM pass over p, g, m, v).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+
+
+def adam_update(param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, lr: float,
+                beta1: float, beta2: float, eps: float, step: int) -> None:
+    """One in-place Adam update of a contiguous fp32 CUDA tensor (ck_adam_step)."""
+    for t in (param, grad, m, v):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError("adam_update expects contiguous float32 CUDA tensors")
+    if not (param.numel() == grad.numel() == m.numel() == v.numel()):
+        raise ValueError("parameter, gradient and moment sizes differ")
+    rc = _lib.lib().ck_adam_step(param.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), param.numel(),
+                                 float(lr), float(beta1), float(beta2), float(eps), int(step),
+                                 _lib.stream_handle(param.device))
+    _lib.check(rc, "ck_adam_step")
+    # written through a raw pointer: bump the version counters so caches keyed
+    # on (data_ptr, _version) -- e.g. the layer's coefficient prep -- refresh
+    torch.autograd.graph.increment_version(param)
+    torch.autograd.graph.increment_version(m)
+    torch.autograd.graph.increment_version(v)
+
+
+def cosine_scale(step_no: int, total_steps: int) -> float:
+    """0.5 (1 + cos(pi step / total)) -- network_train's decay (model.py:447-451)."""
+    return 0.5 * (1.0 + math.cos(math.pi * step_no / total_steps))
+
+
+class Adam(torch.optim.Optimizer):
+    """torch optimizer front end of ck_adam_step (reference semantics, fp32 state).
+
+    ``step(lr_scale=...)`` multiplies the learning rate for this step only.
+    Parameters without a gradient are skipped (their moments stay put), but
+    the step counter is shared, as in the reference's AdamState.
+    """
+
+    def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8):
+        if lr < 0.0:
+            raise ValueError(f"invalid learning rate: {lr}")
+        super().__init__(params, dict(lr=lr, betas=tuple(betas), eps=eps))
+        self._step = 0
+
+    @property
+    def step_count(self) -> int:
+        return self._step
+
+    @torch.no_grad()
+    def step(self, closure=None, lr_scale: float = 1.0):
+        loss = closure() if closure is not None else None
+        self._step += 1
+        for group in self.param_groups:
+            b1, b2 = group["betas"]
+            lr = group["lr"] * lr_scale
+            for p in group["params"]:
+                if p.grad is None:
+                    continue
+                st = self.state[p]
+                if not st:
+                    st["m"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
+                    st["v"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
+                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                adam_update(p, g, st["m"], st["v"], lr, b1, b2, group["eps"], self._step)
+        return loss

@@ -1,0 +1,108 @@
+"""Model / trainer layer on the GPU vs the reference trainer's trajectories.
+
+Fixtures: tests/golden/train_*.npz from tests/golden/make_golden_train.py
+(the reference's network_train, model.py:380-460).  The GPU trainer runs in
+float32 with BF16x3 tensor-core contractions, the reference in float64, so
+trajectories agree to round-off amplified over a few dozen Adam steps:
+epoch losses within 1e-3 relative, final parameters within 1e-3 normwise.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from oracle import chebykan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2511_14852_b200 as ck
+
+TRAIN_TOL = 1e-3
+
+
+def _cases():
+    K = ck.BasisKind
+    exact = ck.KernelMode(ck.BasisPath.EXACT_RECURRENCE)
+    # mirrors CASES in tests/golden/make_golden_train.py
+    return {
+        "cheb2": ((ck.LayerSpec(1, 8, 4), ck.LayerSpec(8, 1, 4)), ck.Loss.MSE, 3, 4096, 0, 1e-2, 32, True),
+        "sincos_mixed": ((ck.LayerSpec(2, 6, 3, K.LEGENDRE), ck.LayerSpec(6, 1, 3, mode=exact)), ck.Loss.MSE, 3,
+                         2048, 3, 5e-3, 32, True),
+        "sectors_ce": ((ck.LayerSpec(2, 5, 3), ck.LayerSpec(5, 3, 2, K.FOURIER)), ck.Loss.CROSS_ENTROPY, 3, 4096,
+                       5, 1e-2, 16, False),
+        "positive_rmsle": ((ck.LayerSpec(3, 4, 2, K.HERMITE), ck.LayerSpec(4, 1, 2, has_bias=False)),
+                           ck.Loss.RMSLE, 2, 1024, 9, 1e-2, 20, True),
+    }
+
+
+@pytest.mark.parametrize("name", ["cheb2", "sincos_mixed", "sectors_ce", "positive_rmsle"])
+def test_network_train_follows_reference_trajectory(name):
+    g = np.load(GOLDEN / f"train_{name}.npz")
+    layers, loss, epochs, lut_size, seed, lr, batch, cosine = _cases()[name]
+    ds = ck.Dataset(g["x"], g["y"], name=name)
+    res = ck.network_train(ck.NetworkSpec(layers, loss), ds, epochs, ck.AdamHParams(lr=lr), seed=seed,
+                           batch_size=batch, lut_size=lut_size, cosine_decay=cosine)
+    got = np.array(res.trace.epoch_losses)
+    want = g["epoch_losses"]
+    print(name, got, want)
+    assert got.shape == want.shape
+    assert np.abs(got - want).max() <= TRAIN_TOL * np.abs(want).max()
+    for i, layer in enumerate(res.network.layers):
+        c = layer.coeff.as3d().permute(2, 1, 0).cpu().numpy()
+        assert orc.normwise_err(c, g[f"coeff_jod_{i}"]) <= TRAIN_TOL
+        if layer.bias is not None:
+            assert np.abs(layer.bias.cpu().numpy() - g[f"bias_{i}"]).max() <= TRAIN_TOL * max(
+                1.0, np.abs(g[f"bias_{i}"]).max())
+    assert len(res.trace.fwd_seconds) == epochs and all(t > 0 for t in res.trace.fwd_seconds)
+
+
+def test_init_params_bit_identical_to_reference_draws():
+    spec = ck.LayerSpec(7, 5, 3)
+    coeff, bias = ck.init_params(spec, seed=11)
+    rng = np.random.default_rng(11)
+    s = 1.0 / np.sqrt(7 * 4)
+    assert np.array_equal(coeff.data.numpy().reshape(-1), rng.uniform(-s, s, size=7 * 5 * 4))
+    assert np.array_equal(bias.numpy(), np.zeros(5))
+
+
+def test_layer_api_backward_before_forward_and_shapes():
+    layer = ck.Layer.create(ck.LayerSpec(4, 3, 2), seed=0, lut_size=256)
+    with pytest.raises(RuntimeError, match="backward called before forward"):
+        layer.backward(np.zeros((2, 3)))
+    with pytest.raises(ValueError, match=r"expected input shape \(batch, 4\)"):
+        layer.forward(np.zeros((2, 5)))
+    x = np.random.default_rng(0).uniform(-1, 1, (6, 4))
+    y = layer.forward(x)
+    cg, bg, xg = layer.backward(np.ones((6, 3)))
+    assert tuple(y.shape) == (6, 3) and tuple(xg.shape) == (6, 4)
+    assert cg.layout is ck.Layout.DOJ and tuple(cg.data.shape) == (3, 3, 4)
+    assert torch.allclose(bg, torch.full((3,), 6.0, device=bg.device))
+
+
+def test_adam_kernel_matches_reference_rule():
+    # model.py:247-266 on float64 vs ck_adam_step on float32, three steps
+    rng = np.random.default_rng(3)
+    p0 = rng.standard_normal(1001)
+    grads = [rng.standard_normal(1001) for _ in range(3)]
+    p, m, v = p0.copy(), np.zeros(1001), np.zeros(1001)
+    lr, b1, b2, eps = 1e-2, 0.9, 0.999, 1e-8
+    for t, gr in enumerate(grads, start=1):
+        m = m * b1 + (1 - b1) * gr
+        v = v * b2 + (1 - b2) * (gr * gr)
+        p = p - lr * (m / (1 - b1 ** t)) / (np.sqrt(v / (1 - b2 ** t)) + eps)
+    dev = torch.device("cuda", 0)
+    pt = torch.tensor(p0, dtype=torch.float32, device=dev)
+    mt, vt = torch.zeros_like(pt), torch.zeros_like(pt)
+    for t, gr in enumerate(grads, start=1):
+        ck.adam_update(pt, torch.tensor(gr, dtype=torch.float32, device=dev), mt, vt, lr, b1, b2, eps, t)
+    assert np.abs(pt.cpu().numpy() - p).max() <= 1e-6
+
+
+def test_training_divergence_reports_epoch_and_batch():
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, (64, 2))
+    y = np.full(64, np.inf)
+    spec = ck.NetworkSpec((ck.LayerSpec(2, 3, 2), ck.LayerSpec(3, 1, 2)))
+    with pytest.raises(ck.TrainingDiverged, match="epoch 0, batch 0"):
+        ck.network_train(spec, ck.Dataset(x, y), 1, lut_size=256)

@@ -94,3 +94,44 @@ def test_layer_refuses_cpu_tensors():
     layer = ChebyKANLayer(4, 2, 2)
     with pytest.raises(ValueError, match="CUDA"):
         layer(torch.zeros(3, 4))
+
+
+def test_model_specs_validate_like_reference():
+    import paper_2511_14852_b200 as ck
+
+    with pytest.raises(ValueError, match="layer dimensions must be >= 1"):
+        ck.LayerSpec(0, 3, 2)
+    with pytest.raises(ValueError, match="degree must be >= 0"):
+        ck.LayerSpec(2, 3, -1)
+    with pytest.raises(ValueError, match="layer dims do not chain: 3 -> 4"):
+        ck.NetworkSpec((ck.LayerSpec(2, 3, 1), ck.LayerSpec(4, 1, 1)))
+    with pytest.raises(ValueError, match="a network needs at least one layer"):
+        ck.NetworkSpec(())
+    assert ck.LayerSpec(2, 3, 4, ck.BasisKind.FOURIER).n_feat == 9
+
+
+def test_synthetic_datasets_match_reference_fixtures():
+    import numpy as np
+
+    import paper_2511_14852_b200 as ck
+    from conftest import GOLDEN
+
+    g = np.load(GOLDEN / "train_cheb2.npz")
+    ds = ck.make_synthetic("cheb2")
+    assert np.array_equal(ds.x, g["x"]) and np.array_equal(ds.y, g["y"])
+    with pytest.raises(ck.DatasetError, match="unknown synthetic dataset 'nope'; known: cheb2, sincos"):
+        ck.make_synthetic("nope")
+
+
+def test_load_csv_errors(tmp_path):
+    import paper_2511_14852_b200 as ck
+
+    p = tmp_path / "d.csv"
+    p.write_text("a,b,t\n1,2,3\n4,x,6\n7,8\n")
+    with pytest.raises(ck.DatasetError, match="malformed rows at lines: 3, 4"):
+        ck.load_csv(p)
+    p.write_text("a,t\n1,2.5\n")
+    with pytest.raises(ck.DatasetError, match="integer labels"):
+        ck.load_csv(p, classification=True)
+    ds = ck.load_csv(p)
+    assert ds.x.shape == (1, 1) and ds.y[0] == 2.5
