@@ -116,9 +116,10 @@ CK_API int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int n_f
  * x [B][I], y [B][O]; bias nullable.  Workspace: ck_forward_workspace_bytes.
  * basis_cache (nullable, ck_basis_cache_bytes): when given, the forward keeps
  * the expanded basis planes there and ck_backward reuses them (the backward of
- * the same x then skips the expansion). */
+ * the same x then skips the expansion).  0 bytes = the layer does not use
+ * basis planes (d_out <= 8 runs on the CUDA-core skinny kernels). */
 CK_API size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
-CK_API size_t ck_basis_cache_bytes(int64_t batch, int d_in, int n_feat);
+CK_API size_t ck_basis_cache_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
                const float* bias, float* y, void* workspace, size_t workspace_bytes, void* basis_cache,
                size_t basis_cache_bytes, void* stream);
@@ -160,8 +161,8 @@ CK_API int ck_adam_step(float* param, const float* grad, float* m, float* v, int
  * and launch count per kernel class, then clears the record.  Classes:
  * 0 GEMM forward, 1 GEMM input-grad, 2 GEMM coeff-grad, 3 expand,
  * 4 expand (transposed), 5 dx combine, 6 split, 7 reduce/merge/fill, 8 lut,
- * 9 optimizer. */
-#define CK_NUM_KERNEL_CLASSES 10
+ * 9 optimizer, 10 skinny-output layer (d_out <= 8, CUDA cores). */
+#define CK_NUM_KERNEL_CLASSES 11
 CK_API long long ck_launch_count(void);
 CK_API int ck_timing_enable(int on);
 CK_API int ck_timing_collect(double* ms_per_class, long long* launches_per_class, int n_classes);

@@ -41,7 +41,7 @@ SIGNATURES = {
     "ck_coeff_prep_bytes": (_c_size, [_c_int, _c_int, _c_int]),
     "ck_coeff_prepare": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_p, _c_size, _c_p]),
     "ck_forward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
-    "ck_basis_cache_bytes": (_c_size, [_c_i64, _c_int, _c_int]),
+    "ck_basis_cache_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
     "ck_forward": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p, _c_size,
                             _c_p]),
     "ck_backward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
@@ -56,7 +56,7 @@ SIGNATURES = {
 }
 
 KERNEL_CLASSES = ("gemm_fwd", "gemm_dx", "gemm_dc", "expand", "expand_t", "dx_combine", "split", "reduce", "lut",
-                  "optim")
+                  "optim", "skinny")
 
 
 def launch_count() -> int:

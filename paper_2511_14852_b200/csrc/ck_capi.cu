@@ -26,8 +26,19 @@ struct PrepLayout {
   int64_t ldI, ldO;
   int n_i;             // inputs per stacked tile (0: DJO layout)
   int64_t dxb_rows;    // rows of the input-gradient operand
+  bool skinny;         // d_out <= 8: only an fp32 DOJ copy at offset 0
   size_t doj_hi, doj_lo, dxb_hi, dxb_lo, c0sum, total;
   PrepLayout(int I, int O, int K) {
+    skinny = skinny_layer(I, O, K);
+    if (skinny) {
+      ldI = I;
+      ldO = O;
+      n_i = 0;
+      dxb_rows = 0;
+      doj_hi = doj_lo = dxb_hi = dxb_lo = c0sum = 0;
+      total = align_up(sizeof(float) * K * O * static_cast<size_t>(I));
+      return;
+    }
     ldI = round_up(I, 8);
     ldO = round_up(O, 8);
     const int d = K - 1;
@@ -80,7 +91,7 @@ struct FwdLayout {
   }
 };
 
-constexpr int kDbSlots = 32;
+constexpr int kDbSlots = 64;  // bias-gradient row blocks per chunk
 
 struct BwdLayout {
   int64_t chunk, n_chunks, ldO;
@@ -259,6 +270,10 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
   auto s = static_cast<cudaStream_t>(stream);
   const ck::PrepLayout L(d_in, d_out, n_feat);
   const int64_t I = d_in, O = d_out, K = n_feat;
+  if (L.skinny) {
+    CK_CUDA(cudaMemcpyAsync(ck::at<float>(prep, 0), coeff_doj, sizeof(float) * K * O * I, cudaMemcpyDeviceToDevice, s));
+    return kOk;
+  }
   // DOJ copies: rows (k,o), unit stride in i
   CK_TRY(ck::launch_split_rows(coeff_doj, 1, K * O, I, 0, ck::at<__nv_bfloat16>(prep, L.doj_hi),
                                ck::at<__nv_bfloat16>(prep, L.doj_lo), L.ldI, 0, s));
@@ -278,11 +293,13 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
 
 extern "C" size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat) {
   if (d_in < 1 || d_out < 1 || n_feat < 1 || batch < 0) return 0;
+  if (ck::skinny_layer(d_in, d_out, n_feat)) return ck::kAlign;
   return ck::FwdLayout(batch, d_in, d_out, n_feat).total;
 }
 
-extern "C" size_t ck_basis_cache_bytes(int64_t batch, int d_in, int n_feat) {
-  if (d_in < 1 || n_feat < 1 || batch < 0) return 0;
+extern "C" size_t ck_basis_cache_bytes(int64_t batch, int d_in, int d_out, int n_feat) {
+  if (d_in < 1 || d_out < 1 || n_feat < 1 || batch < 0) return 0;
+  if (ck::skinny_layer(d_in, d_out, n_feat)) return 0;
   return ck::BasisLayout(batch, d_in, n_feat).total;
 }
 
@@ -292,6 +309,11 @@ extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, co
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
   CK_CHECK(x != nullptr && y != nullptr && prep != nullptr, "ck_forward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
+  if (ck::skinny_layer(d_in, d_out, K)) {
+    // d_out <= 8: CUDA-core dot products on the fp32 copy in prep
+    return ck::launch_skinny_forward(x, batch, d_in, d_out, ck::at<float>(const_cast<void*>(prep), 0), bias, lut, y,
+                                     static_cast<cudaStream_t>(stream));
+  }
   const ck::FwdLayout W(batch, d_in, d_out, K);
   const ck::BasisLayout L(batch, d_in, K);
   if (workspace_bytes < W.total) {
@@ -341,8 +363,25 @@ extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, co
   return kOk;
 }
 
+namespace ck {
+namespace {
+// skinny backward workspace: part_c [slots][K][O][I] float, part_b [slots][O] double
+struct SkinnyBwdLayout {
+  int slots;
+  size_t part_c, part_b, total;
+  SkinnyBwdLayout(int64_t B, int I, int O, int K) {
+    slots = skinny_slots(B, I);
+    part_c = 0;
+    part_b = align_up(sizeof(float) * slots * static_cast<size_t>(K) * O * I);
+    total = part_b + align_up(sizeof(double) * slots * O) + kAlign;
+  }
+};
+}  // namespace
+}  // namespace ck
+
 extern "C" size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat) {
   if (d_in < 1 || d_out < 1 || n_feat < 1 || batch < 0) return 0;
+  if (ck::skinny_layer(d_in, d_out, n_feat)) return ck::SkinnyBwdLayout(batch, d_in, d_out, n_feat).total;
   return ck::BwdLayout(batch, d_in, d_out, n_feat).total;
 }
 
@@ -353,6 +392,28 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
   CK_CHECK(x != nullptr && dy != nullptr && prep != nullptr, "ck_backward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
+  if (ck::skinny_layer(d_in, d_out, K)) {
+    auto s = static_cast<cudaStream_t>(stream);
+    const ck::SkinnyBwdLayout SW(batch, d_in, d_out, K);
+    if (workspace_bytes < SW.total) {
+      ck::set_error("backward workspace too small: need " + std::to_string(SW.total) + " bytes");
+      return ck::kWorkspace;
+    }
+    const int64_t n = static_cast<int64_t>(K) * d_out * d_in;
+    if (batch == 0) {
+      if (dc_doj) CK_CUDA(cudaMemsetAsync(dc_doj, 0, sizeof(float) * n, s));
+      if (db) CK_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * d_out, s));
+      return kOk;
+    }
+    float* part_c = ck::at<float>(workspace, SW.part_c);
+    double* part_b = ck::at<double>(workspace, SW.part_b);
+    CK_TRY(ck::launch_skinny_backward(x, dy, batch, d_in, d_out, ck::at<float>(const_cast<void*>(prep), 0), lut,
+                                      include_tanh_jacobian, dx, part_c, part_b, SW.slots, s));
+    // second stage: ordered slot merges (kernels.py:438-442 order semantics)
+    if (dc_doj) CK_TRY(ck::launch_merge(part_c, SW.slots, n, n, dc_doj, 0, s));
+    if (db) CK_TRY(ck::launch_col_finish(part_b, SW.slots, d_out, db, s));
+    return kOk;
+  }
   const ck::BwdLayout W(batch, d_in, d_out, K);
   const ck::BasisLayout L(batch, d_in, K);
   if (workspace_bytes < W.total) {
@@ -385,13 +446,19 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
     const int64_t rows = batch - r0 < W.chunk ? batch - r0 : W.chunk;
     const float* xc = x + r0 * I;
     const float* dyc = dy + r0 * O;
-    if (need_db) CK_TRY(ck::launch_col_partial(dyc, rows, O, db_part + ci * ck::kDbSlots * O, ck::kDbSlots, s));
+    double* dbp = db_part + ci * ck::kDbSlots * O;
     if (d == 0) {
+      if (need_db) CK_TRY(ck::launch_col_partial(dyc, rows, O, dbp, ck::kDbSlots, s));
       if (dx) CK_CUDA(cudaMemsetAsync(dx + r0 * I, 0, sizeof(float) * rows * I, s));
       continue;
     }
-    // dy hi/lo [rows][ldO]: K-major A of the dX GEMM and MN-major A of the dC GEMM
-    if (dx || dc_doj) CK_TRY(ck::launch_split_rows(dyc, 1, rows, O, 0, dy_hi, dy_lo, W.ldO, 0, s));
+    // dy hi/lo [rows][ldO]: K-major A of the dX GEMM and MN-major A of the dC
+    // GEMM; the same pass leaves the bias gradient's per-block column sums
+    if (dx || dc_doj) {
+      CK_TRY(ck::launch_split_rows_colsum(dyc, rows, O, dy_hi, dy_lo, W.ldO, dbp, ck::kDbSlots, s));
+    } else if (need_db) {
+      CK_TRY(ck::launch_col_partial(dyc, rows, O, dbp, ck::kDbSlots, s));
+    }
     if (dx && W.fused_dx) {
       // one GEMM: N tile = d features x n_i inputs, slope combine + Jacobian in the epilogue
       ck::DxEpilogue epi{xc, dx + r0 * I, ck::view(lut), include_tanh_jacobian, I, P.n_i};

@@ -19,117 +19,6 @@ constexpr int kSmemLutMax = 96 * 1024;  // fp32 API: stage tables up to this siz
 constexpr int kMaxK = 64;                // runtime-degree paths: features <= 64
 constexpr int kMaxPlanesFused = 16;      // specialized (unrolled) kernels: 1..16 planes
 
-// Fast cell choice for value interpolation (float32).  frac is formed with
-// one rounding (fma of t*h against the exact h - idx), so the interpolated
-// value is accurate to ~k^2 * ulp(t); a cell flip at an edge is harmless for
-// values because the interpolant is continuous.
-__device__ __forceinline__ void cell_f32(float xv, int n, int& idx, float& frac) {
-  float t = tanhf(xv);
-  t = fminf(fmaxf(t, -1.0f), 1.0f);
-  const float h = 0.5f * static_cast<float>(n - 1);
-  const float pos = fmaf(t, h, h);
-  int i = static_cast<int>(pos);
-  i = min(i, n - 2);
-  idx = i;
-  frac = fmaf(t, h, h - static_cast<float>(i));
-}
-
-__device__ __forceinline__ float lerp_ref(float v0, float v1, float f) {
-  // v_left (1-f) + v_right f  (lut.py:115), exact at f = 0 and f = 1
-  return fmaf(v1, f, v0 * (1.0f - f));
-}
-
-// Grid node -1 + i*step (lut.py:82-84) rounded to float32: (2i - (N-1)) / (N-1)
-// with an exact integer numerator and one correctly rounded fp32 division
-// (the FP64 pipe is too narrow on B200 to spend it here).
-__device__ __forceinline__ float grid_node_f(int i, int n) {
-  return i >= n - 1 ? 1.0f : __fdiv_rn(static_cast<float>(2 * i - (n - 1)), static_cast<float>(n - 1));
-}
-
-// --- runtime-degree basis (generic paths) -----------------------------------
-// Streams B_1, B_2, ... at one point for a runtime kind (same recurrences as
-// basis_f32 in ck_basis.cuh).
-struct Rec {
-  int kind, k;
-  float x, prev, cur, c1, s1, cm, sm, th;
-  __device__ __forceinline__ void init(int kind_, float x_) {
-    kind = kind_;
-    x = x_;
-    k = 0;
-    prev = 0.0f;
-    cur = 1.0f;
-    if (kind == kFourier) {
-      sincospif(x, &s1, &c1);
-      cm = 1.0f;
-      sm = 0.0f;
-    } else if (kind == kChebTrig) {
-      th = acosf(fminf(fmaxf(x, -1.0f), 1.0f));
-    }
-  }
-  // B_{k+1}
-  __device__ __forceinline__ float next() {
-    float v;
-    if (kind == kFourier) {
-      // features 2m-1 = cos(m pi x), 2m = sin(m pi x)
-      if ((k & 1) == 0) {
-        const float c = fmaf(c1, cm, -s1 * sm), s = fmaf(s1, cm, c1 * sm);
-        cm = c;
-        sm = s;
-        v = cm;
-      } else {
-        v = sm;
-      }
-    } else if (kind == kChebTrig) {
-      v = cosf(static_cast<float>(k + 1) * th);
-    } else if (k == 0) {
-      v = kind == kHermite ? 2.0f * x : x;
-    } else if (kind == kCheb) {
-      v = fmaf(2.0f * x, cur, -prev);
-    } else if (kind == kLegendre) {
-      v = fmaf(static_cast<float>(2 * k + 1) * x, cur, -static_cast<float>(k) * prev) *
-          (1.0f / static_cast<float>(k + 1));
-    } else {
-      v = fmaf(2.0f * x, cur, -static_cast<float>(2 * k) * prev);
-    }
-    prev = cur;
-    cur = v;
-    ++k;
-    return v;
-  }
-};
-
-// v[0..P], dv[0..P] at x for a runtime kind / P (P < kMaxK).
-__device__ void basis_deriv_rt(int kind, int P, float x, float* v, float* dv) {
-  Rec r;
-  r.init(kind, x);
-  v[0] = 1.0f;
-  for (int k = 1; k <= P; ++k) v[k] = r.next();
-  if (dv == nullptr) return;
-  dv[0] = 0.0f;
-  if (kind == kCheb || kind == kChebTrig) {
-    float up = 1.0f, uc = 2.0f * x;
-    if (P >= 1) dv[1] = 1.0f;
-    if (P >= 2) dv[2] = 2.0f * uc;
-    for (int n = 3; n <= P; ++n) {
-      const float un = fmaf(2.0f * x, uc, -up);
-      up = uc;
-      uc = un;
-      dv[n] = static_cast<float>(n) * uc;
-    }
-  } else if (kind == kLegendre) {
-    if (P >= 1) dv[1] = 1.0f;
-    for (int k = 1; k < P; ++k) dv[k + 1] = fmaf(static_cast<float>(2 * k + 1), v[k], dv[k - 1]);
-  } else if (kind == kHermite) {
-    for (int n = 1; n <= P; ++n) dv[n] = static_cast<float>(2 * n) * v[n - 1];
-  } else {
-    constexpr float kPi = 3.14159265358979323846f;
-    for (int m = 1; 2 * m <= P; ++m) {
-      dv[2 * m - 1] = -static_cast<float>(m) * kPi * v[2 * m];
-      dv[2 * m] = static_cast<float>(m) * kPi * v[2 * m - 1];
-    }
-  }
-}
-
 template <bool kSmem>
 __device__ __forceinline__ const float* stage_table(const float* g, int count, float* s) {
   if constexpr (!kSmem) {

@@ -120,16 +120,16 @@ __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_ti
 // Fused dX epilogue for one 128-row tile, degree D (compile time): TMEM
 // column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
 // Each thread owns one row; the two warps of a TMEM lane quarter take
-// alternate 4-column blocks.  Per element: float32 tanh gives a candidate
-// cell; its dx row {lower boundary, slopes} and the next row's boundary are
-// gathered together (L2-resident table), and the rare element outside
-// [b_i, b_{i+1}) re-gathers the neighbouring row -- the exact reference cell
-// without any float64 work; then fold with the d accumulators and apply the
-// Jacobian.
+// alternate column blocks.  Per element: float32 tanh gives a candidate
+// cell; its dx row {b_c, slopes, b_{c+1}} comes in with S/4 16-byte loads
+// (L2-resident table), and the rare element outside [b_c, b_{c+1})
+// re-gathers the neighbouring row -- the exact reference cell without any
+// float64 work; then fold with the d accumulators and apply the Jacobian.
 template <int D>
 __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
-  constexpr int K = D + 1;          // dx row stride (= LUT features)
-  constexpr int W = D <= 8 ? 4 : 2;  // columns per block (register budget)
+  constexpr int K = D + 1;                 // table features
+  constexpr int S = dxrow_stride(K);       // floats per dx row (multiple of 4)
+  constexpr int W = D <= 8 ? 4 : 2;        // columns per block (register budget)
   const int n_i = p.n_tile, N = p.lutN;
   const float* xr = p.x + static_cast<long long>(row) * p.ldo;
   float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
@@ -156,33 +156,35 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
       for (int e = 0; e < W; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
     }
     float t[W], acc[W];
-    float sl[W][D + 2];  // [0] = b_idx, [1..D] = slopes, [D+1] = b_{idx+1}
-    const float* rp[W];
+    float4 sl[W][S / 4];  // b_c at float 0, slopes at 1..D, b_{c+1} at K
+    const float4* rp[W];
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
       t[e] = tt;
       const int c = min(static_cast<int>(fmaf(tt, hN, hN)), N - 2);
-      rp[e] = p.dxrows + static_cast<long long>(c) * K;
+      rp[e] = reinterpret_cast<const float4*>(p.dxrows) + static_cast<long long>(c) * (S / 4);
 #pragma unroll
-      for (int j = 0; j <= K; ++j) sl[e][j] = __ldg(rp[e] + j);  // row c and the next boundary
+      for (int j = 0; j < S / 4; ++j) sl[e][j] = __ldg(rp[e] + j);
     }
 #pragma unroll
     for (int e = 0; e < W; ++e) {
-      // exact reference cell: b_idx <= x < b_{idx+1}; at most one step off
-      const bool lo = xv[e] < sl[e][0], hi = !(xv[e] < sl[e][K]);
+      // exact reference cell: b_c <= x < b_{c+1}; at most one step off
+      const float* f = reinterpret_cast<const float*>(sl[e]);
+      const bool lo = xv[e] < f[0], hi = !(xv[e] < f[K]);
       if (lo || hi) {
-        rp[e] += lo ? -K : K;
+        rp[e] += lo ? -(S / 4) : (S / 4);
 #pragma unroll
-        for (int j = 0; j <= K; ++j) sl[e][j] = __ldg(rp[e] + j);
+        for (int j = 0; j < S / 4; ++j) sl[e][j] = __ldg(rp[e] + j);
       }
     }
     tmem_ld_wait();
 #pragma unroll
     for (int e = 0; e < W; ++e) {
+      const float* f = reinterpret_cast<const float*>(sl[e]);
       float a = 0.0f;
 #pragma unroll
-      for (int k = 0; k < D; ++k) a = fmaf(sl[e][k + 1], __uint_as_float(r[k][e]), a);
+      for (int k = 0; k < D; ++k) a = fmaf(f[k + 1], __uint_as_float(r[k][e]), a);
       acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
     }
     if (row_ok) {

@@ -19,14 +19,19 @@ struct ck_lut {
   double* values64 = nullptr;  // [K][N]   float64 build-precision table (validation)
   float* values_pm = nullptr;  // [N][K]   float32, position-major (gather rows idx, idx+1)
   float* slopes_pm = nullptr;  // [N-1][K] float32 cell slopes, position-major
-  // [N][K] input-gradient rows: [0] = smallest float32 x whose reference
-  // (float64) cell is >= i (-inf for i = 0, +inf sentinel row N-1), [1..d] =
-  // the cell's float32 slopes.  Lets kernels pick the exact reference cell
-  // with float32 compares only.
+  // [N][dxrow_stride(K)] input-gradient rows: [0] = b_i, the smallest
+  // float32 x whose reference (float64) cell is >= i (-inf for i = 0, +inf
+  // sentinel for i = N-1), [1..K-1] = the cell's float32 slopes, [K] =
+  // b_{i+1}, zero padding to a 16-byte multiple.  One vectorised gather
+  // gives a kernel the cell's slopes and both boundaries, so it picks the
+  // exact reference cell with float32 compares only.
   float* dxrows = nullptr;
 };
 
 namespace ck {
+
+// floats per input-gradient row of a K-feature table (see ck_lut::dxrows)
+__host__ __device__ constexpr int dxrow_stride(int K) { return (K + 1 + 3) & ~3; }
 
 // Kernel classes for the launch counter / device timers (ck_timing_*).
 enum KClass : int {
@@ -40,7 +45,8 @@ enum KClass : int {
   kKReduce = 7,
   kKLut = 8,
   kKOptim = 9,
-  kKNumClasses = 10,
+  kKSkinny = 10,
+  kKNumClasses = 11,
 };
 
 // RAII: counts one launch of class `cls` and, when timing is enabled,
@@ -93,6 +99,10 @@ int launch_dx_combine(const float* g, int64_t g_plane_stride, const float* x, in
 int launch_split_rows(const float* in, int64_t nz, int64_t rows, int64_t cols, int64_t in_z_stride,
                       __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t out_z_stride,
                       cudaStream_t s);
+// hi/lo [rows][ld] <- in [rows][cols] plus part[s][c] = float64 sum of row
+// block s (rows split into `slots` equal blocks) of column c, one pass
+int launch_split_rows_colsum(const float* in, int64_t rows, int64_t cols, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                             int64_t ld, double* part, int slots, cudaStream_t s);
 // hi/lo [z][cols][ld] <- transpose of in [z][rows][cols]
 int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t cols, int64_t in_z_stride,
                            __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t out_z_stride,
@@ -119,6 +129,23 @@ int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, con
 int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s);
 // out[r][c] = v[r]  (dC_0 = db broadcast over inputs)
 int launch_broadcast_cols(float* out, int64_t rows, int64_t cols, const float* v, cudaStream_t s);
+
+// --- skinny-output layers (ck_skinny.cu) ----------------------------------
+// d_out <= 8 with n_feat * round_up_pow2(d_out) <= 32: CUDA-core kernels on
+// fp32 DOJ coefficients (no basis planes, no tensor-core tiles).
+constexpr int kSkinnyMaxO = 8;
+constexpr int kSkinnyMaxKO = 32;
+constexpr int kSkinnyMaxSlots = 128;
+bool skinny_layer(int d_in, int d_out, int n_feat);
+// row blocks of the skinny backward's partial reduction for this shape
+int skinny_slots(int64_t rows, int d_in);
+int launch_skinny_forward(const float* x, int64_t rows, int I, int O, const float* c, const float* bias,
+                          const ck_lut* lut, float* y, cudaStream_t s);
+// dx (nullable) written directly; part_c [slots][K][O][I] float and part_b
+// [slots][O] float64 partials for the ordered slot merges
+int launch_skinny_backward(const float* x, const float* dy, int64_t rows, int I, int O, const float* c,
+                           const ck_lut* lut, int jacobian, float* dx, float* part_c, double* part_b, int slots,
+                           cudaStream_t s);
 
 // --- tcgen05 split-precision GEMM (ck_gemm.cu) ----------------------------
 // out[z][m][n] (+)= sum_{s<S} sum_r A[aseg][m][r] * B[bseg][n][r]

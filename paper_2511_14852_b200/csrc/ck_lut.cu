@@ -98,13 +98,15 @@ __device__ __forceinline__ int ref_cell(float x, int n) {
   return idx;
 }
 
-// dxrows[i] = {boundary_i, slope_1..slope_d of cell i}; boundary_i is the
-// smallest float32 x with ref_cell(x) >= i, found from atanh(node_i) by
-// stepping one float32 ulp at a time (ref_cell is monotone in x).
+// dxrows row i = {b_i, slopes_1..slopes_d of cell i, b_{i+1}, 0 pad}; b_i
+// is the smallest float32 x with ref_cell(x) >= i, found from atanh(node_i)
+// by stepping one float32 ulp at a time (ref_cell is monotone in x).  Thread
+// i writes b_i into its own row and into row i-1's upper-boundary slot.
 __global__ void lut_dxrows_kernel(int K, int n, double step, const float* __restrict__ s_pm,
                                   float* __restrict__ rows) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int S = dxrow_stride(K);
   float b;
   if (i == 0) {
     b = -INFINITY;
@@ -120,9 +122,12 @@ __global__ void lut_dxrows_kernel(int K, int n, double step, const float* __rest
     while (ref_cell(x, n) < i && guard++ < 4096) x = nextafterf(x, INFINITY);
     b = x;
   }
-  rows[static_cast<int64_t>(i) * K] = b;
-  for (int k = 1; k < K; ++k)
-    rows[static_cast<int64_t>(i) * K + k] = i < n - 1 ? s_pm[static_cast<int64_t>(i) * K + k] : 0.0f;
+  float* row = rows + static_cast<int64_t>(i) * S;
+  row[0] = b;
+  for (int k = 1; k < K; ++k) row[k] = i < n - 1 ? s_pm[static_cast<int64_t>(i) * K + k] : 0.0f;
+  if (i == n - 1) row[K] = INFINITY;
+  for (int j = K + 1; j < S; ++j) row[j] = 0.0f;
+  if (i > 0) rows[static_cast<int64_t>(i - 1) * S + K] = b;
 }
 
 int check_kind(int kind, int degree, bool exact) {
@@ -151,7 +156,7 @@ int lut_alloc(int kind, int degree, int lut_size, int device, ck_lut** out) {
   cudaError_t e = cudaMalloc(&l->values64, kn * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&l->values_pm, kn * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&l->slopes_pm, kn * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&l->dxrows, kn * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&l->dxrows, static_cast<size_t>(dxrow_stride(K)) * lut_size * sizeof(float));
   if (e != cudaSuccess) {
     ck_lut_destroy(l);
     set_error(std::string("ck_lut: cudaMalloc failed: ") + cudaGetErrorString(e));

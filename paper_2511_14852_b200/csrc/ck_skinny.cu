@@ -1,0 +1,298 @@
+// Skinny-output layers (d_out <= 8, e.g. the tabular regression head
+// [512 -> 1]): CUDA-core kernels that evaluate the basis in registers and
+// never materialise basis planes.  A tensor-core tile would be >= 128 wide
+// in the output dimension, so for a handful of outputs the contraction is a
+// per-row dot product (arithmetic intensity ~ 2*O*K flops per 4-byte input):
+// HBM-bound on x (and dy), not tensor-bound.
+//
+// forward : y[b][o] = sum_i sum_k B_k(tanh x[b][i]) C[k][o][i] + bias[o]
+//           one warp per 4 rows, lanes stride the inputs, fixed shuffle-tree
+//           row reduction (deterministic)
+// backward: one pass over (x, dy): dX in place; dC[k][o][i] and db as
+//           per-row-block partials (fixed warp order), then the ordered
+//           slot merge -- the reference's two-stage reduction
+//           (kernels.py:428-442) without atomics.
+#include "ck_basis.cuh"
+#include "ck_common.cuh"
+#include "ck_internal.h"
+
+namespace ck {
+namespace {
+
+// Basis values v[0..P] of one element (P = compile-time bound >= K-1; the
+// entries past K-1 are finite and meet zero coefficients): the LUT
+// interpolation between the two (float32-rounded) grid nodes of the element's
+// float32 cell, or the basis at t (exact handles).  The kind switch is
+// uniform across the launch; each case is a fully unrolled recurrence.
+template <int P>
+__device__ __forceinline__ void elem_basis(const LutView& L, float xv, float (&v)[P + 1]) {
+  float a[P + 1], b[P + 1];
+  float x0, x1 = 0.0f, f = 0.0f;
+  if (L.exact) {
+    x0 = tanhf(xv);
+  } else {
+    int idx;
+    cell_f32(xv, L.N, idx, f);
+    x0 = grid_node_f(idx, L.N);
+    x1 = grid_node_f(idx + 1, L.N);
+  }
+  switch (L.kind) {
+    case kLegendre:
+      basis_f32<kLegendre, P>(x0, a);
+      if (!L.exact) basis_f32<kLegendre, P>(x1, b);
+      break;
+    case kHermite:
+      basis_f32<kHermite, P>(x0, a);
+      if (!L.exact) basis_f32<kHermite, P>(x1, b);
+      break;
+    case kFourier:
+      basis_f32<kFourier, P>(x0, a);
+      if (!L.exact) basis_f32<kFourier, P>(x1, b);
+      break;
+    case kChebTrig:
+      basis_f32<kChebTrig, P>(x0, a);
+      break;
+    default:
+      basis_f32<kCheb, P>(x0, a);
+      if (!L.exact) basis_f32<kCheb, P>(x1, b);
+      break;
+  }
+#pragma unroll
+  for (int k = 0; k <= P; ++k) v[k] = L.exact ? a[k] : lerp_ref(a[k], b[k], f);
+}
+
+// Analytic derivatives at t (exact handles).
+template <int P>
+__device__ __forceinline__ void elem_deriv(int kind, float t, float (&dv)[P + 1]) {
+  switch (kind) {
+    case kLegendre:
+      deriv_f32<kLegendre, P>(t, dv);
+      break;
+    case kHermite:
+      deriv_f32<kHermite, P>(t, dv);
+      break;
+    case kFourier:
+      deriv_f32<kFourier, P>(t, dv);
+      break;
+    default:
+      deriv_f32<kCheb, P>(t, dv);  // also the trig form (same derivative)
+      break;
+  }
+}
+
+// One warp per row (grid-stride), lanes stride the inputs; fixed shuffle
+// tree for the row reduction (deterministic).  KMAX = P + 1 >= K.
+template <int O, int P>
+__global__ void __launch_bounds__(256) skinny_fwd_kernel(const float* __restrict__ x, int64_t rows, int I, int K,
+                                                         const float* __restrict__ c, const float* __restrict__ bias,
+                                                         LutView L, float* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t plane = static_cast<int64_t>(O) * I;  // C[k] stride
+  for (int64_t b = warp; b < rows; b += nwarps) {
+    float acc[O];
+#pragma unroll
+    for (int o = 0; o < O; ++o) acc[o] = 0.0f;
+    const float* xr = x + b * I;
+    for (int i = lane; i < I; i += 32) {
+      float v[P + 1];
+      elem_basis<P>(L, __ldg(xr + i), v);
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        if (k < K) {
+#pragma unroll
+          for (int o = 0; o < O; ++o) acc[o] = fmaf(v[k], __ldg(c + k * plane + static_cast<int64_t>(o) * I + i), acc[o]);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < O; ++o) {
+      float a = acc[o];
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) a += __shfl_xor_sync(0xffffffffu, a, s);
+      acc[o] = a;
+    }
+    if (lane < O) {
+      float out = acc[0];
+#pragma unroll
+      for (int o = 1; o < O; ++o)
+        if (lane == o) out = acc[o];
+      y[b * O + lane] = out + (bias ? bias[lane] : 0.0f);
+    }
+  }
+}
+
+// grid (slots, ceil(I/32)); block 256 = 8 warps; thread = (warp w, column
+// i = 32*blockIdx.y + lane); rows of slot s: [s*rb, min((s+1)*rb, rows)),
+// warp w takes rows w, w+8, ...  P + 1 = compile-time bound on K (loops are
+// unrolled with k < K guards so the per-thread state stays in registers).
+template <int O, int P>
+__global__ void __launch_bounds__(256) skinny_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy,
+                                                         int64_t rows, int I, int K, const float* __restrict__ c,
+                                                         LutView L, int jacobian, int64_t rb,
+                                                         float* __restrict__ dx, float* __restrict__ part_c,
+                                                         double* __restrict__ part_b) {
+  constexpr int KMAX = P + 1;
+  __shared__ float red[8][KMAX * O][32];
+  __shared__ double redb[8][O];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.y * 32 + lane;
+  const bool col_ok = i < I;
+  const int ic = col_ok ? i : I - 1;
+  const int64_t plane = static_cast<int64_t>(O) * I;
+  float cr[KMAX][O], acc[KMAX][O];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+    for (int o = 0; o < O; ++o) {
+      cr[k][o] = k < K ? __ldg(c + k * plane + static_cast<int64_t>(o) * I + ic) : 0.0f;
+      acc[k][o] = 0.0f;
+    }
+  double db[O];
+#pragma unroll
+  for (int o = 0; o < O; ++o) db[o] = 0.0;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rb;
+  const int64_t r1 = r0 + rb < rows ? r0 + rb : rows;
+  const int S = dxrow_stride(K);
+  const float hN = 0.5f * static_cast<float>(L.N - 1);
+  for (int64_t b = r0 + w; b < r1; b += 8) {
+    float g[O];
+#pragma unroll
+    for (int o = 0; o < O; ++o) g[o] = __ldg(dy + b * O + o);
+    if (blockIdx.y == 0 && lane == 0) {
+#pragma unroll
+      for (int o = 0; o < O; ++o) db[o] += static_cast<double>(g[o]);
+    }
+    const float xv = __ldg(x + b * I + ic);
+    float t = tanhf(xv);
+    float vv[KMAX], sv[KMAX];
+    if (L.exact) {
+      elem_basis<P>(L, xv, vv);
+      elem_deriv<P>(L.kind, t, sv);
+    } else {
+      t = fminf(fmaxf(t, -1.0f), 1.0f);
+      // exact reference cell from the boundary rows (as the fused dX epilogue)
+      int cell = min(static_cast<int>(fmaf(t, hN, hN)), L.N - 2);
+      const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
+      if (xv < row[0]) {
+        --cell;
+      } else if (!(xv < row[K])) {
+        ++cell;
+      }
+      row = L.dxrows + static_cast<int64_t>(cell) * S;
+      elem_basis<P>(L, xv, vv);  // values are continuous: the float32 cell is fine
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) sv[k] = (k >= 1 && k < K) ? __ldg(row + k) : 0.0f;
+    }
+    float gx = 0.0f;
+#pragma unroll
+    for (int k = 1; k < KMAX; ++k) {
+      float gk = 0.0f;
+#pragma unroll
+      for (int o = 0; o < O; ++o) gk = fmaf(g[o], cr[k][o], gk);
+      gx = fmaf(sv[k], gk, gx);
+    }
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+      for (int o = 0; o < O; ++o) acc[k][o] = fmaf(g[o], vv[k], acc[k][o]);
+    if (dx && col_ok) dx[b * I + i] = jacobian ? gx * (1.0f - t * t) : gx;
+  }
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+    for (int o = 0; o < O; ++o) red[w][k * O + o][lane] = acc[k][o];
+  if (lane == 0) {
+#pragma unroll
+    for (int o = 0; o < O; ++o) redb[w][o] = db[o];
+  }
+  __syncthreads();
+  // fold the 8 warps in order
+  for (int e = w; e < K * O; e += 8) {
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += red[j][e][lane];
+    const int k = e / O, o = e - k * O;
+    if (col_ok) part_c[(static_cast<int64_t>(blockIdx.x) * K + k) * plane + static_cast<int64_t>(o) * I + i] = s;
+  }
+  if (blockIdx.y == 0 && threadIdx.x < O) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += redb[j][threadIdx.x];
+    part_b[static_cast<int64_t>(blockIdx.x) * O + threadIdx.x] = s;
+  }
+}
+
+int round_o(int O) { return O <= 1 ? 1 : O <= 2 ? 2 : O <= 4 ? 4 : 8; }
+
+}  // namespace
+
+bool skinny_layer(int d_in, int d_out, int n_feat) {
+  (void)d_in;
+  return d_out <= kSkinnyMaxO && n_feat * round_o(d_out) <= kSkinnyMaxKO;
+}
+
+int skinny_slots(int64_t rows, int d_in) {
+  const int64_t colblocks = ceil_div(d_in, 32);
+  int64_t slots = ceil_div(4 * static_cast<int64_t>(num_sms()), colblocks);
+  const int64_t max_slots = ceil_div(rows > 0 ? rows : 1, 64);  // >= 64 rows per slot
+  if (slots > max_slots) slots = max_slots;
+  if (slots > kSkinnyMaxSlots) slots = kSkinnyMaxSlots;
+  return static_cast<int>(slots < 1 ? 1 : slots);
+}
+
+int launch_skinny_forward(const float* x, int64_t rows, int I, int O, const float* c, const float* bias,
+                          const ck_lut* lut, float* y, cudaStream_t s) {
+  if (rows == 0) return kOk;
+  const LutView L = view(lut);
+  const int64_t want = ceil_div(rows * 32, 256);  // one warp per row
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  const int blocks = static_cast<int>(want < cap ? want : cap);
+  const int K = L.K;
+  LaunchScope scope(kKSkinny, s);
+  // P: smallest of 4 / 8 / 16 / 32 with P + 1 >= K (even, as Fourier needs)
+  const int pm = K <= 5 ? 4 : K <= 9 ? 8 : K <= 17 ? 16 : 32;
+#define CK_SK(OO, PP)                                                                              \
+  if (O == OO && pm == PP) {                                                                       \
+    skinny_fwd_kernel<OO, PP><<<blocks, 256, 0, s>>>(x, rows, I, K, c, bias, L, y);                \
+  } else
+  CK_SK(1, 4) CK_SK(1, 8) CK_SK(1, 16) CK_SK(1, 32) CK_SK(2, 4) CK_SK(2, 8) CK_SK(2, 16)
+  CK_SK(3, 4) CK_SK(3, 8) CK_SK(4, 4) CK_SK(4, 8)
+  CK_SK(5, 4) CK_SK(6, 4) CK_SK(7, 4) CK_SK(8, 4) {
+    set_error("skinny forward: unsupported (d_out, features)");
+    return kUnsupported;
+  }
+#undef CK_SK
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_skinny_backward(const float* x, const float* dy, int64_t rows, int I, int O, const float* c,
+                           const ck_lut* lut, int jacobian, float* dx, float* part_c, double* part_b, int slots,
+                           cudaStream_t s) {
+  const LutView L = view(lut);
+  const int K = L.K;
+  const int64_t rb = ceil_div(rows > 0 ? rows : 1, slots);
+  const dim3 grid(static_cast<unsigned>(slots), static_cast<unsigned>(ceil_div(I, 32)));
+  LaunchScope scope(kKSkinny, s);
+  const int ro = round_o(O);
+  CK_CHECK(K * ro <= kSkinnyMaxKO, "skinny backward: too many features x outputs");
+  // P + 1 >= K with P in 4 / 8 / 16 / 32 (register budget: K * round_o(O) <= 32)
+  const int pm = K <= 5 ? 4 : K <= 9 ? 8 : K <= 17 ? 16 : 32;
+#define CK_SKB(OO, PP)                                                                                        \
+  if (O == OO && pm == PP) {                                                                                  \
+    skinny_bwd_kernel<OO, PP><<<grid, 256, 0, s>>>(x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b); \
+  } else
+  CK_SKB(1, 4) CK_SKB(1, 8) CK_SKB(1, 16) CK_SKB(1, 32) CK_SKB(2, 4) CK_SKB(2, 8) CK_SKB(2, 16)
+  CK_SKB(3, 4) CK_SKB(3, 8) CK_SKB(4, 4) CK_SKB(4, 8)
+  CK_SKB(5, 4) CK_SKB(6, 4) CK_SKB(7, 4) CK_SKB(8, 4) {
+    set_error("skinny backward: unsupported (d_out, features)");
+    return kUnsupported;
+  }
+#undef CK_SKB
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+}  // namespace ck

@@ -37,6 +37,57 @@ __global__ void split_rows_kernel(const float* __restrict__ in, int64_t nz, int6
   }
 }
 
+// dy pass of the backward: hi/lo [r][ld] bf16 split of in [rows][cols] and,
+// in the same read, float64 column sums per row block (the bias gradient's
+// first stage).  grid = (slots, ceil(cols / 64)); block (s, cb) covers rows
+// [s*rb, min((s+1)*rb, rows)) and columns [64 cb, 64 cb + 64): warp w takes
+// rows w, w+8, ...; lane l the column pair 64 cb + 2 l.  The 8 warp partials
+// are folded in warp order, so part[s][c] is deterministic.
+__global__ void __launch_bounds__(256) split_rows_colsum_kernel(const float* __restrict__ in, int64_t rows,
+                                                                int64_t cols, int64_t rb, uint32_t* __restrict__ hi,
+                                                                uint32_t* __restrict__ lo, int64_t ld,
+                                                                double* __restrict__ part) {
+  __shared__ double red[8][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.y) * 64 + 2 * lane;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rb;
+  const int64_t r1 = r0 + rb < rows ? r0 + rb : rows;
+  double s0 = 0.0, s1 = 0.0;
+  if (c < cols) {
+    const bool two = c + 1 < cols;
+    const bool vec = two && ((cols & 1) == 0);
+    for (int64_t r = r0 + w; r < r1; r += 8) {
+      const float* src = in + r * cols + c;
+      float a, b;
+      if (vec) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(src));
+        a = v.x;
+        b = v.y;
+      } else {
+        a = __ldg(src);
+        b = two ? __ldg(src + 1) : 0.0f;
+      }
+      s0 += static_cast<double>(a);
+      s1 += static_cast<double>(b);
+      uint32_t h2, l2;
+      split_pack2(a, b, h2, l2);
+      const int64_t o = (r * ld + c) >> 1;
+      hi[o] = h2;
+      lo[o] = l2;
+    }
+  }
+  red[w][2 * lane] = s0;
+  red[w][2 * lane + 1] = s1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += red[j][threadIdx.x];
+    const int64_t cc = static_cast<int64_t>(blockIdx.y) * 64 + threadIdx.x;
+    if (cc < cols) part[static_cast<int64_t>(blockIdx.x) * cols + cc] = acc;
+  }
+}
+
 // hi/lo [z][c][ld] = transpose of in [z][r][c] via 32x32 smem tiles.
 __global__ void split_transpose_kernel(const float* __restrict__ in, int64_t nz, int64_t rows, int64_t cols,
                                        int64_t in_zs, __nv_bfloat16* __restrict__ hi,
@@ -203,6 +254,18 @@ int launch_split_rows(const float* in, int64_t nz, int64_t rows, int64_t cols, i
   LaunchScope scope(kKSplit, s);
   split_rows_kernel<<<blocks_for(nz * rows * ((cols + 1) / 2)), kThreads, 0, s>>>(
       in, nz, rows, cols, in_zs, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, out_zs);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_split_rows_colsum(const float* in, int64_t rows, int64_t cols, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                             int64_t ld, double* part, int slots, cudaStream_t s) {
+  if (cols == 0) return kOk;
+  CK_CHECK(ld % 2 == 0, "split_rows_colsum: pitch must be even");
+  const int64_t rb = ceil_div(rows > 0 ? rows : 1, slots);
+  LaunchScope scope(kKSplit, s);
+  split_rows_colsum_kernel<<<dim3(static_cast<unsigned>(slots), static_cast<unsigned>(ceil_div(cols, 64))), 256, 0, s>>>(
+      in, rows, cols, rb, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, part);
   CK_CUDA(cudaGetLastError());
   return kOk;
 }

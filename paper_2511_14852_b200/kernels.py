@@ -160,9 +160,10 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
-def basis_cache_bytes(batch: int, d_in: int, n_feat: int) -> int:
-    """Bytes of the forward->backward basis cache (bf16 hi/lo planes, k >= 1)."""
-    return int(_lib.lib().ck_basis_cache_bytes(batch, d_in, n_feat))
+def basis_cache_bytes(batch: int, d_in: int, d_out: int, n_feat: int) -> int:
+    """Bytes of the forward->backward basis cache (bf16 hi/lo planes, k >= 1);
+    0 when the layer does not use basis planes (skinny d_out)."""
+    return int(_lib.lib().ck_basis_cache_bytes(batch, d_in, d_out, n_feat))
 
 
 def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut, bias: torch.Tensor | None,

@@ -57,6 +57,19 @@ class _LayerState:
         return p
 
 
+_TOTAL_MEM: dict = {}
+
+
+def _free_bytes_estimate(device: torch.device) -> int:
+    """Device memory not held by this process's tensors -- host-side counters
+    only (cudaMemGetInfo synchronises and stalls behind other GPU clients)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    total = _TOTAL_MEM.get(idx)
+    if total is None:
+        total = _TOTAL_MEM[idx] = torch.cuda.get_device_properties(idx).total_memory
+    return total - torch.cuda.memory_allocated(idx)
+
+
 class ChebyKANFunction(torch.autograd.Function):
     """y = ChebyKAN(x; C, b).  Forward: ck_forward.  Backward: ck_backward."""
 
@@ -70,8 +83,8 @@ class ChebyKANFunction(torch.autograd.Function):
         cache = None
         if ctx.needs_input_grad[1] and state.cache_basis:
             # keep the expanded basis for dC (saves the backward's re-expansion)
-            nbytes = basis_cache_bytes(x.shape[0], prep.d_in, prep.n_feat)
-            if state.cache_basis is True or nbytes <= 0.35 * torch.cuda.mem_get_info(x.device)[0]:
+            nbytes = basis_cache_bytes(x.shape[0], prep.d_in, prep.d_out, prep.n_feat)
+            if nbytes > 0 and (state.cache_basis is True or nbytes <= 0.35 * _free_bytes_estimate(x.device)):
                 cache = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
         y = forward_raw(x, prep, lut, None if bias is None else bias.detach(), cache)
         ctx.save_for_backward(x, coeff_doj)

@@ -357,3 +357,46 @@ def test_exact_mode_error_paths():
     cj = ck.CoeffTensor(3, 2, 2, ck.Layout.JOD, torch.ones(18, device=_dev()))
     with pytest.raises(ValueError, match="trig path applies to the Chebyshev basis only"):
         ck.reference_forward(torch.zeros(1, 3, device=_dev()), cj, 2, trig=True, kind=ck.BasisKind.HERMITE)
+
+
+@pytest.mark.parametrize("o,d,kind,exact", [(1, 5, "chebyshev", False), (2, 7, "legendre", False),
+                                            (3, 3, "fourier", False), (4, 6, "chebyshev", True),
+                                            (8, 3, "hermite", False), (1, 20, "chebyshev", False),
+                                            (5, 2, "hermite", True)])
+def test_skinny_output_layers_vs_oracle(o, d, kind, exact):
+    # d_out <= 8 runs on the CUDA-core skinny kernels (no tensor-core tiles)
+    b, i, n = 3000, 515, 4096
+    k = orc.feature_count(kind, d)
+    rng = np.random.default_rng(o * 100 + d)
+    s = 1.0 / np.sqrt(i * k)
+    x = rng.uniform(-2, 2, (b, i)).astype(np.float32)
+    c_doj = rng.uniform(-s, s, (k, o, i)).astype(np.float32)
+    dy = rng.standard_normal((b, o)).astype(np.float32)
+    bias = rng.standard_normal(o).astype(np.float32) * 0.1
+    if exact:
+        wy = orc.exact_layer_forward(x, c_doj, kind, bias.astype(np.float64), threads=8)
+        wdc, wdx, wdb = orc.exact_layer_backward(x, c_doj, dy, kind, threads=8)
+        table, mode = None, ck.EXACT_MODE
+    else:
+        vals, slopes, _ = orc.build_table(d, n, kind)
+        wy = orc.layer_forward(x, c_doj, vals, bias.astype(np.float64), threads=8)
+        wdc, wdx, wdb = orc.layer_backward(x, c_doj, dy, vals, slopes, threads=8)
+        table, mode = ck.lut_build(ck.BasisKind(kind), d, n, device=_dev()), ck.LUT_MODE
+    c = ck.CoeffTensor(i, o, k - 1, ck.Layout.DOJ, _t(c_doj))
+    y = ck.fused_forward(_t(x), c, table, None, mode, _t(bias), kind=ck.BasisKind(kind)).cpu().numpy()
+    outs = []
+    for _ in range(2):
+        cg, dx = ck.backward_fused(_t(x), c, _t(dy), table, None, mode, kind=ck.BasisKind(kind))
+        outs.append((cg.data.clone(), dx.clone()))
+    assert all(torch.equal(a, bb) for a, bb in zip(outs[0], outs[1]))  # deterministic two-stage merge
+    e = (orc.normwise_err(y, wy), orc.normwise_err(outs[0][0].cpu().numpy(), wdc),
+         orc.normwise_err(outs[0][1].cpu().numpy(), wdx))
+    print((o, d, kind, exact), [f"{v:.2e}" for v in e])
+    assert max(e) <= TOL, e
+    # bias gradient through the module path
+    layer = ck.ChebyKANLayer(i, o, d, kind=ck.BasisKind(kind), lut_size=n,
+                             basis_path=ck.BasisPath.EXACT_RECURRENCE if exact else ck.BasisPath.LUT_INTERP).to(_dev())
+    with torch.no_grad():
+        layer.coeff_doj.copy_(_t(c_doj))
+    layer(_t(x)).backward(_t(dy))
+    assert orc.normwise_err(layer.bias.grad.cpu().numpy(), wdb) <= 1e-6
