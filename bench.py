@@ -212,7 +212,9 @@ def run_ours(args, wl):
     torch.manual_seed(1234)  # identical synthetic weights on every rank
     layers = [ck.ChebyKANLayer(i, o, d, lut_size=wl["lut_size"]) for i, o in dims]
     model = (torch.nn.Sequential(*layers) if is_net else layers[0]).to(dev)
-    opt = ck.Adam(model.parameters(), lr=1e-4)  # ck_adam_step (reference adam_step rule)
+    use_graph = args.graph if args.graph is not None else is_net
+    # ck_adam_step (reference adam_step rule); device-side step counter when captured
+    opt = ck.Adam(model.parameters(), lr=1e-4, capturable=use_graph)
     reducer = ck.GradientAllreducer(ck.chebykan_parameters(model)) if world > 1 else None
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
@@ -257,32 +259,74 @@ def run_ours(args, wl):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
-        step(x, dy)
-    barrier()
+    graph = None
+    if use_graph:
+        # whole-step CUDA graph (forward, backward, allreduce, Adam): the
+        # small nets are launch-bound, so the step is captured once and
+        # replayed; warm-up runs on a side stream as capture requires
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(args.warmup):
+                step(x, dy)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        barrier()
+        graph = torch.cuda.CUDAGraph()
+        launches_c0 = _lib.launch_count()
+        with torch.cuda.graph(graph):
+            step(x, dy)
+        launches_per_step = _lib.launch_count() - launches_c0
+        barrier()
+    else:
+        for _ in range(args.warmup):
+            step(x, dy)
+        barrier()
+
+    def kernel_breakdown():
+        """Per-class device time of eager steps (library event timers)."""
+        _lib.timing_collect()
+        _lib.timing_enable(True)
+        for _ in range(args.steps):
+            step(x, dy)
+        barrier()
+        _lib.timing_enable(False)
+        return _lib.timing_collect()
 
     # ---- timed region: training steps, device-resident inputs -----------
     clocks = ClockSampler(local) if local == 0 else None
     if clocks:
         clocks.start()
         time.sleep(0.3)
-    _lib.timing_collect()
-    _lib.timing_enable(True)
+    if graph is None:
+        _lib.timing_collect()
+        _lib.timing_enable(True)
     launches0 = _lib.launch_count()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
-        step(x, dy)
+        if graph is not None:
+            graph.replay()
+        else:
+            step(x, dy)
     ev1.record()
     barrier()
-    launches = _lib.launch_count() - launches0
-    _lib.timing_enable(False)
-    kt = _lib.timing_collect()
+    if graph is None:
+        launches = _lib.launch_count() - launches0
+        _lib.timing_enable(False)
+        kt = _lib.timing_collect()
+    else:
+        launches = launches_per_step * args.steps
     clk = clocks.stop() if clocks else None
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms / args.steps
     value = gb / (ms_step / 1e3)
+    if graph is not None:
+        # replays advanced the parameters without Python seeing it: refresh the
+        # version counters so the layers re-split their coefficients
+        for prm in model.parameters():
+            torch.autograd.graph.increment_version(prm)
+        kt = kernel_breakdown()
 
     # ---- forward-only throughput (inference), same shard ---------------
     with torch.no_grad():
@@ -419,6 +463,8 @@ def run_ours(args, wl):
             "gemm_share_of_kernel_time": gemm_ms / total_kernel_ms if total_kernel_ms else None,
         },
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
+        "graph": (f"timed steps replay one captured CUDA graph of the whole step; kernel_ms_per_step and "
+                  f"roofline from {args.steps} eager steps" if graph is not None else None),
         "kernel_launches_per_step": {k: v[1] / args.steps for k, v in kt.items() if v[1]},
         "train_alg_tflops_per_gpu": train_flops / (ms_step / 1e3) / 1e12,
         "clocks": clk,
@@ -452,21 +498,45 @@ def run_sweep(args):
             dy = torch.randn(b, dim, device=dev)
             lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, deg, 32768, device=dev)
             prep = PreparedCoeff(c)
-            for _ in range(3):
+            cache = torch.empty(ck.kernels.basis_cache_bytes(b, dim, dim, deg + 1), dtype=torch.uint8, device=dev)
+
+            def infer():
                 forward_raw(x, prep, lut, None)
-                backward_raw(x, dy, prep, lut, True)
+
+            def train():
+                forward_raw(x, prep, lut, None, cache)
+                backward_raw(x, dy, prep, lut, True, cache=cache)
+
+            for _ in range(3):
+                infer()
+                train()
+            torch.cuda.synchronize()
+            if args.graph is not False:
+                # the small layers are launch-bound: time captured CUDA graphs
+                graphs = []
+                for fn in (infer, train):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        fn()
+                    graphs.append(g.replay)
+                infer_run, train_run = graphs
+            else:
+                infer_run, train_run = infer, train
+            for _ in range(2):
+                infer_run()
+                train_run()
             torch.cuda.synchronize()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record()
             for _ in range(args.steps):
-                forward_raw(x, prep, lut, None)
+                infer_run()
             ev[1].record()
             for _ in range(args.steps):
-                backward_raw(x, dy, prep, lut, True)
+                train_run()
             ev[2].record()
             torch.cuda.synchronize()
             f = ev[0].elapsed_time(ev[1]) / args.steps
-            bw = ev[1].elapsed_time(ev[2]) / args.steps
+            bw = ev[1].elapsed_time(ev[2]) / args.steps - f
             fl = ck.count_flops(b, dim, dim, deg)
             # executed GEMM flops: the T_0 == 1 folds remove one of the d+1
             # planes from the forward and dC GEMMs
@@ -481,7 +551,7 @@ def run_sweep(args):
                  "train_frac_of_bf16x3_burst": ex_t / (f + bw) / 1e9 / peak}
             rows.append(r)
             print(json.dumps(r), flush=True)
-            del x, c, dy, prep
+            del x, c, dy, prep, cache
     out = ROOT / "gpurun_out" / "sweep.json"
     out.parent.mkdir(exist_ok=True)
     out.write_text(json.dumps(rows, indent=1))
@@ -496,6 +566,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     ap.add_argument("--sweep", action="store_true", help="run the C1 sweep table instead of the JSON line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
+                    help="replay a captured CUDA graph of the step (default for the small nets)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and not args.sweep:
         args.warmup = 3

@@ -153,6 +153,13 @@ CK_API int ck_merge(const float* partials, int num_partials, int64_t stride, int
  * step counts from 1 (AdamState.step after increment). */
 CK_API int ck_adam_step(float* param, const float* grad, float* m, float* v, int64_t n, double lr, double beta1,
                  double beta2, double eps, int64_t step, void* stream);
+/* Graph-capturable form (the step counter lives on the device): ck_adam_begin
+ * increments *step_dev and writes bc_dev = {1-b1^step, 1-b2^step}; then
+ * ck_adam_step_dev updates each tensor reading bc_dev.  A captured CUDA graph
+ * of a training step then advances the bias correction on every replay. */
+CK_API int ck_adam_begin(int64_t* step_dev, float* bc_dev, double beta1, double beta2, void* stream);
+CK_API int ck_adam_step_dev(float* param, const float* grad, float* m, float* v, int64_t n, double lr,
+                     double beta1, double beta2, double eps, const float* bc_dev, void* stream);
 
 /* --- Diagnostics --------------------------------------------------------------
  * ck_launch_count: kernels this library has launched in the process.

@@ -44,11 +44,12 @@ __device__ __forceinline__ float lerp_ref(float v0, float v1, float f) {
   return fmaf(v1, f, v0 * (1.0f - f));
 }
 
-// Grid node -1 + i*step (lut.py:82-84) rounded to float32: (2i - (N-1)) / (N-1)
-// with an exact integer numerator and one correctly rounded fp32 division
-// (the FP64 pipe is too narrow on B200 to spend it here).
-__device__ __forceinline__ float grid_node_f(int i, int n) {
-  return i >= n - 1 ? 1.0f : __fdiv_rn(static_cast<float>(2 * i - (n - 1)), static_cast<float>(n - 1));
+// Grid node -1 + i*step (lut.py:82-84) in float32: one FMA with the
+// float32 step 2/(N-1) (within ~1 ulp of the correctly rounded node; the
+// recomputed table entries then match the float64 table to ~k^2 ulp), the
+// last node forced to 1.0 like the reference.
+__device__ __forceinline__ float grid_node_f(int i, int n, float step) {
+  return i >= n - 1 ? 1.0f : fmaf(static_cast<float>(i), step, -1.0f);
 }
 
 // v[0..P] = B_0..B_P at x.

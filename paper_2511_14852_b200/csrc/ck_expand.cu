@@ -84,8 +84,8 @@ __device__ __forceinline__ void elem_planes(float xv, int n, float (&out)[D]) {
     float f;
     cell_f32(xv, n, idx, f);
     float v0[D + 1], v1[D + 1];
-    basis_f32<KIND, D>(grid_node_f(idx, n), v0);
-    basis_f32<KIND, D>(grid_node_f(idx + 1, n), v1);
+    basis_f32<KIND, D>(grid_node_f(idx, n, 2.0f / static_cast<float>(n - 1)), v0);
+    basis_f32<KIND, D>(grid_node_f(idx + 1, n, 2.0f / static_cast<float>(n - 1)), v1);
 #pragma unroll
     for (int k = 1; k <= D; ++k) out[k - 1] = lerp_ref(v0[k], v1[k], f);
   }
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
       } else {
         int idx;
         cell_f32(xs[e], N, idx, fr[e]);
-        ra[e].init(lut.kind, grid_node_f(idx, N));
-        rb[e].init(lut.kind, grid_node_f(idx + 1, N));
+        ra[e].init(lut.kind, grid_node_f(idx, N, 2.0f / static_cast<float>(N - 1)));
+        rb[e].init(lut.kind, grid_node_f(idx + 1, N, 2.0f / static_cast<float>(N - 1)));
       }
     }
     uint32_t* h = hi + ((r * ld + c) >> 1);

@@ -19,6 +19,7 @@
 
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "ck_basis.cuh"
 #include "ck_common.cuh"
@@ -120,65 +121,109 @@ __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_ti
 // Fused dX epilogue for one 128-row tile, degree D (compile time): TMEM
 // column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
 // Each thread owns one row; the two warps of a TMEM lane quarter take
-// alternate column blocks.  Per element: float32 tanh gives a candidate
-// cell; its dx row {b_c, slopes, b_{c+1}} comes in with S/4 16-byte loads
-// (L2-resident table), and the rare element outside [b_c, b_{c+1})
-// re-gathers the neighbouring row -- the exact reference cell without any
-// float64 work; then fold with the d accumulators and apply the Jacobian.
+// alternate column blocks of W inputs.  Per element: float32 tanh gives a
+// candidate cell; its dx row {b_c, slopes, b_{c+1}} comes in with S/4
+// 16-byte loads (L2-resident table), and the rare element outside
+// [b_c, b_{c+1}) re-gathers the neighbouring row -- the exact reference cell
+// without any float64 work; then fold with the d accumulators and apply the
+// Jacobian.  The two dependent global loads (x, then its dx row) are
+// software-pipelined: x is loaded two blocks ahead and the dx rows one block
+// ahead, so a short-K tile's epilogue is not a chain of L2 round trips.
+template <int D>
+struct DxBlock {
+  static constexpr int K = D + 1;
+  static constexpr int S = dxrow_stride(K);
+  // columns per block: as many independent gathers in flight as the
+  // register budget allows
+  static constexpr int W = D <= 4 ? 8 : (D <= 8 ? 4 : 2);
+};
+
+template <int D>
+__device__ __forceinline__ void dx_load_x(const KArgs& p, const float* xr, bool row_ok, int i0,
+                                          float (&xv)[DxBlock<D>::W]) {
+  constexpr int W = DxBlock<D>::W;
+  if (W >= 4 && ((p.ldo & 3) == 0) && row_ok && i0 + W <= p.N) {
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + i0 + 4 * q);
+      xv[4 * q] = v.x;
+      xv[4 * q + 1] = v.y;
+      xv[4 * q + 2] = v.z;
+      xv[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < W; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[W]) {
+  if constexpr (W == 8) {
+    tmem_ld_32x32b_x8(taddr, r);
+  } else if constexpr (W == 4) {
+    tmem_ld_32x32b_x4(taddr, r);
+  } else {
+    tmem_ld_32x32b_x2(taddr, r);
+  }
+}
+
+// tanh, candidate cell and the gather of its dx row for each element
+template <int D>
+__device__ __forceinline__ void dx_gather(const KArgs& p, const float (&xv)[DxBlock<D>::W], float (&t)[DxBlock<D>::W],
+                                          float4 (&sl)[DxBlock<D>::W][DxBlock<D>::S / 4]) {
+  constexpr int W = DxBlock<D>::W, S = DxBlock<D>::S;
+  const float hN = 0.5f * static_cast<float>(p.lutN - 1);
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
+    t[e] = tt;
+    const int c = min(static_cast<int>(fmaf(tt, hN, hN)), p.lutN - 2);
+    const float4* rp = reinterpret_cast<const float4*>(p.dxrows) + static_cast<long long>(c) * (S / 4);
+#pragma unroll
+    for (int j = 0; j < S / 4; ++j) sl[e][j] = __ldg(rp + j);
+  }
+}
+
+// One pass over the tile's columns in blocks of W; x of the next block is
+// prefetched while the current block's dx rows are in flight.
 template <int D>
 __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
-  constexpr int K = D + 1;                 // table features
-  constexpr int S = dxrow_stride(K);       // floats per dx row (multiple of 4)
-  constexpr int W = D <= 8 ? 4 : 2;        // columns per block (register budget)
-  const int n_i = p.n_tile, N = p.lutN;
+  constexpr int K = DxBlock<D>::K, S = DxBlock<D>::S, W = DxBlock<D>::W;
+  const int n_i = p.n_tile;
   const float* xr = p.x + static_cast<long long>(row) * p.ldo;
   float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
   const bool vec = ((p.ldo & 3) == 0);
-  const float hN = 0.5f * static_cast<float>(N - 1);
+  const float hN = 0.5f * static_cast<float>(p.lutN - 1);
+  int cb = W * h;
+  float xv[W];
+  if (cb < n_i) dx_load_x<D>(p, xr, row_ok, n0 + cb, xv);
 #pragma unroll 1
-  for (int cb = W * h; cb < n_i; cb += 2 * W) {
+  for (; cb < n_i; cb += 2 * W) {
     uint32_t r[D][W];
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      if constexpr (W == 4) {
-        tmem_ld_32x32b_x4(tbase + k * n_i + cb, r[k]);
-      } else {
-        tmem_ld_32x32b_x2(tbase + k * n_i + cb, r[k]);
-      }
-    }
-    const int i0 = n0 + cb;
-    float xv[W];
-    if (W == 4 && vec && row_ok && i0 + 4 <= p.N) {
-      const float4 v = *reinterpret_cast<const float4*>(xr + i0);
-      xv[0] = v.x; xv[1] = v.y; xv[W - 2] = v.z; xv[W - 1] = v.w;
-    } else {
+    for (int k = 0; k < D; ++k) tmem_ld_cols<W>(tbase + k * n_i + cb, r[k]);
+    float t[W];
+    float4 sl[W][S / 4];
+    dx_gather<D>(p, xv, t, sl);
+    float x_cur[W];
 #pragma unroll
-      for (int e = 0; e < W; ++e) xv[e] = (row_ok && i0 + e < p.N) ? xr[i0 + e] : 0.0f;
-    }
-    float t[W], acc[W];
-    float4 sl[W][S / 4];  // b_c at float 0, slopes at 1..D, b_{c+1} at K
-    const float4* rp[W];
+    for (int e = 0; e < W; ++e) x_cur[e] = xv[e];
+    if (cb + 2 * W < n_i) dx_load_x<D>(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
+    // exact reference cell: b_c <= x < b_{c+1}; at most one step off
 #pragma unroll
     for (int e = 0; e < W; ++e) {
-      float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
-      t[e] = tt;
-      const int c = min(static_cast<int>(fmaf(tt, hN, hN)), N - 2);
-      rp[e] = reinterpret_cast<const float4*>(p.dxrows) + static_cast<long long>(c) * (S / 4);
-#pragma unroll
-      for (int j = 0; j < S / 4; ++j) sl[e][j] = __ldg(rp[e] + j);
-    }
-#pragma unroll
-    for (int e = 0; e < W; ++e) {
-      // exact reference cell: b_c <= x < b_{c+1}; at most one step off
       const float* f = reinterpret_cast<const float*>(sl[e]);
-      const bool lo = xv[e] < f[0], hi = !(xv[e] < f[K]);
+      const bool lo = x_cur[e] < f[0], hi = !(x_cur[e] < f[K]);
       if (lo || hi) {
-        rp[e] += lo ? -(S / 4) : (S / 4);
+        const int c = min(static_cast<int>(fmaf(t[e], hN, hN)), p.lutN - 2) + (lo ? -1 : 1);
+        const float4* rp = reinterpret_cast<const float4*>(p.dxrows) + static_cast<long long>(c) * (S / 4);
 #pragma unroll
-        for (int j = 0; j < S / 4; ++j) sl[e][j] = __ldg(rp[e] + j);
+        for (int q = 0; q < S / 4; ++q) sl[e][q] = __ldg(rp + q);
       }
     }
     tmem_ld_wait();
+    float acc[W];
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       const float* f = reinterpret_cast<const float*>(sl[e]);
@@ -187,9 +232,13 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
       for (int k = 0; k < D; ++k) a = fmaf(f[k + 1], __uint_as_float(r[k][e]), a);
       acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
     }
+    const int i0 = n0 + cb;
     if (row_ok) {
-      if (W == 4 && vec && i0 + 4 <= p.N) {
-        *reinterpret_cast<float4*>(dxr + i0) = make_float4(acc[0], acc[1], acc[W - 2], acc[W - 1]);
+      if (W >= 4 && vec && i0 + W <= p.N) {
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q)
+          *reinterpret_cast<float4*>(dxr + i0 + 4 * q) =
+              make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
       } else {
 #pragma unroll
         for (int e = 0; e < W; ++e)

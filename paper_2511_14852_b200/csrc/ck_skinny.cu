@@ -33,8 +33,8 @@ __device__ __forceinline__ void elem_basis(const LutView& L, float xv, float (&v
   } else {
     int idx;
     cell_f32(xv, L.N, idx, f);
-    x0 = grid_node_f(idx, L.N);
-    x1 = grid_node_f(idx + 1, L.N);
+    x0 = grid_node_f(idx, L.N, 2.0f / static_cast<float>(L.N - 1));
+    x1 = grid_node_f(idx + 1, L.N, 2.0f / static_cast<float>(L.N - 1));
   }
   switch (L.kind) {
     case kLegendre:

@@ -56,24 +56,37 @@ __global__ void __launch_bounds__(256) split_rows_colsum_kernel(const float* __r
   if (c < cols) {
     const bool two = c + 1 < cols;
     const bool vec = two && ((cols & 1) == 0);
-    for (int64_t r = r0 + w; r < r1; r += 8) {
-      const float* src = in + r * cols + c;
-      float a, b;
-      if (vec) {
-        const float2 v = __ldg(reinterpret_cast<const float2*>(src));
-        a = v.x;
-        b = v.y;
-      } else {
-        a = __ldg(src);
-        b = two ? __ldg(src + 1) : 0.0f;
+    // 4 rows per iteration (independent loads in flight); sums in row order
+    for (int64_t rr = r0 + w; rr < r1; rr += 32) {
+      float a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t r = rr + 8 * u;
+        a[u] = b[u] = 0.0f;
+        if (r < r1) {
+          const float* src = in + r * cols + c;
+          if (vec) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(src));
+            a[u] = v.x;
+            b[u] = v.y;
+          } else {
+            a[u] = __ldg(src);
+            b[u] = two ? __ldg(src + 1) : 0.0f;
+          }
+        }
       }
-      s0 += static_cast<double>(a);
-      s1 += static_cast<double>(b);
-      uint32_t h2, l2;
-      split_pack2(a, b, h2, l2);
-      const int64_t o = (r * ld + c) >> 1;
-      hi[o] = h2;
-      lo[o] = l2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t r = rr + 8 * u;
+        if (r >= r1) break;
+        s0 += static_cast<double>(a[u]);
+        s1 += static_cast<double>(b[u]);
+        uint32_t h2, l2;
+        split_pack2(a[u], b[u], h2, l2);
+        const int64_t o = (r * ld + c) >> 1;
+        hi[o] = h2;
+        lo[o] = l2;
+      }
     }
   }
   red[w][2 * lane] = s0;
@@ -180,12 +193,24 @@ __global__ void col_partial_kernel(const float* __restrict__ in, int64_t rows, i
   }
 }
 
-__global__ void col_finish_kernel(const double* __restrict__ part, int slots, int64_t cols, float* __restrict__ out) {
-  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols;
-       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double acc = 0.0;
-    for (int s = 0; s < slots; ++s) acc += part[s * cols + c];
-    out[c] = static_cast<float>(acc);
+// out[c] = sum_s part[s][c]: block = 32 columns x 8 warps; warp w sums
+// slots w, w+8, ... and the 8 partials are folded in warp order (fixed
+// order for a given slot count: deterministic).
+__global__ void __launch_bounds__(256) col_finish_kernel(const double* __restrict__ part, int slots, int64_t cols,
+                                                         float* __restrict__ out) {
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  double acc = 0.0;
+  if (c < cols)
+    for (int s = w; s < slots; s += 8) acc += part[s * cols + c];
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += red[j][lane];
+    out[c] = static_cast<float>(t);
   }
 }
 
@@ -315,7 +340,7 @@ int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part
 int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s) {
   if (cols == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  col_finish_kernel<<<blocks_for(cols), kThreads, 0, s>>>(part, slots, cols, out);
+  col_finish_kernel<<<static_cast<unsigned>(ceil_div(cols, 32)), 256, 0, s>>>(part, slots, cols, out);
   CK_CUDA(cudaGetLastError());
   return kOk;
 }

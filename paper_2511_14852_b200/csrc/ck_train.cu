@@ -14,6 +14,7 @@ constexpr int kThreads = 256;
 
 struct AdamArgs {
   float lr, b1, omb1, b2, omb2, bc1, bc2, eps;
+  const float* bc_dev;  // nullable: {bc1, bc2} read from device memory (graph-capturable form)
 };
 
 // m = m*b1 + (1-b1)*g; v = v*b2 + (1-b2)*g*g; p -= lr * (m/bc1) / (sqrt(v/bc2) + eps)
@@ -28,6 +29,10 @@ __device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, 
 __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
                                                         float* __restrict__ m, float* __restrict__ v, int64_t n,
                                                         AdamArgs a) {
+  if (a.bc_dev) {
+    a.bc1 = a.bc_dev[0];
+    a.bc2 = a.bc_dev[1];
+  }
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
@@ -53,6 +58,23 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, c
   }
 }
 
+// step += 1; bc = {1 - b1^step, 1 - b2^step} (float64 pow, model.py:262-263)
+__global__ void adam_begin_kernel(int64_t* step, float* bc, double b1, double b2) {
+  const int64_t t = ++(*step);
+  bc[0] = static_cast<float>(1.0 - pow(b1, static_cast<double>(t)));
+  bc[1] = static_cast<float>(1.0 - pow(b2, static_cast<double>(t)));
+}
+
+int adam_launch(float* param, const float* grad, float* m, float* v, int64_t n, const AdamArgs& a, cudaStream_t s) {
+  const int64_t want = ceil_div(ceil_div(n, 4), kThreads);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  const int blocks = static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
+  LaunchScope scope(kKOptim, s);
+  adam_kernel<<<blocks, kThreads, 0, s>>>(param, grad, m, v, n, a);
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
 }  // namespace
 }  // namespace ck
 
@@ -72,12 +94,32 @@ extern "C" int ck_adam_step(float* param, const float* grad, float* m, float* v,
   a.bc1 = static_cast<float>(1.0 - std::pow(beta1, static_cast<double>(step)));
   a.bc2 = static_cast<float>(1.0 - std::pow(beta2, static_cast<double>(step)));
   a.eps = static_cast<float>(eps);
+  a.bc_dev = nullptr;
+  return ck::adam_launch(param, grad, m, v, n, a, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int ck_adam_begin(int64_t* step_dev, float* bc_dev, double beta1, double beta2, void* stream) {
+  CK_CHECK(step_dev && bc_dev, "ck_adam_begin: NULL pointer");
   auto s = static_cast<cudaStream_t>(stream);
-  const int64_t want = ck::ceil_div(ck::ceil_div(n, 4), ck::kThreads);
-  const int64_t cap = static_cast<int64_t>(ck::num_sms()) * 8;
-  const int blocks = static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
   ck::LaunchScope scope(ck::kKOptim, s);
-  ck::adam_kernel<<<blocks, ck::kThreads, 0, s>>>(param, grad, m, v, n, a);
+  ck::adam_begin_kernel<<<1, 1, 0, s>>>(step_dev, bc_dev, beta1, beta2);
   CK_CUDA(cudaGetLastError());
   return ck::kOk;
+}
+
+extern "C" int ck_adam_step_dev(float* param, const float* grad, float* m, float* v, int64_t n, double lr,
+                                double beta1, double beta2, double eps, const float* bc_dev, void* stream) {
+  CK_CHECK(n >= 0, "ck_adam_step_dev: negative size");
+  if (n == 0) return ck::kOk;
+  CK_CHECK(param && grad && m && v && bc_dev, "ck_adam_step_dev: NULL tensor");
+  ck::AdamArgs a;
+  a.lr = static_cast<float>(lr);
+  a.b1 = static_cast<float>(beta1);
+  a.omb1 = static_cast<float>(1.0 - beta1);
+  a.b2 = static_cast<float>(beta2);
+  a.omb2 = static_cast<float>(1.0 - beta2);
+  a.bc1 = a.bc2 = 1.0f;
+  a.eps = static_cast<float>(eps);
+  a.bc_dev = bc_dev;
+  return ck::adam_launch(param, grad, m, v, n, a, static_cast<cudaStream_t>(stream));
 }

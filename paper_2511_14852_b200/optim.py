@@ -45,22 +45,39 @@ class Adam(torch.optim.Optimizer):
     ``step(lr_scale=...)`` multiplies the learning rate for this step only.
     Parameters without a gradient are skipped (their moments stay put), but
     the step counter is shared, as in the reference's AdamState.
+
+    ``capturable=True`` keeps the step counter and the bias corrections on the
+    device (ck_adam_begin / ck_adam_step_dev), so a training step captured in
+    a CUDA graph advances them on every replay; the learning rate (and
+    lr_scale) are then fixed at capture.
     """
 
-    def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8):
+    def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, capturable: bool = False):
         if lr < 0.0:
             raise ValueError(f"invalid learning rate: {lr}")
         super().__init__(params, dict(lr=lr, betas=tuple(betas), eps=eps))
         self._step = 0
+        self.capturable = capturable
+        self._dev_state = {}
 
     @property
     def step_count(self) -> int:
         return self._step
 
+    def _device_counters(self, group_idx: int, device):
+        st = self._dev_state.get((group_idx, device))
+        if st is None:
+            st = (torch.zeros(1, dtype=torch.int64, device=device), torch.ones(2, dtype=torch.float32, device=device))
+            self._dev_state[(group_idx, device)] = st
+        return st
+
     @torch.no_grad()
     def step(self, closure=None, lr_scale: float = 1.0):
         loss = closure() if closure is not None else None
         self._step += 1
+        if self.capturable:
+            self._step_capturable(lr_scale)
+            return loss
         for group in self.param_groups:
             b1, b2 = group["betas"]
             lr = group["lr"] * lr_scale
@@ -74,3 +91,28 @@ class Adam(torch.optim.Optimizer):
                 g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
                 adam_update(p, g, st["m"], st["v"], lr, b1, b2, group["eps"], self._step)
         return loss
+
+    def _step_capturable(self, lr_scale: float) -> None:
+        lib = _lib.lib()
+        for gi, group in enumerate(self.param_groups):
+            b1, b2 = group["betas"]
+            lr = group["lr"] * lr_scale
+            begun = set()
+            for p in group["params"]:
+                if p.grad is None:
+                    continue
+                step_t, bc = self._device_counters(gi, p.device)
+                if p.device not in begun:
+                    _lib.check(lib.ck_adam_begin(step_t.data_ptr(), bc.data_ptr(), float(b1), float(b2),
+                                                 _lib.stream_handle(p.device)), "ck_adam_begin")
+                    begun.add(p.device)
+                st = self.state[p]
+                if not st:
+                    st["m"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
+                    st["v"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
+                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                _lib.check(lib.ck_adam_step_dev(p.data_ptr(), g.data_ptr(), st["m"].data_ptr(), st["v"].data_ptr(),
+                                                p.numel(), float(lr), float(b1), float(b2), float(group["eps"]),
+                                                bc.data_ptr(), _lib.stream_handle(p.device)), "ck_adam_step_dev")
+                for t in (p, st["m"], st["v"]):
+                    torch.autograd.graph.increment_version(t)

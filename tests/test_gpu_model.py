@@ -106,3 +106,47 @@ def test_training_divergence_reports_epoch_and_batch():
     spec = ck.NetworkSpec((ck.LayerSpec(2, 3, 2), ck.LayerSpec(3, 1, 2)))
     with pytest.raises(ck.TrainingDiverged, match="epoch 0, batch 0"):
         ck.network_train(spec, ck.Dataset(x, y), 1, lut_size=256)
+
+
+def test_cuda_graph_training_step_matches_eager():
+    # whole-step capture (forward, backward, capturable Adam) replayed N times
+    # must follow the eager trajectory (device-side Adam step counter)
+    dev = torch.device("cuda", 0)
+
+    def make():
+        torch.manual_seed(0)
+        m = torch.nn.Sequential(ck.ChebyKANLayer(24, 40, 4, lut_size=2048), ck.ChebyKANLayer(40, 3, 3, lut_size=2048),
+                                ).to(dev)
+        return m
+
+    x = torch.randn(512, 24, device=dev)
+    tgt = torch.randn(512, 3, device=dev)
+
+    def run(model, opt):
+        loss = torch.nn.functional.mse_loss(model(x), tgt)
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+
+    eager = make()
+    opt_e = ck.Adam(eager.parameters(), lr=1e-2)
+    for _ in range(7):
+        run(eager, opt_e)
+
+    graphed = make()
+    opt_g = ck.Adam(graphed.parameters(), lr=1e-2, capturable=True)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            run(graphed, opt_g)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run(graphed, opt_g)
+    for _ in range(4):
+        g.replay()
+    torch.cuda.synchronize()
+    # 3 warm-up + 4 replays = 7 updates (capture records, it does not execute)
+    for pe, pg in zip(eager.parameters(), graphed.parameters()):
+        assert torch.allclose(pe, pg, rtol=1e-5, atol=1e-6), (pe - pg).abs().max()
