@@ -1,8 +1,9 @@
 """CPU oracle for the fused Chebyshev-KAN layer -- TEST INFRASTRUCTURE ONLY.
 
-This module is a float64 NumPy restatement of the reference's LUT-mode hot
-path (arxiv 2511.14852 / PolyKAN, package ``polykan`` under
-/root/reference/pkg/src/polykan).  It is the *checker*: only ``tests/``,
+This module is a float64 NumPy restatement of the reference's hot path
+(arxiv 2511.14852 / PolyKAN, package ``polykan`` under
+/root/reference/pkg/src/polykan): the LUT-interpolation and exact-recurrence
+layer for all four basis families (Chebyshev, Legendre, Hermite, Fourier).  It is the *checker*: only ``tests/``,
 ``__graft_entry__.smoke()`` and the ``cpu_baseline`` / ``--impl reference``
 legs of ``bench.py`` may import it.  The product path
 (``paper_2511_14852_b200``) never imports, links or calls anything here and
@@ -11,7 +12,9 @@ fails loudly when its CUDA library is missing.
 Pinning: every function below is checked bit-for-bit (or to <=1e-13 where
 BLAS summation order may differ) against golden vectors produced by running
 the reference itself in the build container (``tests/golden/make_golden.py``
--> ``tests/golden/*.npz``; test ``tests/test_oracle_golden.py``).
+-> ``tests/golden/*.npz``; test ``tests/test_oracle_golden.py``).  The
+trainer and file-format fixtures (``make_golden_train.py``,
+``make_golden_formats.py``) pin the GPU model layer directly.
 
 Citations are ``path:line`` relative to /root/reference/pkg/src/polykan/.
 """
