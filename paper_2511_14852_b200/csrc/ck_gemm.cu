@@ -85,20 +85,27 @@ int gemm_cg() {
   return cg;
 }
 
+int pick_bn(int64_t N) { return N <= 128 ? 128 : 256; }
+
+// CTA group of the store GEMM for a given N tile: pairs for 256-wide tiles.
+int store_cg(int bn) { return bn == 128 ? 1 : gemm_cg(); }
+
+// Split-R factor for a store GEMM: when the output tiles fill less than half
+// a wave of work units (an SM, or an SM pair for cta_group::2), split the
+// reduction so one wave is full -- per-split partials, then the fixed-order
+// merge -- keeping >= 4 K blocks per split.
 int choose_splits(int64_t M, int64_t N, int nz, int64_t R, int bn) {
-  const int64_t tiles = ceil_div(M, kBM) * ceil_div(N, bn) * nz;
+  const int cg = store_cg(bn);
+  const int64_t tiles = ceil_div(M, static_cast<int64_t>(kBM) * cg) * ceil_div(N, bn) * nz;
+  const int64_t units = num_sms() / cg;
+  if (2 * tiles >= units) return 1;
   const int64_t chunks = ceil_div(R, 64);
-  const int64_t sms = num_sms();
-  if (tiles >= sms) return 1;
-  // enough CTAs for ~2 waves, but keep >= 8 64-wide chunks per split
-  int64_t splits = ceil_div(2 * sms, tiles);
-  const int64_t max_splits = chunks / 8 > 1 ? chunks / 8 : 1;
+  int64_t splits = units / tiles;
+  const int64_t max_splits = chunks / 4 > 1 ? chunks / 4 : 1;
   if (splits > max_splits) splits = max_splits;
   if (splits > 64) splits = 64;
   return static_cast<int>(splits < 1 ? 1 : splits);
 }
-
-int pick_bn(int64_t N) { return N <= 128 ? 128 : 256; }
 
 }  // namespace
 

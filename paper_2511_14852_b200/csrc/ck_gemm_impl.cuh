@@ -118,21 +118,11 @@ __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_ti
   return c;
 }
 
-// Fused dX epilogue for one 128-row tile, degree D (compile time): TMEM
-// column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
-// Each thread owns one row; the two warps of a TMEM lane quarter take
-// alternate column blocks of W inputs.  Per element: float32 tanh gives a
-// candidate cell; its dx row {b_c, slopes, b_{c+1}} comes in with S/4
-// 16-byte loads (L2-resident table), and the rare element outside
-// [b_c, b_{c+1}) re-gathers the neighbouring row -- the exact reference cell
-// without any float64 work; then fold with the d accumulators and apply the
-// Jacobian.  The two dependent global loads (x, then its dx row) are
-// software-pipelined: x is loaded two blocks ahead and the dx rows one block
-// ahead, so a short-K tile's epilogue is not a chain of L2 round trips.
 template <int D>
 struct DxBlock {
   static constexpr int K = D + 1;
-  static constexpr int S = dxrow_stride(K);
+  static constexpr int S = dxrow_stride(K);  // floats per dX row
+  static constexpr int NS = (D + 3) / 4;     // 16-byte words holding the D slopes
   // columns per block: as many independent gathers in flight as the
   // register budget allows
   static constexpr int W = D <= 4 ? 8 : (D <= 8 ? 4 : 2);
@@ -168,33 +158,27 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[W]) {
   }
 }
 
-// tanh, candidate cell and the gather of its dx row for each element
-template <int D>
-__device__ __forceinline__ void dx_gather(const KArgs& p, const float (&xv)[DxBlock<D>::W], float (&t)[DxBlock<D>::W],
-                                          float4 (&sl)[DxBlock<D>::W][DxBlock<D>::S / 4]) {
-  constexpr int W = DxBlock<D>::W, S = DxBlock<D>::S;
-  const float hN = 0.5f * static_cast<float>(p.lutN - 1);
-#pragma unroll
-  for (int e = 0; e < W; ++e) {
-    const float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
-    t[e] = tt;
-    const int c = min(static_cast<int>(fmaf(tt, hN, hN)), p.lutN - 2);
-    const float4* rp = reinterpret_cast<const float4*>(p.dxrows) + static_cast<long long>(c) * (S / 4);
-#pragma unroll
-    for (int j = 0; j < S / 4; ++j) sl[e][j] = __ldg(rp + j);
-  }
-}
-
-// One pass over the tile's columns in blocks of W; x of the next block is
-// prefetched while the current block's dx rows are in flight.
+// Fused dX epilogue for one 128-row tile, degree D (compile time): TMEM
+// column (k-1)*n_i + i holds G_k[row][n0+i] = sum_o dy[row][o] C[k][o][n0+i].
+// Each thread owns one row; the two warps of a TMEM lane quarter take
+// alternate column blocks of W inputs, x of the next block prefetched.  Per
+// element: float32 tanh gives the position; its cell's slopes come in with
+// ceil(D/4) 16-byte loads from the L2-resident dX rows.  Only when the
+// float32 position lies within `guard` of a cell edge (where a 2-ulp tanhf
+// error could flip the cell; ~1-3 % of elements) are the cell's
+// reference boundaries {b_c, b_{c+1}} loaded and the cell corrected by one --
+// the exact reference cell without float64 work.  Then fold with the d
+// accumulators and apply the Jacobian.  (Each gather is one L1 wavefront per
+// lane: the load count, not the bytes, bounds short-K tiles.)
 template <int D>
 __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
-  constexpr int K = DxBlock<D>::K, S = DxBlock<D>::S, W = DxBlock<D>::W;
-  const int n_i = p.n_tile;
+  constexpr int K = DxBlock<D>::K, S = DxBlock<D>::S, NS = DxBlock<D>::NS, W = DxBlock<D>::W;
+  const int n_i = p.n_tile, N = p.lutN;
   const float* xr = p.x + static_cast<long long>(row) * p.ldo;
   float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
   const bool vec = ((p.ldo & 3) == 0);
-  const float hN = 0.5f * static_cast<float>(p.lutN - 1);
+  const float hN = 0.5f * static_cast<float>(N - 1);
+  const float4* rows4 = reinterpret_cast<const float4*>(p.dxrows);
   int cb = W * h;
   float xv[W];
   if (cb < n_i) dx_load_x<D>(p, xr, row_ok, n0 + cb, xv);
@@ -203,23 +187,36 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
     uint32_t r[D][W];
 #pragma unroll
     for (int k = 0; k < D; ++k) tmem_ld_cols<W>(tbase + k * n_i + cb, r[k]);
-    float t[W];
-    float4 sl[W][S / 4];
-    dx_gather<D>(p, xv, t, sl);
-    float x_cur[W];
-#pragma unroll
-    for (int e = 0; e < W; ++e) x_cur[e] = xv[e];
-    if (cb + 2 * W < n_i) dx_load_x<D>(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
-    // exact reference cell: b_c <= x < b_{c+1}; at most one step off
+    float x_cur[W], t[W];
+    int cell[W];
+    bool near[W];
+    float4 sl[W][NS];
 #pragma unroll
     for (int e = 0; e < W; ++e) {
-      const float* f = reinterpret_cast<const float*>(sl[e]);
-      const bool lo = x_cur[e] < f[0], hi = !(x_cur[e] < f[K]);
-      if (lo || hi) {
-        const int c = min(static_cast<int>(fmaf(t[e], hN, hN)), p.lutN - 2) + (lo ? -1 : 1);
-        const float4* rp = reinterpret_cast<const float4*>(p.dxrows) + static_cast<long long>(c) * (S / 4);
+      x_cur[e] = xv[e];
+      const float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
+      t[e] = tt;
+      const float pos = fmaf(tt, hN, hN);
+      const int c = min(static_cast<int>(pos), N - 2);
+      const float fr = pos - static_cast<float>(c);
+      cell[e] = c;
+      near[e] = fr < p.guard || fr > 1.0f - p.guard;
 #pragma unroll
-        for (int q = 0; q < S / 4; ++q) sl[e][q] = __ldg(rp + q);
+      for (int j = 0; j < NS; ++j) sl[e][j] = __ldg(rows4 + static_cast<long long>(c) * (S / 4) + j);
+    }
+    if (cb + 2 * W < n_i) dx_load_x<D>(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      if (near[e]) {
+        // exact reference cell: b_c <= x < b_{c+1}; at most one step off
+        const float* rw = p.dxrows + static_cast<long long>(cell[e]) * S;
+        const float bl = __ldg(rw + D), bh = __ldg(rw + K);
+        const bool lo = x_cur[e] < bl, hi = !(x_cur[e] < bh);
+        if (lo || hi) {
+          const long long c2 = cell[e] + (lo ? -1 : 1);
+#pragma unroll
+          for (int j = 0; j < NS; ++j) sl[e][j] = __ldg(rows4 + c2 * (S / 4) + j);
+        }
       }
     }
     tmem_ld_wait();
@@ -229,7 +226,7 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
       const float* f = reinterpret_cast<const float*>(sl[e]);
       float a = 0.0f;
 #pragma unroll
-      for (int k = 0; k < D; ++k) a = fmaf(f[k + 1], __uint_as_float(r[k][e]), a);
+      for (int k = 0; k < D; ++k) a = fmaf(f[k], __uint_as_float(r[k][e]), a);
       acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
     }
     const int i0 = n0 + cb;

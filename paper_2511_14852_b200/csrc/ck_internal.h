@@ -19,12 +19,13 @@ struct ck_lut {
   double* values64 = nullptr;  // [K][N]   float64 build-precision table (validation)
   float* values_pm = nullptr;  // [N][K]   float32, position-major (gather rows idx, idx+1)
   float* slopes_pm = nullptr;  // [N-1][K] float32 cell slopes, position-major
-  // [N][dxrow_stride(K)] input-gradient rows: [0] = b_i, the smallest
-  // float32 x whose reference (float64) cell is >= i (-inf for i = 0, +inf
-  // sentinel for i = N-1), [1..K-1] = the cell's float32 slopes, [K] =
-  // b_{i+1}, zero padding to a 16-byte multiple.  One vectorised gather
-  // gives a kernel the cell's slopes and both boundaries, so it picks the
-  // exact reference cell with float32 compares only.
+  // [N][dxrow_stride(K)] input-gradient rows: [0..K-2] = the cell's float32
+  // slopes of features 1..K-1, [K-1] = b_i, the smallest float32 x whose
+  // reference (float64) cell is >= i (-inf for i = 0, +inf sentinel for
+  // i = N-1), [K] = b_{i+1}, zero padding to a 16-byte multiple.  Kernels
+  // gather the slopes with 16-byte loads and, only when the float32
+  // position lies near a cell edge, the two boundaries -- the exact
+  // reference cell with float32 compares only.
   float* dxrows = nullptr;
 };
 

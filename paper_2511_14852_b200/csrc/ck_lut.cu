@@ -98,15 +98,17 @@ __device__ __forceinline__ int ref_cell(float x, int n) {
   return idx;
 }
 
-// dxrows row i = {b_i, slopes_1..slopes_d of cell i, b_{i+1}, 0 pad}; b_i
-// is the smallest float32 x with ref_cell(x) >= i, found from atanh(node_i)
-// by stepping one float32 ulp at a time (ref_cell is monotone in x).  Thread
-// i writes b_i into its own row and into row i-1's upper-boundary slot.
+// dxrows row i = {slopes_1..slopes_d of cell i, b_i, b_{i+1}, 0 pad} (d =
+// K-1): the slopes first, so the common case (a float32 position safely
+// inside its cell) gathers only ceil(d/4) 16-byte words.  b_i is the
+// smallest float32 x with ref_cell(x) >= i, found from atanh(node_i) by
+// stepping one float32 ulp at a time (ref_cell is monotone in x).  Thread i
+// writes b_i into its own row and into row i-1's upper-boundary slot.
 __global__ void lut_dxrows_kernel(int K, int n, double step, const float* __restrict__ s_pm,
                                   float* __restrict__ rows) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int S = dxrow_stride(K);
+  const int S = dxrow_stride(K), d = K - 1;
   float b;
   if (i == 0) {
     b = -INFINITY;
@@ -123,11 +125,11 @@ __global__ void lut_dxrows_kernel(int K, int n, double step, const float* __rest
     b = x;
   }
   float* row = rows + static_cast<int64_t>(i) * S;
-  row[0] = b;
-  for (int k = 1; k < K; ++k) row[k] = i < n - 1 ? s_pm[static_cast<int64_t>(i) * K + k] : 0.0f;
-  if (i == n - 1) row[K] = INFINITY;
-  for (int j = K + 1; j < S; ++j) row[j] = 0.0f;
-  if (i > 0) rows[static_cast<int64_t>(i - 1) * S + K] = b;
+  for (int k = 1; k < K; ++k) row[k - 1] = i < n - 1 ? s_pm[static_cast<int64_t>(i) * K + k] : 0.0f;
+  row[d] = b;
+  if (i == n - 1) row[d + 1] = INFINITY;
+  for (int j = d + 2; j < S; ++j) row[j] = 0.0f;
+  if (i > 0) rows[static_cast<int64_t>(i - 1) * S + d + 1] = b;
 }
 
 int check_kind(int kind, int degree, bool exact) {

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256) skinny_bwd_kernel(const float* __restrict
       // exact reference cell from the boundary rows (as the fused dX epilogue)
       int cell = min(static_cast<int>(fmaf(t, hN, hN)), L.N - 2);
       const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
-      if (xv < row[0]) {
+      if (xv < row[K - 1]) {
         --cell;
       } else if (!(xv < row[K])) {
         ++cell;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) skinny_bwd_kernel(const float* __restrict
       row = L.dxrows + static_cast<int64_t>(cell) * S;
       elem_basis<P>(L, xv, vv);  // values are continuous: the float32 cell is fine
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k) sv[k] = (k >= 1 && k < K) ? __ldg(row + k) : 0.0f;
+      for (int k = 0; k < KMAX; ++k) sv[k] = (k >= 1 && k < K) ? __ldg(row + k - 1) : 0.0f;
     }
     float gx = 0.0f;
 #pragma unroll
