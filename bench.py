@@ -212,10 +212,21 @@ def run_ours(args, wl):
     torch.manual_seed(1234)  # identical synthetic weights on every rank
     layers = [ck.ChebyKANLayer(i, o, d, lut_size=wl["lut_size"]) for i, o in dims]
     model = (torch.nn.Sequential(*layers) if is_net else layers[0]).to(dev)
-    use_graph = args.graph if args.graph is not None else is_net
+    # graphs on one GPU only (the N>1 exchange brackets its kernel with host barriers)
+    use_graph = (args.graph if args.graph is not None else is_net) and world == 1
     # ck_adam_step (reference adam_step rule); device-side step counter when captured
     opt = ck.Adam(model.parameters(), lr=1e-4, capturable=use_graph)
-    reducer = ck.GradientAllreducer(ck.chebykan_parameters(model)) if world > 1 else None
+    reducer, reducer_kind = None, None
+    if world > 1:
+        params = ck.chebykan_parameters(model)
+        if args.reducer == "peer":
+            try:
+                # the library's fixed-order peer-memory allreduce (CUDA IPC over NVLink)
+                reducer, reducer_kind = ck.PeerAllreducer(params), "ck_allreduce_peers (CUDA IPC, fixed rank order)"
+            except Exception as exc:  # IPC unavailable on this box: NCCL
+                print(f"peer allreduce unavailable ({exc}); using NCCL", file=sys.stderr)
+        if reducer is None:
+            reducer, reducer_kind = ck.GradientAllreducer(params), "NCCL all_reduce (Ring)"
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
     if is_net:
@@ -444,6 +455,7 @@ def run_ours(args, wl):
         "dtype": "fp32 I/O, bf16x3 split tensor-core products, fp32 accumulate", "data": "synthetic",
         "config": {"workload": wl["name"], "global_batch": gb, "rows_per_gpu": rows, "layers": dims,
                    "degree": d, "lut_size": wl["lut_size"], "parallelism": f"dp{world}",
+                   "gradient_exchange": reducer_kind,
                    "l2": ("inputs larger than L2 (x shard >> 126 MB), no flush" if rows * I * 4 > 126e6 else
                           "working set below L2 size; steps run back to back (no flush)")},
         "fwd": {"value": fwd_value, "unit": "samples/s", "ms_per_step": fwd_ms},
@@ -566,6 +578,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     ap.add_argument("--sweep", action="store_true", help="run the C1 sweep table instead of the JSON line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reducer", choices=("peer", "nccl"), default="peer",
+                    help="N>1 gradient exchange: the library's peer-memory kernel or NCCL")
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay a captured CUDA graph of the step (default for the small nets)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")

@@ -161,6 +161,21 @@ CK_API int ck_adam_begin(int64_t* step_dev, float* bc_dev, double beta1, double 
 CK_API int ck_adam_step_dev(float* param, const float* grad, float* m, float* v, int64_t n, double lr,
                      double beta1, double beta2, double eps, const float* bc_dev, void* stream);
 
+/* --- Deterministic cross-rank gradient sum over peer memory ----------------
+ * The data-parallel exchange without NCCL: each rank exports its
+ * flat fp32 gradient buffer (ck_ipc_handle: 64-byte cudaIpcMemHandle of the
+ * enclosing allocation + byte offset), opens every peer's (ck_ipc_open), and
+ * ck_allreduce_peers(bufs[ranks], rank, n) sums shard `rank` of the n
+ * elements over ranks 0..R-1 in ascending order and writes it into every
+ * rank's buffer (reduce-scatter + all-gather by peer stores, in place).
+ * Bit-identical on all ranks and run to run.  Caller brackets it with
+ * cross-rank barriers (inputs complete before; results read after). */
+CK_API int ck_ipc_handle(const void* device_ptr, void* handle_out /*64 bytes*/, int64_t* offset_out);
+CK_API int ck_ipc_open(const void* handle /*64 bytes*/, int64_t offset, void** device_ptr_out);
+CK_API int ck_ipc_close(void* device_ptr, int64_t offset);
+CK_API int ck_allreduce_peers(float* const* bufs /*host array of ranks device pointers*/, int ranks, int rank,
+                       int64_t n, void* stream);
+
 /* --- Diagnostics --------------------------------------------------------------
  * ck_launch_count: kernels this library has launched in the process.
  * ck_timing_enable(1): bracket every launch with CUDA events on its stream;

@@ -66,7 +66,7 @@ from .model import (
     rmsle_loss,
 )
 from .optim import Adam, adam_update, cosine_scale
-from .parallel import GradientAllreducer, allreduce_gradients, chebykan_parameters, shard_bounds
+from .parallel import GradientAllreducer, PeerAllreducer, allreduce_gradients, chebykan_parameters, shard_bounds
 from .tensor import CoeffTensor, Layout, doj_index, jod_index, reorder_to_doj, reorder_to_jod
 
 __version__ = "1.0.0"

@@ -8,10 +8,13 @@ section 8(e)).  Rank shards are contiguous row blocks of the global batch.
 """
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 from torch import nn
 
+from . import _lib
 from .layer import ChebyKANLayer
 
 
@@ -81,6 +84,89 @@ class GradientAllreducer:
                 p.grad = v.view_as(p).clone()
             else:
                 p.grad.copy_(v.view_as(p))
+
+
+class PeerAllreducer(GradientAllreducer):
+    """Deterministic allreduce of the flat gradient over peer memory.
+
+    Same packing as GradientAllreducer, but the exchange is the library's own
+    kernel (ck_allreduce_peers): every rank maps every peer's flat buffer via
+    CUDA IPC (NVLink/NVSwitch peers, or processes sharing a device); rank r
+    sums shard r over ranks 0..R-1 in ascending order and stores it into every
+    rank's buffer.  Results are bit-identical on all ranks and across runs
+    without relying on NCCL's algorithm choice.  The process group (any
+    backend) only carries the handle exchange and the two barriers around the
+    kernel.  Up to 8 ranks.
+    """
+
+    def __init__(self, params: list[torch.nn.Parameter], group=None, average: bool = False):
+        super().__init__(params, group, average)
+        self._peers = None
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            self._open()
+
+    def _open(self) -> None:
+        lib = _lib.lib()
+        world = dist.get_world_size(self.group)
+        if world > 8:
+            raise ValueError("PeerAllreducer supports up to 8 ranks")
+        handle = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_int64()
+        _lib.check(lib.ck_ipc_handle(self.flat.data_ptr(), handle, ctypes.byref(off)), "ck_ipc_handle")
+        mine = (bytes(handle), off.value)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=self.group)
+        me = dist.get_rank(self.group)
+        ptrs = []
+        for r, (h, o) in enumerate(allh):
+            if r == me:
+                ptrs.append(self.flat.data_ptr())
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+            _lib.check(lib.ck_ipc_open(buf, o, ctypes.byref(p)), "ck_ipc_open")
+            ptrs.append(p.value)
+        self._offsets = [o for _, o in allh]
+        self._peers = (ctypes.c_void_p * world)(*ptrs)
+        self._rank, self._world = me, world
+
+    def __call__(self) -> None:
+        if self._peers is None:
+            return
+        views = []
+        off = 0
+        for p in self.params:
+            n = p.numel()
+            v = self.flat[off:off + n]
+            if p.grad is None:
+                v.zero_()
+            else:
+                v.copy_(p.grad.reshape(-1))
+            views.append((p, v))
+            off += n
+        dev = self.flat.device
+        torch.cuda.current_stream(dev).synchronize()
+        dist.barrier(group=self.group)  # every rank's gradient is in its buffer
+        _lib.check(_lib.lib().ck_allreduce_peers(self._peers, self._world, self._rank, self.flat.numel(),
+                                                 _lib.stream_handle(dev)), "ck_allreduce_peers")
+        torch.cuda.current_stream(dev).synchronize()
+        dist.barrier(group=self.group)  # every shard has been written everywhere
+        if self.average:
+            self.flat.div_(self._world)
+        for p, v in views:
+            if p.grad is None:
+                p.grad = v.view_as(p).clone()
+            else:
+                p.grad.copy_(v.view_as(p))
+
+    def close(self) -> None:
+        if self._peers is None:
+            return
+        lib = _lib.lib()
+        for r in range(self._world):
+            if r != self._rank:
+                lib.ck_ipc_close(ctypes.c_void_p(self._peers[r]), self._offsets[r])
+        self._peers = None
 
 
 def allreduce_gradients(module: nn.Module, group=None, average: bool = False) -> None:

@@ -73,3 +73,45 @@ def test_dp_two_ranks_match_full_batch():
         assert orc.normwise_err(rdb, db.cpu().numpy()) <= 1e-6
         assert orc.normwise_err(rdx, dx[lo:hi].cpu().numpy()) <= 1e-6
     assert np.array_equal(res[0][0], res[1][0])  # identical reduced gradients on both ranks
+
+
+def _peer_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2511_14852_b200 as ck
+
+    dev = torch.device("cuda", 0)
+    net = torch.nn.Sequential(ck.ChebyKANLayer(64, 48, 4, lut_size=2048, seed=1),
+                              ck.ChebyKANLayer(48, 5, 3, lut_size=2048, seed=2)).to(dev)
+    params = ck.chebykan_parameters(net)
+    g = torch.Generator().manual_seed(100 + rank)
+    for p in params:  # rank-specific gradients standing in for ck_backward's
+        p.grad = torch.randn(p.shape, generator=g).to(dev)
+    local = [p.grad.clone().cpu() for p in params]
+    red = ck.PeerAllreducer(params)
+    for _ in range(2):  # reusable: second call on fresh copies gives the same bits
+        for p, l in zip(params, local):
+            p.grad.copy_(l.to(dev))
+        red()
+    q.put((rank, [l.numpy() for l in local], [p.grad.cpu().numpy() for p in params]))
+    red.close()
+    dist.destroy_process_group()
+
+
+def test_peer_allreduce_fixed_order_bitwise():
+    # ck_allreduce_peers over CUDA IPC (two processes on one device): the sum
+    # is rank 0 + rank 1 in that order, bit-identical on both ranks
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for i in range(len(res[0][0])):
+        want = (res[0][0][i].astype(np.float32) + res[1][0][i].astype(np.float32)).astype(np.float32)
+        assert np.array_equal(res[0][1][i], want)
+        assert np.array_equal(res[1][1][i], want)
