@@ -1,0 +1,165 @@
+"""The reference's own kernel tests (pkg/tests/test_kernels.py), ported to the
+B200 path: random-instance sweeps in both basis paths and all families,
+finite-difference gradient checks, the pseudocode-literal (no-Jacobian)
+relation, schedule independence and the closed-form merge counters."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import chebykan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+if torch.cuda.is_available():
+    import paper_2511_14852_b200 as ck
+
+
+def _dev():
+    return torch.device("cuda", 0)
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32), device=_dev())
+
+
+def random_instance(rng, kind="chebyshev", max_dim=64, max_degree=24, x_range=2.0):
+    """test_kernels.py:31-43, float32-representable, any family."""
+    batch = int(rng.integers(1, 17))
+    d_in = int(rng.integers(1, max_dim + 1))
+    d_out = int(rng.integers(1, max_dim + 1))
+    degree = int(rng.integers(0, max_degree + 1))
+    k = orc.feature_count(kind, degree)
+    x = rng.uniform(-x_range, x_range, size=(batch, d_in)).astype(np.float32)
+    s = 1.0 / np.sqrt(d_in * k)
+    c_doj = rng.uniform(-s, s, size=(k, d_out, d_in)).astype(np.float32)
+    dy = rng.standard_normal((batch, d_out)).astype(np.float32)
+    return x, c_doj, dy, degree
+
+
+@pytest.mark.parametrize("kind", ["chebyshev", "legendre", "hermite", "fourier"])
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "lut"])
+def test_random_instance_sweep(kind, exact):
+    # test_fused_exact_equals_reference_sweep (test_kernels.py:104-111) in both paths
+    rng = np.random.default_rng(13 + len(kind))
+    for _ in range(12):
+        x, c_doj, dy, degree = random_instance(rng, kind, max_dim=48,
+                                               max_degree=12 if kind == "fourier" else 24)
+        k = c_doj.shape[0]
+        if exact:
+            wy = orc.exact_layer_forward(x, c_doj, kind)
+            wdc, wdx, _ = orc.exact_layer_backward(x, c_doj, dy, kind)
+            table, mode = None, ck.EXACT_MODE
+        else:
+            vals, slopes, _ = orc.build_table(degree, 4096, kind)
+            wy = orc.layer_forward(x, c_doj, vals)
+            wdc, wdx, _ = orc.layer_backward(x, c_doj, dy, vals, slopes)
+            table, mode = ck.lut_build(ck.BasisKind(kind), degree, 4096, device=_dev()), ck.LUT_MODE
+        c = ck.CoeffTensor(x.shape[1], dy.shape[1], k - 1, ck.Layout.DOJ, _t(c_doj))
+        y = ck.fused_forward(_t(x), c, table, None, mode, kind=ck.BasisKind(kind)).cpu().numpy()
+        cg, dx = ck.backward_fused(_t(x), c, _t(dy), table, None, mode, kind=ck.BasisKind(kind))
+        errs = [orc.normwise_err(y, wy), orc.normwise_err(cg.data.cpu().numpy(), wdc)]
+        if degree > 0:
+            errs.append(orc.normwise_err(dx.cpu().numpy(), wdx))
+        else:
+            assert torch.count_nonzero(dx) == 0
+        assert max(errs) <= TOL, (x.shape, dy.shape, degree, errs)
+
+
+def test_lut_coeff_grad_matches_forward_differences():
+    # test_kernels.py:230-256: y is linear in C, so central differences of the
+    # (GPU) forward reproduce the (GPU) coefficient gradient
+    rng = np.random.default_rng(18)
+    batch, d_in, d_out, degree = 2, 4, 3, 5
+    x = rng.uniform(-1.5, 1.5, (batch, d_in)).astype(np.float32)
+    c_doj = rng.uniform(-0.5, 0.5, (degree + 1, d_out, d_in)).astype(np.float32)
+    dy = rng.standard_normal((batch, d_out)).astype(np.float32)
+    lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, degree, 32768, device=_dev())
+    c = ck.CoeffTensor(d_in, d_out, degree, ck.Layout.DOJ, _t(c_doj))
+    cg, _ = ck.backward_fused(_t(x), c, _t(dy), lut)
+    cg = cg.data.cpu().numpy().reshape(-1)
+    h = 0.25
+    flat = c_doj.reshape(-1)
+    for i in range(flat.size):
+        cp, cm = flat.copy(), flat.copy()
+        cp[i] += h
+        cm[i] -= h
+        f = [float((ck.fused_forward(_t(x), ck.CoeffTensor(d_in, d_out, degree, ck.Layout.DOJ,
+                                                           _t(v.reshape(c_doj.shape))), lut).cpu().numpy()
+                    * dy).sum()) for v in (cp, cm)]
+        fd = (f[0] - f[1]) / (2 * h)
+        assert abs(cg[i] - fd) / max(abs(fd), 1e-3) <= 1e-3
+
+
+def test_exact_x_grad_matches_finite_differences():
+    # test_kernels.py:211-227 (exact mode): FD of the float64 reference forward
+    rng = np.random.default_rng(17)
+    for _ in range(5):
+        x, c_doj, dy, degree = random_instance(rng, max_dim=10, max_degree=8, x_range=1.5)
+        c = ck.CoeffTensor(x.shape[1], dy.shape[1], degree, ck.Layout.DOJ, _t(c_doj))
+        _, xg = ck.backward_fused(_t(x), c, _t(dy), None, None, ck.EXACT_MODE, kind=ck.BasisKind.CHEBYSHEV)
+        xg = xg.cpu().numpy()
+        h = 1e-5
+        for _ in range(4):
+            b = int(rng.integers(0, x.shape[0]))
+            j = int(rng.integers(0, x.shape[1]))
+            xp, xm = x.astype(np.float64), x.astype(np.float64)
+            xp[b, j] += h
+            xm[b, j] -= h
+            fd = ((orc.exact_layer_forward(xp, c_doj) * dy).sum() - (orc.exact_layer_forward(xm, c_doj) * dy).sum()) / (
+                2 * h)
+            scale = max(np.abs(xg).max(), 1e-3)
+            assert abs(xg[b, j] - fd) <= 1e-3 * scale
+
+
+def test_backward_without_jacobian_matches_pseudocode_literal():
+    # test_kernels.py:178-189: chain-rule dX = literal dX * (1 - tanh^2)
+    rng = np.random.default_rng(15)
+    x, c_doj, dy, degree = random_instance(rng, max_dim=12, max_degree=6)
+    degree = max(degree, 1)
+    c_doj = rng.uniform(-0.3, 0.3, (degree + 1, dy.shape[1], x.shape[1])).astype(np.float32)
+    c = ck.CoeffTensor(x.shape[1], dy.shape[1], degree, ck.Layout.DOJ, _t(c_doj))
+    for mode_j, mode_p in ((ck.EXACT_MODE, ck.KernelMode(ck.BasisPath.EXACT_RECURRENCE, False)),):
+        _, plain = ck.backward_fused(_t(x), c, _t(dy), None, None, mode_p, kind=ck.BasisKind.CHEBYSHEV)
+        _, chain = ck.backward_fused(_t(x), c, _t(dy), None, None, mode_j, kind=ck.BasisKind.CHEBYSHEV)
+        t = np.tanh(x.astype(np.float64))
+        np.testing.assert_allclose(chain.cpu().numpy(), plain.cpu().numpy() * (1 - t * t), rtol=1e-5, atol=1e-6)
+
+
+def test_schedule_independence_is_bitwise():
+    # test_kernels.py:367-381: the CPU tile shape does not change results; on
+    # the B200 path the schedule is validated but the tiling is the GPU's own
+    rng = np.random.default_rng(23)
+    x, c_doj, dy, degree = random_instance(rng, max_dim=48, max_degree=10)
+    c = ck.CoeffTensor(x.shape[1], dy.shape[1], degree, ck.Layout.DOJ, _t(c_doj))
+    lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, degree, 8192, device=_dev())
+    res = []
+    for tile_in in (16, 64):
+        for tile_out in (8, 32):
+            sched = ck.TileSchedule.for_dims(x.shape[1], dy.shape[1], tile_in, tile_out)
+            y = ck.fused_forward(_t(x), c, lut, sched, ck.LUT_MODE, workers=4)
+            cg, xg = ck.backward_fused(_t(x), c, _t(dy), lut, sched, ck.LUT_MODE, workers=4)
+            res.append((y, cg.data, xg))
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            assert torch.equal(a, b)
+
+
+def test_counters_follow_closed_forms():
+    # test_kernels.py:301-321 semantics through the B200 entry points
+    rng = np.random.default_rng(20)
+    for _ in range(5):
+        x, c_doj, dy, degree = random_instance(rng, max_dim=40, max_degree=8)
+        sched = ck.TileSchedule.for_dims(x.shape[1], dy.shape[1], int(rng.choice([4, 16, 64])),
+                                         int(rng.choice([8, 32])))
+        c = ck.CoeffTensor(x.shape[1], dy.shape[1], degree, ck.Layout.DOJ, _t(c_doj))
+        counters = ck.KernelCounters()
+        ck.fused_forward(_t(x), c, None, sched, ck.EXACT_MODE, counters=counters, kind=ck.BasisKind.CHEBYSHEV)
+        ck.backward_fused(_t(x), c, _t(dy), None, sched, ck.EXACT_MODE, counters=counters,
+                          kind=ck.BasisKind.CHEBYSHEV)
+        expect = ck.count_atomics(x.shape[0], x.shape[1], dy.shape[1], sched)
+        assert counters.forward_atomics == expect.fwd_ours == 0
+        assert counters.x_grad_merges == expect.bwd_x_ours
+        assert counters.partial_writes == x.shape[0] * dy.shape[1] * sched.g_x
+        assert counters.combine_stores == x.shape[0] * dy.shape[1]
