@@ -92,47 +92,6 @@ __device__ __forceinline__ void cell_f64(float xv, int n, int& idx, double& frac
   if (frac > 1.0 - 1e-9) frac = 1.0;
 }
 
-// Cell of tanh(x) with the reference's exact (float64) choice but float32
-// cost: tanhf, then the float64 path only when the float32 position lies
-// within `guard` of a cell edge (where a 2-ulp tanhf error could flip the
-// cell).  Returns t in float32 (for the Jacobian).
-__device__ __forceinline__ int cell_guarded(float xv, int n, float guard, float& t_out) {
-  float t = tanhf(xv);
-  t = fminf(fmaxf(t, -1.0f), 1.0f);
-  const float h = 0.5f * static_cast<float>(n - 1);
-  const float pos = fmaf(t, h, h);
-  int i = min(static_cast<int>(pos), n - 2);
-  const float fr = pos - static_cast<float>(i);
-  t_out = t;
-  if (fr < guard || fr > 1.0f - guard) {
-    double fd, td;
-    cell_f64(xv, n, i, fd, td);
-  }
-  return i;
-}
-
-// fp32(slope) of cell idx for features k = 1..d, recomputed from the two
-// grid nodes by the float64 recurrence: (T_k(x_{i+1}) - T_k(x_i)) * (N-1)/2.
-// Matches the reference's float32 slope table (lut.py:86, 93) except with
-// probability ~2^-29 per value (one float32 ulp) -- no table traffic.
-template <typename F>
-__device__ __forceinline__ void cell_slopes(int idx, int n, double step, int d, F&& emit) {
-  const double x0 = __dadd_rn(-1.0, __dmul_rn(step, static_cast<double>(idx)));
-  const double x1 = idx + 1 >= n - 1 ? 1.0 : __dadd_rn(-1.0, __dmul_rn(step, static_cast<double>(idx + 1)));
-  const double hN = 0.5 * static_cast<double>(n - 1);
-  double pa = 1.0, ca = x0, pb = 1.0, cb = x1;
-  if (d >= 1) emit(1, __double2float_rn((x1 - x0) * hN));
-  const double tx0 = 2.0 * x0, tx1 = 2.0 * x1;
-  for (int k = 2; k <= d; ++k) {
-    const double na = fma(tx0, ca, -pa), nb = fma(tx1, cb, -pb);
-    pa = ca;
-    ca = na;
-    pb = cb;
-    cb = nb;
-    emit(k, __double2float_rn((cb - ca) * hN));
-  }
-}
-
 // --- mbarrier --------------------------------------------------------------
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

@@ -71,10 +71,8 @@ struct KArgs {
   // dx epilogue
   const float* x;
   float* dx;
-  const float* slopes_pm;
   const float* dxrows;
   int lutK, lutN;
-  double step;
   float guard;
   int jacobian;
   int splits;      // R splits per z
@@ -638,11 +636,9 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   if (EPI == kEpiDx) {
     k.x = p.dx->x;
     k.dx = p.dx->dx;
-    k.slopes_pm = p.dx->lut.slopes_pm;
     k.dxrows = p.dx->lut.dxrows;
     k.lutK = p.dx->lut.K;
     k.lutN = p.dx->lut.N;
-    k.step = p.dx->lut.step;
     // float32 position error <= (3e-7 tanhf + ulp) * (N-1)/2; recompute in
     // float64 inside that band
     k.guard = fminf(0.5f, fmaxf(1e-3f, 4e-7f * static_cast<float>(p.dx->lut.N)));
