@@ -252,7 +252,7 @@ extern "C" int ck_device_supported(int device) {
 extern "C" int ck_expand(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi, float* slopes,
                          void* stream) {
   CK_TRY(ck::check_dims(rows, cols, 1, lut));
-  CK_CHECK(x != nullptr && phi != nullptr, "ck_expand: NULL tensor");
+  CK_CHECK(rows == 0 || (x != nullptr && phi != nullptr), "ck_expand: NULL tensor");
   return ck::launch_expand_f32(x, rows, cols, lut, phi, slopes, static_cast<cudaStream_t>(stream));
 }
 
@@ -307,7 +307,7 @@ extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, co
                           const float* bias, float* y, void* workspace, size_t workspace_bytes, void* basis_cache,
                           size_t basis_cache_bytes, void* stream) {
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
-  CK_CHECK(x != nullptr && y != nullptr && prep != nullptr, "ck_forward: NULL tensor");
+  CK_CHECK(prep != nullptr && (batch == 0 || (x != nullptr && y != nullptr)), "ck_forward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
   if (ck::skinny_layer(d_in, d_out, K)) {
     // d_out <= 8: CUDA-core dot products on the fp32 copy in prep
@@ -390,7 +390,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
                            void* workspace, size_t workspace_bytes, const void* basis_cache,
                            size_t basis_cache_bytes, void* stream) {
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
-  CK_CHECK(x != nullptr && dy != nullptr && prep != nullptr, "ck_backward: NULL tensor");
+  CK_CHECK(prep != nullptr && (batch == 0 || (x != nullptr && dy != nullptr)), "ck_backward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
   if (ck::skinny_layer(d_in, d_out, K)) {
     auto s = static_cast<cudaStream_t>(stream);

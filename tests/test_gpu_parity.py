@@ -400,3 +400,43 @@ def test_skinny_output_layers_vs_oracle(o, d, kind, exact):
         layer.coeff_doj.copy_(_t(c_doj))
     layer(_t(x)).backward(_t(dy))
     assert orc.normwise_err(layer.bias.grad.cpu().numpy(), wdb) <= 1e-6
+
+
+@pytest.mark.parametrize("o", [40, 3])
+def test_empty_batch(o):
+    # batch 0: y is (0, O), dC and db are zeros, dX is (0, I) -- both the
+    # tensor-core path and the skinny path
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, 4, 1024, device=_dev())
+    c = ck.CoeffTensor(24, o, 4, ck.Layout.DOJ, torch.randn(5, o, 24, device=_dev()))
+    x = torch.zeros(0, 24, device=_dev())
+    y = ck.fused_forward(x, c, table)
+    assert tuple(y.shape) == (0, o)
+    cg, dx = ck.backward_fused(x, c, torch.zeros(0, o, device=_dev()), table)
+    assert tuple(dx.shape) == (0, 24) and torch.count_nonzero(cg.data) == 0
+    layer = ck.ChebyKANLayer(24, o, 4, lut_size=1024).to(_dev())
+    xx = torch.zeros(0, 24, device=_dev(), requires_grad=True)
+    layer(xx).sum().backward()
+    assert torch.count_nonzero(layer.coeff_doj.grad) == 0 and torch.count_nonzero(layer.bias.grad) == 0
+
+
+def test_multi_chunk_batch_vs_oracle():
+    # 70000 rows = 3 internal 32768-row chunks (ragged last): dC accumulates
+    # across chunks in ascending order, the basis cache holds one slot per
+    # chunk, db sums per-chunk row-block partials
+    b, i, o, d, n = 70000, 64, 48, 3, 2048
+    x, c_jod, dy = orc.bench_inputs(b, i, o, d, seed=11)
+    vals, slopes, _ = orc.build_table(d, n)
+    c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
+    want_y = orc.layer_forward(x, c_doj, vals, threads=8)
+    want_dc, want_dx, want_db = orc.layer_backward(x, c_doj, dy, vals, slopes, threads=8)
+    layer = ck.ChebyKANLayer(i, o, d, lut_size=n).to(_dev())
+    layer.load_jod(c_jod)
+    xt = _t(x).requires_grad_(True)
+    y = layer(xt)
+    y.backward(_t(dy))
+    errs = (orc.normwise_err(y.detach().cpu().numpy(), want_y),
+            orc.normwise_err(layer.coeff_doj.grad.cpu().numpy(), want_dc),
+            orc.normwise_err(xt.grad.cpu().numpy(), want_dx),
+            orc.normwise_err(layer.bias.grad.cpu().numpy(), want_db))
+    print("multi-chunk", [f"{e:.2e}" for e in errs])
+    assert max(errs) <= TOL, errs
