@@ -180,6 +180,14 @@ LaunchScope::~LaunchScope() {
   if (ev_) cudaEventRecord(static_cast<cudaEvent_t>(ev_), stream_);
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CK_PDL");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 void set_error(const std::string& msg) { g_error = msg; }
 const char* last_error() { return g_error.c_str(); }
 

@@ -9,6 +9,7 @@
 
 #include <cstdio>
 #include <string>
+#include <utility>
 
 namespace ck {
 
@@ -54,6 +55,33 @@ __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_
 
 // Number of SMs of the current device (cached per process).
 int num_sms();
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Every library kernel is launched with
+// programmatic stream serialisation, so its launch and prologue (barrier
+// init, TMEM allocation, descriptor prefetch) overlap the tail of the kernel
+// before it on the stream; the kernel calls pdl_wait() -- griddepcontrol.wait:
+// the previous grid has completed and its memory is visible -- before it
+// touches global memory.  CK_PDL=0 disables the attribute (then the wait is a
+// no-op).
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgsT, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgsT...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // Device helpers

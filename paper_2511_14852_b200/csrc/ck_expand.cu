@@ -37,6 +37,7 @@ template <bool kSmem>
 __global__ void __launch_bounds__(kThreads) expand_f32_kernel(const float* __restrict__ x, int64_t n_elem,
                                                               LutView lut, float* __restrict__ phi,
                                                               float* __restrict__ slopes) {
+  pdl_wait();
   extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
   const float* vt = lut.exact ? nullptr : stage_table<kSmem>(lut.values_pm, N * K, sm_tab);
@@ -98,6 +99,7 @@ template <int kSrc, int KIND, int D>
 __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __restrict__ x, int64_t rows, int cols,
                                                                 int lut_n, uint2* __restrict__ hi,
                                                                 uint2* __restrict__ lo, int64_t ld, int64_t plane) {
+  pdl_wait();
   const int64_t pq = plane >> 2;  // plane stride in 8-byte words
   const int quads = (cols + 3) >> 2;
   const int64_t n_items = rows * quads;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
                                                                  uint32_t* __restrict__ hi,
                                                                  uint32_t* __restrict__ lo, int64_t ld,
                                                                  int64_t plane) {
+  pdl_wait();
   const int K = lut.K, N = lut.N;
   const int pairs = (cols + 1) >> 1;
   const int64_t n_items = rows * pairs;
@@ -200,6 +203,7 @@ __global__ void __launch_bounds__(kThreads) dx_combine_kernel(const float* __res
                                                               const float* __restrict__ x, int64_t n_elem,
                                                               LutView lut, int jacobian,
                                                               float* __restrict__ dx) {
+  pdl_wait();
   extern __shared__ float sm_tab[];
   const int K = lut.K, N = lut.N;
   const float* st = lut.exact ? nullptr : stage_table<kSmem>(lut.slopes_pm, N * K, sm_tab);
@@ -237,7 +241,7 @@ int launch_quads_kind(int d, const float* x, int64_t rows, int cols, int lut_n, 
 #define CK_QUADS_CASE(D)                                                                            \
   case D:                                                                                           \
     if constexpr (KIND != kFourier || D % 2 == 0) {                                                 \
-      expand_quads_kernel<kSrc, KIND, D><<<blocks, kThreads, 0, s>>>(x, rows, cols, lut_n, h, l, ld, plane); \
+      CK_CUDA(launch_k((expand_quads_kernel<kSrc, KIND, D>), blocks, kThreads, 0, s, x, rows, cols, lut_n, h, l, ld, plane)); \
       break;                                                                                        \
     } else {                                                                                        \
       return kUnsupported;                                                                          \
@@ -291,9 +295,9 @@ int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut,
   if (tab > 0 && tab <= static_cast<size_t>(kSmemLutMax)) {
     CK_CUDA(cudaFuncSetAttribute(expand_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
-    expand_f32_kernel<true><<<blocks, kThreads, tab, s>>>(x, n, v, phi, slopes);
+    CK_CUDA(launch_k((expand_f32_kernel<true>), blocks, kThreads, tab, s, x, n, v, phi, slopes));
   } else {
-    expand_f32_kernel<false><<<blocks, kThreads, 0, s>>>(x, n, v, phi, slopes);
+    CK_CUDA(launch_k((expand_f32_kernel<false>), blocks, kThreads, 0, s, x, n, v, phi, slopes));
   }
   CK_CUDA(cudaGetLastError());
   return kOk;
@@ -314,8 +318,8 @@ int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* l
     if (rc != kUnsupported) return rc;
   }
   const int blocks = grid_for(rows * ((cols + 1) / 2), 8);
-  expand_planes_kernel<<<blocks, kThreads, 0, s>>>(x, rows, cols, v, k0, reinterpret_cast<uint32_t*>(hi),
-                                                   reinterpret_cast<uint32_t*>(lo), ld, plane);
+  CK_CUDA(launch_k((expand_planes_kernel), blocks, kThreads, 0, s, x, rows, cols, v, k0, reinterpret_cast<uint32_t*>(hi),
+                                                   reinterpret_cast<uint32_t*>(lo), ld, plane));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -332,9 +336,9 @@ int launch_dx_combine(const float* g, int64_t g_plane, const float* x, int64_t r
   if (tab > 0 && tab <= static_cast<size_t>(kSmemLutMax)) {
     CK_CUDA(cudaFuncSetAttribute(dx_combine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(tab)));
-    dx_combine_kernel<true><<<blocks, kThreads, tab, s>>>(g, g_plane, x, n, v, jacobian, dx);
+    CK_CUDA(launch_k((dx_combine_kernel<true>), blocks, kThreads, tab, s, g, g_plane, x, n, v, jacobian, dx));
   } else {
-    dx_combine_kernel<false><<<blocks, kThreads, 0, s>>>(g, g_plane, x, n, v, jacobian, dx);
+    CK_CUDA(launch_k((dx_combine_kernel<false>), blocks, kThreads, 0, s, g, g_plane, x, n, v, jacobian, dx));
   }
   CK_CUDA(cudaGetLastError());
   return kOk;

@@ -86,6 +86,7 @@ template <int O, int P>
 __global__ void __launch_bounds__(256) skinny_fwd_kernel(const float* __restrict__ x, int64_t rows, int I, int K,
                                                          const float* __restrict__ c, const float* __restrict__ bias,
                                                          LutView L, float* __restrict__ y) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(256) skinny_bwd_kernel(const float* __restrict
                                                          LutView L, int jacobian, int64_t rb,
                                                          float* __restrict__ dx, float* __restrict__ part_c,
                                                          double* __restrict__ part_b) {
+  pdl_wait();
   constexpr int KMAX = P + 1;
   __shared__ float red[8][KMAX * O][32];
   __shared__ double redb[8][O];
@@ -255,7 +257,7 @@ int launch_skinny_forward(const float* x, int64_t rows, int I, int O, const floa
   const int pm = K <= 5 ? 4 : K <= 9 ? 8 : K <= 17 ? 16 : 32;
 #define CK_SK(OO, PP)                                                                              \
   if (O == OO && pm == PP) {                                                                       \
-    skinny_fwd_kernel<OO, PP><<<blocks, 256, 0, s>>>(x, rows, I, K, c, bias, L, y);                \
+    CK_CUDA(launch_k((skinny_fwd_kernel<OO, PP>), blocks, 256, 0, s, x, rows, I, K, c, bias, L, y));                \
   } else
   CK_SK(1, 4) CK_SK(1, 8) CK_SK(1, 16) CK_SK(1, 32) CK_SK(2, 4) CK_SK(2, 8) CK_SK(2, 16)
   CK_SK(3, 4) CK_SK(3, 8) CK_SK(4, 4) CK_SK(4, 8)
@@ -282,7 +284,7 @@ int launch_skinny_backward(const float* x, const float* dy, int64_t rows, int I,
   const int pm = K <= 5 ? 4 : K <= 9 ? 8 : K <= 17 ? 16 : 32;
 #define CK_SKB(OO, PP)                                                                                        \
   if (O == OO && pm == PP) {                                                                                  \
-    skinny_bwd_kernel<OO, PP><<<grid, 256, 0, s>>>(x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b); \
+    CK_CUDA(launch_k((skinny_bwd_kernel<OO, PP>), grid, 256, 0, s, x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b)); \
   } else
   CK_SKB(1, 4) CK_SKB(1, 8) CK_SKB(1, 16) CK_SKB(1, 32) CK_SKB(2, 4) CK_SKB(2, 8) CK_SKB(2, 16)
   CK_SKB(3, 4) CK_SKB(3, 8) CK_SKB(4, 4) CK_SKB(4, 8)

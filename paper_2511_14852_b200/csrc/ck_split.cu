@@ -18,6 +18,7 @@ int blocks_for(int64_t items, int per_sm = 8) {
 __global__ void split_rows_kernel(const float* __restrict__ in, int64_t nz, int64_t rows, int64_t cols,
                                   int64_t in_zs, uint32_t* __restrict__ hi, uint32_t* __restrict__ lo,
                                   int64_t ld, int64_t out_zs) {
+  pdl_wait();
   const int64_t pairs = (cols + 1) >> 1;
   const int64_t n = nz * rows * pairs;
   for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n;
@@ -47,6 +48,7 @@ __global__ void __launch_bounds__(256) split_rows_colsum_kernel(const float* __r
                                                                 int64_t cols, int64_t rb, uint32_t* __restrict__ hi,
                                                                 uint32_t* __restrict__ lo, int64_t ld,
                                                                 double* __restrict__ part) {
+  pdl_wait();
   __shared__ double red[8][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.y) * 64 + 2 * lane;
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(256) split_rows_colsum_kernel(const float* __r
 __global__ void split_transpose_kernel(const float* __restrict__ in, int64_t nz, int64_t rows, int64_t cols,
                                        int64_t in_zs, __nv_bfloat16* __restrict__ hi,
                                        __nv_bfloat16* __restrict__ lo, int64_t ld, int64_t out_zs) {
+  pdl_wait();
   __shared__ float tile[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
   const int64_t rt = ceil_div(rows, 32), ct = ceil_div(cols, 32);
@@ -136,6 +139,7 @@ __global__ void split_transpose_kernel(const float* __restrict__ in, int64_t nz,
 __global__ void split_transpose_stacked_kernel(const float* __restrict__ c, int64_t K, int64_t O, int64_t I, int n_i,
                                                __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
                                                int64_t ld) {
+  pdl_wait();
   __shared__ float tile[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t d = K - 1;
@@ -167,6 +171,7 @@ __global__ void split_transpose_stacked_kernel(const float* __restrict__ c, int6
 
 // one warp per row, float64 lane partials combined by a fixed shuffle tree
 __global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, float* __restrict__ out) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -182,6 +187,7 @@ __global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64
 // part[s][c] = sum of rows [s*chunk, min((s+1)*chunk, rows)) of column c
 __global__ void col_partial_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, int64_t chunk,
                                    double* __restrict__ part, int slots) {
+  pdl_wait();
   const int64_t n = static_cast<int64_t>(slots) * cols;
   for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n;
        it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -198,6 +204,7 @@ __global__ void col_partial_kernel(const float* __restrict__ in, int64_t rows, i
 // order for a given slot count: deterministic).
 __global__ void __launch_bounds__(256) col_finish_kernel(const double* __restrict__ part, int slots, int64_t cols,
                                                          float* __restrict__ out) {
+  pdl_wait();
   __shared__ double red[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
@@ -217,6 +224,7 @@ __global__ void __launch_bounds__(256) col_finish_kernel(const double* __restric
 // out[n] = (acc ? out[n] : 0) + sum_s partials[s*stride + n], ascending s
 __global__ void merge_kernel(const float* __restrict__ partials, int S, int64_t stride, int64_t n,
                              float* __restrict__ out, int accumulate) {
+  pdl_wait();
   const bool vec = (stride % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(partials) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -244,6 +252,7 @@ __global__ void merge_kernel(const float* __restrict__ partials, int S, int64_t 
 
 __global__ void fill_rows_kernel(float* __restrict__ out, int64_t rows, int64_t cols, const float* __restrict__ a,
                                  const float* __restrict__ b) {
+  pdl_wait();
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -254,6 +263,7 @@ __global__ void fill_rows_kernel(float* __restrict__ out, int64_t rows, int64_t 
 
 __global__ void add_rows_kernel(float* __restrict__ out, int64_t rows, int64_t cols, const float* __restrict__ a,
                                 const float* __restrict__ b) {
+  pdl_wait();
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -263,6 +273,7 @@ __global__ void add_rows_kernel(float* __restrict__ out, int64_t rows, int64_t c
 }
 
 __global__ void broadcast_cols_kernel(float* __restrict__ out, int64_t rows, int64_t cols, const float* __restrict__ v) {
+  pdl_wait();
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -277,8 +288,8 @@ int launch_split_rows(const float* in, int64_t nz, int64_t rows, int64_t cols, i
   if (nz * rows * cols == 0) return kOk;
   CK_CHECK(ld % 2 == 0 && out_zs % 2 == 0, "split_rows: pitch must be even");
   LaunchScope scope(kKSplit, s);
-  split_rows_kernel<<<blocks_for(nz * rows * ((cols + 1) / 2)), kThreads, 0, s>>>(
-      in, nz, rows, cols, in_zs, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, out_zs);
+  CK_CUDA(launch_k((split_rows_kernel), blocks_for(nz * rows * ((cols + 1) / 2)), kThreads, 0, s, 
+      in, nz, rows, cols, in_zs, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, out_zs));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -289,8 +300,8 @@ int launch_split_rows_colsum(const float* in, int64_t rows, int64_t cols, __nv_b
   CK_CHECK(ld % 2 == 0, "split_rows_colsum: pitch must be even");
   const int64_t rb = ceil_div(rows > 0 ? rows : 1, slots);
   LaunchScope scope(kKSplit, s);
-  split_rows_colsum_kernel<<<dim3(static_cast<unsigned>(slots), static_cast<unsigned>(ceil_div(cols, 64))), 256, 0, s>>>(
-      in, rows, cols, rb, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, part);
+  CK_CUDA(launch_k((split_rows_colsum_kernel), dim3(static_cast<unsigned>(slots), static_cast<unsigned>(ceil_div(cols, 64))), 256, 0, s, 
+      in, rows, cols, rb, reinterpret_cast<uint32_t*>(hi), reinterpret_cast<uint32_t*>(lo), ld, part));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -301,8 +312,8 @@ int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t co
   const int64_t tiles = nz * ceil_div(rows, 32) * ceil_div(cols, 32);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   LaunchScope scope(kKSplit, s);
-  split_transpose_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s>>>(in, nz, rows, cols, in_zs,
-                                                                                         hi, lo, ld, out_zs);
+  CK_CUDA(launch_k((split_transpose_kernel), static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s, in, nz, rows, cols, in_zs,
+                                                                                         hi, lo, ld, out_zs));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -314,8 +325,8 @@ int launch_split_transpose_stacked(const float* c_doj, int64_t K, int64_t O, int
   const int64_t tiles = (K - 1) * ceil_div(O, 32) * ceil_div(i_pad, 32);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   LaunchScope scope(kKSplit, s);
-  split_transpose_stacked_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s>>>(c_doj, K, O, I, n_i,
-                                                                                                 hi, lo, ld);
+  CK_CUDA(launch_k((split_transpose_stacked_kernel), static_cast<int>(tiles < cap ? tiles : cap), kThreads, 0, s, c_doj, K, O, I, n_i,
+                                                                                                 hi, lo, ld));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -323,7 +334,7 @@ int launch_split_transpose_stacked(const float* c_doj, int64_t K, int64_t O, int
 int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s) {
   if (rows == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  row_sum_kernel<<<blocks_for(rows * 32), kThreads, 0, s>>>(in, rows, cols, out);
+  CK_CUDA(launch_k((row_sum_kernel), blocks_for(rows * 32), kThreads, 0, s, in, rows, cols, out));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -332,7 +343,7 @@ int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part
   if (cols == 0) return kOk;
   const int64_t chunk = ceil_div(rows > 0 ? rows : 1, slots);
   LaunchScope scope(kKReduce, s);
-  col_partial_kernel<<<blocks_for(slots * cols), kThreads, 0, s>>>(in, rows, cols, chunk, part, slots);
+  CK_CUDA(launch_k((col_partial_kernel), blocks_for(slots * cols), kThreads, 0, s, in, rows, cols, chunk, part, slots));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -340,7 +351,7 @@ int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part
 int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s) {
   if (cols == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  col_finish_kernel<<<static_cast<unsigned>(ceil_div(cols, 32)), 256, 0, s>>>(part, slots, cols, out);
+  CK_CUDA(launch_k((col_finish_kernel), static_cast<unsigned>(ceil_div(cols, 32)), 256, 0, s, part, slots, cols, out));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -348,7 +359,7 @@ int launch_col_finish(const double* part, int slots, int64_t cols, float* out, c
 int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate, cudaStream_t s) {
   if (n == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  merge_kernel<<<blocks_for(ceil_div(n, 4)), kThreads, 0, s>>>(partials, S, stride, n, out, accumulate);
+  CK_CUDA(launch_k((merge_kernel), blocks_for(ceil_div(n, 4)), kThreads, 0, s, partials, S, stride, n, out, accumulate));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -356,7 +367,7 @@ int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float*
 int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s) {
   if (rows * cols == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  fill_rows_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, a, b);
+  CK_CUDA(launch_k((fill_rows_kernel), blocks_for(rows * cols), kThreads, 0, s, out, rows, cols, a, b));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -364,7 +375,7 @@ int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, con
 int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s) {
   if (rows * cols == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  add_rows_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, a, b);
+  CK_CUDA(launch_k((add_rows_kernel), blocks_for(rows * cols), kThreads, 0, s, out, rows, cols, a, b));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -372,7 +383,7 @@ int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, cons
 int launch_broadcast_cols(float* out, int64_t rows, int64_t cols, const float* v, cudaStream_t s) {
   if (rows * cols == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  broadcast_cols_kernel<<<blocks_for(rows * cols), kThreads, 0, s>>>(out, rows, cols, v);
+  CK_CUDA(launch_k((broadcast_cols_kernel), blocks_for(rows * cols), kThreads, 0, s, out, rows, cols, v));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }

@@ -29,6 +29,7 @@ __device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, 
 __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
                                                         float* __restrict__ m, float* __restrict__ v, int64_t n,
                                                         AdamArgs a) {
+  pdl_wait();
   if (a.bc_dev) {
     a.bc1 = a.bc_dev[0];
     a.bc2 = a.bc_dev[1];
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, c
 
 // step += 1; bc = {1 - b1^step, 1 - b2^step} (float64 pow, model.py:262-263)
 __global__ void adam_begin_kernel(int64_t* step, float* bc, double b1, double b2) {
+  pdl_wait();
   const int64_t t = ++(*step);
   bc[0] = static_cast<float>(1.0 - pow(b1, static_cast<double>(t)));
   bc[1] = static_cast<float>(1.0 - pow(b2, static_cast<double>(t)));
@@ -70,7 +72,7 @@ int adam_launch(float* param, const float* grad, float* m, float* v, int64_t n, 
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   const int blocks = static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
   LaunchScope scope(kKOptim, s);
-  adam_kernel<<<blocks, kThreads, 0, s>>>(param, grad, m, v, n, a);
+  CK_CUDA(launch_k((adam_kernel), blocks, kThreads, 0, s, param, grad, m, v, n, a));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -102,7 +104,7 @@ extern "C" int ck_adam_begin(int64_t* step_dev, float* bc_dev, double beta1, dou
   CK_CHECK(step_dev && bc_dev, "ck_adam_begin: NULL pointer");
   auto s = static_cast<cudaStream_t>(stream);
   ck::LaunchScope scope(ck::kKOptim, s);
-  ck::adam_begin_kernel<<<1, 1, 0, s>>>(step_dev, bc_dev, beta1, beta2);
+  CK_CUDA(ck::launch_k((ck::adam_begin_kernel), 1, 1, 0, s, step_dev, bc_dev, beta1, beta2));
   CK_CUDA(cudaGetLastError());
   return ck::kOk;
 }
