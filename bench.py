@@ -189,11 +189,18 @@ def run_ours(args, wl):
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # CK_BENCH_BACKEND=gloo lets N ranks share fewer GPUs (plumbing checks on a
+    # 1-GPU box; NCCL refuses two ranks per device); the default is NCCL
+    backend = os.environ.get("CK_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("NCCL_ALGO", "Ring")  # fixed reduction order -> reproducible dC
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     if _lib.lib().ck_device_supported(local) != 1:
         raise SystemExit(f"device {torch.cuda.get_device_name(local)} is not sm_100 (B200)")
 
@@ -260,13 +267,13 @@ def run_ours(args, wl):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         torch.cuda.synchronize(dev)
 
     def max_over_ranks(ms):
         if world == 1:
             return ms
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
