@@ -537,8 +537,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                      static_cast<long long>(tc.split) * p.out_split_stride;
         float* orow = out + static_cast<long long>(row) * p.ldo;
         const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+        // 32-column chunks of the (runtime) tile width, alternating between
+        // the two warps of this TMEM lane quarter
 #pragma unroll 1
-        for (int c = h * (BN / 2); c < (h + 1) * (BN / 2); c += 32) {
+        for (int c = 32 * h; c < p.n_tile; c += 64) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tbase + c, r);
           tmem_ld_wait();
@@ -617,7 +619,18 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   using C = Cfg<BN, BK, STAGES, CG>;
   constexpr int kRowBytes = C::kRowBytes;
   const int r_chunks = static_cast<int>(ceil_div(p.R, BK));
-  const int n_tile = EPI == kEpiDx ? p.dx->n_i : BN;
+  // store GEMMs: the N tile width is a runtime multiple of 32 (64 per CTA for
+  // MN-major B slabs) <= BN, spreading N evenly over ceil(N/BN) tiles -- a
+  // ragged N (e.g. 257) then wastes one 32-column step, not half a tile
+  int n_tile = BN;
+  if (EPI != kEpiDx) {
+    const int gran = BMN ? 64 * CG : 32;
+    const int64_t tiles = ceil_div(p.b.rows, BN);
+    n_tile = static_cast<int>(round_up(ceil_div(p.b.rows, tiles), gran));
+    if (n_tile > BN) n_tile = BN;
+  } else {
+    n_tile = p.dx->n_i;
+  }
   const int b_boxes = EPI == kEpiDx ? p.S : 1;
   const int n_mma = n_tile * b_boxes;
   CK_CHECK(n_mma % (8 * CG) == 0 && n_mma <= BN, "gemm: bad MMA N");
