@@ -410,6 +410,41 @@ def run_ours(args, wl):
         opt.zero_grad(set_to_none=True)
         return float(loss.item())  # D2H of the step's result
 
+    e2e_mode = f"eager, {n_mb} micro-batches of {mb} rows (copy of j+1 overlaps compute of j)"
+    if graph is not None and n_mb == 1:
+        # launch-bound nets: the whole e2e step -- H2D copies of x/dy from
+        # pinned memory, forward, backward, Adam, D2H copy of the loss -- is
+        # one captured CUDA graph; every step still moves its inputs in and
+        # reads its loss back on the host
+        loss_h = torch.zeros((), dtype=torch.float32, pin_memory=True)
+
+        def e2e_body():
+            xb[0][:rows].copy_(x_h, non_blocking=True)
+            dyb[0][:rows].copy_(dy_h, non_blocking=True)
+            y = model(xb[0][:rows])
+            loss = torch.nn.functional.mse_loss(y, dyb[0][:rows])
+            loss.backward()
+            opt.step()
+            opt.zero_grad(set_to_none=True)
+            loss_h.copy_(loss.detach(), non_blocking=True)
+
+        side2 = torch.cuda.Stream(device=dev)
+        side2.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side2):
+            for _ in range(2):
+                e2e_body()
+        torch.cuda.current_stream(dev).wait_stream(side2)
+        barrier()
+        g_e2e = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_e2e):
+            e2e_body()
+
+        def e2e_step():  # noqa: F811 (graph-replay form of the same step)
+            g_e2e.replay()
+            torch.cuda.current_stream(dev).synchronize()
+            return float(loss_h)
+
+        e2e_mode = "one captured CUDA graph per step (H2D x/dy from pinned memory, step, D2H loss)"
     e2e_step()  # warm the copy path
     barrier()
     e2e_steps = max(1, min(args.steps, 3))
@@ -468,8 +503,7 @@ def run_ours(args, wl):
         "fwd": {"value": fwd_value, "unit": "samples/s", "ms_per_step": fwd_ms},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": 4 * rows * (I + O),
                 "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms, "wall_ms_per_step": e2e_wall * 1e3,
-                "path": "ChebyKANLayer forward/backward + Adam; x/dy streamed from pinned host in "
-                        f"{n_mb} micro-batches of {mb} rows (copy of j+1 overlaps compute of j)"},
+                "path": f"ChebyKANLayer forward/backward + Adam; x/dy from pinned host: {e2e_mode}"},
         "gpu_launches": launches,
         "roofline": {
             "bound": "tensor", "kernel": "gemm_bf16x3 (tcgen05 fwd + dX + dC, BF16x3)",
