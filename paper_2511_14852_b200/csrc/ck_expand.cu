@@ -102,12 +102,22 @@ __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __r
   pdl_wait();
   const int64_t pq = plane >> 2;  // plane stride in 8-byte words
   const int quads = (cols + 3) >> 2;
-  const int64_t n_items = rows * quads;
   const bool vec = (cols & 3) == 0;
-  for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < n_items;
-       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = it / quads;
-    const int c = static_cast<int>(it - r * quads) * 4;
+  // grid-stride over (row, quad) items, advanced incrementally (one division
+  // per thread instead of a 64-bit division per item)
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t it0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t sr = stride / quads;
+  const int sq = static_cast<int>(stride - sr * quads);
+  int64_t r = it0 / quads;
+  int q = static_cast<int>(it0 - r * quads);
+  for (; r < rows; r += sr, q += sq) {
+    if (q >= quads) {
+      q -= quads;
+      ++r;
+      if (r >= rows) break;
+    }
+    const int c = q * 4;
     const float* xr = x + r * cols + c;
     float xv[4];
     if (vec) {
