@@ -123,7 +123,7 @@ struct DxBlock {
   static constexpr int NS = (D + 3) / 4;     // 16-byte words holding the D slopes
   // columns per block: as many independent gathers in flight as the
   // register budget allows
-  static constexpr int W = D <= 4 ? 8 : (D <= 8 ? 4 : 2);
+  static constexpr int W = D <= 4 ? 8 : 4;
 };
 
 template <int D>

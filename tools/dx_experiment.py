@@ -1,10 +1,20 @@
-import sys, torch
+"""Device time of the input-gradient path (fused dX GEMM, or the unfused
+GEMM + combine) at a few short-K shapes (dev tool).
+
+    python tools/dx_experiment.py LABEL
+"""
+import sys
+
+import torch
+
 sys.path.insert(0, ".")
-import paper_2511_14852_b200 as ck
-from paper_2511_14852_b200.kernels import PreparedCoeff, backward_raw
-from paper_2511_14852_b200 import _lib
+import paper_2511_14852_b200 as ck  # noqa: E402
+from paper_2511_14852_b200 import _lib  # noqa: E402
+from paper_2511_14852_b200.kernels import PreparedCoeff, backward_raw  # noqa: E402
+
 dev = torch.device("cuda", 0)
-for (b, i, o, d) in [(16384, 256, 256, 3), (16384, 512, 512, 5), (16384, 256, 256, 8)]:
+for (b, i, o, d) in [(16384, 256, 256, 3), (16384, 512, 512, 5), (16384, 256, 256, 8), (32000, 512, 512, 15),
+                     (16384, 1024, 1024, 8)]:
     x = torch.rand(b, i, device=dev) * 3 - 1.5
     c = (torch.rand(d + 1, o, i, device=dev) * 2 - 1) / (i * (d + 1)) ** 0.5
     dy = torch.randn(b, o, device=dev)
@@ -13,9 +23,13 @@ for (b, i, o, d) in [(16384, 256, 256, 3), (16384, 512, 512, 5), (16384, 256, 25
     for _ in range(3):
         backward_raw(x, dy, prep, lut, True, want_dc=False, want_db=False)
     torch.cuda.synchronize()
-    _lib.timing_collect(); _lib.timing_enable(True)
+    _lib.timing_collect()
+    _lib.timing_enable(True)
     for _ in range(10):
         backward_raw(x, dy, prep, lut, True, want_dc=False, want_db=False)
-    torch.cuda.synchronize(); _lib.timing_enable(False)
+    torch.cuda.synchronize()
+    _lib.timing_enable(False)
     kt = _lib.timing_collect()
-    print(sys.argv[1], (b, i, o, d), "gemm_dx us/launch", round(kt["gemm_dx"][0] / kt["gemm_dx"][1] * 1e3, 1))
+    tot = sum(v[0] for k, v in kt.items() if k in ("gemm_dx", "dx_combine")) / 10 * 1e3
+    print(sys.argv[1] if len(sys.argv) > 1 else "", (b, i, o, d), "dX path us", round(tot, 1),
+          {k: round(v[0] / 10 * 1e3, 1) for k, v in kt.items() if v[1]})
