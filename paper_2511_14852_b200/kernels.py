@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from .basis import BasisKind, as_kind, degree_for
-from .lut import ExactBasis, LutTable, exact_basis
+from .lut import ExactBasis, exact_basis
 from .tensor import CoeffTensor, Layout
 
 

@@ -1,7 +1,6 @@
 import pathlib
 import sys
 
-import pytest
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import GOLDEN, golden_kind_cases, golden_kind_lut_cases, golden_layer_cases, golden_lut_cases
+from conftest import golden_kind_cases, golden_kind_lut_cases, golden_layer_cases, golden_lut_cases
 from oracle import chebykan_oracle as orc
 
 pytestmark = pytest.mark.gpu

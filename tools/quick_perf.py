@@ -1,6 +1,5 @@
 """Quick CUDA-event timing of fused forward / backward at a few shapes (dev tool)."""
 import sys
-import time
 
 import numpy as np
 import torch
