@@ -85,19 +85,24 @@ int gemm_cg() {
   return cg;
 }
 
-int pick_bn(int64_t N) { return N <= 128 ? 128 : 256; }
+// Store-GEMM tile configuration: the tile capacity BN and the CTA group.
+// N <= 128: single-CTA 128x128 tiles; otherwise 256-wide tiles on CTA pairs.
+// (128-wide pair tiles would fill partial waves better at some shapes, but
+// measured 5-12 % slower: twice the A-operand traffic per MMA.)
+struct StoreCfg {
+  int bn, cg;
+};
 
-// CTA group of the store GEMM for a given N tile: pairs for 256-wide tiles.
-int store_cg(int bn) { return bn == 128 ? 1 : gemm_cg(); }
+StoreCfg pick_store(int64_t N) { return N <= 128 ? StoreCfg{128, 1} : StoreCfg{256, gemm_cg()}; }
 
 // Split-R factor for a store GEMM: when the output tiles fill less than half
 // a wave of work units (an SM, or an SM pair for cta_group::2), split the
 // reduction so one wave is full -- per-split partials, then the fixed-order
 // merge -- keeping >= 4 K blocks per split.
-int choose_splits(int64_t M, int64_t N, int nz, int64_t R, int bn) {
-  const int cg = store_cg(bn);
-  const int64_t tiles = ceil_div(M, static_cast<int64_t>(kBM) * cg) * ceil_div(N, bn) * nz;
-  const int64_t units = num_sms() / cg;
+int choose_splits(int64_t M, int64_t N, int nz, int64_t R, const StoreCfg& c, bool mn_major) {
+  const int nt = store_ntile(N, c.bn, c.cg, mn_major);
+  const int64_t tiles = ceil_div(M, static_cast<int64_t>(kBM) * c.cg) * ceil_div(N, nt) * nz;
+  const int64_t units = num_sms() / c.cg;
   if (2 * tiles >= units) return 1;
   const int64_t chunks = ceil_div(R, 64);
   int64_t splits = units / tiles;
@@ -110,7 +115,13 @@ int choose_splits(int64_t M, int64_t N, int nz, int64_t R, int bn) {
 }  // namespace
 
 int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R) {
-  const int splits = choose_splits(M, N, nz, R, pick_bn(N));
+  // the larger of the two operand majornesses' choices (the workspace is
+  // sized before the caller knows which GEMM runs)
+  int splits = 1;
+  for (bool mn : {false, true}) {
+    const int sp = choose_splits(M, N, nz, R, pick_store(N), mn);
+    if (sp > splits) splits = sp;
+  }
   return splits > 1 ? static_cast<int64_t>(splits) * nz * M * N : 0;
 }
 
@@ -136,8 +147,9 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   }
   CK_CHECK(p.a.rows >= 1 && p.b.rows >= 1, "gemm: empty output");
   CK_CHECK(p.a.rows < (1ll << 31) && p.b.rows < (1ll << 31), "gemm: extent too large");
-  const int bn = pick_bn(p.b.rows);
-  int splits = choose_splits(p.a.rows, p.b.rows, p.nz, p.R, bn);
+  const bool mn = p.a.mn_major || p.b.mn_major;
+  const StoreCfg cfg = pick_store(p.b.rows);
+  int splits = choose_splits(p.a.rows, p.b.rows, p.nz, p.R, cfg, mn);
   const int64_t need = static_cast<int64_t>(splits) * p.nz * p.a.rows * p.b.rows;
   if (splits > 1 && (p.split_ws == nullptr || p.split_ws_elems < need)) splits = 1;
   const bool dense_out = p.ldo == p.b.rows && p.out_z_stride == p.a.rows * p.b.rows;
@@ -157,19 +169,19 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   // partial slot layout: [split][z][M][N]; the kernel offsets by split first
   int rc;
   const bool bk64 = gemm_bk() == 64;
-  if (p.a.mn_major || p.b.mn_major) {
+  if (mn) {
     CK_CHECK(p.a.mn_major && p.b.mn_major, "gemm: mixed-majorness store GEMM not instantiated");
-    if (bn == 128) {
+    if (cfg.bn == 128) {
       rc = launch<128, 64, 3, kEpiStore, 1, 1, 1>(q, splits, out, split_stride, acc, s);
-    } else if (gemm_cg() == 2) {
+    } else if (cfg.cg == 2) {
       rc = launch<256, 64, 3, kEpiStore, 2, 1, 1>(q, splits, out, split_stride, acc, s);
     } else {
       rc = launch<256, 64, 2, kEpiStore, 1, 1, 1>(q, splits, out, split_stride, acc, s);
     }
-  } else if (bn == 128) {
+  } else if (cfg.bn == 128) {
     rc = bk64 ? launch<128, 64, 3, kEpiStore, 1>(q, splits, out, split_stride, acc, s)
               : launch<128, 32, 6, kEpiStore, 1>(q, splits, out, split_stride, acc, s);
-  } else if (gemm_cg() == 2) {
+  } else if (cfg.cg == 2) {
     rc = bk64 ? launch<256, 64, 3, kEpiStore, 2>(q, splits, out, split_stride, acc, s)
               : launch<256, 32, 6, kEpiStore, 2>(q, splits, out, split_stride, acc, s);
   } else {

@@ -31,6 +31,14 @@ namespace ck {
 int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t rows, int64_t segs, int64_t ld,
              int64_t seg_stride, int box_rows, int bk, int mn_major = 0);
 int gemm_group();
+// Store-GEMM N tile: a multiple of 32 (64 per CTA for MN-major B slabs) <= BN
+// spreading N evenly over ceil(N/BN) tiles.
+inline int store_ntile(int64_t N, int BN, int CG, bool mn_major) {
+  const int gran = mn_major ? 64 * CG : 32;
+  const int64_t tiles = ceil_div(N, BN);
+  const int nt = static_cast<int>(round_up(ceil_div(N, tiles), gran));
+  return nt > BN ? BN : nt;
+}
 // fused dX GEMM with the exact-mode (analytic derivative) epilogue (ck_gemm_dx_exact.cu)
 int launch_dx_exact(const struct GemmProblem& p, cudaStream_t s);
 
@@ -622,15 +630,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   // store GEMMs: the N tile width is a runtime multiple of 32 (64 per CTA for
   // MN-major B slabs) <= BN, spreading N evenly over ceil(N/BN) tiles -- a
   // ragged N (e.g. 257) then wastes one 32-column step, not half a tile
-  int n_tile = BN;
-  if (EPI != kEpiDx) {
-    const int gran = BMN ? 64 * CG : 32;
-    const int64_t tiles = ceil_div(p.b.rows, BN);
-    n_tile = static_cast<int>(round_up(ceil_div(p.b.rows, tiles), gran));
-    if (n_tile > BN) n_tile = BN;
-  } else {
-    n_tile = p.dx->n_i;
-  }
+  const int n_tile = EPI != kEpiDx ? store_ntile(p.b.rows, BN, CG, BMN) : p.dx->n_i;
   const int b_boxes = EPI == kEpiDx ? p.S : 1;
   const int n_mma = n_tile * b_boxes;
   CK_CHECK(n_mma % (8 * CG) == 0 && n_mma <= BN, "gemm: bad MMA N");
