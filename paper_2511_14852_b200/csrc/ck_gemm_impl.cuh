@@ -17,6 +17,8 @@
 #pragma once
 #include <cudaTypedefs.h>
 
+#include <atomic>
+
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -677,10 +679,14 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.bias1 = splits == 1 ? p.bias1 : nullptr;
   k.accumulate = accumulate;
   auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the opt-in shared-memory size is a per-device function attribute
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  CK_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
     CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
-    attr_set = true;
+    attr_set.fetch_or(bit);
   }
   k.group_m = gemm_group();
   k.n_tiles = static_cast<int>(ceil_div(k.N, n_tile));
