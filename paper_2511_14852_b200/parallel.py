@@ -129,6 +129,29 @@ class PeerAllreducer(GradientAllreducer):
         self._offsets = [o for _, o in allh]
         self._peers = (ctypes.c_void_p * world)(*ptrs)
         self._rank, self._world = me, world
+        self._self_test()
+
+    def _self_test(self) -> None:
+        """One exchange on a known pattern before use: every rank must see
+        sum_r (r + 1) everywhere, agreed by all ranks, else ValueError (the
+        caller falls back to NCCL)."""
+        dev = self.flat.device
+        saved = self.flat.clone()
+        self.flat.fill_(float(self._rank + 1))
+        torch.cuda.current_stream(dev).synchronize()
+        dist.barrier(group=self.group)
+        _lib.check(_lib.lib().ck_allreduce_peers(self._peers, self._world, self._rank, self.flat.numel(),
+                                                 _lib.stream_handle(dev)), "ck_allreduce_peers")
+        torch.cuda.current_stream(dev).synchronize()
+        dist.barrier(group=self.group)
+        want = self._world * (self._world + 1) / 2
+        on = dev if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        ok = torch.tensor([1.0 if bool((self.flat == want).all()) else 0.0], device=on)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        self.flat.copy_(saved)
+        if ok.item() != 1.0:
+            self.close()
+            raise ValueError("peer-memory allreduce self-test failed")
 
     def __call__(self) -> None:
         if self._peers is None:
