@@ -530,6 +530,11 @@ def run_ours(args, wl):
                           f"{gemm_tf / (peaks['bf16_sus'] / 3.0):.3f}",
             "algorithmic_flops_per_step": step_gemm,
             "gemm_share_of_kernel_time": gemm_ms / total_kernel_ms if total_kernel_ms else None,
+            # the part is power-capped: the same achieved rate against the
+            # tensor pipe's per-clock peak (148 SMs x 8192 dense bf16 flop/clk,
+            # / 3 for BF16x3) at the SM clock sampled during the timed region
+            "frac_at_sampled_clock": (gemm_tf / (148 * 8192 * clk["sm_mhz"] * 1e6 / 3 / 1e12)
+                                      if clk and clk.get("sm_mhz") else None),
         },
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
         "graph": (f"timed steps replay one captured CUDA graph of the whole step; kernel_ms_per_step and "
