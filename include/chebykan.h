@@ -124,6 +124,18 @@ CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const 
                const float* bias, float* y, void* workspace, size_t workspace_bytes, void* basis_cache,
                size_t basis_cache_bytes, void* stream);
 
+/* --- The two stages separately: forward_partial (kernels.py:263-318) and
+ * combine (kernels.py:321-348), for callers of the partial buffer itself.
+ * partial[to][ti][b][ty] = sum_{j in input tile ti} sum_k B_k(tanh x[b][j])
+ * C[k][to*tile_out+ty][j] (PartialBuffer layout, kernels.py:108-137; g_x =
+ * ceil(d_in/tile_in), g_y = ceil(d_out/tile_out); slots of padding lanes are
+ * not written).  ck_combine folds the input tiles in ascending order and adds
+ * bias (nullable).  fp32 CUDA-core arithmetic; ck_forward is the fast path. */
+CK_API int ck_forward_partial(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut,
+                       const float* coeff_doj, int tile_in, int tile_out, float* partial, void* stream);
+CK_API int ck_combine(const float* partial, int64_t batch, int d_out, int g_x, int tile_out, const float* bias,
+               float* y, void* stream);
+
 /* --- Backward: replaces backward_fused (kernels.py:374-447) plus the bias
  * gradient of Layer.backward (model.py:147) --------------------------------
  * dc_doj[k][o][i] = sum_b dy[b][o] T_k(tanh x[b][i])

@@ -16,10 +16,13 @@ from .kernels import (
     KernelCounters,
     KernelMode,
     NonFiniteInputError,
+    PartialBuffer,
     PreparedCoeff,
     TileSchedule,
     backward_fused,
+    combine,
     count_atomics,
+    forward_partial,
     count_flops,
     fused_forward,
     reference_backward,

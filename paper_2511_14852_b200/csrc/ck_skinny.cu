@@ -298,3 +298,122 @@ int launch_skinny_backward(const float* x, const float* dy, int64_t rows, int I,
 }
 
 }  // namespace ck
+
+// ---------------------------------------------------------------------------
+// The reference's two-stage forward, stage by stage (forward_partial /
+// combine, kernels.py:263-348), for callers that use the partial buffer
+// itself.  One warp per (row b, output tile to): lanes own the tile's
+// outputs; the features of 32 inputs at a time are evaluated one per lane
+// (table interpolation or exact, streamed by Rec) and broadcast by shuffles;
+// every (b, to, ti) slot is written exactly once, in fp32 FMA order
+// j ascending, k ascending.  CUDA cores: the fast path is ck_forward.
+namespace ck {
+namespace {
+
+__global__ void __launch_bounds__(256) forward_partial_kernel(const float* __restrict__ x, int64_t rows, int I, int O,
+                                                              int K, const float* __restrict__ c, LutView L,
+                                                              int tile_in, int tile_out, int g_x, int g_y,
+                                                              float* __restrict__ part) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t items = rows * g_y;
+  for (int64_t w = warp; w < items; w += nwarps) {
+    const int64_t b = w / g_y;
+    const int to = static_cast<int>(w - b * g_y);
+    const float* xr = x + b * I;
+    for (int ty0 = 0; ty0 < tile_out; ty0 += 32) {
+      const int ty = ty0 + lane;
+      const int o = to * tile_out + ty;
+      const bool o_ok = ty < tile_out && o < O;
+      for (int ti = 0; ti < g_x; ++ti) {
+        const int j_begin = ti * tile_in;
+        const int j_end = min(I, j_begin + tile_in);
+        float acc = 0.0f;
+        for (int j0 = j_begin; j0 < j_end; j0 += 32) {
+          const int jl = j0 + lane;
+          const bool j_ok = jl < j_end;
+          const float xv = j_ok ? __ldg(xr + jl) : 0.0f;
+          Rec ra, rb;
+          float f = 0.0f;
+          if (L.exact) {
+            ra.init(L.kind, tanhf(xv));
+          } else {
+            int idx;
+            cell_f32(xv, L.N, idx, f);
+            const float step = 2.0f / static_cast<float>(L.N - 1);
+            ra.init(L.kind, grid_node_f(idx, L.N, step));
+            rb.init(L.kind, grid_node_f(idx + 1, L.N, step));
+          }
+          const int nj = min(32, j_end - j0);
+          for (int k = 0; k < K; ++k) {
+            float v = 1.0f;
+            if (k > 0) {
+              const float a = ra.next();
+              v = L.exact ? a : lerp_ref(a, rb.next(), f);
+            }
+            const float* crow = c + (static_cast<int64_t>(k) * O + (o_ok ? o : 0)) * I + j0;
+            for (int jj = 0; jj < nj; ++jj) {
+              const float vj = __shfl_sync(0xffffffffu, v, jj);
+              if (o_ok) acc = fmaf(vj, __ldg(crow + jj), acc);
+            }
+          }
+        }
+        if (o_ok) part[((static_cast<int64_t>(to) * g_x + ti) * rows + b) * tile_out + ty] = acc;
+      }
+    }
+  }
+}
+
+// y[b][o] = sum_{ti ascending} part[to][ti][b][ty] (+ bias[o])
+__global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ part, int64_t rows, int O, int tile_out,
+                                                      int g_x, const float* __restrict__ bias, float* __restrict__ y) {
+  pdl_wait();
+  const int64_t n = rows * O;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = e / O;
+    const int o = static_cast<int>(e - b * O);
+    const int to = o / tile_out, ty = o - to * tile_out;
+    float acc = part[((static_cast<int64_t>(to) * g_x) * rows + b) * tile_out + ty];
+    for (int ti = 1; ti < g_x; ++ti) acc += part[((static_cast<int64_t>(to) * g_x + ti) * rows + b) * tile_out + ty];
+    y[e] = bias ? acc + bias[o] : acc;
+  }
+}
+
+}  // namespace
+}  // namespace ck
+
+extern "C" int ck_forward_partial(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut,
+                                  const float* coeff_doj, int tile_in, int tile_out, float* partial, void* stream) {
+  CK_CHECK(lut != nullptr, "LUT mode requires a LutTable");
+  CK_CHECK(batch >= 0 && d_in >= 1 && d_out >= 1, "d_in and d_out must be >= 1");
+  CK_CHECK(tile_in >= 1 && tile_out >= 1, "tile and lane sizes must be >= 1");
+  if (batch == 0) return ck::kOk;
+  CK_CHECK(x && coeff_doj && partial, "ck_forward_partial: NULL tensor");
+  const int g_x = static_cast<int>(ck::ceil_div(d_in, tile_in)), g_y = static_cast<int>(ck::ceil_div(d_out, tile_out));
+  const ck::LutView L = ck::view(lut);
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t warps = batch * g_y;
+  const int64_t want = ck::ceil_div(warps * 32, 256);
+  const int64_t cap = static_cast<int64_t>(ck::num_sms()) * 16;
+  ck::LaunchScope scope(ck::kKSkinny, s);
+  CK_CUDA(ck::launch_k((ck::forward_partial_kernel), static_cast<int>(want < cap ? want : cap), 256, 0, s, x, batch,
+                       d_in, d_out, L.K, coeff_doj, L, tile_in, tile_out, g_x, g_y, partial));
+  return ck::kOk;
+}
+
+extern "C" int ck_combine(const float* partial, int64_t batch, int d_out, int tile_in_groups, int tile_out,
+                          const float* bias, float* y, void* stream) {
+  CK_CHECK(batch >= 0 && d_out >= 1 && tile_in_groups >= 1 && tile_out >= 1, "ck_combine: bad extents");
+  if (batch == 0) return ck::kOk;
+  CK_CHECK(partial && y, "ck_combine: NULL tensor");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t want = ck::ceil_div(batch * d_out, 256);
+  const int64_t cap = static_cast<int64_t>(ck::num_sms()) * 8;
+  ck::LaunchScope scope(ck::kKReduce, s);
+  CK_CUDA(ck::launch_k((ck::combine_kernel), static_cast<int>(want < cap ? want : cap), 256, 0, s, partial, batch,
+                       d_out, tile_out, tile_in_groups, bias, y));
+  return ck::kOk;
+}

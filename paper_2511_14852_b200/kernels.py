@@ -79,6 +79,30 @@ class TileSchedule:
 
 
 @dataclass
+class PartialBuffer:
+    """Partial-stage workspace (kernels.py:108-137) on the device; flat order
+    gIdx = (tileO * g_x + tileI) * B * tile_out + b * tile_out + t_y.  Slots of
+    padding lanes of a ragged last output tile stay zero; ``write_counts``
+    (instrumented buffers) records one write per real slot."""
+
+    g_x: int
+    g_y: int
+    batch: int
+    tile_out: int
+    data: torch.Tensor
+    write_counts: torch.Tensor | None = None
+
+    @classmethod
+    def allocate(cls, sched: "TileSchedule", batch: int, instrument: bool = False, device=None) -> "PartialBuffer":
+        if batch < 1:
+            raise ValueError("batch must be >= 1")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        shape = (sched.g_y, sched.g_x, batch, sched.tile_out)
+        return cls(sched.g_x, sched.g_y, batch, sched.tile_out, torch.zeros(shape, dtype=torch.float32, device=dev),
+                   torch.zeros(shape, dtype=torch.int64, device=dev) if instrument else None)
+
+
+@dataclass
 class KernelCounters:
     """Merge/store counts (kernels.py:140-147).  The B200 kernels have no
     atomics either; the counts follow the reference's closed forms for the
@@ -294,6 +318,55 @@ def backward_fused(x, coeff: CoeffTensor, dy, lut, sched: TileSchedule | None = 
         sched = sched or TileSchedule.for_dims(coeff.d_in, coeff.d_out)
         counters.x_grad_merges += x.shape[0] * coeff.d_in * sched.g_y
     return CoeffTensor(coeff.d_in, coeff.d_out, coeff.degree, Layout.DOJ, dc), dx
+
+
+def forward_partial(x, coeff: CoeffTensor, lut, sched: TileSchedule, mode: KernelMode, out: PartialBuffer, *,
+                    workers: int = 1, counters: KernelCounters | None = None, validate: bool = False,
+                    kind: BasisKind | None = None) -> None:
+    """Partial stage (kernels.py:263-318): slot (tileO, tileI, b, t_y) receives
+    sum_{j in tile} sum_k coeff[k, out, j] B_k(tanh x[b, j]); each slot has one
+    writer.  Runs on the GPU (ck_forward_partial, fp32 CUDA cores); the fused
+    tensor-core path is fused_forward."""
+    dev = out.data.device
+    basis = _basis_for(coeff, lut, None, mode, kind, "forward_partial", dev)
+    x = _as_f32(x, dev)
+    if x.dim() != 2:
+        raise ValueError(f"input must be 2-D (batch, d_in), got shape {tuple(x.shape)}")
+    if x.shape[1] != coeff.d_in:
+        raise ValueError(f"input width {x.shape[1]} != coefficient d_in {coeff.d_in}")
+    if sched.d_in != coeff.d_in or sched.d_out != coeff.d_out:
+        raise ValueError("schedule dimensions do not match the coefficient tensor")
+    if (out.g_x, out.g_y, out.batch, out.tile_out) != (sched.g_x, sched.g_y, x.shape[0], sched.tile_out):
+        raise ValueError("partial buffer does not match the schedule and batch")
+    if validate:
+        _check_finite(x)
+    c = _as_f32(coeff.as3d(), dev)
+    rc = _lib.lib().ck_forward_partial(x.data_ptr(), x.shape[0], coeff.d_in, coeff.d_out, basis.handle, c.data_ptr(),
+                                       sched.tile_in, sched.tile_out, out.data.data_ptr(), _lib.stream_handle(dev))
+    _lib.check(rc, "ck_forward_partial")
+    if out.write_counts is not None:
+        valid = torch.arange(sched.g_y * sched.tile_out, device=dev).reshape(sched.g_y, 1, 1, sched.tile_out)
+        out.write_counts += (valid < coeff.d_out).to(torch.int64).expand_as(out.write_counts)
+    if counters is not None:
+        counters.partial_writes += x.shape[0] * sched.d_out * sched.g_x
+
+
+def combine(partial: PartialBuffer, sched: TileSchedule, bias=None, *,
+            counters: KernelCounters | None = None) -> torch.Tensor:
+    """Combine stage (kernels.py:321-348): fold input tiles in ascending order,
+    add the bias; one store per output (ck_combine)."""
+    dev = partial.data.device
+    if bias is not None:
+        bias = _as_f32(bias, dev)
+        if tuple(bias.shape) != (sched.d_out,):
+            raise ValueError(f"bias must have shape ({sched.d_out},), got {tuple(bias.shape)}")
+    y = torch.empty((partial.batch, sched.d_out), dtype=torch.float32, device=dev)
+    rc = _lib.lib().ck_combine(partial.data.data_ptr(), partial.batch, sched.d_out, partial.g_x, partial.tile_out,
+                               _lib.ptr(bias), y.data_ptr(), _lib.stream_handle(dev))
+    _lib.check(rc, "ck_combine")
+    if counters is not None:
+        counters.combine_stores += partial.batch * sched.d_out
+    return y
 
 
 def _exact_for(kind, n_feat: int, trig: bool, device) -> ExactBasis:

@@ -163,3 +163,44 @@ def test_counters_follow_closed_forms():
         assert counters.x_grad_merges == expect.bwd_x_ours
         assert counters.partial_writes == x.shape[0] * dy.shape[1] * sched.g_x
         assert counters.combine_stores == x.shape[0] * dy.shape[1]
+
+
+@pytest.mark.parametrize("kind,exact", [("chebyshev", False), ("legendre", True), ("fourier", False)])
+def test_forward_partial_and_combine(kind, exact):
+    # kernels.py:263-348 stage by stage: every slot vs the float64 tile sums,
+    # one writer per real slot, padding lanes untouched, combine == fused_forward
+    rng = np.random.default_rng(31)
+    for tile_in, tile_out in ((4, 8), (16, 32), (64, 32), (64, 40)):
+        x, c_doj, dy, degree = random_instance(rng, kind, max_dim=70, max_degree=8)
+        b, i = x.shape
+        o, k = c_doj.shape[1], c_doj.shape[0]
+        sched = ck.TileSchedule.for_dims(i, o, tile_in, tile_out, lane_y=tile_out)
+        if exact:
+            planes = orc.basis_rows(kind, degree, np.tanh(x.astype(np.float64)))
+            table, mode = None, ck.EXACT_MODE
+        else:
+            vals, _, _ = orc.build_table(degree, 4096, kind)
+            planes = orc.lut_values(np.tanh(x.astype(np.float64)), vals).transpose(2, 0, 1)
+            table, mode = ck.lut_build(ck.BasisKind(kind), degree, 4096, device=_dev()), ck.LUT_MODE
+        c = ck.CoeffTensor(i, o, k - 1, ck.Layout.DOJ, _t(c_doj))
+        buf = ck.PartialBuffer.allocate(sched, b, instrument=True, device=_dev())
+        counters = ck.KernelCounters()
+        ck.forward_partial(_t(x), c, table, sched, mode, buf, counters=counters, kind=ck.BasisKind(kind))
+        got = buf.data.cpu().numpy()
+        want = np.zeros_like(got, dtype=np.float64)
+        for to in range(sched.g_y):
+            os_ = slice(to * tile_out, min(o, (to + 1) * tile_out))
+            for ti in range(sched.g_x):
+                js = slice(ti * tile_in, min(i, (ti + 1) * tile_in))
+                prod = np.einsum("kbj,koj->bo", planes[:, :, js], c_doj[:, os_, js].astype(np.float64))
+                want[to, ti, :, : os_.stop - os_.start] = prod
+        assert orc.normwise_err(got, want) <= 1e-5
+        counts = buf.write_counts.cpu().numpy()
+        assert set(np.unique(counts)) <= {0, 1}
+        assert int(counts.sum()) == b * o * sched.g_x  # padding lanes excluded
+        assert counters.partial_writes == b * o * sched.g_x
+        bias = rng.standard_normal(o).astype(np.float32)
+        y = ck.combine(buf, sched, _t(bias), counters=counters).cpu().numpy()
+        yf = ck.fused_forward(_t(x), c, table, sched, mode, _t(bias), kind=ck.BasisKind(kind)).cpu().numpy()
+        assert orc.normwise_err(y, yf) <= TOL
+        assert counters.combine_stores == b * o
