@@ -135,3 +135,29 @@ def test_load_csv_errors(tmp_path):
         ck.load_csv(p, classification=True)
     ds = ck.load_csv(p)
     assert ds.x.shape == (1, 1) and ds.y[0] == 2.5
+
+
+def test_roofline_formulas_match_reference():
+    # test_acceptance.py:279-298 (closed forms of perf.py:77-90) and the CLI
+    # lambda case of test_cli.py:100-113
+    import numpy as np
+
+    import paper_2511_14852_b200 as ck
+
+    r = ck.roofline(ck.LayerConfig(128, 40, 256, 8, 4))
+    assert r.flops == 23_674_880 and r.bytes == 888_832
+    assert abs(r.intensity - 23_674_880 / 888_832) < 1e-9
+    rng = np.random.default_rng(1006)
+    for _ in range(200):
+        b, din, dout = (int(rng.integers(1, v)) for v in (512, 2048, 2048))
+        d, lam = int(rng.integers(0, 33)), int(rng.choice([4, 8]))
+        rep = ck.roofline(ck.LayerConfig(b, din, dout, d, lam))
+        assert rep.flops == 2 * b * din * (d + (d + 1) * dout)
+        assert rep.bytes == lam * (b * din + b * dout + 2 * b * din * (d + 1) + din * dout * (d + 1))
+    assert ck.roofline(ck.LayerConfig(2, 3, 4, 1, 8)).bytes == 2 * 4 * (2 * 3 + 2 * 4 + 2 * 2 * 3 * 2 + 3 * 4 * 2)
+    rep = ck.two_stage_benefit(ck.LayerConfig(8, 128, 64, 3), ck.TileSchedule.for_dims(128, 64),
+                               ck.CostModel(10.0, 1.0, 1.0))
+    assert rep.beneficial and rep.margin == 2 * 10.0 - (2 * 2.0 + 1.0) and rep.partial_bytes == 4 * 8 * 64 * 2
+    assert [c.degree for c in ck.paper_configs()] == [8, 15, 24]
+    with pytest.raises(ValueError, match="elem_bytes"):
+        ck.LayerConfig(1, 1, 1, 1, 2)
