@@ -101,6 +101,13 @@ CK_API int ck_lut_read(const ck_lut* lut, double* values_host, float* slopes_hos
 CK_API int ck_expand(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi, float* slopes,
               void* stream);
 
+/* Basis at normalized points t (no tanh): values[e][k] and (nullable)
+ * slopes[e][k].  Table handles: lut_interp / lut_interp_with_slope
+ * (lut.py:126-140, float64 cell as the reference); exact handles:
+ * eval_basis / eval_basis_derivative / eval_basis_trig (basis.py:122-141,
+ * 207-212) in float32. */
+CK_API int ck_basis_eval(const float* t, int64_t n, const ck_lut* lut, float* values, float* slopes, void* stream);
+
 /* --- Coefficient preparation (reorder_to_doj consumer, tensor.py:77-82) ---
  * Converts fp32 DOJ coefficients into the kernels' tensor-core operands:
  * bf16 hi/lo split copies in DOJ [K][O][I] (forward, unit stride in i) and

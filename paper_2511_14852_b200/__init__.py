@@ -7,7 +7,19 @@ Public surface mirrors the reference package ``polykan`` for this path:
 ``ChebyKANLayer`` and data-parallel helpers.  All compute runs in the
 sm_100a kernels of ``lib/libchebykan.so``; there is no CPU fallback.
 """
-from .basis import BasisKind, degree_for, feature_count
+from .basis import (
+    BasisKind,
+    basis_rows,
+    chebyshev_second_derivative_max,
+    degree_for,
+    derivative_rows,
+    eval_basis,
+    eval_basis_derivative,
+    eval_basis_trig,
+    feature_count,
+    parse_kind,
+    trig_rows,
+)
 from .kernels import (
     EXACT_MODE,
     LUT_MODE,
@@ -36,8 +48,12 @@ from .lut import (
     exact_basis,
     expand,
     interp_error_bound,
+    interp_rows,
+    interp_rows_with_slope,
     lut_build,
     lut_from_arrays,
+    lut_interp,
+    lut_interp_with_slope,
     lut_max_error_bound,
     lut_size_for_budget,
 )

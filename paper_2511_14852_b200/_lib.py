@@ -38,6 +38,7 @@ SIGNATURES = {
     "ck_lut_kind": (_c_int, [_c_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)]),
     "ck_lut_read": (_c_int, [_c_p, _c_dp, _c_fp]),
     "ck_expand": (_c_int, [_c_p, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p]),
+    "ck_basis_eval": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "ck_coeff_prep_bytes": (_c_size, [_c_int, _c_int, _c_int]),
     "ck_coeff_prepare": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_p, _c_size, _c_p]),
     "ck_forward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),

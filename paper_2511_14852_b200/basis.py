@@ -58,3 +58,94 @@ def degree_for(kind: BasisKind, n_feat: int) -> int:
             raise ValueError("Fourier feature count must be odd (2 * degree + 1)")
         return (n_feat - 1) // 2
     return n_feat - 1
+
+
+def parse_kind(name: str) -> BasisKind:
+    """basis.py:220-225."""
+    try:
+        return BasisKind(name.lower())
+    except ValueError:
+        valid = ", ".join(k.value for k in BasisKind)
+        raise ValueError(f"unknown basis {name!r}; expected one of: {valid}") from None
+
+
+def chebyshev_second_derivative_max(k: int) -> float:
+    """max over [-1,1] of |T_k''| = k^2 (k^2 - 1) / 3 (basis.py:215-217)."""
+    return k * k * (k * k - 1) / 3.0
+
+
+# ---------------------------------------------------------------------------
+# Point evaluation on the GPU (ck_basis_eval on an exact-evaluation handle):
+# the reference's basis_rows / derivative_rows / trig_rows / eval_basis*
+# (basis.py:87-212) in float32.  NumPy in -> NumPy out (float64 dtype holding
+# float32 values); torch CUDA tensors in -> torch out.
+
+
+def _eval(kind, degree: int, x, trig: bool, want_deriv: bool):
+    import numpy as np
+    import torch
+
+    from . import _lib
+    from .lut import exact_basis
+
+    kind = as_kind(kind)
+    if degree < 0:
+        raise ValueError(f"degree must be >= 0, got {degree}")
+    is_torch = isinstance(x, torch.Tensor)
+    xt = x.detach() if is_torch else torch.as_tensor(np.asarray(x, dtype=np.float64))
+    if not bool(torch.isfinite(xt).all()):
+        raise ValueError("basis evaluation requires finite inputs")
+    if trig and bool((xt.abs() > 1.0).any()):
+        raise ValueError("trig evaluation requires |x| <= 1")
+    dev = xt.device if (is_torch and xt.is_cuda) else torch.device("cuda", torch.cuda.current_device())
+    flat = xt.to(device=dev, dtype=torch.float32).reshape(-1).contiguous()
+    h = exact_basis(kind, degree, device=dev, trig=trig)
+    k = h.n_features
+    vals = torch.empty((flat.numel(), k), dtype=torch.float32, device=dev)
+    der = torch.empty_like(vals) if want_deriv else None
+    rc = _lib.lib().ck_basis_eval(flat.data_ptr(), flat.numel(), h.handle, vals.data_ptr(), _lib.ptr(der),
+                                  _lib.stream_handle(dev))
+    _lib.check(rc, "ck_basis_eval")
+    out = (der if want_deriv else vals).t().reshape((k,) + tuple(xt.shape))
+    if is_torch:
+        return out
+    return out.cpu().numpy().astype(np.float64)
+
+
+def basis_rows(kind: BasisKind, degree: int, x):
+    """All features at each point; shape (n_features,) + x.shape (basis.py:87-119)."""
+    return _eval(kind, degree, x, False, False)
+
+
+def derivative_rows(kind: BasisKind, degree: int, x):
+    """Analytic derivatives dB_k/dx; shape (n_features,) + x.shape (basis.py:155-204)."""
+    return _eval(kind, degree, x, False, True)
+
+
+def trig_rows(degree: int, x):
+    """cos(n arccos x), shape (degree+1,) + x.shape (basis.py:144-152)."""
+    return _eval(BasisKind.CHEBYSHEV, degree, x, True, False)
+
+
+def _scalar(x, what: str):
+    import numpy as np
+
+    xv = np.asarray(x, dtype=np.float64)
+    if xv.ndim != 0:
+        raise ValueError(what)
+    return xv.reshape(1)
+
+
+def eval_basis(kind: BasisKind, degree: int, x: float):
+    """Feature vector [B_0(x), ..., B_d(x)] at one normalized point (basis.py:122-128)."""
+    return basis_rows(kind, degree, _scalar(x, "eval_basis takes a scalar; use basis_rows for arrays"))[:, 0]
+
+
+def eval_basis_trig(degree: int, x: float):
+    """Chebyshev values via cos(n arccos x) at one point (basis.py:131-141)."""
+    return trig_rows(degree, _scalar(x, "eval_basis_trig takes a scalar"))[:, 0]
+
+
+def eval_basis_derivative(kind: BasisKind, degree: int, x: float):
+    """Analytic derivative vector at one point (basis.py:205-210)."""
+    return derivative_rows(kind, degree, _scalar(x, "eval_basis_derivative takes a scalar"))[:, 0]

@@ -264,6 +264,14 @@ extern "C" int ck_expand(const float* x, int64_t rows, int cols, const ck_lut* l
   return ck::launch_expand_f32(x, rows, cols, lut, phi, slopes, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" int ck_basis_eval(const float* t, int64_t n, const ck_lut* lut, float* values, float* slopes,
+                             void* stream) {
+  CK_CHECK(lut != nullptr, "ck_basis_eval: NULL basis handle");
+  CK_CHECK(n >= 0, "ck_basis_eval: negative size");
+  CK_CHECK(n == 0 || (t != nullptr && values != nullptr), "ck_basis_eval: NULL tensor");
+  return ck::launch_basis_eval(t, n, lut, values, slopes, static_cast<cudaStream_t>(stream));
+}
+
 extern "C" size_t ck_coeff_prep_bytes(int d_in, int d_out, int n_feat) {
   if (d_in < 1 || d_out < 1 || n_feat < 1) return 0;
   return ck::PrepLayout(d_in, d_out, n_feat).total + ck::kAlign;

@@ -108,8 +108,7 @@ __device__ __forceinline__ void split_pack2(float a, float b, uint32_t& hi2, uin
 
 // Exact cell choice (float64), lut.py:97-106: clip, pos = (t+1)*0.5*(N-1),
 // idx = min(trunc(pos), N-2), frac snapped to {0,1} within 1e-9.
-__device__ __forceinline__ void cell_f64(float xv, int n, int& idx, double& frac, double& t) {
-  t = tanh(static_cast<double>(xv));
+__device__ __forceinline__ void cell_f64_at(double t, int n, int& idx, double& frac) {
   const double tc = fmin(fmax(t, -1.0), 1.0);
   const double pos = __dmul_rn(__dmul_rn(__dadd_rn(tc, 1.0), 0.5), static_cast<double>(n - 1));
   long long i = static_cast<long long>(pos);
@@ -118,6 +117,12 @@ __device__ __forceinline__ void cell_f64(float xv, int n, int& idx, double& frac
   frac = __dsub_rn(pos, static_cast<double>(idx));
   if (frac < 1e-9) frac = 0.0;
   if (frac > 1.0 - 1e-9) frac = 1.0;
+}
+
+// the same cell for t = tanh(x) (kernels.py:288 then lut.py:97-106)
+__device__ __forceinline__ void cell_f64(float xv, int n, int& idx, double& frac, double& t) {
+  t = tanh(static_cast<double>(xv));
+  cell_f64_at(t, n, idx, frac);
 }
 
 // --- mbarrier --------------------------------------------------------------

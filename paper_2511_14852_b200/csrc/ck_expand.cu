@@ -65,6 +65,37 @@ __global__ void __launch_bounds__(kThreads) expand_f32_kernel(const float* __res
   }
 }
 
+// Basis at normalized points t (no tanh): table interpolation with the
+// reference's float64 cell and slopes (lut_interp / interp_rows_with_slope,
+// lut.py:109-140), or basis_rows / derivative_rows (basis.py:87-204).
+__global__ void __launch_bounds__(kThreads) basis_eval_kernel(const float* __restrict__ t, int64_t n_elem,
+                                                              LutView lut, float* __restrict__ vals,
+                                                              float* __restrict__ slopes) {
+  pdl_wait();
+  const int K = lut.K, N = lut.N;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_elem;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (lut.exact) {
+      float v[kMaxFeaturesRt], dv[kMaxFeaturesRt];
+      basis_deriv_rt(lut.kind, K - 1, t[e], v, slopes ? dv : nullptr);
+      for (int k = 0; k < K; ++k) vals[e * K + k] = v[k];
+      if (slopes)
+        for (int k = 0; k < K; ++k) slopes[e * K + k] = dv[k];
+      continue;
+    }
+    int idx;
+    double frac;
+    cell_f64_at(static_cast<double>(t[e]), N, idx, frac);
+    const float f = static_cast<float>(frac);
+    const float* v0 = lut.values_pm + static_cast<int64_t>(idx) * K;
+    for (int k = 0; k < K; ++k) vals[e * K + k] = lerp_ref(v0[k], v0[k + K], f);
+    if (slopes) {
+      const float* s0 = lut.slopes_pm + static_cast<int64_t>(idx) * K;
+      for (int k = 0; k < K; ++k) slopes[e * K + k] = s0[k];
+    }
+  }
+}
+
 // --- specialized planes kernels ----------------------------------------------
 // Values of features k = 1..D at one element.  kLutNodes: the two table
 // entries bracketing the cell are recomputed at the (float32-rounded) grid
@@ -310,6 +341,15 @@ int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut,
     CK_CUDA(launch_k((expand_f32_kernel<false>), blocks, kThreads, 0, s, x, n, v, phi, slopes));
   }
   CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_basis_eval(const float* t, int64_t n, const ck_lut* lut, float* vals, float* slopes, cudaStream_t s) {
+  if (n == 0) return kOk;
+  const LutView v = view(lut);
+  CK_CHECK(v.K <= kMaxFeaturesRt, "ck_basis_eval: at most 64 features");
+  LaunchScope scope(kKExpand, s);
+  CK_CUDA(launch_k((basis_eval_kernel), grid_for(n, 8), kThreads, 0, s, t, n, v, vals, slopes));
   return kOk;
 }
 

@@ -87,6 +87,8 @@ inline LutView view(const ck_lut* l) {
 // phi[r][c][k] (f32) and optional slopes[r][c][k] for every k.
 int launch_expand_f32(const float* x, int64_t rows, int cols, const ck_lut* lut, float* phi,
                       float* slopes, cudaStream_t s);
+// vals[e][k] (and slopes) of the basis at normalized points t[e] (no tanh)
+int launch_basis_eval(const float* t, int64_t n, const ck_lut* lut, float* vals, float* slopes, cudaStream_t s);
 // Split planes hi/lo [nk][rows][ld] for k = k0..K-1 (bf16, ld % 8 == 0).
 int launch_expand_planes(const float* x, int64_t rows, int cols, const ck_lut* lut, int k0,
                          __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ld, int64_t plane_stride,

@@ -271,3 +271,55 @@ def expand(x, table, with_slopes: bool = False):
                               _lib.ptr(slopes), _lib.stream_handle(x.device))
     _lib.check(rc, "ck_expand")
     return (phi, slopes) if with_slopes else phi
+
+
+# ---------------------------------------------------------------------------
+# Interpolation at normalized points (no tanh), on the GPU (ck_basis_eval):
+# interp_rows / interp_rows_with_slope / lut_interp / lut_interp_with_slope
+# (lut.py:109-140) with the reference's float64 cell; float32 values.
+# NumPy (or scalar) in -> NumPy out; torch CUDA tensors in -> torch out.
+
+
+def _interp(table: LutTable, x, with_slope: bool):
+    import torch
+
+    is_torch = isinstance(x, torch.Tensor)
+    xt = x.detach() if is_torch else torch.as_tensor(np.asarray(x, dtype=np.float64))
+    dev = torch.device("cuda", table.device)
+    flat = xt.to(device=dev, dtype=torch.float32).reshape(-1).contiguous()
+    k = table.n_features
+    vals = torch.empty((flat.numel(), k), dtype=torch.float32, device=dev)
+    sl = torch.empty_like(vals) if with_slope else None
+    _lib.check(_lib.lib().ck_basis_eval(flat.data_ptr(), flat.numel(), table.handle, vals.data_ptr(), _lib.ptr(sl),
+                                        _lib.stream_handle(dev)), "ck_basis_eval")
+    shape = tuple(xt.shape) + (k,)
+    vals, sl = vals.reshape(shape), (None if sl is None else sl.reshape(shape))
+    if not is_torch:
+        vals = vals.cpu().numpy().astype(np.float64)
+        sl = None if sl is None else sl.cpu().numpy().astype(np.float64)
+    return (vals, sl) if with_slope else vals
+
+
+def interp_rows(table: LutTable, x):
+    """Interpolated feature values; (...,) -> (..., n_features) (lut.py:109-115)."""
+    return _interp(table, x, False)
+
+
+def interp_rows_with_slope(table: LutTable, x):
+    """Values plus the active cell's slope per feature (lut.py:118-123)."""
+    return _interp(table, x, True)
+
+
+def lut_interp(table: LutTable, x: float):
+    """Approximate feature vector at one point (lut.py:126-131)."""
+    if not np.all(np.isfinite(np.asarray(x, dtype=np.float64))):
+        raise ValueError("lut_interp requires finite input")
+    return _interp(table, np.asarray(x, dtype=np.float64).reshape(1), False)[0]
+
+
+def lut_interp_with_slope(table: LutTable, x: float):
+    """Values and the piecewise-constant surrogate derivative at one point (lut.py:134-140)."""
+    if not np.all(np.isfinite(np.asarray(x, dtype=np.float64))):
+        raise ValueError("lut_interp_with_slope requires finite input")
+    v, s = _interp(table, np.asarray(x, dtype=np.float64).reshape(1), True)
+    return v[0], s[0]

@@ -204,3 +204,52 @@ def test_forward_partial_and_combine(kind, exact):
         yf = ck.fused_forward(_t(x), c, table, sched, mode, _t(bias), kind=ck.BasisKind(kind)).cpu().numpy()
         assert orc.normwise_err(y, yf) <= TOL
         assert counters.combine_stores == b * o
+
+
+def test_point_evaluation_known_answers():
+    # test_basis.py:20-110 and test_lut.py:29-99 through ck_basis_eval (float32)
+    K = ck.BasisKind
+    assert np.array_equal(ck.eval_basis(K.CHEBYSHEV, 2, 1.0), [1.0, 1.0, 1.0])
+    assert np.array_equal(ck.eval_basis(K.LEGENDRE, 2, 1.0), [1.0, 1.0, 1.0])
+    np.testing.assert_allclose(ck.eval_basis(K.CHEBYSHEV, 3, 0.5), [1.0, 0.5, -0.5, -1.0], atol=1e-6)
+    np.testing.assert_allclose(ck.eval_basis_trig(3, 0.5), [1.0, 0.5, -0.5, -1.0], atol=1e-6)
+    np.testing.assert_allclose(ck.eval_basis_trig(4, -1.0), [1, -1, 1, -1, 1], atol=1e-6)
+    x = 0.37
+    want = [1.0]
+    for k in range(1, 4):
+        want += [np.cos(k * np.pi * x), np.sin(k * np.pi * x)]
+    np.testing.assert_allclose(ck.eval_basis(K.FOURIER, 3, x), want, atol=1e-6)
+    np.testing.assert_allclose(ck.eval_basis(K.HERMITE, 3, x), [1, 2 * x, 4 * x * x - 2, 8 * x ** 3 - 12 * x],
+                               atol=1e-5)
+    np.testing.assert_allclose(ck.eval_basis_derivative(K.FOURIER, 1, 0.0), [0.0, 0.0, np.pi], atol=1e-6)
+    for kind in ("chebyshev", "legendre", "hermite", "fourier"):
+        xs = np.linspace(-1, 1, 2001).astype(np.float32).astype(np.float64)  # the kernels' float32 points
+        for deg in (0, 5, 12):
+            tol = 1e-7 * (deg + 1) ** 2  # float32 recurrence round-off grows ~k^2 ulp
+            got = ck.basis_rows(K(kind), deg, xs)
+            want = orc.basis_rows(kind, deg, xs)
+            assert got.shape == want.shape
+            assert np.abs(got - want).max() <= tol * max(1.0, np.abs(want).max())
+            gd, wd = ck.derivative_rows(K(kind), deg, xs), orc.derivative_rows(kind, deg, xs)
+            assert np.abs(gd - wd).max() <= tol * max(1.0, np.abs(wd).max())
+    with pytest.raises(ValueError, match="trig evaluation requires"):
+        ck.trig_rows(3, np.array([1.5]))
+    with pytest.raises(ValueError, match="finite inputs"):
+        ck.basis_rows(K.CHEBYSHEV, 3, np.array([np.nan]))
+    with pytest.raises(ValueError, match="takes a scalar"):
+        ck.eval_basis(K.CHEBYSHEV, 3, np.zeros(2))
+    # coarse table KATs (test_lut.py:81-99): lerp of T_2 at 0.5 is 0; cell-0 slope of T_2 is -2
+    t = ck.lut_build(K.CHEBYSHEV, 2, 3, device=_dev())
+    np.testing.assert_allclose(ck.lut_interp(t, 0.5), [1.0, 0.5, 0.0], atol=1e-7)
+    _, s = ck.lut_interp_with_slope(t, -0.4)
+    assert s[2] == -2.0
+    # grid points reproduce stored columns (snap), and batch interp == oracle
+    t = ck.lut_build(K.LEGENDRE, 6, 1025, device=_dev())
+    grid = t.grid()
+    v = ck.interp_rows(t, grid)
+    assert np.array_equal(v, t.values.T.astype(np.float32).astype(np.float64))
+    pts = np.random.default_rng(3).uniform(-1.2, 1.2, 5000)
+    vals, slopes = ck.interp_rows_with_slope(t, pts.astype(np.float32))
+    wv, ws = orc.lut_values_and_slopes(pts.astype(np.float32).astype(np.float64), *orc.build_table(6, 1025, "legendre")[:2])
+    assert np.abs(vals - wv).max() <= 2e-6
+    assert np.array_equal(slopes, ws)
