@@ -8,7 +8,9 @@ Public surface mirrors the reference package ``polykan`` for this path:
 sm_100a kernels of ``lib/libchebykan.so``; there is no CPU fallback.
 """
 from .basis import (
+    RECURRENCES,
     BasisKind,
+    RecurrenceCoeffs,
     basis_rows,
     chebyshev_second_derivative_max,
     degree_for,

@@ -9,7 +9,9 @@ kernels (csrc/ck_basis.cuh).
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
 from enum import Enum
+from typing import Callable
 
 
 class BasisKind(Enum):
@@ -18,6 +20,27 @@ class BasisKind(Enum):
     HERMITE = "hermite"
     FOURIER = "fourier"
 
+
+@dataclass(frozen=True)
+class RecurrenceCoeffs:
+    """alpha_k B_{k+1} = beta_k(x) B_k - gamma_k B_{k-1} with seeds (basis.py:37-49).
+    The data the table builder and the kernels' recurrences implement."""
+
+    alpha_k: Callable[[int], float]
+    beta_k: Callable
+    gamma_k: Callable[[int], float]
+    seed0: Callable
+    seed1: Callable
+
+
+RECURRENCES = {  # basis.py:52-77
+    BasisKind.CHEBYSHEV: RecurrenceCoeffs(lambda k: 1.0, lambda k, x: 2.0 * x, lambda k: 1.0,
+                                          lambda x: x * 0 + 1.0, lambda x: x * 1.0),
+    BasisKind.LEGENDRE: RecurrenceCoeffs(lambda k: float(k + 1), lambda k, x: (2.0 * k + 1.0) * x,
+                                         lambda k: float(k), lambda x: x * 0 + 1.0, lambda x: x * 1.0),
+    BasisKind.HERMITE: RecurrenceCoeffs(lambda k: 1.0, lambda k, x: 2.0 * x, lambda k: 2.0 * k,
+                                        lambda x: x * 0 + 1.0, lambda x: 2.0 * x),
+}
 
 # ck_basis_kind codes (include/chebykan.h) == the PKLT basis tags (lut.py:35-40)
 BASIS_TAGS = {
