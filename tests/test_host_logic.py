@@ -161,3 +161,20 @@ def test_roofline_formulas_match_reference():
     assert [c.degree for c in ck.paper_configs()] == [8, 15, 24]
     with pytest.raises(ValueError, match="elem_bytes"):
         ck.LayerConfig(1, 1, 1, 1, 2)
+
+
+def test_reference_public_names_are_exported():
+    # every name polykan/__init__.py exports (its public surface, __init__.py:8-83)
+    import paper_2511_14852_b200 as ck
+
+    names = """BasisKind RecurrenceCoeffs eval_basis eval_basis_derivative eval_basis_trig feature_count
+    AtomicCounts BasisPath EXACT_MODE KernelCounters KernelMode LUT_MODE NonFiniteInputError PartialBuffer
+    TileSchedule backward_fused combine count_atomics forward_partial fused_forward reference_forward
+    DEFAULT_LUT_SIZE LutTable load_lut lut_build lut_interp lut_interp_with_slope lut_max_error_bound save_lut
+    AdamHParams AdamState Dataset Layer LayerSpec Loss Network NetworkSpec init_params layer_forward
+    load_checkpoint load_csv make_synthetic network_train save_checkpoint
+    BenchResult CostModel LayerConfig Regime RooflineReport TwoStageReport paper_configs roofline run_bench
+    two_stage_benefit CoeffTensor Layout doj_index jod_index load_coeff reorder_to_doj reorder_to_jod
+    save_coeff""".split()
+    missing = [n for n in names if not hasattr(ck, n)]
+    assert not missing, missing
