@@ -76,6 +76,18 @@ int gemm_group() {
 
 namespace {
 
+// LUT-mode fused dX: chord slopes recomputed in the epilogue (1, default for
+// the three-term families) or gathered from the dX rows (CK_DX_CHORD=0).
+int dx_chord() {
+  static int v = [] {
+    const char* e = getenv("CK_DX_CHORD");
+    return (e && std::string(e) == "0") ? 0 : 1;
+  }();
+  return v;
+}
+
+bool chord_kind(int kind) { return kind == kCheb || kind == kLegendre || kind == kHermite; }
+
 // CTA group for the GEMMs: 2 (SM pairs, default) or 1 (CK_GEMM_CG=1).
 int gemm_cg() {
   static int cg = [] {
@@ -139,6 +151,7 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
     CK_CHECK(p.nz == 1 && p.dx->n_i == dx_tile_inputs(p.S), "gemm: bad fused-dx configuration");
     if (p.dx->lut.exact) return launch_dx_exact(p, s);
     const bool bk64 = gemm_bk() == 64;
+    if (dx_chord() && bk64 && gemm_cg() == 2 && chord_kind(p.dx->lut.kind)) return launch_dx_chord(p, s);
     if (gemm_cg() == 2)
       return bk64 ? launch<256, 64, 3, kEpiDx, 2>(p, 1, nullptr, 0, 0, s)
                   : launch<256, 32, 6, kEpiDx, 2>(p, 1, nullptr, 0, 0, s);

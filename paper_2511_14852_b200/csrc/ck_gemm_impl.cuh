@@ -43,6 +43,9 @@ inline int store_ntile(int64_t N, int BN, int CG, bool mn_major) {
 }
 // fused dX GEMM with the exact-mode (analytic derivative) epilogue (ck_gemm_dx_exact.cu)
 int launch_dx_exact(const struct GemmProblem& p, cudaStream_t s);
+// LUT-mode fused dX with recomputed chord slopes (ck_gemm_dx_chord.cu);
+// kUnsupported for kinds without a three-term recurrence
+int launch_dx_chord(const struct GemmProblem& p, cudaStream_t s);
 
 namespace {
 
@@ -69,6 +72,7 @@ struct Cfg {
 
 constexpr int kEpiStore = 0;  // out (+)= acc (+ bias)
 constexpr int kEpiDx = 1;     // dx = J * sum_k slope_k * acc_k (stacked B)
+constexpr int kDxmChord = 8;  // DXM offset of the chord-slope LUT epilogues
 
 struct KArgs {
   int M, N;
@@ -136,10 +140,8 @@ struct DxBlock {
   static constexpr int W = D <= 4 ? 8 : 4;
 };
 
-template <int D>
-__device__ __forceinline__ void dx_load_x(const KArgs& p, const float* xr, bool row_ok, int i0,
-                                          float (&xv)[DxBlock<D>::W]) {
-  constexpr int W = DxBlock<D>::W;
+template <int W>
+__device__ __forceinline__ void dx_load_x(const KArgs& p, const float* xr, bool row_ok, int i0, float (&xv)[W]) {
   if (W >= 4 && ((p.ldo & 3) == 0) && row_ok && i0 + W <= p.N) {
 #pragma unroll
     for (int q = 0; q < W / 4; ++q) {
@@ -189,7 +191,7 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
   const float4* rows4 = reinterpret_cast<const float4*>(p.dxrows);
   int cb = W * h;
   float xv[W];
-  if (cb < n_i) dx_load_x<D>(p, xr, row_ok, n0 + cb, xv);
+  if (cb < n_i) dx_load_x(p, xr, row_ok, n0 + cb, xv);
 #pragma unroll 1
   for (; cb < n_i; cb += 2 * W) {
     uint32_t r[D][W];
@@ -212,7 +214,7 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
 #pragma unroll
       for (int j = 0; j < NS; ++j) sl[e][j] = __ldg(rows4 + static_cast<long long>(c) * (S / 4) + j);
     }
-    if (cb + 2 * W < n_i) dx_load_x<D>(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
+    if (cb + 2 * W < n_i) dx_load_x(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       if (near[e]) {
@@ -235,6 +237,119 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
       float a = 0.0f;
 #pragma unroll
       for (int k = 0; k < D; ++k) a = fmaf(f[k], __uint_as_float(r[k][e]), a);
+      acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
+    }
+    const int i0 = n0 + cb;
+    if (row_ok) {
+      if (W >= 4 && vec && i0 + W <= p.N) {
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q)
+          *reinterpret_cast<float4*>(dxr + i0 + 4 * q) =
+              make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < W; ++e)
+          if (i0 + e < p.N) dxr[i0 + e] = acc[e];
+      }
+    }
+  }
+}
+
+// Chord slopes S_k = (B_k(a) - B_k(b)) / (a - b), k = 1..D, of the family's
+// features over the cell [b, a] -- the LUT slopes (values[:,1:] -
+// values[:,:-1]) / step (lut.py:86, 93) -- by the divided-difference form of
+// the three-term recurrence: with B_{k+1} = (A_k x + E_k) B_k - C_k B_{k-1},
+//   S_{k+1} = (A_k a + E_k) S_k + A_k B_k(b) - C_k S_{k-1},
+// which has no cancellation (unlike differencing two recomputed values, whose
+// k^2-ulp errors divided by the step would reach 1e-3).  Endpoint rounding of
+// the float32 nodes moves a chord by B''/2 * 1 ulp: <= 1e-6 relative for d <= 8.
+template <int KIND, int D>
+__device__ __forceinline__ void chord_slopes(float b, float a, float (&s)[D]) {
+  float pv = 1.0f, cv = KIND == kHermite ? 2.0f * b : b;  // B_0(b), B_1(b)
+  float sp = 0.0f, sc = KIND == kHermite ? 2.0f : 1.0f;   // S_0, S_1
+  s[0] = sc;
+#pragma unroll
+  for (int k = 1; k < D; ++k) {
+    float sn, vn;
+    if constexpr (KIND == kCheb) {
+      sn = fmaf(2.0f * a, sc, fmaf(2.0f, cv, -sp));
+      vn = fmaf(2.0f * b, cv, -pv);
+    } else if constexpr (KIND == kLegendre) {
+      const float c2 = static_cast<float>(2 * k + 1), ck = static_cast<float>(k);
+      const float inv = 1.0f / static_cast<float>(k + 1);
+      sn = fmaf(c2, fmaf(a, sc, cv), -ck * sp) * inv;
+      vn = fmaf(c2 * b, cv, -ck * pv) * inv;  // as basis_f32
+    } else {
+      const float c2k = static_cast<float>(2 * k);
+      sn = fmaf(2.0f, fmaf(a, sc, cv), -c2k * sp);
+      vn = fmaf(2.0f * b, cv, -c2k * pv);
+    }
+    s[k] = sn;
+    sp = sc;
+    sc = sn;
+    pv = cv;
+    cv = vn;
+  }
+}
+
+// LUT-mode input-gradient epilogue with recomputed chord slopes (three-term
+// families): the reference cell as in dx_epilogue (float32 position, the
+// cell boundaries gathered only inside the guard band), then the cell's
+// slopes from chord_slopes at its float32 grid nodes -- the node recomputation
+// the expansion kernels use for the values (DESIGN decision 2).  No per-element
+// table gather: short-K dX tiles were bound by that gather's L2 round trip.
+template <int KIND, int D>
+__device__ __forceinline__ void dx_epilogue_chord(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok,
+                                                  int h) {
+  // no slope registers to hold: 8 columns per block up to d = 8
+  constexpr int K = DxBlock<D>::K, S = DxBlock<D>::S, W = D <= 8 ? 8 : 4;
+  const int n_i = p.n_tile, N = p.lutN;
+  const float* xr = p.x + static_cast<long long>(row) * p.ldo;
+  float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
+  const bool vec = ((p.ldo & 3) == 0);
+  const float hN = 0.5f * static_cast<float>(N - 1);
+  const float stepf = 2.0f / static_cast<float>(N - 1);
+  int cb = W * h;
+  float xv[W];
+  if (cb < n_i) dx_load_x(p, xr, row_ok, n0 + cb, xv);
+#pragma unroll 1
+  for (; cb < n_i; cb += 2 * W) {
+    uint32_t r[D][W];
+#pragma unroll
+    for (int k = 0; k < D; ++k) tmem_ld_cols<W>(tbase + k * n_i + cb, r[k]);
+    float x_cur[W], t[W];
+    int cell[W];
+    bool near[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      x_cur[e] = xv[e];
+      const float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
+      t[e] = tt;
+      const float pos = fmaf(tt, hN, hN);
+      const int c = min(static_cast<int>(pos), N - 2);
+      const float fr = pos - static_cast<float>(c);
+      cell[e] = c;
+      near[e] = fr < p.guard || fr > 1.0f - p.guard;
+    }
+    if (cb + 2 * W < n_i) dx_load_x(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      if (near[e]) {
+        // exact reference cell: b_c <= x < b_{c+1}; at most one step off
+        const float* rw = p.dxrows + static_cast<long long>(cell[e]) * S;
+        const float bl = __ldg(rw + D), bh = __ldg(rw + K);
+        cell[e] += x_cur[e] < bl ? -1 : (x_cur[e] < bh ? 0 : 1);
+      }
+    }
+    tmem_ld_wait();
+    float acc[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      float sl[D];
+      chord_slopes<KIND, D>(grid_node_f(cell[e], N, stepf), grid_node_f(cell[e] + 1, N, stepf), sl);
+      float a = 0.0f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) a = fmaf(sl[k], __uint_as_float(r[k][e]), a);
       acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
     }
     const int i0 = n0 + cb;
@@ -313,8 +428,9 @@ __device__ __forceinline__ void dx_epilogue_exact(const KArgs& p, uint32_t tbase
   }
 }
 
-// DXM: input-gradient epilogue flavour -- 0 = LUT slopes (exact reference
-// cell), 1 + kind = analytic derivatives of that basis kind.
+// DXM: input-gradient epilogue flavour -- 0 = LUT slopes gathered from the
+// dX rows (exact reference cell), 1 + kind = analytic derivatives of that
+// basis kind (exact mode), kDxmChord + kind = LUT slopes recomputed as chords.
 template <int BN, int BK, int STAGES, int EPI, int CG, int AMN, int BMN, int DXM = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
@@ -516,6 +632,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define CK_DX_CASE(D) \
   case D:             \
     dx_epilogue<D>(p, tbase, tc.n0, row, row_ok, h); \
+    break;
+            CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
+            CK_DX_CASE(8) CK_DX_CASE(9) CK_DX_CASE(10) CK_DX_CASE(11) CK_DX_CASE(12) CK_DX_CASE(13)
+            CK_DX_CASE(14) CK_DX_CASE(15) CK_DX_CASE(16)
+#undef CK_DX_CASE
+            default:
+              break;
+          }
+        } else if constexpr (DXM >= kDxmChord) {
+          constexpr int KIND = DXM - kDxmChord;
+          switch (p.b_boxes) {
+#define CK_DX_CASE(D)                                            \
+  case D:                                                        \
+    dx_epilogue_chord<KIND, D>(p, tbase, tc.n0, row, row_ok, h); \
     break;
             CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
             CK_DX_CASE(8) CK_DX_CASE(9) CK_DX_CASE(10) CK_DX_CASE(11) CK_DX_CASE(12) CK_DX_CASE(13)

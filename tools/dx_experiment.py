@@ -1,7 +1,7 @@
 """Device time of the input-gradient path (fused dX GEMM, or the unfused
 GEMM + combine) at a few short-K shapes (dev tool).
 
-    python tools/dx_experiment.py LABEL
+    python tools/dx_experiment.py LABEL [lut|exact] [LUT_SIZE]
 """
 import sys
 
@@ -18,7 +18,10 @@ for (b, i, o, d) in [(16384, 256, 256, 3), (16384, 512, 512, 5), (16384, 256, 25
     x = torch.rand(b, i, device=dev) * 3 - 1.5
     c = (torch.rand(d + 1, o, i, device=dev) * 2 - 1) / (i * (d + 1)) ** 0.5
     dy = torch.randn(b, o, device=dev)
-    lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, 32768, device=dev)
+    mode = sys.argv[2] if len(sys.argv) > 2 else "lut"
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 32768
+    lut = (ck.exact_basis(ck.BasisKind.CHEBYSHEV, d, device=dev) if mode == "exact"
+           else ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=dev))
     prep = PreparedCoeff(c)
     for _ in range(3):
         backward_raw(x, dy, prep, lut, True, want_dc=False, want_db=False)
