@@ -27,9 +27,14 @@ struct PrepLayout {
   int n_i;             // inputs per stacked tile (0: DJO layout)
   int64_t dxb_rows;    // rows of the input-gradient operand
   bool skinny;         // d_out <= 8: only an fp32 DOJ copy at offset 0
-  size_t doj_hi, doj_lo, dxb_hi, dxb_lo, c0sum, total;
+  bool gen;            // narrow output: + the generated forward's coefficient copy
+  int64_t gen_elems;   // O * gen_chunks * 64 per hi / lo
+  size_t doj_hi, doj_lo, dxb_hi, dxb_lo, c0sum, gen_hi, gen_lo, total;
   PrepLayout(int I, int O, int K) {
     skinny = skinny_layer(I, O, K);
+    gen = false;
+    gen_elems = 0;
+    gen_hi = gen_lo = 0;
     if (skinny) {
       ldI = I;
       ldO = O;
@@ -52,6 +57,13 @@ struct PrepLayout {
     dxb_lo = dxb_hi + dxb;
     c0sum = dxb_lo + dxb;
     total = c0sum + align_up(sizeof(float) * O);
+    gen = gen_layer(I, O, K);
+    if (gen) {
+      gen_elems = static_cast<int64_t>(O) * gen_chunks(I, d) * 64;
+      gen_hi = total;
+      gen_lo = gen_hi + align_up(sizeof(__nv_bfloat16) * gen_elems);
+      total = gen_lo + align_up(sizeof(__nv_bfloat16) * gen_elems);
+    }
   }
 };
 
@@ -304,6 +316,10 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
   }
   // k = 0 term: T_0 == 1 so its contribution is the per-output constant
   CK_TRY(ck::launch_row_sum(coeff_doj, O, I, ck::at<float>(prep, L.c0sum), s));
+  if (L.gen) {
+    CK_TRY(ck::launch_gen_coeff(coeff_doj, d_in, d_out, n_feat - 1, ck::at<__nv_bfloat16>(prep, L.gen_hi),
+                                ck::at<__nv_bfloat16>(prep, L.gen_lo), s));
+  }
   return kOk;
 }
 
@@ -345,6 +361,12 @@ extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, co
   const ck::PrepLayout P(d_in, d_out, K);
   void* pv = const_cast<void*>(prep);
   const float* c0sum = ck::at<float>(pv, P.c0sum);
+  if (basis_cache == nullptr && d > 0 && P.gen && ck::gen_supported(ck::view(lut))) {
+    // narrow output, no planes wanted by a backward: the basis is generated
+    // in shared memory inside the GEMM (one launch for the whole batch)
+    return ck::gemm_gen_forward(x, batch, d_in, d_out, ck::view(lut), ck::at<__nv_bfloat16>(pv, P.gen_hi),
+                                ck::at<__nv_bfloat16>(pv, P.gen_lo), bias, c0sum, y, s);
+  }
   int64_t ci = 0;
   for (int64_t r0 = 0; r0 < batch; r0 += W.chunk, ++ci) {
     const int64_t rows = batch - r0 < W.chunk ? batch - r0 : W.chunk;

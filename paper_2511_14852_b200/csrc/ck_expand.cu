@@ -97,32 +97,6 @@ __global__ void __launch_bounds__(kThreads) basis_eval_kernel(const float* __res
 }
 
 // --- specialized planes kernels ----------------------------------------------
-// Values of features k = 1..D at one element.  kLutNodes: the two table
-// entries bracketing the cell are recomputed at the (float32-rounded) grid
-// nodes by the family's recurrence -- the same table entries to ~k^2 ulp,
-// with no memory traffic -- then interpolated v0 (1-f) + v1 f.  kExact:
-// the basis at t = tanh(x) itself.
-enum PlaneSource : int { kSrcNodes = 0, kSrcExact = 1 };
-
-template <int kSrc, int KIND, int D>
-__device__ __forceinline__ void elem_planes(float xv, int n, float (&out)[D]) {
-  if constexpr (kSrc == kSrcExact) {
-    float v[D + 1];
-    basis_f32<KIND, D>(tanhf(xv), v);
-#pragma unroll
-    for (int k = 1; k <= D; ++k) out[k - 1] = v[k];
-  } else {
-    int idx;
-    float f;
-    cell_f32(xv, n, idx, f);
-    float v0[D + 1], v1[D + 1];
-    basis_f32<KIND, D>(grid_node_f(idx, n, 2.0f / static_cast<float>(n - 1)), v0);
-    basis_f32<KIND, D>(grid_node_f(idx + 1, n, 2.0f / static_cast<float>(n - 1)), v1);
-#pragma unroll
-    for (int k = 1; k <= D; ++k) out[k - 1] = lerp_ref(v0[k], v1[k], f);
-  }
-}
-
 // Planes k = 1..D, hi/lo [k-1][r][ld]: each thread expands 4 adjacent
 // columns of one row (two bf16x2 pairs) and writes one 8-byte word per plane
 // for hi and lo (a warp stores 256 contiguous bytes per plane).

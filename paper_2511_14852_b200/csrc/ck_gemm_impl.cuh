@@ -98,6 +98,9 @@ struct KArgs {
   const float* bias0;
   const float* bias1;
   int accumulate;
+  // generated-operand forward (ck_gemm_gen.cu): x pitch and input count
+  long long gen_ldx;
+  int gen_I;
 };
 
 // Tile decode shared by all roles (persistent static schedule: CTA c takes
@@ -428,6 +431,71 @@ __device__ __forceinline__ void dx_epilogue_exact(const KArgs& p, uint32_t tbase
   }
 }
 
+// Store epilogue, one 32-row x 32-column accumulator chunk of a warp (lane =
+// row, r[j] = column j): staged through a warp-private 4 KB shared tile
+// (16-byte slots XOR-swizzled by row, conflict-free both ways) so that each
+// global store instruction writes four full 128-byte row segments instead of
+// 32 scattered 16-byte pieces -- the partial-line writes made the store
+// epilogue of a one-tile-per-CTA launch take ~7 us.
+constexpr int kEpiTileBytes = 32 * 32 * 4;
+
+__device__ __forceinline__ void store_chunk_coalesced(const uint32_t (&r)[32], float* tile, int lane, int row0,
+                                                      int M, int nb, int N, float* out, long long ldo,
+                                                      const float* bias0, const float* bias1, int accumulate,
+                                                      bool vec) {
+#pragma unroll
+  for (int c4 = 0; c4 < 8; ++c4) {
+    const int slot = c4 ^ (lane & 7);
+    *reinterpret_cast<float4*>(tile + lane * 32 + slot * 4) =
+        make_float4(__uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1]), __uint_as_float(r[4 * c4 + 2]),
+                    __uint_as_float(r[4 * c4 + 3]));
+  }
+  __syncwarp();
+  const int c4 = lane & 7;      // this lane's 4 columns
+  const int rsub = lane >> 3;   // row within each group of 4
+  const int n = nb + 4 * c4;
+  float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (vec && n + 4 <= N) {
+    if (bias0) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias0 + n));
+      bv.x += b.x; bv.y += b.y; bv.z += b.z; bv.w += b.w;
+    }
+    if (bias1) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias1 + n));
+      bv.x += b.x; bv.y += b.y; bv.z += b.z; bv.w += b.w;
+    }
+  }
+#pragma unroll 4
+  for (int rg = 0; rg < 32; rg += 4) {
+    const int lr = rg + rsub;
+    const int row = row0 + lr;
+    float4 v = *reinterpret_cast<const float4*>(tile + lr * 32 + ((c4 ^ (lr & 7)) * 4));
+    if (row >= M) continue;
+    float* dst = out + static_cast<long long>(row) * ldo + n;
+    if (vec && n + 4 <= N) {
+      v.x += bv.x; v.y += bv.y; v.z += bv.z; v.w += bv.w;
+      if (accumulate) {
+        const float4 prev = *reinterpret_cast<const float4*>(dst);
+        v.x += prev.x; v.y += prev.y; v.z += prev.z; v.w += prev.w;
+      }
+      *reinterpret_cast<float4*>(dst) = v;
+    } else {
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (n + q < N) {
+          float o = e[q];
+          if (bias0) o += bias0[n + q];
+          if (bias1) o += bias1[n + q];
+          if (accumulate) o += dst[q];
+          dst[q] = o;
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // DXM: input-gradient epilogue flavour -- 0 = LUT slopes gathered from the
 // dX rows (exact reference cell), 1 + kind = analytic derivatives of that
 // basis kind (exact mode), kDxmChord + kind = LUT slopes recomputed as chords.
@@ -675,8 +743,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------- store epilogue -------------
         float* out = p.out + static_cast<long long>(tc.z) * p.out_z_stride +
                      static_cast<long long>(tc.split) * p.out_split_stride;
-        float* orow = out + static_cast<long long>(row) * p.ldo;
         const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+        float* tile = reinterpret_cast<float*>(smem + STAGES * C::kStageBytes + C::kBarrierBytes) +
+                      (warp - 4) * (kEpiTileBytes / 4);
+        const int row0 = tc.m0 + row_off + q * 32;
         // 32-column chunks of the (runtime) tile width, alternating between
         // the two warps of this TMEM lane quarter
 #pragma unroll 1
@@ -685,40 +755,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x32(tbase + c, r);
           tmem_ld_wait();
           const int nb = tc.n0 + c;
-          if (!row_ok || nb >= p.N) continue;
-          if (vec && nb + 32 <= p.N) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 o = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                     __uint_as_float(r[j + 3]));
-              if (p.bias0) {
-                const float4 bv = __ldg(reinterpret_cast<const float4*>(p.bias0 + nb + j));
-                o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
-              }
-              if (p.bias1) {
-                const float4 bv = __ldg(reinterpret_cast<const float4*>(p.bias1 + nb + j));
-                o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
-              }
-              float4* dst = reinterpret_cast<float4*>(orow + nb + j);
-              if (p.accumulate) {
-                const float4 prev = *dst;
-                o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
-              }
-              *dst = o;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int n = nb + j;
-              if (n < p.N) {
-                float o = __uint_as_float(r[j]);
-                if (p.bias0) o += p.bias0[n];
-                if (p.bias1) o += p.bias1[n];
-                if (p.accumulate) o += orow[n];
-                orow[n] = o;
-              }
-            }
-          }
+          if (nb >= p.N) continue;
+          store_chunk_coalesced(r, tile, lane, row0, p.M, nb, p.N, out, p.ldo, p.bias0, p.bias1, p.accumulate,
+                                vec);
         }
       }
       tc_fence_before();
@@ -809,13 +848,16 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.bias1 = splits == 1 ? p.bias1 : nullptr;
   k.accumulate = accumulate;
   auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM>;
+  // store kernels: + a 4 KB staging tile per epilogue warp
+  constexpr int kSmem = C::kSmemBytes + (EPI == kEpiStore ? kEpiWarps * kEpiTileBytes : 0);
+  static_assert(kSmem <= 232448, "smem budget");
   // the opt-in shared-memory size is a per-device function attribute
   static std::atomic<uint64_t> attr_set{0};
   int dev = 0;
   CK_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = uint64_t(1) << (dev & 63);
   if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
-    CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr_set.fetch_or(bit);
   }
   k.group_m = gemm_group();
@@ -830,7 +872,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(units * CG));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;

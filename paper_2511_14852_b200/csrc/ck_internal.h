@@ -196,6 +196,19 @@ struct GemmProblem {
   const DxEpilogue* dx = nullptr;  // non-null: stacked-B fused dX path
 };
 int gemm_bf16x3(const GemmProblem& p, cudaStream_t s);
+
+// --- forward with the basis generated in shared memory (ck_gemm_gen.cu) -----
+// 64-wide reduction chunks of 64/d whole inputs (0: degree not supported)
+int gen_chunks(int I, int d);
+// layers whose prepared coefficients carry the generated operand's copy
+bool gen_layer(int I, int O, int K);
+bool gen_supported(const LutView& v);
+// coefficients [O][gen_chunks*64] bf16 hi/lo in the generated operand's order
+int launch_gen_coeff(const float* coeff_doj, int I, int O, int d, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                     cudaStream_t s);
+// y[M][O] = Φ(x) C^T + bias0 + bias1 (per column), Φ never materialised
+int gemm_gen_forward(const float* x, int64_t M, int I, int O, const LutView& v, const __nv_bfloat16* c_hi,
+                     const __nv_bfloat16* c_lo, const float* bias0, const float* bias1, float* y, cudaStream_t s);
 // Workspace (floats) the split-R path may want for this problem shape.
 int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R);
 

@@ -440,3 +440,64 @@ def test_multi_chunk_batch_vs_oracle():
             orc.normwise_err(layer.bias.grad.cpu().numpy(), want_db))
     print("multi-chunk", [f"{e:.2e}" for e in errs])
     assert max(errs) <= TOL, errs
+
+
+_GEN_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import paper_2511_14852_b200 as ck
+from paper_2511_14852_b200 import _lib
+from oracle import chebykan_oracle as orc
+dev = torch.device("cuda", 0)
+t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+worst = 0.0
+for (b, i, o, d, n) in {cases!r}:
+    x, c_jod, _ = orc.bench_inputs(b, i, o, d, seed=b + i + o + d)
+    c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
+    bias = np.random.default_rng(d).standard_normal(o).astype(np.float32)
+    if n == 0:
+        want = orc.exact_layer_forward(x, c_doj, "chebyshev", bias=bias, threads=8)
+        table, mode = None, ck.EXACT_MODE
+    else:
+        vals, _, _ = orc.build_table(d, n)
+        want = orc.layer_forward(x, c_doj, vals, bias=bias, threads=8)
+        table, mode = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=dev), ck.LUT_MODE
+    c = ck.CoeffTensor(i, o, d, ck.Layout.DOJ, t(c_doj.astype(np.float32)))
+    _lib.timing_collect()
+    _lib.timing_enable(True)
+    y = ck.fused_forward(t(x).contiguous(), c, table, mode=mode, bias=t(bias), kind=ck.BasisKind.CHEBYSHEV)
+    y = y.cpu().numpy()
+    torch.cuda.synchronize()
+    _lib.timing_enable(False)
+    kt = _lib.timing_collect()
+    assert kt.get("expand", (0, 0))[1] == 0, ("planes were materialised", kt)
+    e = orc.normwise_err(y, want)
+    print((b, i, o, d, n), f"{{e:.2e}}")
+    worst = max(worst, e)
+print("WORST", worst)
+"""
+
+
+def test_generated_forward_vs_oracle():
+    """The forward with the basis generated in shared memory (ck_gemm_gen.cu)
+    on every degree class, ragged inputs / outputs, two N tiles, LUT and exact
+    mode -- in a subprocess with CK_GEN=all (the default rule only picks it
+    for d >= 4, d*I >= 1536)."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    cases = [(300, 257, 130, 3, 512), (2048, 512, 256, 5, 1024), (96, 40, 300, 16, 32768), (1000, 100, 60, 1, 4096),
+             (5000, 129, 256, 8, 32768), (700, 64, 200, 2, 2048), (513, 130, 96, 11, 32768), (600, 96, 128, 6, 0)]
+    script = _GEN_SCRIPT.format(root=str(root), tests=str(root / "tests"), cases=cases)
+    env = dict(os.environ, CK_GEN="all", CK_GEN_MAX_O="512")
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    print(out.stdout[-3000:], out.stderr[-3000:])
+    assert out.returncode == 0
+    worst = float(out.stdout.strip().splitlines()[-1].split()[1])
+    assert worst <= TOL, worst
