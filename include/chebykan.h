@@ -111,7 +111,9 @@ CK_API int ck_basis_eval(const float* t, int64_t n, const ck_lut* lut, float* va
 /* --- Coefficient preparation (reorder_to_doj consumer, tensor.py:77-82) ---
  * Converts fp32 DOJ coefficients into the kernels' tensor-core operands:
  * bf16 hi/lo split copies in DOJ [K][O][I] (forward, unit stride in i) and
- * DJO [K][I][O] (input-gradient GEMM), plus sum_i C[0][o][i].  Call once
+ * DJO [K][I][O] (input-gradient GEMM), plus sum_i C[0][o][i]; narrow layers
+ * (d_out <= 256, d >= 4) also get an input-major copy for the forward that
+ * generates the basis in shared memory.  Call once
  * per parameter update; `prep` is an opaque caller-owned device buffer of
  * ck_coeff_prep_bytes(...) bytes. */
 CK_API size_t ck_coeff_prep_bytes(int d_in, int d_out, int n_feat);
@@ -124,7 +126,9 @@ CK_API int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int n_f
  * basis_cache (nullable, ck_basis_cache_bytes): when given, the forward keeps
  * the expanded basis planes there and ck_backward reuses them (the backward of
  * the same x then skips the expansion).  0 bytes = the layer does not use
- * basis planes (d_out <= 8 runs on the CUDA-core skinny kernels). */
+ * basis planes (d_out <= 8 runs on the CUDA-core skinny kernels).  Without a
+ * cache, narrow layers (see ck_coeff_prepare) never materialise the planes:
+ * the GEMM's generator warps write the basis into shared memory. */
 CK_API size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API size_t ck_basis_cache_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
