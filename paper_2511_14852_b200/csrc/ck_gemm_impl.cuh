@@ -7,13 +7,17 @@
 // tcgen05.mma.kind::f16 into one fp32 TMEM accumulator:
 // hi*hi + hi*lo + lo*hi (the lo*lo term is below fp32 round-off).
 //
-// Warp roles (256 threads, 1 CTA/SM):
-//   warp 0      TMA producer (one elected lane), SWIZZLE_128B K-major tiles
-//   warp 1      MMA issuer (one elected lane)
-//   warp 2      TMEM allocator
-//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> (+bias) -> global
-// Pipelines: smem full/empty mbarrier ring (TMA <-> MMA), one tmem-full
-// barrier (MMA -> epilogue).
+// Persistent, 1 CTA/SM; CG = 2 runs CTA pairs (cta_group::2, M = 256 per
+// pair tile, each CTA stages its 128 A rows and half of B).  Warp roles
+// (384 threads):
+//   warp 0       TMA producer (one elected lane), SWIZZLE_128B tiles, K- or
+//                MN-major
+//   warp 1       MMA issuer (one elected lane of the leader CTA)
+//   warp 2       TMEM allocator
+//   warps 4..11  epilogue: tcgen05.ld 32x32b -> registers -> store (staged
+//                through shared memory, + bias) or the fused dX fold
+// Pipelines: smem full/empty mbarrier ring (TMA <-> MMA), double-buffered
+// TMEM accumulator with tmem-full / tmem-empty barriers (MMA <-> epilogue).
 #pragma once
 #include <cudaTypedefs.h>
 
