@@ -51,33 +51,8 @@ int launch_dx_exact(const struct GemmProblem& p, cudaStream_t s);
 // kUnsupported for kinds without a three-term recurrence
 int launch_dx_chord(const struct GemmProblem& p, cudaStream_t s);
 
-namespace {
-
-constexpr int kBM = 128;
-constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
-constexpr int kEpiWarps = 8;
-constexpr int kMaxDFused = 16;       // fused dX epilogue: degree <= 16
-
-// BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
-// or 32 (64-byte rows, SWIZZLE_64B, twice the stages for the same smem).
-// CG = CTA group: 1 (one SM per 128 x BN tile) or 2 (an SM pair per 256 x BN
-// tile; each CTA stages its 128 rows of A and half of the B rows).
-template <int BN, int BK, int STAGES, int CG = 1>
-struct Cfg {
-  static constexpr int kRowBytes = BK * 2;
-  static constexpr int kABytes = kBM * kRowBytes;   // one of hi / lo
-  static constexpr int kBBytes = (BN / CG) * kRowBytes;
-  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
-  static constexpr int kBarrierBytes = 256;
-  static constexpr int kSmemBytes = STAGES * kStageBytes + kBarrierBytes + 1024;
-  static_assert(kSmemBytes <= 232448, "smem budget");
-};
-
-constexpr int kEpiStore = 0;  // out (+)= acc (+ bias)
-constexpr int kEpiDx = 1;     // dx = J * sum_k slope_k * acc_k (stacked B)
-constexpr int kDxmChord = 8;  // DXM offset of the chord-slope LUT epilogues
-
+// Kernel arguments (external linkage: the per-family generated-forward
+// launchers in separate translation units share this type).
 struct KArgs {
   int M, N;
   int S;
@@ -106,6 +81,34 @@ struct KArgs {
   long long gen_ldx;
   int gen_I;
 };
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
+constexpr int kMaxDFused = 16;       // fused dX epilogue: degree <= 16
+
+// BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
+// or 32 (64-byte rows, SWIZZLE_64B, twice the stages for the same smem).
+// CG = CTA group: 1 (one SM per 128 x BN tile) or 2 (an SM pair per 256 x BN
+// tile; each CTA stages its 128 rows of A and half of the B rows).
+template <int BN, int BK, int STAGES, int CG = 1>
+struct Cfg {
+  static constexpr int kRowBytes = BK * 2;
+  static constexpr int kABytes = kBM * kRowBytes;   // one of hi / lo
+  static constexpr int kBBytes = (BN / CG) * kRowBytes;
+  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
+  static constexpr int kBarrierBytes = 256;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + kBarrierBytes + 1024;
+  static_assert(kSmemBytes <= 232448, "smem budget");
+};
+
+constexpr int kEpiStore = 0;  // out (+)= acc (+ bias)
+constexpr int kEpiDx = 1;     // dx = J * sum_k slope_k * acc_k (stacked B)
+constexpr int kDxmChord = 8;  // DXM offset of the chord-slope LUT epilogues
+
 
 // Tile decode shared by all roles (persistent static schedule: CTA c takes
 // tiles c, c + grid, ...; n fastest so co-resident CTAs share A rows in L2).

@@ -454,28 +454,30 @@ from oracle import chebykan_oracle as orc
 dev = torch.device("cuda", 0)
 t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
 worst = 0.0
-for (b, i, o, d, n) in {cases!r}:
-    x, c_jod, _ = orc.bench_inputs(b, i, o, d, seed=b + i + o + d)
-    c_doj = orc.jod_to_doj(c_jod.astype(np.float64))
-    bias = np.random.default_rng(d).standard_normal(o).astype(np.float32)
+for (b, i, o, d, n, kind) in {cases!r}:
+    k = orc.feature_count(kind, d)
+    rng = np.random.default_rng(b + i + o + d)
+    s = 1.0 / np.sqrt(i * k)
+    x = rng.uniform(-1.5, 1.5, (b, i)).astype(np.float32)
+    c_doj = rng.uniform(-s, s, (k, o, i)).astype(np.float32)
+    bias = rng.standard_normal(o).astype(np.float32)
     if n == 0:
-        want = orc.exact_layer_forward(x, c_doj, "chebyshev", bias=bias, threads=8)
+        want = orc.exact_layer_forward(x, c_doj, kind, bias=bias, threads=8)
         table, mode = None, ck.EXACT_MODE
     else:
-        vals, _, _ = orc.build_table(d, n)
+        vals, _, _ = orc.build_table(d, n, kind)
         want = orc.layer_forward(x, c_doj, vals, bias=bias, threads=8)
-        table, mode = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=dev), ck.LUT_MODE
-    c = ck.CoeffTensor(i, o, d, ck.Layout.DOJ, t(c_doj.astype(np.float32)))
+        table, mode = ck.lut_build(ck.BasisKind(kind), d, n, device=dev), ck.LUT_MODE
+    c = ck.CoeffTensor(i, o, k - 1, ck.Layout.DOJ, t(c_doj))
     _lib.timing_collect()
     _lib.timing_enable(True)
-    y = ck.fused_forward(t(x).contiguous(), c, table, mode=mode, bias=t(bias), kind=ck.BasisKind.CHEBYSHEV)
-    y = y.cpu().numpy()
+    y = ck.fused_forward(t(x), c, table, mode=mode, bias=t(bias), kind=ck.BasisKind(kind)).cpu().numpy()
     torch.cuda.synchronize()
     _lib.timing_enable(False)
     kt = _lib.timing_collect()
     assert kt.get("expand", (0, 0))[1] == 0, ("planes were materialised", kt)
     e = orc.normwise_err(y, want)
-    print((b, i, o, d, n), f"{{e:.2e}}")
+    print((b, i, o, d, n, kind), f"{{e:.2e}}")
     worst = max(worst, e)
 print("WORST", worst)
 """
@@ -483,17 +485,22 @@ print("WORST", worst)
 
 def test_generated_forward_vs_oracle():
     """The forward with the basis generated in shared memory (ck_gemm_gen.cu)
-    on every degree class, ragged inputs / outputs, two N tiles, LUT and exact
-    mode -- in a subprocess with CK_GEN=all (the default rule only picks it
-    for d >= 4, d*I >= 1536)."""
+    on every degree class and basis family, ragged inputs / outputs, two N
+    tiles, LUT and exact mode -- in a subprocess with CK_GEN=all (the default
+    rule only picks it for d >= 4, d*I >= 1536)."""
     import os
     import pathlib
     import subprocess
     import sys
 
     root = pathlib.Path(__file__).resolve().parents[1]
-    cases = [(300, 257, 130, 3, 512), (2048, 512, 256, 5, 1024), (96, 40, 300, 16, 32768), (1000, 100, 60, 1, 4096),
-             (5000, 129, 256, 8, 32768), (700, 64, 200, 2, 2048), (513, 130, 96, 11, 32768), (600, 96, 128, 6, 0)]
+    cases = [(300, 257, 130, 3, 512, "chebyshev"), (2048, 512, 256, 5, 1024, "chebyshev"),
+             (96, 40, 300, 16, 32768, "chebyshev"), (1000, 100, 60, 1, 4096, "chebyshev"),
+             (5000, 129, 256, 8, 32768, "chebyshev"), (700, 64, 200, 2, 2048, "chebyshev"),
+             (513, 130, 96, 11, 32768, "chebyshev"), (600, 96, 128, 6, 0, "chebyshev"),
+             (700, 200, 160, 5, 4096, "legendre"), (400, 96, 64, 7, 0, "legendre"),
+             (700, 200, 160, 4, 4096, "hermite"), (400, 96, 64, 3, 0, "hermite"),
+             (700, 200, 160, 3, 4096, "fourier"), (400, 96, 64, 8, 0, "fourier")]
     script = _GEN_SCRIPT.format(root=str(root), tests=str(root / "tests"), cases=cases)
     env = dict(os.environ, CK_GEN="all", CK_GEN_MAX_O="512")
     out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
