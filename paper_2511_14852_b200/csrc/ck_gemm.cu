@@ -107,21 +107,35 @@ struct StoreCfg {
 
 StoreCfg pick_store(int64_t N) { return N <= 128 ? StoreCfg{128, 1} : StoreCfg{256, gemm_cg()}; }
 
-// Split-R factor for a store GEMM: when the output tiles fill less than half
-// a wave of work units (an SM, or an SM pair for cta_group::2), split the
-// reduction so one wave is full -- per-split partials, then the fixed-order
-// merge -- keeping >= 4 K blocks per split.
+// Split-R factor for a store GEMM, from a cost model in units of one
+// pipeline iteration of one tile (~0.8 us x n_tile/256 on a CTA pair):
+// rounds of the persistent schedule x iterations per split, plus the
+// fixed-order merge of the partials (read s, write 1 output at ~4 TB/s, and
+// a launch).  Splitting fills partial waves: 80 dC tiles on 74 SM pairs
+// (1024^2, d5) ran as two rounds, the second 8 % full; 8 splits run 9 rounds
+// of 1/8 the length.  >= 4 K blocks per split, <= 64 splits, partials
+// <= 1.5 GB.
 int choose_splits(int64_t M, int64_t N, int nz, int64_t R, const StoreCfg& c, bool mn_major) {
   const int nt = store_ntile(N, c.bn, c.cg, mn_major);
   const int64_t tiles = ceil_div(M, static_cast<int64_t>(kBM) * c.cg) * ceil_div(N, nt) * nz;
   const int64_t units = num_sms() / c.cg;
-  if (2 * tiles >= units) return 1;
   const int64_t chunks = ceil_div(R, 64);
-  int64_t splits = units / tiles;
-  const int64_t max_splits = chunks / 4 > 1 ? chunks / 4 : 1;
-  if (splits > max_splits) splits = max_splits;
-  if (splits > 64) splits = 64;
-  return static_cast<int>(splits < 1 ? 1 : splits);
+  const double t_it = 0.8e-6 * nt / 256.0 * (c.cg == 2 ? 1.0 : 0.5);
+  const double out_bytes = 4.0 * static_cast<double>(nz) * static_cast<double>(M) * static_cast<double>(N);
+  int64_t max_splits = chunks / 4 > 1 ? chunks / 4 : 1;
+  if (max_splits > 64) max_splits = 64;
+  double best = static_cast<double>(ceil_div(tiles, units) * chunks);
+  int best_s = 1;
+  for (int64_t s = 2; s <= max_splits; ++s) {
+    if (s * out_bytes > 1.5e9) break;
+    const double work = static_cast<double>(ceil_div(tiles * s, units) * ceil_div(chunks, s));
+    const double merge = ((s + 1) * out_bytes / 4e12 + 4e-6) / t_it;
+    if (work + merge < 0.97 * best) {
+      best = work + merge;
+      best_s = static_cast<int>(s);
+    }
+  }
+  return best_s;
 }
 
 }  // namespace
