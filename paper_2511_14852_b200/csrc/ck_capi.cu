@@ -122,6 +122,8 @@ struct BwdLayout {
     const size_t dbp = align_up(sizeof(double) * n_chunks * kDbSlots * O);
     int64_t s1 = d > 0 ? gemm_split_ws_elems(chunk, I, static_cast<int>(d), O) : 0;
     int64_t s2 = d > 0 ? gemm_split_ws_elems(O, I, static_cast<int>(d), chunk) : 0;
+    const int64_t s3 = d > 0 ? gemm_split_ws_elems(I, O, static_cast<int>(d), chunk) : 0;  // transposed dC
+    if (s3 > s2) s2 = s3;
     split_elems = s1 > s2 ? s1 : s2;
     dy_hi = 0;
     dy_lo = dy_hi + dy;
@@ -540,13 +542,23 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
         ph = w;
       }
       const __nv_bfloat16* pl = ph + L.half / sizeof(__nv_bfloat16);
-      // dC_k[o][i] = sum_b dy[b][o] Φ_k[b][i]: both operands MN-major (batch = K)
+      // dC_k[o][i] = sum_b dy[b][o] Φ_k[b][i]: both operands MN-major (batch = K).
+      // Orientation: M = O (dy as A) or, when that pads fewer output cells,
+      // M = I (planes as A) with a transposed store into the same [k][O][I].
       ck::GemmProblem gc{};
-      gc.a = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
-      gc.b = {ph, pl, I, L.ldI, L.plane, d, 1};
+      const bool trans = ck::gemm_store_padded(I, O, true) < ck::gemm_store_padded(O, I, true);
+      if (trans) {
+        gc.a = {ph, pl, I, L.ldI, L.plane, d, 1};
+        gc.b = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
+        gc.a_seg_z = 1;  // plane z holds k = z + 1
+        gc.out_trans = 1;
+      } else {
+        gc.a = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
+        gc.b = {ph, pl, I, L.ldI, L.plane, d, 1};
+        gc.b_seg_z = 1;  // plane z holds k = z + 1
+      }
       gc.R = rows;
       gc.S = 1;
-      gc.b_seg_z = 1;  // plane z holds k = z + 1
       gc.nz = d;
       gc.out = dc_doj + O * I;
       gc.ldo = I;

@@ -151,6 +151,12 @@ int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R) {
   return splits > 1 ? static_cast<int64_t>(splits) * nz * M * N : 0;
 }
 
+int64_t gemm_store_padded(int64_t M, int64_t N, bool mn_major) {
+  const StoreCfg c = pick_store(N);
+  const int nt = store_ntile(N, c.bn, c.cg, mn_major);
+  return ceil_div(M, static_cast<int64_t>(kBM) * c.cg) * kBM * c.cg * (ceil_div(N, nt) * nt);
+}
+
 int dx_tile_inputs(int d) {
   if (d < 1 || d > kMaxDFused) return 0;
   for (int n_i = (256 / d) / 8 * 8; n_i >= 8; n_i -= 8)
@@ -179,7 +185,7 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   int splits = choose_splits(p.a.rows, p.b.rows, p.nz, p.R, cfg, mn);
   const int64_t need = static_cast<int64_t>(splits) * p.nz * p.a.rows * p.b.rows;
   if (splits > 1 && (p.split_ws == nullptr || p.split_ws_elems < need)) splits = 1;
-  const bool dense_out = p.ldo == p.b.rows && p.out_z_stride == p.a.rows * p.b.rows;
+  const bool dense_out = p.ldo == (p.out_trans ? p.a.rows : p.b.rows) && p.out_z_stride == p.a.rows * p.b.rows;
   if (splits > 1 && !dense_out) splits = 1;
 
   float* out = p.out;

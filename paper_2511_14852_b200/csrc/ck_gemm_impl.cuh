@@ -41,6 +41,14 @@ int gemm_group();
 // spreading N evenly over ceil(N/BN) tiles.
 inline int store_ntile(int64_t N, int BN, int CG, bool mn_major) {
   const int gran = mn_major ? 64 * CG : 32;
+  if (mn_major) {
+    // coarse granule (64-wide slabs per CTA): the width with the least
+    // padding, ties to the wider tile (N = 257: 3 x 128, not 2 x 256)
+    int best = gran;
+    for (int nt = gran; nt <= BN; nt += gran)
+      if (ceil_div(N, nt) * nt <= ceil_div(N, best) * best) best = nt;
+    return best;
+  }
   const int64_t tiles = ceil_div(N, BN);
   const int nt = static_cast<int>(round_up(ceil_div(N, tiles), gran));
   return nt > BN ? BN : nt;
@@ -77,6 +85,7 @@ struct KArgs {
   const float* bias0;
   const float* bias1;
   int accumulate;
+  int out_trans;   // store out[n][m] (see GemmProblem::out_trans)
   // generated-operand forward (ck_gemm_gen.cu): x pitch and input count
   long long gen_ldx;
   int gen_I;
@@ -754,6 +763,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* tile = reinterpret_cast<float*>(smem + STAGES * C::kStageBytes + C::kBarrierBytes) +
                       (warp - 4) * (kEpiTileBytes / 4);
         const int row0 = tc.m0 + row_off + q * 32;
+        if (p.out_trans) {
+          // transposed: column n of the tile is a row of the output; lanes
+          // (= tile rows) are contiguous there, so each store is 128 bytes
+#pragma unroll 1
+          for (int c = 32 * h; c < p.n_tile; c += 64) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tbase + c, r);
+            tmem_ld_wait();
+            const int nb = tc.n0 + c;
+            if (row_ok && nb < p.N) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int n = nb + j;
+                if (n < p.N) {
+                  float o = __uint_as_float(r[j]);
+                  if (p.bias0) o += p.bias0[n];
+                  if (p.bias1) o += p.bias1[n];
+                  float* dst = out + static_cast<long long>(n) * p.ldo + row;
+                  if (p.accumulate) o += *dst;
+                  *dst = o;
+                }
+              }
+            }
+          }
+        } else {
         // 32-column chunks of the (runtime) tile width, alternating between
         // the two warps of this TMEM lane quarter
 #pragma unroll 1
@@ -765,6 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (nb >= p.N) continue;
           store_chunk_coalesced(r, tile, lane, row0, p.M, nb, p.N, out, p.ldo, p.bias0, p.bias1, p.accumulate,
                                 vec);
+        }
         }
       }
       tc_fence_before();
@@ -854,6 +889,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.bias0 = splits == 1 ? p.bias0 : nullptr;
   k.bias1 = splits == 1 ? p.bias1 : nullptr;
   k.accumulate = accumulate;
+  k.out_trans = p.out_trans;
   auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM>;
   // store kernels: + a 4 KB staging tile per epilogue warp
   constexpr int kSmem = C::kSmemBytes + (EPI == kEpiStore ? kEpiWarps * kEpiTileBytes : 0);

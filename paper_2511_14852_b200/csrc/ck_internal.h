@@ -193,6 +193,7 @@ struct GemmProblem {
   float* split_ws;     // workspace for split-R partials (nullable -> no split)
   int64_t split_ws_elems;
   int kclass = kKGemmFwd;  // timing / counting class
+  int out_trans = 0;       // 1: store out[z][n][m] (row pitch ldo) -- the transposed orientation
   const DxEpilogue* dx = nullptr;  // non-null: stacked-B fused dX path
 };
 int gemm_bf16x3(const GemmProblem& p, cudaStream_t s);
@@ -209,6 +210,8 @@ int launch_gen_coeff(const float* coeff_doj, int I, int O, int d, __nv_bfloat16*
 // y[M][O] = Φ(x) C^T + bias0 + bias1 (per column), Φ never materialised
 int gemm_gen_forward(const float* x, int64_t M, int I, int O, const LutView& v, const __nv_bfloat16* c_hi,
                      const __nv_bfloat16* c_lo, const float* bias0, const float* bias1, float* y, cudaStream_t s);
+// Output cells a store GEMM computes, tile padding included (orientation choice).
+int64_t gemm_store_padded(int64_t M, int64_t N, bool mn_major);
 // Workspace (floats) the split-R path may want for this problem shape.
 int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R);
 
