@@ -112,7 +112,10 @@ def test_module_autograd_matches_reference_golden(path):
 @pytest.mark.parametrize("shape", [(512, 1024, 1024, 8, 32768), (300, 257, 130, 3, 512),
                                    (1024, 64, 64, 4, 4096), (2048, 512, 512, 5, 1024),
                                    (257, 96, 1, 5, 1024), (64, 257, 512, 15, 16384),
-                                   (128, 64, 48, 17, 2048), (96, 40, 300, 24, 32768)])
+                                   (128, 64, 48, 17, 2048), (96, 40, 300, 24, 32768),
+                                   # d_out = 257 < d_in: the dC GEMM runs transposed (M = d_in);
+                                   # the second one over two 32768-row chunks (accumulated dC)
+                                   (700, 512, 257, 3, 1024), (33000, 256, 257, 1, 256)])
 def test_random_shapes_vs_oracle(shape):
     b, i, o, d, n = shape
     x, c_jod, dy = orc.bench_inputs(b, i, o, d, seed=b + i + o)
