@@ -274,43 +274,6 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
   }
 }
 
-// Chord slopes S_k = (B_k(a) - B_k(b)) / (a - b), k = 1..D, of the family's
-// features over the cell [b, a] -- the LUT slopes (values[:,1:] -
-// values[:,:-1]) / step (lut.py:86, 93) -- by the divided-difference form of
-// the three-term recurrence: with B_{k+1} = (A_k x + E_k) B_k - C_k B_{k-1},
-//   S_{k+1} = (A_k a + E_k) S_k + A_k B_k(b) - C_k S_{k-1},
-// which has no cancellation (unlike differencing two recomputed values, whose
-// k^2-ulp errors divided by the step would reach 1e-3).  Endpoint rounding of
-// the float32 nodes moves a chord by B''/2 * 1 ulp: <= 1e-6 relative for d <= 8.
-template <int KIND, int D>
-__device__ __forceinline__ void chord_slopes(float b, float a, float (&s)[D]) {
-  float pv = 1.0f, cv = KIND == kHermite ? 2.0f * b : b;  // B_0(b), B_1(b)
-  float sp = 0.0f, sc = KIND == kHermite ? 2.0f : 1.0f;   // S_0, S_1
-  s[0] = sc;
-#pragma unroll
-  for (int k = 1; k < D; ++k) {
-    float sn, vn;
-    if constexpr (KIND == kCheb) {
-      sn = fmaf(2.0f * a, sc, fmaf(2.0f, cv, -sp));
-      vn = fmaf(2.0f * b, cv, -pv);
-    } else if constexpr (KIND == kLegendre) {
-      const float c2 = static_cast<float>(2 * k + 1), ck = static_cast<float>(k);
-      const float inv = 1.0f / static_cast<float>(k + 1);
-      sn = fmaf(c2, fmaf(a, sc, cv), -ck * sp) * inv;
-      vn = fmaf(c2 * b, cv, -ck * pv) * inv;  // as basis_f32
-    } else {
-      const float c2k = static_cast<float>(2 * k);
-      sn = fmaf(2.0f, fmaf(a, sc, cv), -c2k * sp);
-      vn = fmaf(2.0f * b, cv, -c2k * pv);
-    }
-    s[k] = sn;
-    sp = sc;
-    sc = sn;
-    pv = cv;
-    cv = vn;
-  }
-}
-
 // LUT-mode input-gradient epilogue with recomputed chord slopes (three-term
 // families): the reference cell as in dx_epilogue (float32 position, the
 // cell boundaries gathered only inside the guard band), then the cell's

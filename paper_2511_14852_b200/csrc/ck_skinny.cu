@@ -46,8 +46,10 @@ __device__ __forceinline__ void elem_basis(const LutView& L, float xv, float (&v
       if (!L.exact) basis_f32<kHermite, P>(x1, b);
       break;
     case kFourier:
-      basis_f32<kFourier, P>(x0, a);
-      if (!L.exact) basis_f32<kFourier, P>(x1, b);
+      if constexpr (P % 2 == 0) {  // Fourier K = 2d + 1: P = K - 1 is even
+        basis_f32<kFourier, P>(x0, a);
+        if (!L.exact) basis_f32<kFourier, P>(x1, b);
+      }
       break;
     case kChebTrig:
       basis_f32<kChebTrig, P>(x0, a);
@@ -72,7 +74,7 @@ __device__ __forceinline__ void elem_deriv(int kind, float t, float (&dv)[P + 1]
       deriv_f32<kHermite, P>(t, dv);
       break;
     case kFourier:
-      deriv_f32<kFourier, P>(t, dv);
+      if constexpr (P % 2 == 0) deriv_f32<kFourier, P>(t, dv);
       break;
     default:
       deriv_f32<kCheb, P>(t, dv);  // also the trig form (same derivative)
@@ -80,8 +82,48 @@ __device__ __forceinline__ void elem_deriv(int kind, float t, float (&dv)[P + 1]
   }
 }
 
-// One warp per row (grid-stride), lanes stride the inputs; fixed shuffle
-// tree for the row reduction (deterministic).  KMAX = P + 1 >= K.
+// LUT cell slopes sv[1..P] of one element (sv[0] = 0, entries >= K zero):
+// the exact reference cell as in the fused dX epilogue (float32 position; the
+// cell boundaries loaded only inside the guard band), then the chord slopes
+// recomputed at the cell's float32 grid nodes (three-term families) or the
+// table's slopes (Fourier).
+template <int P>
+__device__ __forceinline__ void elem_slopes_lut(const LutView& L, float xv, float t, float (&sv)[P + 1]) {
+  const float hN = 0.5f * static_cast<float>(L.N - 1);
+  const float pos = fmaf(t, hN, hN);
+  int cell = min(static_cast<int>(pos), L.N - 2);
+  const float fr = pos - static_cast<float>(cell);
+  const float guard = fminf(0.5f, fmaxf(1e-3f, 4e-7f * static_cast<float>(L.N)));
+  const int S = dxrow_stride(L.K);
+  if (fr < guard || fr > 1.0f - guard) {
+    const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
+    const float bl = __ldg(row + L.K - 1), bh = __ldg(row + L.K);
+    cell += xv < bl ? -1 : (xv < bh ? 0 : 1);
+  }
+  float sl[P];
+  if (L.kind == kFourier) {
+    const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
+#pragma unroll
+    for (int k = 1; k <= P; ++k) sl[k - 1] = k < L.K ? __ldg(row + k - 1) : 0.0f;
+  } else {
+    const float stepf = 2.0f / static_cast<float>(L.N - 1);
+    const float b = grid_node_f(cell, L.N, stepf), a = grid_node_f(cell + 1, L.N, stepf);
+    if (L.kind == kLegendre) {
+      chord_slopes<kLegendre, P>(b, a, sl);
+    } else if (L.kind == kHermite) {
+      chord_slopes<kHermite, P>(b, a, sl);
+    } else {
+      chord_slopes<kCheb, P>(b, a, sl);
+    }
+  }
+  sv[0] = 0.0f;
+#pragma unroll
+  for (int k = 1; k <= P; ++k) sv[k] = k < L.K ? sl[k - 1] : 0.0f;
+}
+
+// One warp per row (grid-stride), lanes stride the inputs four at a time
+// (independent basis evaluations in flight); fixed shuffle tree for the row
+// reduction (deterministic).  KMAX = P + 1 >= K.
 template <int O, int P>
 __global__ void __launch_bounds__(256) skinny_fwd_kernel(const float* __restrict__ x, int64_t rows, int I, int K,
                                                          const float* __restrict__ c, const float* __restrict__ bias,
@@ -96,14 +138,24 @@ __global__ void __launch_bounds__(256) skinny_fwd_kernel(const float* __restrict
 #pragma unroll
     for (int o = 0; o < O; ++o) acc[o] = 0.0f;
     const float* xr = x + b * I;
-    for (int i = lane; i < I; i += 32) {
-      float v[P + 1];
-      elem_basis<P>(L, __ldg(xr + i), v);
+    for (int i0 = lane; i0 < I; i0 += 128) {
+      float xv[4];
 #pragma unroll
-      for (int k = 0; k <= P; ++k) {
-        if (k < K) {
+      for (int u = 0; u < 4; ++u) xv[u] = i0 + 32 * u < I ? __ldg(xr + i0 + 32 * u) : 0.0f;
 #pragma unroll
-          for (int o = 0; o < O; ++o) acc[o] = fmaf(v[k], __ldg(c + k * plane + static_cast<int64_t>(o) * I + i), acc[o]);
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u;
+        float v[P + 1];
+        elem_basis<P>(L, xv[u], v);
+        if (i < I) {
+#pragma unroll
+          for (int k = 0; k <= P; ++k) {
+            if (k < K) {
+#pragma unroll
+              for (int o = 0; o < O; ++o)
+                acc[o] = fmaf(v[k], __ldg(c + k * plane + static_cast<int64_t>(o) * I + i), acc[o]);
+            }
+          }
         }
       }
     }
@@ -156,50 +208,67 @@ __global__ void __launch_bounds__(256) skinny_bwd_kernel(const float* __restrict
   for (int o = 0; o < O; ++o) db[o] = 0.0;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rb;
   const int64_t r1 = r0 + rb < rows ? r0 + rb : rows;
-  const int S = dxrow_stride(K);
-  const float hN = 0.5f * static_cast<float>(L.N - 1);
-  for (int64_t b = r0 + w; b < r1; b += 8) {
-    float g[O];
+  // Rows in groups of R (independent basis evaluations in flight); x and dy
+  // of the next group are loaded while the current one is evaluated -- the
+  // row loop was bound by the HBM latency of x (ncu: long-scoreboard stalls
+  // on tanh's input).
+  constexpr int R = KMAX * O <= 8 ? 4 : (KMAX * O <= 16 ? 2 : 1);  // register budget
+  float xn[R], gn[R][O];
+  auto load_group = [&](int64_t bg) {
 #pragma unroll
-    for (int o = 0; o < O; ++o) g[o] = __ldg(dy + b * O + o);
+    for (int u = 0; u < R; ++u) {
+      const int64_t b = bg + 8 * u;
+      const bool ok = b < r1;
+      xn[u] = ok ? __ldg(x + b * I + ic) : 0.0f;
+#pragma unroll
+      for (int o = 0; o < O; ++o) gn[u][o] = ok ? __ldg(dy + b * O + o) : 0.0f;
+    }
+  };
+  load_group(r0 + w);
+  for (int64_t bg = r0 + w; bg < r1; bg += 8 * R) {
+    float xg[R], g[R][O];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      xg[u] = xn[u];
+#pragma unroll
+      for (int o = 0; o < O; ++o) g[u][o] = gn[u][o];
+    }
+    load_group(bg + 8 * R);
     if (blockIdx.y == 0 && lane == 0) {
 #pragma unroll
-      for (int o = 0; o < O; ++o) db[o] += static_cast<double>(g[o]);
+      for (int u = 0; u < R; ++u)
+#pragma unroll
+        for (int o = 0; o < O; ++o) db[o] += static_cast<double>(g[u][o]);  // zero past r1
     }
-    const float xv = __ldg(x + b * I + ic);
-    float t = tanhf(xv);
-    float vv[KMAX], sv[KMAX];
-    if (L.exact) {
-      elem_basis<P>(L, xv, vv);
-      elem_deriv<P>(L.kind, t, sv);
-    } else {
-      t = fminf(fmaxf(t, -1.0f), 1.0f);
-      // exact reference cell from the boundary rows (as the fused dX epilogue)
-      int cell = min(static_cast<int>(fmaf(t, hN, hN)), L.N - 2);
-      const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
-      if (xv < row[K - 1]) {
-        --cell;
-      } else if (!(xv < row[K])) {
-        ++cell;
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int64_t b = bg + 8 * u;
+      if (b >= r1) break;
+      const float xv = xg[u];
+      float t = tanhf(xv);
+      float vv[KMAX], sv[KMAX];
+      if (L.exact) {
+        elem_basis<P>(L, xv, vv);
+        elem_deriv<P>(L.kind, t, sv);
+      } else {
+        t = fminf(fmaxf(t, -1.0f), 1.0f);
+        elem_basis<P>(L, xv, vv);  // values are continuous: the float32 cell is fine
+        elem_slopes_lut<P>(L, xv, t, sv);
       }
-      row = L.dxrows + static_cast<int64_t>(cell) * S;
-      elem_basis<P>(L, xv, vv);  // values are continuous: the float32 cell is fine
+      float gx = 0.0f;
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k) sv[k] = (k >= 1 && k < K) ? __ldg(row + k - 1) : 0.0f;
+      for (int k = 1; k < KMAX; ++k) {
+        float gk = 0.0f;
+#pragma unroll
+        for (int o = 0; o < O; ++o) gk = fmaf(g[u][o], cr[k][o], gk);
+        gx = fmaf(sv[k], gk, gx);
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+        for (int o = 0; o < O; ++o) acc[k][o] = fmaf(g[u][o], vv[k], acc[k][o]);
+      if (dx && col_ok) dx[b * I + i] = jacobian ? gx * (1.0f - t * t) : gx;
     }
-    float gx = 0.0f;
-#pragma unroll
-    for (int k = 1; k < KMAX; ++k) {
-      float gk = 0.0f;
-#pragma unroll
-      for (int o = 0; o < O; ++o) gk = fmaf(g[o], cr[k][o], gk);
-      gx = fmaf(sv[k], gk, gx);
-    }
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-#pragma unroll
-      for (int o = 0; o < O; ++o) acc[k][o] = fmaf(g[o], vv[k], acc[k][o]);
-    if (dx && col_ok) dx[b * I + i] = jacobian ? gx * (1.0f - t * t) : gx;
   }
 #pragma unroll
   for (int k = 0; k < KMAX; ++k)
@@ -228,6 +297,11 @@ __global__ void __launch_bounds__(256) skinny_bwd_kernel(const float* __restrict
 
 int round_o(int O) { return O <= 1 ? 1 : O <= 2 ? 2 : O <= 4 ? 4 : 8; }
 
+int skinny_p(int O, int K) {
+  if (O == 1 && K <= 9) return K > 2 ? K - 1 : (K == 2 ? 1 : 1);
+  return K <= 5 ? 4 : K <= 9 ? 8 : K <= 17 ? 16 : 32;
+}
+
 }  // namespace
 
 bool skinny_layer(int d_in, int d_out, int n_feat) {
@@ -253,12 +327,14 @@ int launch_skinny_forward(const float* x, int64_t rows, int I, int O, const floa
   const int blocks = static_cast<int>(want < cap ? want : cap);
   const int K = L.K;
   LaunchScope scope(kKSkinny, s);
-  // P: smallest of 4 / 8 / 16 / 32 with P + 1 >= K (even, as Fourier needs)
-  const int pm = K <= 5 ? 4 : K <= 9 ? 8 : K <= 17 ? 16 : 32;
+  // P: smallest of 4 / 8 / 16 / 32 with P + 1 >= K (even, as Fourier needs);
+  // single-output heads get P = K - 1 exactly up to K = 9
+  const int pm = skinny_p(O, K);
 #define CK_SK(OO, PP)                                                                              \
   if (O == OO && pm == PP) {                                                                       \
     CK_CUDA(launch_k((skinny_fwd_kernel<OO, PP>), blocks, 256, 0, s, x, rows, I, K, c, bias, L, y));                \
   } else
+  CK_SK(1, 1) CK_SK(1, 2) CK_SK(1, 3) CK_SK(1, 5) CK_SK(1, 6) CK_SK(1, 7)
   CK_SK(1, 4) CK_SK(1, 8) CK_SK(1, 16) CK_SK(1, 32) CK_SK(2, 4) CK_SK(2, 8) CK_SK(2, 16)
   CK_SK(3, 4) CK_SK(3, 8) CK_SK(4, 4) CK_SK(4, 8)
   CK_SK(5, 4) CK_SK(6, 4) CK_SK(7, 4) CK_SK(8, 4) {
@@ -280,12 +356,13 @@ int launch_skinny_backward(const float* x, const float* dy, int64_t rows, int I,
   LaunchScope scope(kKSkinny, s);
   const int ro = round_o(O);
   CK_CHECK(K * ro <= kSkinnyMaxKO, "skinny backward: too many features x outputs");
-  // P + 1 >= K with P in 4 / 8 / 16 / 32 (register budget: K * round_o(O) <= 32)
-  const int pm = K <= 5 ? 4 : K <= 9 ? 8 : K <= 17 ? 16 : 32;
+  // P + 1 >= K as in the forward (register budget: K * round_o(O) <= 32)
+  const int pm = skinny_p(O, K);
 #define CK_SKB(OO, PP)                                                                                        \
   if (O == OO && pm == PP) {                                                                                  \
     CK_CUDA(launch_k((skinny_bwd_kernel<OO, PP>), grid, 256, 0, s, x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b)); \
   } else
+  CK_SKB(1, 1) CK_SKB(1, 2) CK_SKB(1, 3) CK_SKB(1, 5) CK_SKB(1, 6) CK_SKB(1, 7)
   CK_SKB(1, 4) CK_SKB(1, 8) CK_SKB(1, 16) CK_SKB(1, 32) CK_SKB(2, 4) CK_SKB(2, 8) CK_SKB(2, 16)
   CK_SKB(3, 4) CK_SKB(3, 8) CK_SKB(4, 4) CK_SKB(4, 8)
   CK_SKB(5, 4) CK_SKB(6, 4) CK_SKB(7, 4) CK_SKB(8, 4) {
