@@ -572,8 +572,8 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
   }
   if (need_db) {
     float* dbo = db != nullptr ? db : ck::at<float>(workspace, W.db_tmp);
-    CK_TRY(ck::launch_col_finish(db_part, static_cast<int>(W.n_chunks * ck::kDbSlots), O, dbo, s));
-    if (dc_doj) CK_TRY(ck::launch_broadcast_cols(dc_doj, O, I, dbo, s));  // dC_0 = db (T_0 == 1)
+    // db, and dC_0 = db (T_0 == 1) written by the same launch
+    CK_TRY(ck::launch_col_finish(db_part, static_cast<int>(W.n_chunks * ck::kDbSlots), O, dbo, s, dc_doj, I));
   }
   return kOk;
 }

@@ -121,7 +121,10 @@ int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cuda
 int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part, int slots,
                        cudaStream_t s);
 // out[c] = sum_{s<slots} part[s][c] -> float
-int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s);
+// out[c] = sum_s part[s][c] in fixed order; bcast (nullable): also
+// bcast[c][0..bcast_cols) = out[c]
+int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s,
+                      float* bcast = nullptr, int64_t bcast_cols = 0);
 // out[n] = (accumulate ? out[n] : 0) + sum_{s<S} partials[s * stride + n]
 int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate,
                  cudaStream_t s);
@@ -130,8 +133,6 @@ int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, con
                      cudaStream_t s);
 // out[r][c] += a[c] + b[c] (either nullable)
 int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s);
-// out[r][c] = v[r]  (dC_0 = db broadcast over inputs)
-int launch_broadcast_cols(float* out, int64_t rows, int64_t cols, const float* v, cudaStream_t s);
 
 // --- skinny-output layers (ck_skinny.cu) ----------------------------------
 // d_out <= 8 with n_feat * round_up_pow2(d_out) <= 32: CUDA-core kernels on

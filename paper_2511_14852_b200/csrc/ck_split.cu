@@ -202,22 +202,37 @@ __global__ void col_partial_kernel(const float* __restrict__ in, int64_t rows, i
 // out[c] = sum_s part[s][c]: block = 32 columns x 8 warps; warp w sums
 // slots w, w+8, ... and the 8 partials are folded in warp order (fixed
 // order for a given slot count: deterministic).
+// With bcast != nullptr the block also writes bcast[c][0..bcast_cols) =
+// out[c] for its 32 columns (dC_0 = db, the B_0 == 1 fold) -- one launch
+// instead of a separate broadcast.
 __global__ void __launch_bounds__(256) col_finish_kernel(const double* __restrict__ part, int slots, int64_t cols,
-                                                         float* __restrict__ out) {
+                                                         float* __restrict__ out, float* __restrict__ bcast,
+                                                         int64_t bcast_cols) {
   pdl_wait();
   __shared__ double red[8][32];
+  __shared__ float val[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t c = c0 + lane;
   double acc = 0.0;
   if (c < cols)
     for (int s = w; s < slots; s += 8) acc += part[s * cols + c];
   red[w][lane] = acc;
   __syncthreads();
-  if (w == 0 && c < cols) {
+  if (w == 0) {
     double t = 0.0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) t += red[j][lane];
-    out[c] = static_cast<float>(t);
+    val[lane] = static_cast<float>(t);
+    if (c < cols) out[c] = static_cast<float>(t);
+  }
+  if (bcast == nullptr) return;
+  __syncthreads();
+  const int nr = cols - c0 < 32 ? static_cast<int>(cols - c0) : 32;
+  for (int r = 0; r < nr; ++r) {
+    float* row = bcast + (c0 + r) * bcast_cols;
+    const float v = val[r];
+    for (int64_t i = threadIdx.x; i < bcast_cols; i += blockDim.x) row[i] = v;
   }
 }
 
@@ -269,15 +284,6 @@ __global__ void add_rows_kernel(float* __restrict__ out, int64_t rows, int64_t c
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t c = i % cols;
     out[i] += (a ? a[c] : 0.0f) + (b ? b[c] : 0.0f);
-  }
-}
-
-__global__ void broadcast_cols_kernel(float* __restrict__ out, int64_t rows, int64_t cols, const float* __restrict__ v) {
-  pdl_wait();
-  const int64_t n = rows * cols;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    out[i] = v[i / cols];
   }
 }
 
@@ -348,10 +354,12 @@ int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part
   return kOk;
 }
 
-int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s) {
+int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s, float* bcast,
+                      int64_t bcast_cols) {
   if (cols == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  CK_CUDA(launch_k((col_finish_kernel), static_cast<unsigned>(ceil_div(cols, 32)), 256, 0, s, part, slots, cols, out));
+  CK_CUDA(launch_k((col_finish_kernel), static_cast<unsigned>(ceil_div(cols, 32)), 256, 0, s, part, slots, cols, out,
+                   bcast, bcast_cols));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
@@ -380,12 +388,5 @@ int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, cons
   return kOk;
 }
 
-int launch_broadcast_cols(float* out, int64_t rows, int64_t cols, const float* v, cudaStream_t s) {
-  if (rows * cols == 0) return kOk;
-  LaunchScope scope(kKReduce, s);
-  CK_CUDA(launch_k((broadcast_cols_kernel), blocks_for(rows * cols), kThreads, 0, s, out, rows, cols, v));
-  CK_CUDA(cudaGetLastError());
-  return kOk;
-}
 
 }  // namespace ck
