@@ -118,14 +118,31 @@ class PeerAllreducer(GradientAllreducer):
         dist.all_gather_object(allh, mine, group=self.group)
         me = dist.get_rank(self.group)
         ptrs = []
+        opened = []
+        err = None
         for r, (h, o) in enumerate(allh):
             if r == me:
                 ptrs.append(self.flat.data_ptr())
                 continue
             p = ctypes.c_void_p()
             buf = (ctypes.c_uint8 * 64).from_buffer_copy(h)
-            _lib.check(lib.ck_ipc_open(buf, o, ctypes.byref(p)), "ck_ipc_open")
+            rc = lib.ck_ipc_open(buf, o, ctypes.byref(p))
+            if rc != 0:
+                err = _lib.last_error() or f"code {rc}"
+                break
+            opened.append((p.value, o))
             ptrs.append(p.value)
+        # every rank must have mapped every peer before any uses the mappings:
+        # agree on it, so a rank-local failure sends all ranks to the fallback
+        # together instead of leaving the others in the self-test's barriers
+        dev = self.flat.device
+        on = dev if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        ok = torch.tensor([0.0 if err else 1.0], device=on)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if ok.item() != 1.0:
+            for ptr, o in opened:
+                lib.ck_ipc_close(ctypes.c_void_p(ptr), o)
+            raise ValueError(f"peer-memory mapping failed on some rank ({err or 'a peer'})")
         self._offsets = [o for _, o in allh]
         self._peers = (ctypes.c_void_p * world)(*ptrs)
         self._rank, self._world = me, world
