@@ -242,7 +242,8 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
         const float bl = __ldg(rw + D), bh = __ldg(rw + K);
         const bool lo = x_cur[e] < bl, hi = !(x_cur[e] < bh);
         if (lo || hi) {
-          const long long c2 = cell[e] + (lo ? -1 : 1);
+          // clamped like the reference's idx = min(., N-2) (x = +inf lands past b_{N-1})
+          const long long c2 = min(cell[e] + (lo ? -1 : 1), N - 2);
 #pragma unroll
           for (int j = 0; j < NS; ++j) sl[e][j] = __ldg(rows4 + c2 * (S / 4) + j);
         }
@@ -320,7 +321,7 @@ __device__ __forceinline__ void dx_epilogue_chord(const KArgs& p, uint32_t tbase
         // exact reference cell: b_c <= x < b_{c+1}; at most one step off
         const float* rw = p.dxrows + static_cast<long long>(cell[e]) * S;
         const float bl = __ldg(rw + D), bh = __ldg(rw + K);
-        cell[e] += x_cur[e] < bl ? -1 : (x_cur[e] < bh ? 0 : 1);
+        cell[e] = min(cell[e] + (x_cur[e] < bl ? -1 : (x_cur[e] < bh ? 0 : 1)), N - 2);  // x = +inf: N-2
       }
     }
     tmem_ld_wait();

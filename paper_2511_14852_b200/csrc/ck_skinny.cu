@@ -98,7 +98,7 @@ __device__ __forceinline__ void elem_slopes_lut(const LutView& L, float xv, floa
   if (fr < guard || fr > 1.0f - guard) {
     const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
     const float bl = __ldg(row + L.K - 1), bh = __ldg(row + L.K);
-    cell += xv < bl ? -1 : (xv < bh ? 0 : 1);
+    cell = min(cell + (xv < bl ? -1 : (xv < bh ? 0 : 1)), L.N - 2);  // x = +inf: N-2 as the reference
   }
   float sl[P];
   if (L.kind == kFourier) {

@@ -253,3 +253,32 @@ def test_point_evaluation_known_answers():
     wv, ws = orc.lut_values_and_slopes(pts.astype(np.float32).astype(np.float64), *orc.build_table(6, 1025, "legendre")[:2])
     assert np.abs(vals - wv).max() <= 2e-6
     assert np.array_equal(slopes, ws)
+
+
+@pytest.mark.parametrize("o", [1, 96])
+def test_saturated_inputs_use_the_last_cell(o):
+    # tanh(+-inf) = +-1 and |x| >= 10 saturate; the reference clamps the cell to
+    # N-2 (lut.py:101-103): the LUT-mode slopes (no Jacobian, so they reach dX
+    # unscaled) and values at the ends of the table, on the tensor-core path
+    # (o = 96) and the skinny path (o = 1)
+    rng = np.random.default_rng(31)
+    b, i, d, n = 257, 40, 5, 1024
+    x = rng.uniform(-1.5, 1.5, (b, i)).astype(np.float32)
+    x[::7, 0] = np.inf
+    x[1::7, 1] = -np.inf
+    x[2::7, 2] = 1e30
+    x[3::7, 3] = -1e30
+    x[4::7, 4] = 20.0
+    c_doj = rng.uniform(-0.3, 0.3, (d + 1, o, i)).astype(np.float32)
+    dy = rng.standard_normal((b, o)).astype(np.float32)
+    vals, slopes, _ = orc.build_table(d, n)
+    want_y = orc.layer_forward(x, c_doj, vals)
+    want_dc, want_dx, _ = orc.layer_backward(x, c_doj, dy, vals, slopes, include_tanh_jacobian=False)
+    lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, d, n, device=_dev())
+    c = ck.CoeffTensor(i, o, d, ck.Layout.DOJ, _t(c_doj))
+    mode = ck.KernelMode(ck.BasisPath.LUT_INTERP, False)
+    y = ck.fused_forward(_t(x), c, lut, None, mode).cpu().numpy()
+    cg, dx = ck.backward_fused(_t(x), c, _t(dy), lut, None, mode)
+    assert orc.normwise_err(y, want_y) <= 1e-4
+    assert orc.normwise_err(cg.data.cpu().numpy(), want_dc) <= 1e-4
+    assert orc.normwise_err(dx.cpu().numpy(), want_dx) <= 1e-4
