@@ -181,6 +181,13 @@ CK_API int ck_adam_step(float* param, const float* grad, float* m, float* v, int
  * ck_adam_step_dev updates each tensor reading bc_dev.  A captured CUDA graph
  * of a training step then advances the bias correction on every replay. */
 CK_API int ck_adam_begin(int64_t* step_dev, float* bc_dev, double beta1, double beta2, void* stream);
+/* The same update for `count` tensors in one launch (a step's whole parameter
+ * list): arrays of device pointers and sizes (host memory).  bc_dev != NULL:
+ * bias corrections from the device (capturable, `step` ignored); else from
+ * `step` like ck_adam_step. */
+CK_API int ck_adam_step_multi(int count, float* const* params, const float* const* grads, float* const* m,
+                              float* const* v, const int64_t* sizes, double lr, double beta1, double beta2,
+                              double eps, int64_t step, const float* bc_dev, void* stream);
 CK_API int ck_adam_step_dev(float* param, const float* grad, float* m, float* v, int64_t n, double lr,
                      double beta1, double beta2, double eps, const float* bc_dev, void* stream);
 

@@ -56,6 +56,9 @@ SIGNATURES = {
     "ck_adam_begin": (_c_int, [_c_p, _c_p, ctypes.c_double, ctypes.c_double, _c_p]),
     "ck_adam_step_dev": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_double, _c_p, _c_p]),
+    "ck_adam_step_multi": (_c_int, [_c_int, ctypes.POINTER(_c_p), ctypes.POINTER(_c_p), ctypes.POINTER(_c_p),
+                                    ctypes.POINTER(_c_p), ctypes.POINTER(_c_i64), ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_double, _c_i64, _c_p, _c_p]),
     "ck_ipc_handle": (_c_int, [_c_p, _c_p, ctypes.POINTER(_c_i64)]),
     "ck_ipc_open": (_c_int, [_c_p, _c_i64, ctypes.POINTER(_c_p)]),
     "ck_ipc_close": (_c_int, [_c_p, _c_i64]),

@@ -59,6 +59,61 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, c
   }
 }
 
+// Several tensors in one launch (a training step's whole parameter list):
+// the tensors are cut into chunks of kMultiChunk elements, a block walks
+// chunks grid-stride and finds its tensor in the chunk prefix table.
+constexpr int kMultiMax = 32;
+constexpr int kMultiChunk = 2048;
+
+struct MultiTensors {
+  int count;
+  float* p[kMultiMax];
+  const float* g[kMultiMax];
+  float* m[kMultiMax];
+  float* v[kMultiMax];
+  int64_t n[kMultiMax];
+  int64_t chunk0[kMultiMax + 1];  // first chunk of each tensor; chunk0[count] = total
+};
+
+__global__ void __launch_bounds__(kThreads) adam_multi_kernel(const __grid_constant__ MultiTensors T, AdamArgs a) {
+  pdl_wait();
+  if (a.bc_dev) {
+    a.bc1 = a.bc_dev[0];
+    a.bc2 = a.bc_dev[1];
+  }
+  const int64_t total = T.chunk0[T.count];
+  for (int64_t c = blockIdx.x; c < total; c += gridDim.x) {
+    int t = 0;
+    while (t + 1 < T.count && T.chunk0[t + 1] <= c) ++t;
+    const int64_t e0 = (c - T.chunk0[t]) * kMultiChunk;
+    const int64_t e1 = e0 + kMultiChunk < T.n[t] ? e0 + kMultiChunk : T.n[t];
+    float* p = T.p[t];
+    const float* g = T.g[t];
+    float* m = T.m[t];
+    float* v = T.v[t];
+    const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                       reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
+                     e1 - e0 == kMultiChunk;
+    if (vec) {
+      for (int64_t i = e0 / 4 + threadIdx.x; i < e1 / 4; i += blockDim.x) {
+        float4 pp = reinterpret_cast<float4*>(p)[i];
+        const float4 gg = reinterpret_cast<const float4*>(g)[i];
+        float4 mm = reinterpret_cast<float4*>(m)[i];
+        float4 vv = reinterpret_cast<float4*>(v)[i];
+        adam_one(pp.x, gg.x, mm.x, vv.x, a);
+        adam_one(pp.y, gg.y, mm.y, vv.y, a);
+        adam_one(pp.z, gg.z, mm.z, vv.z, a);
+        adam_one(pp.w, gg.w, mm.w, vv.w, a);
+        reinterpret_cast<float4*>(p)[i] = pp;
+        reinterpret_cast<float4*>(m)[i] = mm;
+        reinterpret_cast<float4*>(v)[i] = vv;
+      }
+    } else {
+      for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) adam_one(p[i], g[i], m[i], v[i], a);
+    }
+  }
+}
+
 // step += 1; bc = {1 - b1^step, 1 - b2^step} (float64 pow, model.py:262-263)
 __global__ void adam_begin_kernel(int64_t* step, float* bc, double b1, double b2) {
   pdl_wait();
@@ -124,4 +179,50 @@ extern "C" int ck_adam_step_dev(float* param, const float* grad, float* m, float
   a.eps = static_cast<float>(eps);
   a.bc_dev = bc_dev;
   return ck::adam_launch(param, grad, m, v, n, a, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int ck_adam_step_multi(int count, float* const* params, const float* const* grads, float* const* m,
+                                  float* const* v, const int64_t* sizes, double lr, double beta1, double beta2,
+                                  double eps, int64_t step, const float* bc_dev, void* stream) {
+  CK_CHECK(count >= 0, "ck_adam_step_multi: negative count");
+  CK_CHECK(count == 0 || (params && grads && m && v && sizes), "ck_adam_step_multi: NULL array");
+  CK_CHECK(bc_dev != nullptr || step >= 1, "ck_adam_step_multi: step counts from 1");
+  ck::AdamArgs a;
+  a.lr = static_cast<float>(lr);
+  a.b1 = static_cast<float>(beta1);
+  a.omb1 = static_cast<float>(1.0 - beta1);
+  a.b2 = static_cast<float>(beta2);
+  a.omb2 = static_cast<float>(1.0 - beta2);
+  a.bc1 = bc_dev ? 1.0f : static_cast<float>(1.0 - std::pow(beta1, static_cast<double>(step)));
+  a.bc2 = bc_dev ? 1.0f : static_cast<float>(1.0 - std::pow(beta2, static_cast<double>(step)));
+  a.eps = static_cast<float>(eps);
+  a.bc_dev = bc_dev;
+  auto s = static_cast<cudaStream_t>(stream);
+  for (int base = 0; base < count; base += ck::kMultiMax) {
+    ck::MultiTensors T{};
+    int k = 0;
+    int64_t chunks = 0;
+    for (int t = base; t < count && k < ck::kMultiMax; ++t) {
+      CK_CHECK(sizes[t] >= 0, "ck_adam_step_multi: negative size");
+      if (sizes[t] == 0) continue;
+      CK_CHECK(params[t] && grads[t] && m[t] && v[t], "ck_adam_step_multi: NULL tensor");
+      T.p[k] = params[t];
+      T.g[k] = grads[t];
+      T.m[k] = m[t];
+      T.v[k] = v[t];
+      T.n[k] = sizes[t];
+      T.chunk0[k] = chunks;
+      chunks += ck::ceil_div(sizes[t], static_cast<int64_t>(ck::kMultiChunk));
+      ++k;
+    }
+    if (k == 0) continue;
+    T.count = k;
+    T.chunk0[k] = chunks;
+    const int64_t cap = static_cast<int64_t>(ck::num_sms()) * 8;
+    ck::LaunchScope scope(ck::kKOptim, s);
+    CK_CUDA(ck::launch_k((ck::adam_multi_kernel), static_cast<int>(chunks < cap ? chunks : cap), ck::kThreads, 0, s,
+                         T, a));
+    CK_CUDA(cudaGetLastError());
+  }
+  return ck::kOk;
 }

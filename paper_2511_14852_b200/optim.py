@@ -4,10 +4,12 @@ The update rule is the reference trainer's ``adam_step`` (model.py:247-266):
 m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2, p -= lr * m_hat / (sqrt(v_hat) + eps),
 one step counter per optimizer, an optional per-step ``lr_scale`` (the cosine
 decay of network_train, model.py:447-451).  ``ck_adam_step`` runs it in place
-on each fp32 parameter tensor (one HBM pass over p, g, m, v).
+on one fp32 tensor (one HBM pass over p, g, m, v); ``Adam.step`` updates all
+of a device's parameters with one ``ck_adam_step_multi`` launch.
 """
 from __future__ import annotations
 
+import ctypes
 import math
 
 import torch
@@ -81,38 +83,48 @@ class Adam(torch.optim.Optimizer):
         for group in self.param_groups:
             b1, b2 = group["betas"]
             lr = group["lr"] * lr_scale
-            for p in group["params"]:
-                if p.grad is None:
-                    continue
-                st = self.state[p]
-                if not st:
-                    st["m"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
-                    st["v"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
-                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
-                adam_update(p, g, st["m"], st["v"], lr, b1, b2, group["eps"], self._step)
+            for dev, items in self._grouped(group).items():
+                self._multi(items, lr, b1, b2, group["eps"], self._step, None, dev)
         return loss
+
+    def _grouped(self, group) -> dict:
+        """{device: [(p, g, m, v)]} of the group's parameters with gradients
+        (moment buffers created on first use)."""
+        out = {}
+        for p in group["params"]:
+            if p.grad is None:
+                continue
+            if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
+                raise ValueError("Adam: parameters must be contiguous fp32 CUDA tensors")
+            st = self.state[p]
+            if not st:
+                st["m"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
+                st["v"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
+            g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+            out.setdefault(p.device, []).append((p, g, st["m"], st["v"]))
+        return out
+
+    @staticmethod
+    def _multi(items, lr, b1, b2, eps, step, bc, dev) -> None:
+        """One ck_adam_step_multi launch for all of a device's tensors."""
+        n = len(items)
+        arr = lambda k: (ctypes.c_void_p * n)(*[it[k].data_ptr() for it in items])  # noqa: E731
+        sizes = (ctypes.c_int64 * n)(*[it[0].numel() for it in items])
+        _lib.check(_lib.lib().ck_adam_step_multi(n, arr(0), arr(1), arr(2), arr(3), sizes, float(lr), float(b1),
+                                                 float(b2), float(eps), int(step),
+                                                 bc.data_ptr() if bc is not None else None,
+                                                 _lib.stream_handle(dev)), "ck_adam_step_multi")
+        for p, _, m, v in items:
+            for t in (p, m, v):
+                torch.autograd.graph.increment_version(t)
 
     def _step_capturable(self, lr_scale: float) -> None:
         lib = _lib.lib()
         for gi, group in enumerate(self.param_groups):
             b1, b2 = group["betas"]
             lr = group["lr"] * lr_scale
-            begun = set()
-            for p in group["params"]:
-                if p.grad is None:
-                    continue
-                step_t, bc = self._device_counters(gi, p.device)
-                if p.device not in begun:
-                    _lib.check(lib.ck_adam_begin(step_t.data_ptr(), bc.data_ptr(), float(b1), float(b2),
-                                                 _lib.stream_handle(p.device)), "ck_adam_begin")
-                    begun.add(p.device)
-                st = self.state[p]
-                if not st:
-                    st["m"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
-                    st["v"] = torch.zeros_like(p, memory_format=torch.contiguous_format)
-                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
-                _lib.check(lib.ck_adam_step_dev(p.data_ptr(), g.data_ptr(), st["m"].data_ptr(), st["v"].data_ptr(),
-                                                p.numel(), float(lr), float(b1), float(b2), float(group["eps"]),
-                                                bc.data_ptr(), _lib.stream_handle(p.device)), "ck_adam_step_dev")
-                for t in (p, st["m"], st["v"]):
-                    torch.autograd.graph.increment_version(t)
+            for dev, items in self._grouped(group).items():
+                step_t, bc = self._device_counters(gi, dev)
+                _lib.check(lib.ck_adam_begin(step_t.data_ptr(), bc.data_ptr(), float(b1), float(b2),
+                                             _lib.stream_handle(dev)), "ck_adam_begin")
+                self._multi(items, lr, b1, b2, group["eps"], 0, bc, dev)
