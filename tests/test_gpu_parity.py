@@ -479,6 +479,8 @@ for (b, i, o, d, n, kind) in {cases!r}:
     _lib.timing_enable(False)
     kt = _lib.timing_collect()
     assert kt.get("expand", (0, 0))[1] == 0, ("planes were materialised", kt)
+    y2 = ck.fused_forward(t(x), c, table, mode=mode, bias=t(bias), kind=ck.BasisKind(kind)).cpu().numpy()
+    assert np.array_equal(y, y2), "generated forward not bitwise reproducible"
     e = orc.normwise_err(y, want)
     print((b, i, o, d, n, kind), f"{{e:.2e}}")
     worst = max(worst, e)
