@@ -410,7 +410,7 @@ struct SkinnyBwdLayout {
   int slots;
   size_t part_c, part_b, total;
   SkinnyBwdLayout(int64_t B, int I, int O, int K) {
-    slots = skinny_slots(B, I);
+    slots = skinny_slots(B, I, O, K);
     part_c = 0;
     part_b = align_up(sizeof(float) * slots * static_cast<size_t>(K) * O * I);
     total = part_b + align_up(sizeof(double) * slots * O) + kAlign;

@@ -142,7 +142,7 @@ constexpr int kSkinnyMaxKO = 32;
 constexpr int kSkinnyMaxSlots = 128;
 bool skinny_layer(int d_in, int d_out, int n_feat);
 // row blocks of the skinny backward's partial reduction for this shape
-int skinny_slots(int64_t rows, int d_in);
+int skinny_slots(int64_t rows, int d_in, int d_out, int n_feat);
 int launch_skinny_forward(const float* x, int64_t rows, int I, int O, const float* c, const float* bias,
                           const ck_lut* lut, float* y, cudaStream_t s);
 // dx (nullable) written directly; part_c [slots][K][O][I] float and part_b

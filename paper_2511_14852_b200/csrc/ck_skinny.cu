@@ -309,9 +309,30 @@ bool skinny_layer(int d_in, int d_out, int n_feat) {
   return d_out <= kSkinnyMaxO && n_feat * round_o(d_out) <= kSkinnyMaxKO;
 }
 
-int skinny_slots(int64_t rows, int d_in) {
+// Resident blocks per SM of the backward instantiation for (O, K): the grid
+// is sized to one full wave (a partial second wave cost up to a third of the
+// kernel: 592 blocks of the C2 head on 444 slots).
+int skinny_bwd_blocks_per_sm(int O, int K) {
+  const int pm = skinny_p(O, K);
+  int n = 0;
+#define CK_OCC(OO, PP)                                                                           \
+  if (O == OO && pm == PP) {                                                                     \
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, skinny_bwd_kernel<OO, PP>, 256, 0) != \
+        cudaSuccess)                                                                             \
+      n = 0;                                                                                     \
+  } else
+  CK_OCC(1, 1) CK_OCC(1, 2) CK_OCC(1, 3) CK_OCC(1, 5) CK_OCC(1, 6) CK_OCC(1, 7)
+  CK_OCC(1, 4) CK_OCC(1, 8) CK_OCC(1, 16) CK_OCC(1, 32) CK_OCC(2, 4) CK_OCC(2, 8) CK_OCC(2, 16)
+  CK_OCC(3, 4) CK_OCC(3, 8) CK_OCC(4, 4) CK_OCC(4, 8)
+  CK_OCC(5, 4) CK_OCC(6, 4) CK_OCC(7, 4) CK_OCC(8, 4) {}
+#undef CK_OCC
+  return n > 0 ? n : 1;
+}
+
+int skinny_slots(int64_t rows, int d_in, int d_out, int n_feat) {
   const int64_t colblocks = ceil_div(d_in, 32);
-  int64_t slots = ceil_div(4 * static_cast<int64_t>(num_sms()), colblocks);
+  const int64_t wave = static_cast<int64_t>(skinny_bwd_blocks_per_sm(d_out, n_feat)) * num_sms();
+  int64_t slots = wave / colblocks;
   const int64_t max_slots = ceil_div(rows > 0 ? rows : 1, 64);  // >= 64 rows per slot
   if (slots > max_slots) slots = max_slots;
   if (slots > kSkinnyMaxSlots) slots = kSkinnyMaxSlots;
