@@ -99,6 +99,29 @@ def test_adam_kernel_matches_reference_rule():
     assert np.abs(pt.cpu().numpy() - p).max() <= 1e-6
 
 
+@pytest.mark.parametrize("capturable", [False, True])
+def test_multi_tensor_adam_bitwise_equals_per_tensor(capturable):
+    # ck_adam_step_multi (one launch, 40 tensors -> two launches of <= 32, ragged
+    # sizes with tails that are not whole float4s) == ck_adam_step per tensor, bit for bit
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    sizes = [1, 3, 2047, 2048, 2049, 4096 + 5, 17, 100000] + [int(s) for s in torch.randint(1, 5000, (32,), generator=g)]
+    params = [torch.nn.Parameter(torch.randn(n, generator=g).to(dev)) for n in sizes]
+    ref = [p.detach().clone() for p in params]
+    ms = [torch.zeros_like(p) for p in ref]
+    vs = [torch.zeros_like(p) for p in ref]
+    opt = ck.Adam(params, lr=3e-3, capturable=capturable)
+    for t in range(1, 4):
+        grads = [torch.randn(n, generator=g).to(dev) for n in sizes]
+        for p, gr in zip(params, grads):
+            p.grad = gr.clone()
+        opt.step()
+        for r, gr, m, v in zip(ref, grads, ms, vs):
+            ck.adam_update(r, gr, m, v, 3e-3, 0.9, 0.999, 1e-8, t)
+    for p, r in zip(params, ref):
+        assert torch.equal(p.detach(), r)
+
+
 def test_training_divergence_reports_epoch_and_batch():
     rng = np.random.default_rng(0)
     x = rng.uniform(-1, 1, (64, 2))
