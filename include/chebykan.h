@@ -114,11 +114,20 @@ CK_API int ck_basis_eval(const float* t, int64_t n, const ck_lut* lut, float* va
  * DJO [K][I][O] (input-gradient GEMM), plus sum_i C[0][o][i]; narrow layers
  * (d_out <= 256, d >= 4) also get an input-major copy for the forward that
  * generates the basis in shared memory.  Call once
- * per parameter update; `prep` is an opaque caller-owned device buffer of
- * ck_coeff_prep_bytes(...) bytes. */
+ * per parameter update (any write to the coefficients, including in-place
+ * writes the caller makes, needs a new ck_coeff_prepare before the next
+ * forward/backward); `prep` is an opaque caller-owned device buffer of
+ * ck_coeff_prep_bytes(...) bytes.  The buffer starts with a header
+ * {magic, version, d_in, d_out, n_feat, flags, bytes}; the library also
+ * records (host side) the shape each buffer was prepared for, and
+ * ck_forward / ck_backward return CK_INVALID_ARGUMENT for a buffer that is
+ * too small, was never prepared, or was prepared for another shape. */
 CK_API size_t ck_coeff_prep_bytes(int d_in, int d_out, int n_feat);
 CK_API int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int n_feat, void* prep,
                      size_t prep_bytes, void* stream);
+/* Validation (synchronous): the host record and the device header of `prep`
+ * match (d_in, d_out, n_feat); CK_INVALID_ARGUMENT otherwise. */
+CK_API int ck_coeff_prep_check(const void* prep, size_t prep_bytes, int d_in, int d_out, int n_feat);
 
 /* --- Forward: replaces fused_forward (kernels.py:351-371) ------------------
  * y[b][o] = sum_i sum_k T_k(tanh x[b][i]) C[k][o][i] + bias[o]
@@ -132,8 +141,8 @@ CK_API int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int n_f
 CK_API size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API size_t ck_basis_cache_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
-               const float* bias, float* y, void* workspace, size_t workspace_bytes, void* basis_cache,
-               size_t basis_cache_bytes, void* stream);
+               size_t prep_bytes, const float* bias, float* y, void* workspace, size_t workspace_bytes,
+               void* basis_cache, size_t basis_cache_bytes, void* stream);
 
 /* --- The two stages separately: forward_partial (kernels.py:263-318) and
  * combine (kernels.py:321-348), for callers of the partial buffer itself.
@@ -157,9 +166,18 @@ CK_API int ck_combine(const float* partial, int64_t batch, int d_out, int g_x, i
  * fixed-order two-stage merge: bit-reproducible run to run. */
 CK_API size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
-                const void* prep, int include_tanh_jacobian, float* dx, float* dc_doj, float* db,
-                void* workspace, size_t workspace_bytes, const void* basis_cache, size_t basis_cache_bytes,
-                void* stream);
+                const void* prep, size_t prep_bytes, int include_tanh_jacobian, float* dx, float* dc_doj,
+                float* db, void* workspace, size_t workspace_bytes, const void* basis_cache,
+                size_t basis_cache_bytes, void* stream);
+
+/* Rows per internal batch chunk of ck_forward / ck_backward (default 32768;
+ * CK_CHUNK_ROWS in the environment at load).  Chunks run in ascending order
+ * on the caller's stream and dC accumulates over them in that order.
+ * Process-wide; workspace and basis-cache sizes follow it, so change it only
+ * between layer calls, never between a forward and the backward that reuses
+ * its basis cache.  rows <= 0 restores the default.  Returns the previous
+ * value. */
+CK_API int64_t ck_set_chunk_rows(int64_t rows);
 
 /* --- Deterministic merge: replaces combine's ordered fold (kernels.py:321-348)
  * and the ordered x-grad merge (kernels.py:438-442) as a standalone op.

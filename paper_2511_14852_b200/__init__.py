@@ -34,6 +34,7 @@ from .kernels import (
     PreparedCoeff,
     TileSchedule,
     backward_fused,
+    chunk_rows,
     combine,
     count_atomics,
     forward_partial,

@@ -43,10 +43,12 @@ SIGNATURES = {
     "ck_coeff_prepare": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_p, _c_size, _c_p]),
     "ck_forward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
     "ck_basis_cache_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
-    "ck_forward": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p, _c_size,
-                            _c_p]),
+    "ck_coeff_prep_check": (_c_int, [_c_p, _c_size, _c_int, _c_int, _c_int]),
+    "ck_set_chunk_rows": (_c_i64, [_c_i64]),
+    "ck_forward": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_size, _c_p, _c_p, _c_p, _c_size, _c_p,
+                            _c_size, _c_p]),
     "ck_backward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
-    "ck_backward": (_c_int, [_c_p, _c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_p, _c_p, _c_p,
+    "ck_backward": (_c_int, [_c_p, _c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_size, _c_int, _c_p, _c_p, _c_p,
                              _c_p, _c_size, _c_p, _c_size, _c_p]),
     "ck_merge": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_int, _c_p]),
     "ck_forward_partial": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_int, _c_p, _c_p]),

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "ck_common.cuh"
@@ -18,30 +19,34 @@ thread_local std::string g_error;
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-// Opaque coefficient-prep buffer: bf16 hi/lo DOJ [K][O][ldI] (forward B
-// operand); the input-gradient B operand, either "stacked" -- rows
-// (i-tile, k, i) so one TMA box feeds a d x n_i N tile -- or plain DJO
-// [K][I][ldO] when the degree is too large to stack; and c0sum[O].
+// Opaque coefficient-prep buffer: a PrepHeader slot; bf16 hi/lo DOJ
+// [K][O][ldI] (forward B operand); the input-gradient B operand, either
+// "stacked" -- rows (i-tile, k, i) so one TMA box feeds a d x n_i N tile --
+// or plain DJO [K][I][ldO] when the degree is too large to stack; and
+// c0sum[O].  Skinny layers keep only an fp32 DOJ copy after the header.
 struct PrepLayout {
   int64_t ldI, ldO;
   int n_i;             // inputs per stacked tile (0: DJO layout)
   int64_t dxb_rows;    // rows of the input-gradient operand
-  bool skinny;         // d_out <= 8: only an fp32 DOJ copy at offset 0
+  bool skinny;         // d_out <= 8: only an fp32 DOJ copy (at f32)
   bool gen;            // narrow output: + the generated forward's coefficient copy
   int64_t gen_elems;   // O * gen_chunks * 64 per hi / lo
-  size_t doj_hi, doj_lo, dxb_hi, dxb_lo, c0sum, gen_hi, gen_lo, total;
+  size_t hdr, f32, doj_hi, doj_lo, dxb_hi, dxb_lo, c0sum, gen_hi, gen_lo, total;
   PrepLayout(int I, int O, int K) {
     skinny = skinny_layer(I, O, K);
     gen = false;
     gen_elems = 0;
     gen_hi = gen_lo = 0;
+    hdr = 0;
+    f32 = 0;
     if (skinny) {
       ldI = I;
       ldO = O;
       n_i = 0;
       dxb_rows = 0;
       doj_hi = doj_lo = dxb_hi = dxb_lo = c0sum = 0;
-      total = align_up(sizeof(float) * K * O * static_cast<size_t>(I));
+      f32 = kAlign;
+      total = f32 + align_up(sizeof(float) * K * O * static_cast<size_t>(I));
       return;
     }
     ldI = round_up(I, 8);
@@ -51,7 +56,7 @@ struct PrepLayout {
     dxb_rows = n_i > 0 ? ceil_div(I, n_i) * d * n_i : static_cast<int64_t>(K) * I;
     const size_t doj = align_up(sizeof(__nv_bfloat16) * K * O * ldI);
     const size_t dxb = align_up(sizeof(__nv_bfloat16) * dxb_rows * ldO);
-    doj_hi = 0;
+    doj_hi = kAlign;
     doj_lo = doj_hi + doj;
     dxb_hi = doj_lo + doj;
     dxb_lo = dxb_hi + dxb;
@@ -67,6 +72,45 @@ struct PrepLayout {
   }
 };
 
+// Host-side record of every prep buffer ck_coeff_prepare has filled: device
+// address -> (I, O, K).  ck_forward / ck_backward reject a buffer prepared
+// for another layer shape (or never prepared) before any kernel reads it.
+struct PrepShape {
+  int d_in, d_out, n_feat;
+};
+std::mutex g_prep_mu;
+std::unordered_map<uintptr_t, PrepShape> g_preps;
+
+int check_prep(const void* prep, size_t prep_bytes, int d_in, int d_out, int n_feat) {
+  CK_CHECK(prep != nullptr, "coefficient prep is NULL");
+  const size_t need = PrepLayout(d_in, d_out, n_feat).total + kAlign;
+  if (prep_bytes < need) {
+    set_error("coefficient prep buffer too small: " + std::to_string(prep_bytes) + " bytes, the layer needs " +
+              std::to_string(need));
+    return kInvalidArgument;
+  }
+  std::lock_guard<std::mutex> lk(g_prep_mu);
+  auto it = g_preps.find(reinterpret_cast<uintptr_t>(prep));
+  if (it == g_preps.end()) {
+    set_error("coefficient prep buffer was not filled by ck_coeff_prepare");
+    return kInvalidArgument;
+  }
+  const PrepShape& p = it->second;
+  if (p.d_in != d_in || p.d_out != d_out || p.n_feat != n_feat) {
+    set_error("coefficient prep was prepared for (d_in, d_out, n_feat) = (" + std::to_string(p.d_in) + ", " +
+              std::to_string(p.d_out) + ", " + std::to_string(p.n_feat) + "), not (" + std::to_string(d_in) + ", " +
+              std::to_string(d_out) + ", " + std::to_string(n_feat) + ")");
+    return kInvalidArgument;
+  }
+  return kOk;
+}
+
+std::atomic<int64_t> g_chunk_rows{[] {
+  const char* e = getenv("CK_CHUNK_ROWS");
+  const long long v = e ? atoll(e) : 0;
+  return static_cast<int64_t>(v >= 1 ? v : kChunkRowsDefault);
+}()};
+
 // Basis planes of one chunk: Φ_k hi/lo for k = 1..d, [d][chunk][ldI] bf16.
 // The forward writes them; the backward's dC GEMM reads them as its MN-major
 // B operand.  With a caller-provided cache the planes of every chunk persist
@@ -75,7 +119,8 @@ struct BasisLayout {
   int64_t chunk, n_chunks, ldI, plane;
   size_t half, per_chunk, total;
   BasisLayout(int64_t B, int I, int K) {
-    chunk = B < kChunkRows ? B : kChunkRows;
+    const int64_t cr = chunk_rows();
+    chunk = B < cr ? B : cr;
     if (chunk < 1) chunk = 1;
     n_chunks = ceil_div(B > 0 ? B : 1, chunk);
     ldI = round_up(I, 8);
@@ -218,6 +263,8 @@ int num_sms() {
   return cached[dev];
 }
 
+int64_t chunk_rows() { return g_chunk_rows.load(std::memory_order_relaxed); }
+
 }  // namespace ck
 
 using ck::kOk;
@@ -300,29 +347,58 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
   auto s = static_cast<cudaStream_t>(stream);
   const ck::PrepLayout L(d_in, d_out, n_feat);
   const int64_t I = d_in, O = d_out, K = n_feat;
+  {
+    // forget the buffer's previous shape until it is rewritten
+    std::lock_guard<std::mutex> lk(ck::g_prep_mu);
+    ck::g_preps.erase(reinterpret_cast<uintptr_t>(prep));
+  }
+  ck::PrepHeader h{ck::kPrepMagic, ck::kPrepVersion, d_in, d_out, n_feat, (L.skinny ? 1 : 0) | (L.gen ? 2 : 0),
+                   static_cast<uint64_t>(ck_coeff_prep_bytes(d_in, d_out, n_feat))};
+  CK_TRY(ck::launch_prep_header(ck::at<void>(prep, L.hdr), h, s));
   if (L.skinny) {
-    CK_CUDA(cudaMemcpyAsync(ck::at<float>(prep, 0), coeff_doj, sizeof(float) * K * O * I, cudaMemcpyDeviceToDevice, s));
-    return kOk;
-  }
-  // DOJ copies: rows (k,o), unit stride in i
-  CK_TRY(ck::launch_split_rows(coeff_doj, 1, K * O, I, 0, ck::at<__nv_bfloat16>(prep, L.doj_hi),
-                               ck::at<__nv_bfloat16>(prep, L.doj_lo), L.ldI, 0, s));
-  if (L.n_i > 0) {
-    // stacked input-gradient operand (k = 1..d), padded inputs zeroed
-    CK_TRY(ck::launch_split_transpose_stacked(coeff_doj, K, O, I, L.n_i, ck::at<__nv_bfloat16>(prep, L.dxb_hi),
-                                              ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, s));
+    CK_CUDA(cudaMemcpyAsync(ck::at<float>(prep, L.f32), coeff_doj, sizeof(float) * K * O * I, cudaMemcpyDeviceToDevice,
+                            s));
   } else {
-    // DJO copies: per k, transpose [O][I] -> [I][O]
-    CK_TRY(ck::launch_split_transpose(coeff_doj, K, O, I, O * I, ck::at<__nv_bfloat16>(prep, L.dxb_hi),
-                                      ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, I * L.ldO, s));
+    // DOJ copies: rows (k,o), unit stride in i
+    CK_TRY(ck::launch_split_rows(coeff_doj, 1, K * O, I, 0, ck::at<__nv_bfloat16>(prep, L.doj_hi),
+                                 ck::at<__nv_bfloat16>(prep, L.doj_lo), L.ldI, 0, s));
+    if (L.n_i > 0) {
+      // stacked input-gradient operand (k = 1..d), padded inputs zeroed
+      CK_TRY(ck::launch_split_transpose_stacked(coeff_doj, K, O, I, L.n_i, ck::at<__nv_bfloat16>(prep, L.dxb_hi),
+                                                ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, s));
+    } else {
+      // DJO copies: per k, transpose [O][I] -> [I][O]
+      CK_TRY(ck::launch_split_transpose(coeff_doj, K, O, I, O * I, ck::at<__nv_bfloat16>(prep, L.dxb_hi),
+                                        ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, I * L.ldO, s));
+    }
+    // k = 0 term: T_0 == 1 so its contribution is the per-output constant
+    CK_TRY(ck::launch_row_sum(coeff_doj, O, I, ck::at<float>(prep, L.c0sum), s));
+    if (L.gen) {
+      CK_TRY(ck::launch_gen_coeff(coeff_doj, d_in, d_out, n_feat - 1, ck::at<__nv_bfloat16>(prep, L.gen_hi),
+                                  ck::at<__nv_bfloat16>(prep, L.gen_lo), s));
+    }
   }
-  // k = 0 term: T_0 == 1 so its contribution is the per-output constant
-  CK_TRY(ck::launch_row_sum(coeff_doj, O, I, ck::at<float>(prep, L.c0sum), s));
-  if (L.gen) {
-    CK_TRY(ck::launch_gen_coeff(coeff_doj, d_in, d_out, n_feat - 1, ck::at<__nv_bfloat16>(prep, L.gen_hi),
-                                ck::at<__nv_bfloat16>(prep, L.gen_lo), s));
+  std::lock_guard<std::mutex> lk(ck::g_prep_mu);
+  ck::g_preps[reinterpret_cast<uintptr_t>(prep)] = ck::PrepShape{d_in, d_out, n_feat};
+  return kOk;
+}
+
+extern "C" int ck_coeff_prep_check(const void* prep, size_t prep_bytes, int d_in, int d_out, int n_feat) {
+  CK_TRY(ck::check_prep(prep, prep_bytes, d_in, d_out, n_feat));
+  // the device-side header as well (synchronous read; validation mode)
+  ck::PrepHeader h{};
+  CK_CUDA(cudaMemcpy(&h, ck::at<void>(const_cast<void*>(prep), 0), sizeof(h), cudaMemcpyDeviceToHost));
+  if (h.magic != ck::kPrepMagic || h.version != ck::kPrepVersion || h.d_in != d_in || h.d_out != d_out ||
+      h.n_feat != n_feat || h.bytes != ck_coeff_prep_bytes(d_in, d_out, n_feat)) {
+    ck::set_error("coefficient prep header does not match (d_in, d_out, n_feat) = (" + std::to_string(d_in) + ", " +
+                  std::to_string(d_out) + ", " + std::to_string(n_feat) + ")");
+    return ck::kInvalidArgument;
   }
   return kOk;
+}
+
+extern "C" int64_t ck_set_chunk_rows(int64_t rows) {
+  return ck::g_chunk_rows.exchange(rows >= 1 ? rows : ck::kChunkRowsDefault);
 }
 
 extern "C" size_t ck_forward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat) {
@@ -338,15 +414,17 @@ extern "C" size_t ck_basis_cache_bytes(int64_t batch, int d_in, int d_out, int n
 }
 
 extern "C" int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut, const void* prep,
-                          const float* bias, float* y, void* workspace, size_t workspace_bytes, void* basis_cache,
-                          size_t basis_cache_bytes, void* stream) {
+                          size_t prep_bytes, const float* bias, float* y, void* workspace, size_t workspace_bytes,
+                          void* basis_cache, size_t basis_cache_bytes, void* stream) {
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
   CK_CHECK(prep != nullptr && (batch == 0 || (x != nullptr && y != nullptr)), "ck_forward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
+  CK_TRY(ck::check_prep(prep, prep_bytes, d_in, d_out, K));
   if (ck::skinny_layer(d_in, d_out, K)) {
     // d_out <= 8: CUDA-core dot products on the fp32 copy in prep
-    return ck::launch_skinny_forward(x, batch, d_in, d_out, ck::at<float>(const_cast<void*>(prep), 0), bias, lut, y,
-                                     static_cast<cudaStream_t>(stream));
+    const ck::PrepLayout P(d_in, d_out, K);
+    return ck::launch_skinny_forward(x, batch, d_in, d_out, ck::at<float>(const_cast<void*>(prep), P.f32), bias, lut,
+                                     y, static_cast<cudaStream_t>(stream));
   }
   const ck::FwdLayout W(batch, d_in, d_out, K);
   const ck::BasisLayout L(batch, d_in, K);
@@ -426,12 +504,13 @@ extern "C" size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out
 }
 
 extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
-                           const void* prep, int include_tanh_jacobian, float* dx, float* dc_doj, float* db,
-                           void* workspace, size_t workspace_bytes, const void* basis_cache,
+                           const void* prep, size_t prep_bytes, int include_tanh_jacobian, float* dx, float* dc_doj,
+                           float* db, void* workspace, size_t workspace_bytes, const void* basis_cache,
                            size_t basis_cache_bytes, void* stream) {
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
   CK_CHECK(prep != nullptr && (batch == 0 || (x != nullptr && dy != nullptr)), "ck_backward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
+  CK_TRY(ck::check_prep(prep, prep_bytes, d_in, d_out, K));
   if (ck::skinny_layer(d_in, d_out, K)) {
     auto s = static_cast<cudaStream_t>(stream);
     const ck::SkinnyBwdLayout SW(batch, d_in, d_out, K);
@@ -447,7 +526,8 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
     }
     float* part_c = ck::at<float>(workspace, SW.part_c);
     double* part_b = ck::at<double>(workspace, SW.part_b);
-    CK_TRY(ck::launch_skinny_backward(x, dy, batch, d_in, d_out, ck::at<float>(const_cast<void*>(prep), 0), lut,
+    const ck::PrepLayout P(d_in, d_out, K);
+    CK_TRY(ck::launch_skinny_backward(x, dy, batch, d_in, d_out, ck::at<float>(const_cast<void*>(prep), P.f32), lut,
                                       include_tanh_jacobian, dx, part_c, part_b, SW.slots, s));
     // second stage: ordered slot merges (kernels.py:438-442 order semantics)
     if (dc_doj) CK_TRY(ck::launch_merge(part_c, SW.slots, n, n, dc_doj, 0, s));

@@ -65,8 +65,11 @@ class LaunchScope {
 
 // Rows processed per internal chunk by ck_forward / ck_backward (bounds the
 // workspace; chunks are processed in ascending order on one stream, so the
-// accumulated dC is bit-reproducible).
-constexpr int64_t kChunkRows = 32768;
+// accumulated dC is bit-reproducible).  Default 32768; ck_set_chunk_rows (or
+// CK_CHUNK_ROWS at load) changes it process-wide, e.g. so tests run the
+// multi-chunk dC accumulation of a wide layer on a small batch.
+constexpr int64_t kChunkRowsDefault = 32768;
+int64_t chunk_rows();
 
 // --- LUT view passed by value to kernels ----------------------------------
 struct LutView {
@@ -133,6 +136,18 @@ int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, con
                      cudaStream_t s);
 // out[r][c] += a[c] + b[c] (either nullable)
 int launch_add_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b, cudaStream_t s);
+
+// Header at the start of an opaque coefficient-prep buffer (written by
+// ck_coeff_prepare on the device; read back by ck_coeff_prep_check).
+struct PrepHeader {
+  uint32_t magic;     // kPrepMagic
+  uint32_t version;   // layout version
+  int32_t d_in, d_out, n_feat, flags;  // flags: 1 = skinny (fp32 copy), 2 = generated-forward copy
+  uint64_t bytes;     // ck_coeff_prep_bytes(d_in, d_out, n_feat)
+};
+constexpr uint32_t kPrepMagic = 0x52504b43u;  // "CKPR"
+constexpr uint32_t kPrepVersion = 2;
+int launch_prep_header(void* dst, const PrepHeader& h, cudaStream_t s);
 
 // --- skinny-output layers (ck_skinny.cu) ----------------------------------
 // d_out <= 8 with n_feat * round_up_pow2(d_out) <= 32: CUDA-core kernels on

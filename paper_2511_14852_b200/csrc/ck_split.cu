@@ -184,6 +184,11 @@ __global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64
   }
 }
 
+__global__ void prep_header_kernel(PrepHeader* dst, PrepHeader h) {
+  pdl_wait();
+  *dst = h;
+}
+
 // part[s][c] = sum of rows [s*chunk, min((s+1)*chunk, rows)) of column c
 __global__ void col_partial_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, int64_t chunk,
                                    double* __restrict__ part, int slots) {
@@ -341,6 +346,13 @@ int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cuda
   if (rows == 0) return kOk;
   LaunchScope scope(kKReduce, s);
   CK_CUDA(launch_k((row_sum_kernel), blocks_for(rows * 32), kThreads, 0, s, in, rows, cols, out));
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int launch_prep_header(void* dst, const PrepHeader& h, cudaStream_t s) {
+  LaunchScope scope(kKSplit, s);
+  CK_CUDA(launch_k((prep_header_kernel), 1, 1, 0, s, static_cast<PrepHeader*>(dst), h));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }

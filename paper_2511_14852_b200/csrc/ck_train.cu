@@ -198,11 +198,14 @@ extern "C" int ck_adam_step_multi(int count, float* const* params, const float* 
   a.eps = static_cast<float>(eps);
   a.bc_dev = bc_dev;
   auto s = static_cast<cudaStream_t>(stream);
-  for (int base = 0; base < count; base += ck::kMultiMax) {
+  // batches of up to kMultiMax non-empty tensors; the next batch resumes at
+  // the first tensor this one did not take (zero-size ones are skipped, not
+  // counted, so a fixed stride would revisit tensors)
+  for (int t = 0; t < count;) {
     ck::MultiTensors T{};
     int k = 0;
     int64_t chunks = 0;
-    for (int t = base; t < count && k < ck::kMultiMax; ++t) {
+    for (; t < count && k < ck::kMultiMax; ++t) {
       CK_CHECK(sizes[t] >= 0, "ck_adam_step_multi: negative size");
       if (sizes[t] == 0) continue;
       CK_CHECK(params[t] && grads[t] && m[t] && v[t], "ck_adam_step_multi: NULL tensor");

@@ -9,6 +9,7 @@ the reference's ``np.asarray(x, dtype=float64)``).
 """
 from __future__ import annotations
 
+import contextlib
 import math
 from dataclasses import dataclass
 from enum import Enum
@@ -171,7 +172,34 @@ class PreparedCoeff:
         rc = _lib.lib().ck_coeff_prepare(c.data_ptr(), self.d_in, self.d_out, self.n_feat, self.buffer.data_ptr(),
                                          self.buffer.numel(), _lib.stream_handle(c.device))
         _lib.check(rc, "ck_coeff_prepare")
-        self.key = (coeff_doj.data_ptr(), coeff_doj._version)
+        self.key = self.key_of(coeff_doj)
+
+    @staticmethod
+    def key_of(coeff_doj: torch.Tensor) -> tuple:
+        """Identity of the coefficient values the prep was built from: storage,
+        address and autograd version counter (see _LayerState.prepared)."""
+        return (coeff_doj.untyped_storage()._cdata, coeff_doj.data_ptr(), coeff_doj._version)
+
+    def check(self) -> None:
+        """Synchronous validation of the prep buffer's host record and device
+        header against this layer shape (ck_coeff_prep_check)."""
+        _lib.check(_lib.lib().ck_coeff_prep_check(self.buffer.data_ptr(), self.buffer.numel(), self.d_in, self.d_out,
+                                                  self.n_feat), "ck_coeff_prep_check")
+
+
+@contextlib.contextmanager
+def chunk_rows(rows: int):
+    """Temporarily set the rows per internal batch chunk of ck_forward /
+    ck_backward (ck_set_chunk_rows; default 32768).  dC accumulates over the
+    chunks in ascending order, so a small value runs a wide layer's
+    multi-chunk accumulation on a small batch.  Process-wide: keep a forward
+    and the backward that reuses its basis cache inside the same setting."""
+    lib = _lib.lib()
+    prev = lib.ck_set_chunk_rows(int(rows))
+    try:
+        yield
+    finally:
+        lib.ck_set_chunk_rows(prev)
 
 
 def _as_f32(t: torch.Tensor, device) -> torch.Tensor:
@@ -201,7 +229,8 @@ def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut, bias: torch.Tensor | 
     y = torch.empty((b, prep.d_out), dtype=torch.float32, device=x.device)
     lb = _lib.lib()
     ws = _workspace(lb.ck_forward_workspace_bytes(b, prep.d_in, prep.d_out, prep.n_feat), x.device)
-    rc = lb.ck_forward(x.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(), _lib.ptr(bias),
+    rc = lb.ck_forward(x.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(), prep.buffer.numel(),
+                       _lib.ptr(bias),
                        y.data_ptr(), ws.data_ptr(), ws.numel(), _lib.ptr(cache), 0 if cache is None else cache.numel(),
                        _lib.stream_handle(x.device))
     _lib.check(rc, "ck_forward")
@@ -223,7 +252,7 @@ def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut, ja
     lb = _lib.lib()
     ws = _workspace(lb.ck_backward_workspace_bytes(b, prep.d_in, prep.d_out, prep.n_feat), dev)
     rc = lb.ck_backward(x.data_ptr(), dy.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(),
-                        1 if jacobian else 0, _lib.ptr(dx), _lib.ptr(dc), _lib.ptr(db), ws.data_ptr(), ws.numel(),
+                        prep.buffer.numel(), 1 if jacobian else 0, _lib.ptr(dx), _lib.ptr(dc), _lib.ptr(db), ws.data_ptr(), ws.numel(),
                         _lib.ptr(cache), 0 if cache is None else cache.numel(), _lib.stream_handle(dev))
     _lib.check(rc, "ck_backward")
     return dc, dx, db

@@ -47,14 +47,21 @@ class _LayerState:
         return t
 
     def prepared(self, coeff_doj: torch.Tensor) -> PreparedCoeff:
-        key = (coeff_doj.data_ptr(), coeff_doj._version)
+        """The bf16 operands of the current coefficients, re-split when the
+        parameter changed.  Change detection is the tensor's storage, address
+        and autograd version counter; writes that bypass the counter
+        (``param.data.copy_()``, raw-pointer kernels) need invalidate()."""
         p = self._prep
         if p is None or p.device != coeff_doj.device or tuple(coeff_doj.shape) != (p.n_feat, p.d_out, p.d_in):
             p = PreparedCoeff(coeff_doj)
             self._prep = p
-        elif p.key != key:
+        elif p.key != PreparedCoeff.key_of(coeff_doj):
             p.update(coeff_doj)
         return p
+
+    def invalidate(self) -> None:
+        if self._prep is not None:
+            self._prep.key = None
 
 
 _TOTAL_MEM: dict = {}
@@ -74,14 +81,17 @@ class ChebyKANFunction(torch.autograd.Function):
     """y = ChebyKAN(x; C, b).  Forward: ck_forward.  Backward: ck_backward."""
 
     @staticmethod
-    def forward(ctx, x, coeff_doj, bias, state: _LayerState):
+    def forward(ctx, x, coeff_doj, bias, state: _LayerState, want_cache: bool = False):
         if not x.is_cuda:
             raise ValueError("ChebyKAN kernels run on CUDA tensors only (no CPU fallback)")
         x = x.to(torch.float32).contiguous()
         lut = state.lut(x.device)
         prep = state.prepared(coeff_doj)
         cache = None
-        if ctx.needs_input_grad[1] and state.cache_basis:
+        # (ctx.needs_input_grad says True for a Parameter even under no_grad:
+        # the caller decides, so inference never fills a basis cache and
+        # narrow layers keep the shared-memory generated forward)
+        if want_cache and state.cache_basis:
             # keep the expanded basis for dC (saves the backward's re-expansion)
             nbytes = basis_cache_bytes(x.shape[0], prep.d_in, prep.d_out, prep.n_feat)
             if nbytes > 0 and (state.cache_basis is True or nbytes <= 0.35 * _free_bytes_estimate(x.device)):
@@ -103,7 +113,7 @@ class ChebyKANFunction(torch.autograd.Function):
         dc, dx, db = backward_raw(x, dy, prep, state.lut(x.device), state.jacobian, want_dx=need_x,
                                   want_dc=need_c, want_db=need_b and ctx.has_bias, cache=ctx.cache)
         ctx.cache = None
-        return dx, dc, db, None
+        return dx, dc, db, None, None
 
 
 class ChebyKANLayer(nn.Module):
@@ -181,8 +191,18 @@ class ChebyKANLayer(nn.Module):
         if x.shape[-1] != self.input_dim:
             raise ValueError(f"expected input shape (batch, {self.input_dim}), got {tuple(x.shape)}")
         lead = x.shape[:-1]
-        y = ChebyKANFunction.apply(x.reshape(-1, self.input_dim), self.coeff_doj, self.bias, self._state)
+        want_cache = torch.is_grad_enabled() and self.coeff_doj.requires_grad
+        y = ChebyKANFunction.apply(x.reshape(-1, self.input_dim), self.coeff_doj, self.bias, self._state, want_cache)
         return y.reshape(*lead, self.output_dim)
+
+    def invalidate_prep(self) -> None:
+        """Force the next forward to re-split the coefficients.  Needed after
+        writes the autograd version counter does not see: ``coeff_doj.data``
+        in-place ops (EMA, clipping), raw-pointer kernels, CUDA-graph replays
+        of an optimizer step.  ``load_jod``, ``reset_parameters``, in-place ops
+        on the parameter itself, the library's Adam and load_state_dict bump
+        the counter and need nothing."""
+        self._state.invalidate()
 
     def extra_repr(self) -> str:
         return (f"input_dim={self.input_dim}, output_dim={self.output_dim}, degree={self.degree}, "

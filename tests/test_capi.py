@@ -48,7 +48,7 @@ def test_version_and_sizes_are_host_only():
 
 def test_forward_without_lut_is_a_value_error():
     lib = _lib.lib()
-    rc = lib.ck_forward(None, 4, 8, 8, None, None, None, None, None, 0, None, 0, None)
+    rc = lib.ck_forward(None, 4, 8, 8, None, None, 0, None, None, None, 0, None, 0, None)
     assert rc == _lib.CK_INVALID_ARGUMENT
     assert "LUT mode requires a LutTable" in _lib.last_error()
     with pytest.raises(ValueError, match="LUT mode requires a LutTable"):
@@ -72,3 +72,33 @@ def test_lut_build_argument_errors_match_reference_wording():
 def test_merge_rejects_bad_extents():
     lib = _lib.lib()
     assert lib.ck_merge(None, 2, 4, 8, None, 0, None) == _lib.CK_INVALID_ARGUMENT
+
+
+def test_chunk_rows_setter_round_trip():
+    # ck_set_chunk_rows is host-only state; the workspace queries follow it
+    import paper_2511_14852_b200 as ck
+
+    lib = _lib.lib()
+    prev = lib.ck_set_chunk_rows(1000)
+    try:
+        assert lib.ck_set_chunk_rows(2000) == 1000
+    finally:
+        lib.ck_set_chunk_rows(prev)
+    with ck.chunk_rows(77):
+        assert lib.ck_set_chunk_rows(77) == 77
+    assert lib.ck_set_chunk_rows(prev) == prev
+    with ck.chunk_rows(256):
+        small = lib.ck_backward_workspace_bytes(65536, 1024, 1024, 9)
+        cache_small = lib.ck_basis_cache_bytes(65536, 1024, 1024, 9)
+    assert small < lib.ck_backward_workspace_bytes(65536, 1024, 1024, 9)
+    # the basis cache holds every chunk's planes: same bytes up to alignment
+    assert abs(cache_small - lib.ck_basis_cache_bytes(65536, 1024, 1024, 9)) < 256 * 512
+
+
+def test_prep_check_rejects_null_and_small_buffers():
+    lib = _lib.lib()
+    assert lib.ck_coeff_prep_check(None, 0, 8, 8, 3) == _lib.CK_INVALID_ARGUMENT
+    assert lib.ck_coeff_prep_check(ctypes.c_void_p(4096), 16, 8, 8, 3) == _lib.CK_INVALID_ARGUMENT
+    assert "too small" in _lib.last_error()
+    assert lib.ck_coeff_prep_check(ctypes.c_void_p(4096), 1 << 30, 8, 8, 3) == _lib.CK_INVALID_ARGUMENT
+    assert "not filled by ck_coeff_prepare" in _lib.last_error()

@@ -102,10 +102,13 @@ def test_adam_kernel_matches_reference_rule():
 @pytest.mark.parametrize("capturable", [False, True])
 def test_multi_tensor_adam_bitwise_equals_per_tensor(capturable):
     # ck_adam_step_multi (one launch, 40 tensors -> two launches of <= 32, ragged
-    # sizes with tails that are not whole float4s) == ck_adam_step per tensor, bit for bit
+    # sizes with tails that are not whole float4s) == ck_adam_step per tensor, bit for bit.
+    # Zero-size tensors inside the first batch must not shift the batch
+    # boundary (each tensor updated exactly once).
     dev = torch.device("cuda", 0)
     g = torch.Generator(device="cpu").manual_seed(5)
-    sizes = [1, 3, 2047, 2048, 2049, 4096 + 5, 17, 100000] + [int(s) for s in torch.randint(1, 5000, (32,), generator=g)]
+    sizes = [1, 0, 3, 2047, 0, 2048, 2049, 4096 + 5, 17, 100000] + [
+        int(s) for s in torch.randint(1, 5000, (32,), generator=g)]
     params = [torch.nn.Parameter(torch.randn(n, generator=g).to(dev)) for n in sizes]
     ref = [p.detach().clone() for p in params]
     ms = [torch.zeros_like(p) for p in ref]
