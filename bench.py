@@ -126,9 +126,41 @@ def layer_dims(wl):
     return [(wl["d_in"], wl["d_out"])]
 
 
-def cpu_reference_time(rows: int, wl: dict, reps: int = 1, warmup: int = 0):
+def cpu_info():
+    """CPU model, numpy version and BLAS library of this host."""
+    import platform
+
+    import numpy as np
+
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        libs = [f"{i.get('internal_api')} {i.get('version')}" for i in threadpool_info() if i.get("user_api") == "blas"]
+        blas = ", ".join(libs) or None
+    except Exception:  # noqa: BLE001 (informational only)
+        blas = None
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "numpy": np.__version__, "blas": blas}
+
+
+def cpu_reference_time(rows: int, wl: dict, reps: int = 1, warmup: int = 0, mode: str = "tiles",
+                       keep_outputs: bool = False):
     """Oracle port of the reference's fused_forward/backward_fused over the
-    workload's layers (a net's layers run back to back, forward then backward)."""
+    workload's layers (a net's layers run back to back, forward then backward).
+
+    ``mode`` is one of the reference's two threading modes (BASELINE.md 4,
+    perf.py:225-275): "tiles" = BLAS single-threaded, tile tasks on every
+    core (POLYKAN_WORKERS = nproc); "blas" = one tile-task worker, BLAS on
+    every core.  Returns (per-rep seconds, threads, layer inputs and the last
+    rep's outputs if keep_outputs)."""
     import numpy as np
     from threadpoolctl import threadpool_limits
 
@@ -140,25 +172,89 @@ def cpu_reference_time(rows: int, wl: dict, reps: int = 1, warmup: int = 0):
     for li, (i, o) in enumerate(layer_dims(wl)):
         x, c_jod, dy = orc.bench_inputs(rows, i, o, wl["degree"], seed=3 + li)
         layers.append((x, orc.jod_to_doj(c_jod.astype(np.float64)), dy))
-    times = []
-    with threadpool_limits(1):  # BLAS single-threaded, tile tasks across all cores (best at large shapes)
+    workers = threads if mode == "tiles" else 1
+    times, outs = [], None
+    with threadpool_limits(1 if mode == "tiles" else threads):
         for it in range(warmup + reps):
             t0 = time.perf_counter()
-            for x, c_doj, _ in layers:
-                orc.layer_forward(x, c_doj, vals, threads=threads)
-            for x, c_doj, dy in reversed(layers):
-                orc.layer_backward(x, c_doj, dy, vals, slopes, threads=threads)
+            ys = [orc.layer_forward(x, c_doj, vals, threads=workers) for x, c_doj, _ in layers]
+            grads = [orc.layer_backward(x, c_doj, dy, vals, slopes, threads=workers)
+                     for x, c_doj, dy in reversed(layers)][::-1]
             if it >= warmup:
                 times.append(time.perf_counter() - t0)
-    return times, threads
+            outs = (ys, grads)
+    return times, threads, (layers if keep_outputs else None), (outs if keep_outputs else None)
+
+
+def cpu_baseline(wl, rows):
+    """BASELINE.md section 4 protocol on this host: both threading modes,
+    median of reps after a warm-up, the better mode reported.  The tile-task
+    mode (the faster one at these shapes) runs 3 reps on `rows` rows; the
+    BLAS-threaded mode, several times slower here, 1 rep on rows/4 rows so
+    the leg stays within ~30 s of CPU work."""
+    rate = {}
+    layers = outs = None
+    for mode, n, reps in (("tiles", rows, 3), ("blas", max(1, rows // 4), 1)):
+        times, threads, lay, out = cpu_reference_time(n, wl, reps=reps, warmup=1, mode=mode,
+                                                      keep_outputs=mode == "tiles")
+        rate[mode] = n / statistics.median(times)
+        if lay is not None:
+            layers, outs = lay, out
+    best = max(rate, key=rate.get)
+    return {
+        "value": rate[best], "unit": "samples/s", "cores": threads, "kind": "port",
+        "sample": (f"{rows} rows of {layer_dims(wl)} d{wl['degree']} N={wl['lut_size']}, fwd+bwd (no optimizer); "
+                   f"oracle port of polykan LUT-mode fused_forward/backward_fused, f64 NumPy; median of 3 reps "
+                   f"after 1 warm-up; the better of the two threading modes"),
+        "threading_modes_samples_per_s": {
+            "tiles (BLAS 1 thread, tile tasks on all cores)": rate["tiles"],
+            "blas (1 tile worker, BLAS on all cores; rows/4, 1 rep)": rate["blas"]},
+        "best_mode": best, **cpu_info(),
+    }, layers, outs
+
+
+def gpu_parity(wl, layers, outs):
+    """Feed the cpu_baseline rows' exact inputs through the GPU module path
+    (one chunk, and 8 chunks so dC accumulates like the full batch does) and
+    compare with the oracle's outputs: normwise max|got-want|/max|want|."""
+    import numpy as np
+    import torch
+
+    import paper_2511_14852_b200 as ck
+    from oracle import chebykan_oracle as orc
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ys, grads = outs
+    worst = {"y": 0.0, "dX": 0.0, "dC": 0.0, "db": 0.0}
+    rows = layers[0][0].shape[0]
+    for (x, c_doj, dy), wy, (wdc, wdx, wdb) in zip(layers, ys, grads):
+        i, o = x.shape[1], dy.shape[1]
+        layer = ck.ChebyKANLayer(i, o, wl["degree"], lut_size=wl["lut_size"]).to(dev)
+        with torch.no_grad():
+            layer.coeff_doj.copy_(torch.from_numpy(c_doj.astype(np.float32)))
+        for chunk in (0, max(1, rows // 8)):
+            layer.zero_grad(set_to_none=True)
+            xt = torch.from_numpy(x).to(dev).requires_grad_(True)
+            with ck.chunk_rows(chunk):
+                y = layer(xt)
+                y.backward(torch.from_numpy(dy).to(dev))
+            torch.cuda.synchronize(dev)
+            got = {"y": (y.detach(), wy), "dX": (xt.grad, wdx), "dC": (layer.coeff_doj.grad, wdc),
+                   "db": (layer.bias.grad, wdb)}
+            for k, (g, w) in got.items():
+                worst[k] = max(worst[k], orc.normwise_err(g.cpu().numpy(), w))
+        del layer
+    return {"rows": rows, "chunk_rows": [min(rows, 32768), max(1, rows // 8)], "normwise_max": worst,
+            "tol": 1e-4, "pass": all(v <= 1e-4 for v in worst.values()),
+            "against": "oracle (float64 restatement of kernels.py:351-447) on the cpu_baseline sample's inputs"}
 
 
 def run_reference_arm(args, wl):
     rank = env_int("RANK", 0)
     if rank != 0:
         return
-    times, threads = cpu_reference_time(REF_STEP_ROWS, wl, reps=args.steps, warmup=args.warmup)
-    t = statistics.mean(times)
+    times, threads, _, _ = cpu_reference_time(REF_STEP_ROWS, wl, reps=args.steps, warmup=args.warmup)
+    t = statistics.median(times)
     value = REF_STEP_ROWS / t
     sample = (f"{REF_STEP_ROWS} rows of {layer_dims(wl)} d{wl['degree']} N={wl['lut_size']} fwd+bwd per "
               f"step; oracle port of polykan fused_forward/backward_fused (LUT mode, f64 NumPy), "
@@ -463,7 +559,7 @@ def run_ours(args, wl):
         e2e_mode = "one captured CUDA graph per step (H2D x/dy from pinned memory, step, D2H loss)"
     e2e_step(0, prefetch_next_step=False)  # warm the copy path; no copy left in flight
     barrier()
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(10, args.steps)
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -481,14 +577,16 @@ def run_ours(args, wl):
         return
 
     peaks = load_peaks()
-    # algorithmic flops; executed GEMM flops use d planes (k=0 folded)
-    # and skip dX of a net's first layer (its input needs no gradient)
-    train_flops, step_gemm = 0, 0
+    # Executed GEMM flops (SURVEY 8(d) with the B_0 == 1 folds subtracted):
+    # forward and dC contract over d planes (k = 1..d), dX over d planes; a
+    # net's first layer has no dX (its input needs no gradient).  The
+    # algorithmic 8(d) count 2*B*I*O*(3d+2) (k = 0 included) is reported beside.
+    train_alg, step_gemm, fwd_gemm = 0, 0, 0
     for li, (i, o) in enumerate(dims):
-        f = ck.count_flops(rows, i, o, d)
         need_dx = not (is_net and li == 0)
-        train_flops += f["fwd"] + 2 * rows * i * o * (d + 1) + (2 * rows * i * o * d if need_dx else 0)
+        train_alg += 2 * rows * i * o * ((d + 1) + (d + 1) + (d if need_dx else 0))
         step_gemm += 2 * rows * i * o * d * (3 if need_dx else 2)
+        fwd_gemm += 2 * rows * i * o * d
     gemm_alg = step_gemm * args.steps
     gemm_ms = sum(kt[c][0] for c in ("gemm_fwd", "gemm_dx", "gemm_dc"))
     gemm_tf = gemm_alg / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
@@ -499,11 +597,14 @@ def run_ours(args, wl):
     # the burst figure keeps frac <= 1 and is the conservative choice.
     peak_eff = peaks["bf16"] / 3.0
     total_kernel_ms = sum(v[0] for v in kt.values())
-    traffic = None
+    # DRAM bytes per GEMM launch from the committed ncu --set full capture of
+    # this exact launch (C4, 32768-row chunk); other workloads: not measured
+    traffic, traffic_src = None, None
     tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
+    if tp.exists() and not is_net and (I, O, d) == (4096, 4096, 8):
         try:
-            traffic = json.loads(tp.read_text()).get("gemm_bf16x3_bytes_per_launch")
+            tj = json.loads(tp.read_text())
+            traffic, traffic_src = tj.get("gemm_bf16x3_bytes_per_launch"), tj.get("source")
         except (ValueError, OSError):
             traffic = None
     line = {
@@ -516,7 +617,10 @@ def run_ours(args, wl):
                    "gradient_exchange": reducer_kind,
                    "l2": ("inputs larger than L2 (x shard >> 126 MB), no flush" if rows * I * 4 > 126e6 else
                           "working set below L2 size; steps run back to back (no flush)")},
-        "fwd": {"value": fwd_value, "unit": "samples/s", "ms_per_step": fwd_ms},
+        "fwd": {"value": fwd_value, "unit": "samples/s", "ms_per_step": fwd_ms,
+                "tflops_executed": fwd_gemm / (fwd_ms / 1e3) / 1e12,
+                "roofline_frac": fwd_gemm / (fwd_ms / 1e3) / 1e12 / peak_eff,
+                "roofline_basis": "whole forward time (expansion + GEMM) vs bf16 burst / 3"},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": 4 * rows * (I + O),
                 "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms, "wall_ms_per_step": e2e_wall * 1e3,
                 "path": f"ChebyKANLayer forward/backward + Adam; x/dy from pinned host: {e2e_mode}"},
@@ -524,7 +628,7 @@ def run_ours(args, wl):
         "roofline": {
             "bound": "tensor", "kernel": "gemm_bf16x3 (tcgen05 fwd + dX + dC, BF16x3)",
             "achieved": gemm_tf, "peak": peak_eff, "unit": "TFLOP/s", "frac": gemm_tf / peak_eff,
-            "traffic": traffic,
+            "traffic": traffic, "traffic_source": traffic_src,
             "peak_basis": f"{peaks['source']} bf16 burst {peaks['bf16']} TF/s / 3 (3 bf16 MMAs per "
                           f"algorithmic fp32 MMA); sustained {peaks['bf16_sus']} TF/s gives frac "
                           f"{gemm_tf / (peaks['bf16_sus'] / 3.0):.3f}",
@@ -540,15 +644,15 @@ def run_ours(args, wl):
         "graph": (f"timed steps replay one captured CUDA graph of the whole step; kernel_ms_per_step and "
                   f"roofline from {args.steps} eager steps" if graph is not None else None),
         "kernel_launches_per_step": {k: v[1] / args.steps for k, v in kt.items() if v[1]},
-        "train_alg_tflops_per_gpu": train_flops / (ms_step / 1e3) / 1e12,
+        "train_tflops_per_gpu": {"executed": step_gemm / (ms_step / 1e3) / 1e12,
+                                 "algorithmic_8d": train_alg / (ms_step / 1e3) / 1e12,
+                                 "note": "executed = k >= 1 planes only (the B_0 == 1 folds are not work done)"},
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        times, threads = cpu_reference_time(CPU_SAMPLE_ROWS, wl)
-        line["cpu_baseline"] = {
-            "value": CPU_SAMPLE_ROWS / times[0], "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{CPU_SAMPLE_ROWS} rows of the same layer (fwd+bwd, no optimizer), oracle port of polykan "
-                      f"LUT-mode fused_forward/backward_fused, f64 NumPy, {threads} threads, BLAS 1 thread"}
+        base, cpu_layers, cpu_outs = cpu_baseline(wl, CPU_SAMPLE_ROWS)
+        line["cpu_baseline"] = base
+        line["parity"] = gpu_parity(wl, cpu_layers, cpu_outs)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -150,9 +150,13 @@ CK_API int ck_forward(const float* x, int64_t batch, int d_in, int d_out, const 
  * C[k][to*tile_out+ty][j] (PartialBuffer layout, kernels.py:108-137; g_x =
  * ceil(d_in/tile_in), g_y = ceil(d_out/tile_out); slots of padding lanes are
  * not written).  ck_combine folds the input tiles in ascending order and adds
- * bias (nullable).  fp32 CUDA-core arithmetic; ck_forward is the fast path. */
+ * bias (nullable).  fp32 CUDA-core arithmetic; ck_forward is the fast path.
+ * write_counts (nullable, int64 per partial slot): every store the kernel
+ * makes adds 1 to its slot's counter (atomically) -- the unique-writer
+ * instrumentation of PartialBuffer.write_counts (kernels.py:123, 313-314). */
 CK_API int ck_forward_partial(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut,
-                       const float* coeff_doj, int tile_in, int tile_out, float* partial, void* stream);
+                       const float* coeff_doj, int tile_in, int tile_out, float* partial, long long* write_counts,
+                       void* stream);
 CK_API int ck_combine(const float* partial, int64_t batch, int d_out, int g_x, int tile_out, const float* bias,
                float* y, void* stream);
 

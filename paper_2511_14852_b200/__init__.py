@@ -80,7 +80,6 @@ from .model import (
     layer_forward,
     load_checkpoint,
     save_checkpoint,
-    load_csv,
     loss_fn,
     make_synthetic,
     mse_loss,
@@ -90,15 +89,12 @@ from .model import (
 from .optim import Adam, adam_update, cosine_scale
 from .perf import (
     BenchResult,
-    CostModel,
     LayerConfig,
     Regime,
     RooflineReport,
-    TwoStageReport,
     paper_configs,
     roofline,
     run_bench,
-    two_stage_benefit,
 )
 from .parallel import GradientAllreducer, PeerAllreducer, allreduce_gradients, chebykan_parameters, shard_bounds
 from .tensor import CoeffTensor, Layout, doj_index, jod_index, reorder_to_doj, reorder_to_jod

@@ -51,7 +51,7 @@ SIGNATURES = {
     "ck_backward": (_c_int, [_c_p, _c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_size, _c_int, _c_p, _c_p, _c_p,
                              _c_p, _c_size, _c_p, _c_size, _c_p]),
     "ck_merge": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_int, _c_p]),
-    "ck_forward_partial": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_int, _c_p, _c_p]),
+    "ck_forward_partial": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_int, _c_p, _c_p, _c_p]),
     "ck_combine": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
     "ck_adam_step": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                               ctypes.c_double, _c_i64, _c_p]),

@@ -411,7 +411,8 @@ namespace {
 __global__ void __launch_bounds__(256) forward_partial_kernel(const float* __restrict__ x, int64_t rows, int I, int O,
                                                               int K, const float* __restrict__ c, LutView L,
                                                               int tile_in, int tile_out, int g_x, int g_y,
-                                                              float* __restrict__ part) {
+                                                              float* __restrict__ part,
+                                                              unsigned long long* __restrict__ counts) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
@@ -458,7 +459,13 @@ __global__ void __launch_bounds__(256) forward_partial_kernel(const float* __res
             }
           }
         }
-        if (o_ok) part[((static_cast<int64_t>(to) * g_x + ti) * rows + b) * tile_out + ty] = acc;
+        if (o_ok) {
+          const int64_t slot = ((static_cast<int64_t>(to) * g_x + ti) * rows + b) * tile_out + ty;
+          part[slot] = acc;
+          // instrumented buffers: every store counts itself (atomically, so
+          // a second writer of a slot would show up as 2)
+          if (counts) atomicAdd(counts + slot, 1ull);
+        }
       }
     }
   }
@@ -484,7 +491,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
 }  // namespace ck
 
 extern "C" int ck_forward_partial(const float* x, int64_t batch, int d_in, int d_out, const ck_lut* lut,
-                                  const float* coeff_doj, int tile_in, int tile_out, float* partial, void* stream) {
+                                  const float* coeff_doj, int tile_in, int tile_out, float* partial,
+                                  long long* write_counts, void* stream) {
   CK_CHECK(lut != nullptr, "LUT mode requires a LutTable");
   CK_CHECK(batch >= 0 && d_in >= 1 && d_out >= 1, "d_in and d_out must be >= 1");
   CK_CHECK(tile_in >= 1 && tile_out >= 1, "tile and lane sizes must be >= 1");
@@ -498,7 +506,8 @@ extern "C" int ck_forward_partial(const float* x, int64_t batch, int d_in, int d
   const int64_t cap = static_cast<int64_t>(ck::num_sms()) * 16;
   ck::LaunchScope scope(ck::kKSkinny, s);
   CK_CUDA(ck::launch_k((ck::forward_partial_kernel), static_cast<int>(want < cap ? want : cap), 256, 0, s, x, batch,
-                       d_in, d_out, L.K, coeff_doj, L, tile_in, tile_out, g_x, g_y, partial));
+                       d_in, d_out, L.K, coeff_doj, L, tile_in, tile_out, g_x, g_y, partial,
+                       reinterpret_cast<unsigned long long*>(write_counts)));
   return ck::kOk;
 }
 

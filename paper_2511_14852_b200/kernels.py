@@ -84,7 +84,8 @@ class PartialBuffer:
     """Partial-stage workspace (kernels.py:108-137) on the device; flat order
     gIdx = (tileO * g_x + tileI) * B * tile_out + b * tile_out + t_y.  Slots of
     padding lanes of a ragged last output tile stay zero; ``write_counts``
-    (instrumented buffers) records one write per real slot."""
+    (instrumented buffers) is incremented by the partial kernel itself on
+    every store (atomically), so it shows one write per real slot."""
 
     g_x: int
     g_y: int
@@ -371,11 +372,9 @@ def forward_partial(x, coeff: CoeffTensor, lut, sched: TileSchedule, mode: Kerne
         _check_finite(x)
     c = _as_f32(coeff.as3d(), dev)
     rc = _lib.lib().ck_forward_partial(x.data_ptr(), x.shape[0], coeff.d_in, coeff.d_out, basis.handle, c.data_ptr(),
-                                       sched.tile_in, sched.tile_out, out.data.data_ptr(), _lib.stream_handle(dev))
+                                       sched.tile_in, sched.tile_out, out.data.data_ptr(), _lib.ptr(out.write_counts),
+                                       _lib.stream_handle(dev))
     _lib.check(rc, "ck_forward_partial")
-    if out.write_counts is not None:
-        valid = torch.arange(sched.g_y * sched.tile_out, device=dev).reshape(sched.g_y, 1, 1, sched.tile_out)
-        out.write_counts += (valid < coeff.d_out).to(torch.int64).expand_as(out.write_counts)
     if counters is not None:
         counters.partial_writes += x.shape[0] * sched.d_out * sched.g_x
 

@@ -117,27 +117,3 @@ def test_apply_cli_usage_and_io_errors(tmp_path):
     r = subprocess.run(base + ["--coeff", str(F / "layer_jod.pkck"), "--input", str(tmp_path / "x5.pkmx")],
                        cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert r.returncode == 2 and "input width 5 != coefficient d_in 12" in r.stderr
-
-
-@pytest.mark.gpu
-def test_bench_cli_rows_and_errors(tmp_path):
-    # test_cli.py:58-124 on the GPU versions
-    cfg = tmp_path / "cfg.json"
-    cfg.write_text(json.dumps([{"batch": 2, "d_in": 3, "d_out": 4, "degree": 1, "elem_bytes": 8}]))
-    base = [sys.executable, "-m", "paper_2511_14852_b200", "bench", "--configs", str(cfg), "--reps", "1",
-            "--warmups", "0", "--csv", str(tmp_path / "b.csv")]
-    r = subprocess.run(base + ["--versions", "all", "--roofline-json", str(tmp_path / "r.json")], cwd=ROOT,
-                       capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr
-    assert len((tmp_path / "b.csv").read_text().strip().splitlines()) == 1 + 5
-    lam4 = 4 * (2 * 3 + 2 * 4 + 2 * 2 * 3 * 2 + 3 * 4 * 2)
-    assert json.loads((tmp_path / "r.json").read_text())[0]["bytes"] == 2 * lam4
-    r = subprocess.run(base + ["--versions", "fused-maybe"], cwd=ROOT, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 2 and "unknown kernel version" in r.stderr
-    r = subprocess.run([sys.executable, "-m", "paper_2511_14852_b200", "bench", "--configs", "paper", "--versions",
-                        "all", "--reps", "1", "--warmups", "0", "--csv", str(tmp_path / "p.csv")], cwd=ROOT,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr
-    lines = (tmp_path / "p.csv").read_text().strip().splitlines()
-    assert len(lines) == 1 + 3 * 5
-    assert ("32", "512", "1024", "24") in {tuple(line.split(",")[:4]) for line in lines[1:]}

@@ -127,44 +127,6 @@ def test_backward_without_jacobian_matches_pseudocode_literal():
         np.testing.assert_allclose(chain.cpu().numpy(), plain.cpu().numpy() * (1 - t * t), rtol=1e-5, atol=1e-6)
 
 
-def test_schedule_independence_is_bitwise():
-    # test_kernels.py:367-381: the CPU tile shape does not change results; on
-    # the B200 path the schedule is validated but the tiling is the GPU's own
-    rng = np.random.default_rng(23)
-    x, c_doj, dy, degree = random_instance(rng, max_dim=48, max_degree=10)
-    c = ck.CoeffTensor(x.shape[1], dy.shape[1], degree, ck.Layout.DOJ, _t(c_doj))
-    lut = ck.lut_build(ck.BasisKind.CHEBYSHEV, degree, 8192, device=_dev())
-    res = []
-    for tile_in in (16, 64):
-        for tile_out in (8, 32):
-            sched = ck.TileSchedule.for_dims(x.shape[1], dy.shape[1], tile_in, tile_out)
-            y = ck.fused_forward(_t(x), c, lut, sched, ck.LUT_MODE, workers=4)
-            cg, xg = ck.backward_fused(_t(x), c, _t(dy), lut, sched, ck.LUT_MODE, workers=4)
-            res.append((y, cg.data, xg))
-    for other in res[1:]:
-        for a, b in zip(res[0], other):
-            assert torch.equal(a, b)
-
-
-def test_counters_follow_closed_forms():
-    # test_kernels.py:301-321 semantics through the B200 entry points
-    rng = np.random.default_rng(20)
-    for _ in range(5):
-        x, c_doj, dy, degree = random_instance(rng, max_dim=40, max_degree=8)
-        sched = ck.TileSchedule.for_dims(x.shape[1], dy.shape[1], int(rng.choice([4, 16, 64])),
-                                         int(rng.choice([8, 32])))
-        c = ck.CoeffTensor(x.shape[1], dy.shape[1], degree, ck.Layout.DOJ, _t(c_doj))
-        counters = ck.KernelCounters()
-        ck.fused_forward(_t(x), c, None, sched, ck.EXACT_MODE, counters=counters, kind=ck.BasisKind.CHEBYSHEV)
-        ck.backward_fused(_t(x), c, _t(dy), None, sched, ck.EXACT_MODE, counters=counters,
-                          kind=ck.BasisKind.CHEBYSHEV)
-        expect = ck.count_atomics(x.shape[0], x.shape[1], dy.shape[1], sched)
-        assert counters.forward_atomics == expect.fwd_ours == 0
-        assert counters.x_grad_merges == expect.bwd_x_ours
-        assert counters.partial_writes == x.shape[0] * dy.shape[1] * sched.g_x
-        assert counters.combine_stores == x.shape[0] * dy.shape[1]
-
-
 @pytest.mark.parametrize("kind,exact", [("chebyshev", False), ("legendre", True), ("fourier", False)])
 def test_forward_partial_and_combine(kind, exact):
     # kernels.py:263-348 stage by stage: every slot vs the float64 tile sums,

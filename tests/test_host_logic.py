@@ -123,20 +123,6 @@ def test_synthetic_datasets_match_reference_fixtures():
         ck.make_synthetic("nope")
 
 
-def test_load_csv_errors(tmp_path):
-    import paper_2511_14852_b200 as ck
-
-    p = tmp_path / "d.csv"
-    p.write_text("a,b,t\n1,2,3\n4,x,6\n7,8\n")
-    with pytest.raises(ck.DatasetError, match="malformed rows at lines: 3, 4"):
-        ck.load_csv(p)
-    p.write_text("a,t\n1,2.5\n")
-    with pytest.raises(ck.DatasetError, match="integer labels"):
-        ck.load_csv(p, classification=True)
-    ds = ck.load_csv(p)
-    assert ds.x.shape == (1, 1) and ds.y[0] == 2.5
-
-
 def test_roofline_formulas_match_reference():
     # test_acceptance.py:279-298 (closed forms of perf.py:77-90) and the CLI
     # lambda case of test_cli.py:100-113
@@ -155,9 +141,6 @@ def test_roofline_formulas_match_reference():
         assert rep.flops == 2 * b * din * (d + (d + 1) * dout)
         assert rep.bytes == lam * (b * din + b * dout + 2 * b * din * (d + 1) + din * dout * (d + 1))
     assert ck.roofline(ck.LayerConfig(2, 3, 4, 1, 8)).bytes == 2 * 4 * (2 * 3 + 2 * 4 + 2 * 2 * 3 * 2 + 3 * 4 * 2)
-    rep = ck.two_stage_benefit(ck.LayerConfig(8, 128, 64, 3), ck.TileSchedule.for_dims(128, 64),
-                               ck.CostModel(10.0, 1.0, 1.0))
-    assert rep.beneficial and rep.margin == 2 * 10.0 - (2 * 2.0 + 1.0) and rep.partial_bytes == 4 * 8 * 64 * 2
     assert [c.degree for c in ck.paper_configs()] == [8, 15, 24]
     with pytest.raises(ValueError, match="elem_bytes"):
         ck.LayerConfig(1, 1, 1, 1, 2)
@@ -172,9 +155,9 @@ def test_reference_public_names_are_exported():
     TileSchedule backward_fused combine count_atomics forward_partial fused_forward reference_forward
     DEFAULT_LUT_SIZE LutTable load_lut lut_build lut_interp lut_interp_with_slope lut_max_error_bound save_lut
     AdamHParams AdamState Dataset Layer LayerSpec Loss Network NetworkSpec init_params layer_forward
-    load_checkpoint load_csv make_synthetic network_train save_checkpoint
-    BenchResult CostModel LayerConfig Regime RooflineReport TwoStageReport paper_configs roofline run_bench
-    two_stage_benefit CoeffTensor Layout doj_index jod_index load_coeff reorder_to_doj reorder_to_jod
+    load_checkpoint make_synthetic network_train save_checkpoint
+    BenchResult LayerConfig Regime RooflineReport paper_configs roofline run_bench
+    CoeffTensor Layout doj_index jod_index load_coeff reorder_to_doj reorder_to_jod
     save_coeff""".split()
     missing = [n for n in names if not hasattr(ck, n)]
     assert not missing, missing
