@@ -167,12 +167,15 @@ CK_API int ck_combine(const float* partial, int64_t batch, int d_out, int g_x, i
  *            J = 1 - tanh^2 x when include_tanh_jacobian (KernelMode, kernels.py:35-44)
  * db[o] = sum_b dy[b][o]
  * Any of dx / dc_doj / db may be NULL to skip.  dc is reduced by a
- * fixed-order two-stage merge: bit-reproducible run to run. */
+ * fixed-order two-stage merge: bit-reproducible run to run.
+ * grads_ready_event (nullable cudaEvent_t): recorded on `stream` as soon as
+ * dc_doj and db are final -- before the last input-gradient GEMM, which then
+ * runs after it -- so a gradient exchange waiting on the event overlaps dX. */
 CK_API size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out, int n_feat);
 CK_API int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
                 const void* prep, size_t prep_bytes, int include_tanh_jacobian, float* dx, float* dc_doj,
                 float* db, void* workspace, size_t workspace_bytes, const void* basis_cache,
-                size_t basis_cache_bytes, void* stream);
+                size_t basis_cache_bytes, void* grads_ready_event, void* stream);
 
 /* Rows per internal batch chunk of ck_forward / ck_backward (default 32768;
  * CK_CHUNK_ROWS in the environment at load).  Chunks run in ascending order
@@ -182,6 +185,12 @@ CK_API int ck_backward(const float* x, const float* dy, int64_t batch, int d_in,
  * its basis cache.  rows <= 0 restores the default.  Returns the previous
  * value. */
 CK_API int64_t ck_set_chunk_rows(int64_t rows);
+
+/* SMs the persistent GEMMs leave free (process-wide, default 0), for a
+ * gradient exchange kernel running concurrently on another stream.  Results
+ * do not depend on it (tiles are independent of the CTA computing them).
+ * Returns the previous value. */
+CK_API int ck_set_gemm_sm_reserve(int sms);
 
 /* --- Deterministic merge: replaces combine's ordered fold (kernels.py:321-348)
  * and the ordered x-grad merge (kernels.py:438-442) as a standalone op.
@@ -227,6 +236,21 @@ CK_API int ck_ipc_open(const void* handle /*64 bytes*/, int64_t offset, void** d
 CK_API int ck_ipc_close(void* device_ptr, int64_t offset);
 CK_API int ck_allreduce_peers(float* const* bufs /*host array of ranks device pointers*/, int ranks, int rank,
                        int64_t n, void* stream);
+/* The same exchange for elements [lo, lo + n) with device-side
+ * synchronisation instead of host barriers: flags[q] is rank q's array of
+ * ck_peer_flag_words() uint64 flags (zero-initialised, IPC-mapped like the
+ * buffers).  The kernel publishes "rank's gradients ready" to every rank,
+ * waits until every rank's arrived, reduces its shard in ascending rank
+ * order, stores it everywhere, publishes "done" and returns only when every
+ * rank is done -- so it can be enqueued behind the producing kernels on any
+ * stream with no host round trip.  `epoch` increases by one per call and
+ * all ranks issue the same calls in the same order.  A rank that never
+ * arrives turns into a device trap after 20 s (no hang).  max_blocks caps
+ * the grid (0 = two per SM). */
+CK_API int ck_peer_flag_words(void);
+CK_API int ck_allreduce_peers_flags(float* const* bufs, unsigned long long* const* flags, int ranks, int rank,
+                                    int64_t lo, int64_t n, unsigned long long epoch, int max_blocks,
+                                    void* stream);
 
 /* --- Diagnostics --------------------------------------------------------------
  * ck_launch_count: kernels this library has launched in the process.

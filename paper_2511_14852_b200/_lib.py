@@ -49,7 +49,8 @@ SIGNATURES = {
                             _c_size, _c_p]),
     "ck_backward_workspace_bytes": (_c_size, [_c_i64, _c_int, _c_int, _c_int]),
     "ck_backward": (_c_int, [_c_p, _c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_size, _c_int, _c_p, _c_p, _c_p,
-                             _c_p, _c_size, _c_p, _c_size, _c_p]),
+                             _c_p, _c_size, _c_p, _c_size, _c_p, _c_p]),
+    "ck_set_gemm_sm_reserve": (_c_int, [_c_int]),
     "ck_merge": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_int, _c_p]),
     "ck_forward_partial": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_int, _c_int, _c_p, _c_p, _c_p]),
     "ck_combine": (_c_int, [_c_p, _c_i64, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
@@ -65,6 +66,9 @@ SIGNATURES = {
     "ck_ipc_open": (_c_int, [_c_p, _c_i64, ctypes.POINTER(_c_p)]),
     "ck_ipc_close": (_c_int, [_c_p, _c_i64]),
     "ck_allreduce_peers": (_c_int, [ctypes.POINTER(_c_p), _c_int, _c_int, _c_i64, _c_p]),
+    "ck_peer_flag_words": (_c_int, []),
+    "ck_allreduce_peers_flags": (_c_int, [ctypes.POINTER(_c_p), ctypes.POINTER(_c_p), _c_int, _c_int, _c_i64, _c_i64,
+                                          ctypes.c_uint64, _c_int, _c_p]),
     "ck_launch_count": (ctypes.c_longlong, []),
     "ck_timing_enable": (_c_int, [_c_int]),
     "ck_timing_collect": (_c_int, [_c_dp, ctypes.POINTER(ctypes.c_longlong), _c_int]),

@@ -265,6 +265,15 @@ int num_sms() {
 
 int64_t chunk_rows() { return g_chunk_rows.load(std::memory_order_relaxed); }
 
+namespace {
+std::atomic<int> g_sm_reserve{0};
+}
+
+int gemm_sms() {
+  const int n = num_sms() - g_sm_reserve.load(std::memory_order_relaxed);
+  return n >= 2 ? n : 2;
+}
+
 }  // namespace ck
 
 using ck::kOk;
@@ -397,6 +406,11 @@ extern "C" int ck_coeff_prep_check(const void* prep, size_t prep_bytes, int d_in
   return kOk;
 }
 
+extern "C" int ck_set_gemm_sm_reserve(int sms) {
+  CK_CHECK(sms >= 0 && sms < ck::num_sms(), "ck_set_gemm_sm_reserve: 0 <= sms < SM count");
+  return ck::g_sm_reserve.exchange(sms);
+}
+
 extern "C" int64_t ck_set_chunk_rows(int64_t rows) {
   return ck::g_chunk_rows.exchange(rows >= 1 ? rows : ck::kChunkRowsDefault);
 }
@@ -506,7 +520,7 @@ extern "C" size_t ck_backward_workspace_bytes(int64_t batch, int d_in, int d_out
 extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d_in, int d_out, const ck_lut* lut,
                            const void* prep, size_t prep_bytes, int include_tanh_jacobian, float* dx, float* dc_doj,
                            float* db, void* workspace, size_t workspace_bytes, const void* basis_cache,
-                           size_t basis_cache_bytes, void* stream) {
+                           size_t basis_cache_bytes, void* grads_ready, void* stream) {
   CK_TRY(ck::check_dims(batch, d_in, d_out, lut));
   CK_CHECK(prep != nullptr && (batch == 0 || (x != nullptr && dy != nullptr)), "ck_backward: NULL tensor");
   const int K = lut->n_feat, d = K - 1;
@@ -522,6 +536,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
     if (batch == 0) {
       if (dc_doj) CK_CUDA(cudaMemsetAsync(dc_doj, 0, sizeof(float) * n, s));
       if (db) CK_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * d_out, s));
+      if (grads_ready != nullptr) CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
       return kOk;
     }
     float* part_c = ck::at<float>(workspace, SW.part_c);
@@ -532,6 +547,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
     // second stage: ordered slot merges (kernels.py:438-442 order semantics)
     if (dc_doj) CK_TRY(ck::launch_merge(part_c, SW.slots, n, n, dc_doj, 0, s));
     if (db) CK_TRY(ck::launch_col_finish(part_b, SW.slots, d_out, db, s));
+    if (grads_ready != nullptr) CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
     return kOk;
   }
   const ck::BwdLayout W(batch, d_in, d_out, K);
@@ -549,6 +565,7 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
   if (batch == 0) {
     if (dc_doj) CK_CUDA(cudaMemsetAsync(dc_doj, 0, sizeof(float) * K * O * I, s));
     if (db) CK_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * O, s));
+    if (grads_ready != nullptr) CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
     return kOk;
   }
   const ck::PrepLayout P(d_in, d_out, K);
@@ -561,6 +578,14 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
   // db is needed for dC_0 as well; keep a private copy when the caller skips it
   const bool need_db = db != nullptr || dc_doj != nullptr;
 
+  bool db_done = false;
+  auto finish_db = [&]() -> int {
+    if (!need_db) return kOk;
+    float* dbo = db != nullptr ? db : ck::at<float>(workspace, W.db_tmp);
+    // db, and dC_0 = db (T_0 == 1) written by the same launch
+    CK_TRY(ck::launch_col_finish(db_part, static_cast<int>(W.n_chunks * ck::kDbSlots), O, dbo, s, dc_doj, I));
+    return kOk;
+  };
   int64_t ci = 0;
   for (int64_t r0 = 0; r0 < batch; r0 += W.chunk, ++ci) {
     const int64_t rows = batch - r0 < W.chunk ? batch - r0 : W.chunk;
@@ -579,81 +604,100 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
     } else if (need_db) {
       CK_TRY(ck::launch_col_partial(dyc, rows, O, dbp, ck::kDbSlots, s));
     }
-    if (dx && W.fused_dx) {
-      // one GEMM: N tile = d features x n_i inputs, slope combine + Jacobian in the epilogue
-      ck::DxEpilogue epi{xc, dx + r0 * I, ck::view(lut), include_tanh_jacobian, I, P.n_i};
-      ck::GemmProblem gx{};
-      gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
-      gx.b = {ck::at<__nv_bfloat16>(pv, P.dxb_hi), ck::at<__nv_bfloat16>(pv, P.dxb_lo), P.dxb_rows, P.ldO,
-              P.dxb_rows * P.ldO, 1};
-      gx.R = O;
-      gx.S = d;
-      gx.nz = 1;
-      gx.ldo = I;
-      gx.kclass = ck::kKGemmDx;
-      gx.dx = &epi;
-      CK_TRY(ck::gemm_bf16x3(gx, s));
-    } else if (dx) {
-      ck::GemmProblem gx{};
-      gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
-      gx.b = {ck::at<__nv_bfloat16>(pv, P.dxb_hi), ck::at<__nv_bfloat16>(pv, P.dxb_lo), I, P.ldO, I * P.ldO, K};
-      gx.R = O;
-      gx.S = 1;
-      gx.b_seg0 = 1;   // z = k - 1
-      gx.b_seg_z = 1;
-      gx.nz = d;
-      gx.out = g;
-      gx.ldo = I;
-      gx.out_z_stride = rows * I;
-      gx.split_ws = split_ws;
-      gx.split_ws_elems = W.split_elems;
-      gx.kclass = ck::kKGemmDx;
-      CK_TRY(ck::gemm_bf16x3(gx, s));
-      CK_TRY(ck::launch_dx_combine(g, rows * I, xc, rows, d_in, lut, include_tanh_jacobian, dx + r0 * I, s));
-    }
-    if (dc_doj) {
-      const __nv_bfloat16* ph;
-      if (basis_cache != nullptr) {
-        ph = ck::at<__nv_bfloat16>(const_cast<void*>(basis_cache), ci * L.per_chunk);  // from the forward
-      } else {
-        auto* w = ck::at<__nv_bfloat16>(workspace, W.planes);
-        CK_TRY(ck::launch_expand_planes(xc, rows, d_in, lut, 1, w, w + L.half / sizeof(__nv_bfloat16), L.ldI,
-                                        L.plane, s));
-        ph = w;
+    // the input gradient and the coefficient gradient of this chunk
+    auto run_dx = [&]() -> int {
+      if (dx && W.fused_dx) {
+        // one GEMM: N tile = d features x n_i inputs, slope combine + Jacobian in the epilogue
+        ck::DxEpilogue epi{xc, dx + r0 * I, ck::view(lut), include_tanh_jacobian, I, P.n_i};
+        ck::GemmProblem gx{};
+        gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
+        gx.b = {ck::at<__nv_bfloat16>(pv, P.dxb_hi), ck::at<__nv_bfloat16>(pv, P.dxb_lo), P.dxb_rows, P.ldO,
+                P.dxb_rows * P.ldO, 1};
+        gx.R = O;
+        gx.S = d;
+        gx.nz = 1;
+        gx.ldo = I;
+        gx.kclass = ck::kKGemmDx;
+        gx.dx = &epi;
+        CK_TRY(ck::gemm_bf16x3(gx, s));
+      } else if (dx) {
+        ck::GemmProblem gx{};
+        gx.a = {dy_hi, dy_lo, rows, W.ldO, rows * W.ldO, 1};
+        gx.b = {ck::at<__nv_bfloat16>(pv, P.dxb_hi), ck::at<__nv_bfloat16>(pv, P.dxb_lo), I, P.ldO, I * P.ldO, K};
+        gx.R = O;
+        gx.S = 1;
+        gx.b_seg0 = 1;   // z = k - 1
+        gx.b_seg_z = 1;
+        gx.nz = d;
+        gx.out = g;
+        gx.ldo = I;
+        gx.out_z_stride = rows * I;
+        gx.split_ws = split_ws;
+        gx.split_ws_elems = W.split_elems;
+        gx.kclass = ck::kKGemmDx;
+        CK_TRY(ck::gemm_bf16x3(gx, s));
+        CK_TRY(ck::launch_dx_combine(g, rows * I, xc, rows, d_in, lut, include_tanh_jacobian, dx + r0 * I, s));
       }
-      const __nv_bfloat16* pl = ph + L.half / sizeof(__nv_bfloat16);
-      // dC_k[o][i] = sum_b dy[b][o] Φ_k[b][i]: both operands MN-major (batch = K).
-      // Orientation: M = O (dy as A) or, when that pads fewer output cells,
-      // M = I (planes as A) with a transposed store into the same [k][O][I].
-      ck::GemmProblem gc{};
-      const bool trans = ck::gemm_store_padded(I, O, true) < ck::gemm_store_padded(O, I, true);
-      if (trans) {
-        gc.a = {ph, pl, I, L.ldI, L.plane, d, 1};
-        gc.b = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
-        gc.a_seg_z = 1;  // plane z holds k = z + 1
-        gc.out_trans = 1;
-      } else {
-        gc.a = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
-        gc.b = {ph, pl, I, L.ldI, L.plane, d, 1};
-        gc.b_seg_z = 1;  // plane z holds k = z + 1
+      return kOk;
+    };
+    auto run_dc = [&]() -> int {
+      if (dc_doj) {
+        const __nv_bfloat16* ph;
+        if (basis_cache != nullptr) {
+          ph = ck::at<__nv_bfloat16>(const_cast<void*>(basis_cache), ci * L.per_chunk);  // from the forward
+        } else {
+          auto* w = ck::at<__nv_bfloat16>(workspace, W.planes);
+          CK_TRY(ck::launch_expand_planes(xc, rows, d_in, lut, 1, w, w + L.half / sizeof(__nv_bfloat16), L.ldI,
+                                          L.plane, s));
+          ph = w;
+        }
+        const __nv_bfloat16* pl = ph + L.half / sizeof(__nv_bfloat16);
+        // dC_k[o][i] = sum_b dy[b][o] Φ_k[b][i]: both operands MN-major (batch = K).
+        // Orientation: M = O (dy as A) or, when that pads fewer output cells,
+        // M = I (planes as A) with a transposed store into the same [k][O][I].
+        ck::GemmProblem gc{};
+        const bool trans = ck::gemm_store_padded(I, O, true) < ck::gemm_store_padded(O, I, true);
+        if (trans) {
+          gc.a = {ph, pl, I, L.ldI, L.plane, d, 1};
+          gc.b = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
+          gc.a_seg_z = 1;  // plane z holds k = z + 1
+          gc.out_trans = 1;
+        } else {
+          gc.a = {dy_hi, dy_lo, O, W.ldO, rows * W.ldO, 1, 1};
+          gc.b = {ph, pl, I, L.ldI, L.plane, d, 1};
+          gc.b_seg_z = 1;  // plane z holds k = z + 1
+        }
+        gc.R = rows;
+        gc.S = 1;
+        gc.nz = d;
+        gc.out = dc_doj + O * I;
+        gc.ldo = I;
+        gc.out_z_stride = O * I;
+        gc.accumulate = ci > 0 ? 1 : 0;  // ascending chunk order: reproducible
+        gc.split_ws = split_ws;
+        gc.split_ws_elems = W.split_elems;
+        gc.kclass = ck::kKGemmDc;
+        CK_TRY(ck::gemm_bf16x3(gc, s));
       }
-      gc.R = rows;
-      gc.S = 1;
-      gc.nz = d;
-      gc.out = dc_doj + O * I;
-      gc.ldo = I;
-      gc.out_z_stride = O * I;
-      gc.accumulate = ci > 0 ? 1 : 0;  // ascending chunk order: reproducible
-      gc.split_ws = split_ws;
-      gc.split_ws_elems = W.split_elems;
-      gc.kclass = ck::kKGemmDc;
-      CK_TRY(ck::gemm_bf16x3(gc, s));
+      return kOk;
+    };
+    if (grads_ready != nullptr && r0 + rows >= batch) {
+      // last chunk with a grads-ready event: dC and db first, the event, then
+      // the input-gradient GEMM -- a gradient exchange on another stream can
+      // start while dX is computed
+      CK_TRY(run_dc());
+      CK_TRY(finish_db());
+      CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
+      db_done = true;
+      CK_TRY(run_dx());
+    } else {
+      CK_TRY(run_dx());
+      CK_TRY(run_dc());
     }
   }
-  if (need_db) {
-    float* dbo = db != nullptr ? db : ck::at<float>(workspace, W.db_tmp);
-    // db, and dC_0 = db (T_0 == 1) written by the same launch
-    CK_TRY(ck::launch_col_finish(db_part, static_cast<int>(W.n_chunks * ck::kDbSlots), O, dbo, s, dc_doj, I));
+  if (!db_done) {
+    CK_TRY(finish_db());
+    if (grads_ready != nullptr) CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
   }
   return kOk;
 }

@@ -74,6 +74,15 @@ int gemm_group() {
   return g;
 }
 
+int gemm_seg() {
+  static int v = [] {
+    const char* e = getenv("CK_GEMM_SEG");
+    const int n = e ? atoi(e) : kSegIters;
+    return n >= 0 ? n : kSegIters;
+  }();
+  return v;
+}
+
 namespace {
 
 // LUT-mode fused dX: chord slopes recomputed in the epilogue (1, default for
@@ -140,10 +149,21 @@ int choose_splits(int64_t M, int64_t N, int nz, int64_t R, const StoreCfg& c, bo
 
 }  // namespace
 
+// CK_GEMM_SPLITS=s forces s reduction splits on every store GEMM whose
+// workspace allows it (accuracy / traffic experiments; 0 = cost model).
+int forced_splits() {
+  static int v = [] {
+    const char* e = getenv("CK_GEMM_SPLITS");
+    const int s = e ? atoi(e) : 0;
+    return s >= 1 && s <= 64 ? s : 0;
+  }();
+  return v;
+}
+
 int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R) {
   // the larger of the two operand majornesses' choices (the workspace is
   // sized before the caller knows which GEMM runs)
-  int splits = 1;
+  int splits = forced_splits() > 0 ? forced_splits() : 1;
   for (bool mn : {false, true}) {
     const int sp = choose_splits(M, N, nz, R, pick_store(N), mn);
     if (sp > splits) splits = sp;
@@ -183,6 +203,7 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   const bool mn = p.a.mn_major || p.b.mn_major;
   const StoreCfg cfg = pick_store(p.b.rows);
   int splits = choose_splits(p.a.rows, p.b.rows, p.nz, p.R, cfg, mn);
+  if (forced_splits() > 0) splits = forced_splits();  // experiments (CK_GEMM_SPLITS)
   const int64_t need = static_cast<int64_t>(splits) * p.nz * p.a.rows * p.b.rows;
   if (splits > 1 && (p.split_ws == nullptr || p.split_ws_elems < need)) splits = 1;
   const bool dense_out = p.ldo == (p.out_trans ? p.a.rows : p.b.rows) && p.out_z_stride == p.a.rows * p.b.rows;

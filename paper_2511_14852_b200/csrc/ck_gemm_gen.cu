@@ -45,6 +45,8 @@ int gen_max_o() {
 // (d >= 4) and the reduction is long enough to amortise the fill (d*I >=
 // 1536); below that the materialised planes are as fast or faster.
 // CK_GEN=all drops the degree / length rule (tests).
+constexpr int kGenMaxChain = 8192;  // reduction terms
+
 bool gen_layer(int I, int O, int K) {
   static const bool all = [] {
     const char* e = getenv("CK_GEN");
@@ -52,6 +54,12 @@ bool gen_layer(int I, int O, int K) {
   }();
   const int d = K - 1;
   if (skinny_layer(I, O, K) || O > gen_max_o() || gen_chunks(I, d) == 0) return false;
+  // the generated forward accumulates the whole reduction in one TMEM
+  // buffer (no segment folding: its epilogue warps have no registers to
+  // spare), so it is limited to reductions whose biased tensor-core
+  // accumulation stays <= ~3e-5 normwise (8192 terms; ck_gemm_impl.cuh,
+  // kSegIters); longer ones take expand + the segmented store GEMM
+  if (gen_chunks(I, d) * 64 > kGenMaxChain) return false;
   return all || (d >= 4 && static_cast<int64_t>(d) * I >= 1536);
 }
 
@@ -112,7 +120,7 @@ int gemm_gen_forward(const float* x, int64_t M, int I, int O, const LutView& v, 
   const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles;
   CK_CHECK(total < (1ll << 31), "gemm_gen: too many tiles");
   k.total_tiles = static_cast<int>(total);
-  const int units_max = num_sms() / 2;
+  const int units_max = gemm_sms() / 2;
   const int grid = 2 * static_cast<int>(total < units_max ? total : units_max);
   LaunchScope scope(kKGemmFwd, s);
   switch (v.kind) {

@@ -37,6 +37,9 @@ namespace ck {
 int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t rows, int64_t segs, int64_t ld,
              int64_t seg_stride, int box_rows, int bk, int mn_major = 0);
 int gemm_group();
+// pipeline iterations per accumulation segment of the store GEMMs
+// (kSegIters; CK_GEMM_SEG overrides, 0 = whole tile)
+int gemm_seg();
 // Store-GEMM N tile: a multiple of 32 (64 per CTA for MN-major B slabs) <= BN
 // spreading N evenly over ceil(N/BN) tiles.
 inline int store_ntile(int64_t N, int BN, int CG, bool mn_major) {
@@ -89,7 +92,20 @@ struct KArgs {
   // generated-operand forward (ck_gemm_gen.cu): x pitch and input count
   long long gen_ldx;
   int gen_I;
+  // store GEMMs: pipeline iterations accumulated in TMEM per segment before
+  // the epilogue folds the segment into fp32 registers (0: whole tile)
+  int seg_iters;
 };
+
+// Accumulation segments.  The tensor core's fp32 accumulation of a long
+// reduction is biased (the error grows linearly with the chain: 1.06e-4
+// normwise for the 32768-term C4 forward, 5.5e-5 / 2.6e-5 / 1.2e-5 with 2 /
+// 4 / 8 reduction splits -- tools/accum_error.py), so store GEMMs accumulate
+// kSegIters pipeline iterations (1024 reduction terms at BK = 64) in one
+// TMEM buffer, then the epilogue warps add the segment into fp32 registers
+// (round to nearest) while the MMAs fill the other buffer.
+constexpr int kSegIters = 16;
+__host__ __device__ inline int seg_len(int seg_iters, int iters) { return seg_iters > 0 ? seg_iters : iters; }
 
 namespace {
 
@@ -601,14 +617,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader CTA of a pair) ----------------
       const uint32_t idesc = umma_idesc_bf16_f32(kBM * CG, p.n_mma, AMN, BMN);
-      uint32_t g = 0, lt = 0;
-      for (int t = unit; t < total; t += n_units, ++lt) {
+      uint32_t g = 0, seg = 0;
+      for (int t = unit; t < total; t += n_units) {
         const TileCoord tc = decode_tile(p, t, kBM * CG);
-        const uint32_t acc = lt & 1, use = lt >> 1;
+        const int D = seg_len(p.seg_iters, tc.iters);
+        for (int s0 = 0; s0 < tc.iters; s0 += D, ++seg) {
+        // one accumulation segment: iterations [s0, s1) into buffer seg & 1
+        const uint32_t acc = seg & 1, use = seg >> 1;
         mbar_wait(&tempty[acc], (use & 1) ^ 1);  // epilogue has drained this buffer
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int it = 0; it < tc.iters; ++it, ++g) {
+        const int s1 = min(s0 + D, tc.iters);
+        for (int it = s0; it < s1; ++it, ++g) {
           const int stage = g % STAGES;
           const uint32_t phase = (g / STAGES) & 1;
           mbar_wait(&full[stage], phase);
@@ -637,12 +657,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               dbh = umma_desc_kmajor<kRowBytes>(b_hi + kk * 32);
               dbl = umma_desc_kmajor<kRowBytes>(b_lo + kk * 32);
             }
+            const uint32_t accum = ((it - s0) | kk) != 0 ? 1u : 0u;
             if constexpr (CG == 2) {
-              umma_bf16_pair(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+              umma_bf16_pair(d_tmem, dah, dbh, idesc, accum);
               umma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);
               umma_bf16_pair(d_tmem, dal, dbh, idesc, 1u);
             } else {
-              umma_bf16(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+              umma_bf16(d_tmem, dah, dbh, idesc, accum);
               umma_bf16(d_tmem, dah, dbl, idesc, 1u);
               umma_bf16(d_tmem, dal, dbh, idesc, 1u);
             }
@@ -659,21 +680,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           umma_commit(&tfull[acc]);
         }
+        }
       }
     }
   } else if (warp >= 4) {
     const int q = warp & 3;          // TMEM lane quarter this warp may access
     const int h = (warp - 4) >> 2;   // which half of the tile's columns
-    uint32_t lt = 0;
-    for (int t = unit; t < total; t += n_units, ++lt) {
+    uint32_t seg = 0;
+    for (int t = unit; t < total; t += n_units) {
       const TileCoord tc = decode_tile(p, t, kBM * CG);
-      const uint32_t acc = lt & 1, use = lt >> 1;
-      mbar_wait(&tfull[acc], use & 1);
-      tc_fence_after();
-      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int row = tc.m0 + row_off + q * 32 + lane;
       const bool row_ok = row < p.M;
       if constexpr (EPI == kEpiDx) {
+        // one segment per tile (seg_iters = 0)
+        const uint32_t acc = seg & 1, use = seg >> 1;
+        ++seg;
+        mbar_wait(&tfull[acc], use & 1);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
         // ------------- fused dX epilogue (degree-specialized) -------------
         if constexpr (DXM == 0) {
           switch (p.b_boxes) {
@@ -719,29 +743,77 @@ __global__ void __launch_bounds__(kThreads, 1)
               break;
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) {
+            mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits on it
+          } else {
+            mbar_arrive(&tempty[acc]);
+          }
+        }
       } else {
         // ------------- store epilogue -------------
+        // Fold the tile's accumulation segments into fp32 registers: this
+        // thread's row, columns 32 h + 64 ch + [0, 32) (round-to-nearest adds;
+        // see kSegIters).  Each drained buffer is released before the next
+        // wait, so the MMAs of the following segment overlap the fold.
+        constexpr int NCH = BN / 64;
+        uint32_t sums[NCH][32];
+        const int D = seg_len(p.seg_iters, tc.iters);
+        const int nseg = (tc.iters + D - 1) / D;
+        for (int j = 0; j < nseg; ++j, ++seg) {
+          const uint32_t acc = seg & 1, use = seg >> 1;
+          mbar_wait(&tfull[acc], use & 1);
+          tc_fence_after();
+          const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int c = 32 * h + 64 * ch;
+            if (c < p.n_tile) {
+              // 8 columns per load: the 128 sums + one load stay in registers
+#pragma unroll
+              for (int e0 = 0; e0 < 32; e0 += 8) {
+                uint32_t r[8];
+                tmem_ld_32x32b_x8(tbase + c + e0, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  sums[ch][e0 + e] =
+                      j == 0 ? r[e] : __float_as_uint(__uint_as_float(sums[ch][e0 + e]) + __uint_as_float(r[e]));
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) {
+              mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits on it
+            } else {
+              mbar_arrive(&tempty[acc]);
+            }
+          }
+        }
         float* out = p.out + static_cast<long long>(tc.z) * p.out_z_stride +
                      static_cast<long long>(tc.split) * p.out_split_stride;
         const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
         float* tile = reinterpret_cast<float*>(smem + STAGES * C::kStageBytes + C::kBarrierBytes) +
                       (warp - 4) * (kEpiTileBytes / 4);
         const int row0 = tc.m0 + row_off + q * 32;
-        if (p.out_trans) {
-          // transposed: column n of the tile is a row of the output; lanes
-          // (= tile rows) are contiguous there, so each store is 128 bytes
-#pragma unroll 1
-          for (int c = 32 * h; c < p.n_tile; c += 64) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(tbase + c, r);
-            tmem_ld_wait();
-            const int nb = tc.n0 + c;
-            if (row_ok && nb < p.N) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int n = nb + j;
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int c = 32 * h + 64 * ch;  // 32-column chunks alternate between the quarter's two warps
+          const int nb = tc.n0 + c;
+          if (c >= p.n_tile || nb >= p.N) continue;
+          if (p.out_trans) {
+            // transposed: column n of the tile is a row of the output; lanes
+            // (= tile rows) are contiguous there, so each store is 128 bytes
+            if (row_ok) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const int n = nb + e;
                 if (n < p.N) {
-                  float o = __uint_as_float(r[j]);
+                  float o = __uint_as_float(sums[ch][e]);
                   if (p.bias0) o += p.bias0[n];
                   if (p.bias1) o += p.bias1[n];
                   float* dst = out + static_cast<long long>(n) * p.ldo + row;
@@ -750,29 +822,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             }
+          } else {
+            store_chunk_coalesced(sums[ch], tile, lane, row0, p.M, nb, p.N, out, p.ldo, p.bias0, p.bias1,
+                                  p.accumulate, vec);
           }
-        } else {
-        // 32-column chunks of the (runtime) tile width, alternating between
-        // the two warps of this TMEM lane quarter
-#pragma unroll 1
-        for (int c = 32 * h; c < p.n_tile; c += 64) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tbase + c, r);
-          tmem_ld_wait();
-          const int nb = tc.n0 + c;
-          if (nb >= p.N) continue;
-          store_chunk_coalesced(r, tile, lane, row0, p.M, nb, p.N, out, p.ldo, p.bias0, p.bias1, p.accumulate,
-                                vec);
-        }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) {
-          mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits on it
-        } else {
-          mbar_arrive(&tempty[acc]);
         }
       }
     }
@@ -853,6 +906,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.bias0 = splits == 1 ? p.bias0 : nullptr;
   k.bias1 = splits == 1 ? p.bias1 : nullptr;
   k.accumulate = accumulate;
+  k.seg_iters = EPI == kEpiStore ? gemm_seg() : 0;
   k.out_trans = p.out_trans;
   auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM>;
   // store kernels: + a 4 KB staging tile per epilogue warp
@@ -873,7 +927,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles * p.nz * splits;
   CK_CHECK(total < (1ll << 31), "gemm: too many tiles");
   k.total_tiles = static_cast<int>(total);
-  const int units_max = num_sms() / CG;
+  const int units_max = gemm_sms() / CG;
   const int units = static_cast<int>(total < units_max ? total : units_max);
   LaunchScope scope(p.kclass, s);
   cudaLaunchConfig_t cfg{};

@@ -23,6 +23,9 @@ namespace ck {
 namespace {
 
 constexpr int kMaxPeers = 8;
+}  // namespace
+constexpr int kFlagWordsPublic = 32;  // uint64 flag words per rank (3 * 8 used)
+namespace {
 
 struct PeerPtrs {
   float* p[kMaxPeers];
@@ -49,6 +52,94 @@ __global__ void __launch_bounds__(256) allreduce_peers_kernel(PeerPtrs bufs, int
     float acc = bufs.p[0][e];
     for (int r = 1; r < ranks; ++r) acc += bufs.p[r][e];
     for (int r = 0; r < ranks; ++r) bufs.p[r][e] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Flag-synchronised variant: no host barriers.  Each rank owns a small array
+// of 64-bit flags inside its IPC-mapped exchange buffer (kFlagWords words):
+//   [kReady + q]  epoch at which rank q's gradients for this exchange are complete
+//   [kDone + q]   epoch at which rank q has stored its reduced shard everywhere
+//   [kCounter]    blocks of this rank's kernel finished (local)
+// Epochs grow by one per exchange and every rank issues its exchanges in
+// the same order, so a flag value >= epoch means "this exchange".  Waits
+// give up after kSpinLimitNs with a trap: a missing peer becomes a CUDA
+// error on the next synchronisation instead of a hang.
+constexpr int kReady = 0, kDone = kMaxPeers, kCounter = 2 * kMaxPeers;
+constexpr unsigned long long kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
+
+struct PeerFlags {
+  unsigned long long* f[kMaxPeers];
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// one thread: until every rank's flag slot [base + q] reached epoch
+__device__ void wait_all(const unsigned long long* mine, int base, int ranks, unsigned long long epoch) {
+  const unsigned long long t0 = globaltimer();
+  for (int q = 0; q < ranks; ++q) {
+    while (ld_acquire_sys(mine + base + q) < epoch) {
+      if (globaltimer() - t0 > kSpinLimitNs) __trap();
+      __nanosleep(200);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) allreduce_flags_kernel(PeerPtrs bufs, PeerFlags flags, int ranks, int rank,
+                                                             int64_t lo, int64_t hi, unsigned long long epoch) {
+  unsigned long long* mine = flags.f[rank];
+  // (this rank's gradients are complete: the kernel runs after the producing
+  // kernels on the stream)
+  if (blockIdx.x == 0 && threadIdx.x < ranks) st_release_sys(flags.f[threadIdx.x] + kReady + rank, epoch);
+  if (threadIdx.x == 0) wait_all(mine, kReady, ranks, epoch);
+  __syncthreads();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t n4 = (hi - lo) >> 2;
+  for (int64_t i = t0; i < n4; i += stride) {
+    const int64_t e = lo + 4 * i;
+    float4 acc = __ldcv(reinterpret_cast<const float4*>(bufs.p[0] + e));
+    for (int r = 1; r < ranks; ++r) {
+      const float4 v = __ldcv(reinterpret_cast<const float4*>(bufs.p[r] + e));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    for (int r = 0; r < ranks; ++r) *reinterpret_cast<float4*>(bufs.p[r] + e) = acc;
+  }
+  for (int64_t e = lo + 4 * n4 + t0; e < hi; e += stride) {
+    float acc = __ldcv(bufs.p[0] + e);
+    for (int r = 1; r < ranks; ++r) acc += __ldcv(bufs.p[r] + e);
+    for (int r = 0; r < ranks; ++r) bufs.p[r][e] = acc;
+  }
+  // the last block to finish publishes DONE to every rank, then waits until
+  // every rank's DONE arrived: when this kernel ends, all shards are stored
+  // in this rank's buffer and no peer still reads it
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long prev = atomicAdd(mine + kCounter, 1ull);
+    if (prev == gridDim.x - 1) {
+      mine[kCounter] = 0;
+      __threadfence_system();
+      for (int q = 0; q < ranks; ++q) st_release_sys(flags.f[q] + kDone + rank, epoch);
+      wait_all(mine, kDone, ranks, epoch);
+    }
   }
 }
 
@@ -125,6 +216,40 @@ extern "C" int ck_allreduce_peers(float* const* bufs, int ranks, int rank, int64
   ck::LaunchScope scope(ck::kKReduce, s);
   ck::allreduce_peers_kernel<<<static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap)), 256, 0, s>>>(pp, ranks,
                                                                                                        lo, hi);
+  CK_CUDA(cudaGetLastError());
+  return ck::kOk;
+}
+
+extern "C" int ck_peer_flag_words(void) { return ck::kFlagWordsPublic; }
+
+extern "C" int ck_allreduce_peers_flags(float* const* bufs, unsigned long long* const* flags, int ranks, int rank,
+                                        int64_t lo, int64_t n, unsigned long long epoch, int max_blocks,
+                                        void* stream) {
+  CK_CHECK(ranks >= 1 && ranks <= ck::kMaxPeers, "ck_allreduce_peers_flags: 1..8 ranks");
+  CK_CHECK(rank >= 0 && rank < ranks, "ck_allreduce_peers_flags: rank out of range");
+  CK_CHECK(lo >= 0 && n >= 0 && bufs != nullptr && flags != nullptr && epoch >= 1,
+           "ck_allreduce_peers_flags: bad arguments");
+  ck::PeerPtrs pp{};
+  ck::PeerFlags pf{};
+  for (int r = 0; r < ranks; ++r) {
+    CK_CHECK(bufs[r] != nullptr && flags[r] != nullptr && (reinterpret_cast<uintptr_t>(bufs[r]) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(flags[r]) & 7) == 0,
+             "ck_allreduce_peers_flags: buffers must be 16-byte and flags 8-byte aligned");
+    pp.p[r] = bufs[r];
+    pf.f[r] = flags[r];
+  }
+  CK_CHECK(lo % 4 == 0, "ck_allreduce_peers_flags: range start must be a multiple of 4 elements");
+  // shard `rank` of [lo, lo + n), boundaries on 4-element multiples
+  const int64_t per = ck::round_up(ck::ceil_div(n, ranks), 4);
+  const int64_t a = lo + (rank * per < n ? rank * per : n);
+  const int64_t b = (a + per < lo + n) ? a + per : lo + n;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t want = ck::ceil_div(ck::ceil_div(b > a ? b - a : 1, 4), 512);
+  int64_t cap = max_blocks > 0 ? max_blocks : static_cast<int64_t>(ck::num_sms()) * 2;
+  const int blocks = static_cast<int>(want < cap ? want : cap);
+  ck::LaunchScope scope(ck::kKReduce, s);
+  // (an empty shard still takes part in the flag exchange)
+  ck::allreduce_flags_kernel<<<blocks < 1 ? 1 : blocks, 512, 0, s>>>(pp, pf, ranks, rank, a, b > a ? b : a, epoch);
   CK_CUDA(cudaGetLastError());
   return ck::kOk;
 }

@@ -240,21 +240,40 @@ def forward_raw(x: torch.Tensor, prep: PreparedCoeff, lut, bias: torch.Tensor | 
 
 def backward_raw(x: torch.Tensor, dy: torch.Tensor, prep: PreparedCoeff, lut, jacobian: bool,
                  want_dx: bool = True, want_dc: bool = True, want_db: bool = True,
-                 cache: torch.Tensor | None = None):
+                 cache: torch.Tensor | None = None, dc_out: torch.Tensor | None = None,
+                 db_out: torch.Tensor | None = None, grads_ready=None):
     """(dC DOJ, dX, db) on prepared coefficients; unrequested outputs are None.
 
     ``cache``: the basis cache filled by forward_raw on the same x (optional).
+    ``dc_out`` / ``db_out``: contiguous fp32 tensors to write dC / db into
+    (e.g. views of a data-parallel exchange buffer) instead of new ones.
+    ``grads_ready``: a torch.cuda.Event recorded as soon as dC and db are
+    final, before the last input-gradient GEMM (ck_backward's event).
     """
     b = x.shape[0]
     dev = x.device
     dx = torch.empty((b, prep.d_in), dtype=torch.float32, device=dev) if want_dx else None
-    dc = torch.empty((prep.n_feat, prep.d_out, prep.d_in), dtype=torch.float32, device=dev) if want_dc else None
-    db = torch.empty((prep.d_out,), dtype=torch.float32, device=dev) if want_db else None
+    dc, db = None, None
+    if want_dc:
+        dc = dc_out if dc_out is not None else torch.empty((prep.n_feat, prep.d_out, prep.d_in), dtype=torch.float32,
+                                                           device=dev)
+        if tuple(dc.shape) != (prep.n_feat, prep.d_out, prep.d_in) or not dc.is_contiguous():
+            raise ValueError("dc_out must be a contiguous [K, O, I] tensor")
+    if want_db:
+        db = db_out if db_out is not None else torch.empty((prep.d_out,), dtype=torch.float32, device=dev)
+        if tuple(db.shape) != (prep.d_out,) or not db.is_contiguous():
+            raise ValueError("db_out must be a contiguous [O] tensor")
+    ev = None
+    if grads_ready is not None:
+        ev = grads_ready.cuda_event
+        if not ev:  # torch creates the event lazily
+            grads_ready.record()
+            ev = grads_ready.cuda_event
     lb = _lib.lib()
     ws = _workspace(lb.ck_backward_workspace_bytes(b, prep.d_in, prep.d_out, prep.n_feat), dev)
     rc = lb.ck_backward(x.data_ptr(), dy.data_ptr(), b, prep.d_in, prep.d_out, lut.handle, prep.buffer.data_ptr(),
                         prep.buffer.numel(), 1 if jacobian else 0, _lib.ptr(dx), _lib.ptr(dc), _lib.ptr(db), ws.data_ptr(), ws.numel(),
-                        _lib.ptr(cache), 0 if cache is None else cache.numel(), _lib.stream_handle(dev))
+                        _lib.ptr(cache), 0 if cache is None else cache.numel(), ev, _lib.stream_handle(dev))
     _lib.check(rc, "ck_backward")
     return dc, dx, db
 

@@ -33,6 +33,7 @@ class _LayerState:
         self.cache_basis = cache_basis
         self._luts: dict = {}
         self._prep: PreparedCoeff | None = None
+        self.grad_sink = None  # set by a data-parallel reducer's bind() (parallel.py)
 
     def lut(self, device: torch.device):
         idx = device.index if device.index is not None else torch.cuda.current_device()
@@ -110,8 +111,16 @@ class ChebyKANFunction(torch.autograd.Function):
         dy = dy.to(torch.float32).contiguous()
         need_x, need_c, need_b = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
         prep = state.prepared(coeff_doj)
+        # data-parallel binding (parallel.py): dC / db straight into the
+        # exchange buffer, and the exchange started on its grads-ready event
+        sink = state.grad_sink if need_c else None
+        outs = sink.try_begin() if sink is not None else None
+        dc_out, db_out, ev = outs if outs is not None else (None, None, None)
         dc, dx, db = backward_raw(x, dy, prep, state.lut(x.device), state.jacobian, want_dx=need_x,
-                                  want_dc=need_c, want_db=need_b and ctx.has_bias, cache=ctx.cache)
+                                  want_dc=need_c, want_db=need_b and ctx.has_bias, cache=ctx.cache,
+                                  dc_out=dc_out, db_out=db_out if need_b and ctx.has_bias else None, grads_ready=ev)
+        if outs is not None:
+            sink.done()
         ctx.cache = None
         return dx, dc, db, None, None
 

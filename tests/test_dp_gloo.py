@@ -32,7 +32,8 @@ def _worker(rank, world, port, out_q):
             g = torch.arange(p.numel(), dtype=torch.float32).reshape(p.shape) * (i + 1)
             p.grad = g * (b - a)  # proportional to the rows this rank owns
         red = GradientAllreducer(params)
-        assert red.nbytes == 4 * sum(p.numel() for p in params)
+        # one flat buffer, every slot 16-byte aligned
+        assert red.nbytes == 4 * sum((p.numel() + 3) // 4 * 4 for p in params)
         red()
         out_q.put((rank, [p.grad.clone().numpy() for p in params]))
     finally:
@@ -47,7 +48,7 @@ def test_gradient_allreduce_world2():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    results = dict(q.get(timeout=120) for _ in range(world))
+    results = dict(q.get(timeout=60) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

@@ -45,7 +45,8 @@ def _bwd(prep_ptr, prep_bytes, x, dy, i, o, lut):
     ws = torch.empty(max(1, lib.ck_backward_workspace_bytes(x.shape[0], i, o, lut.n_features)), dtype=torch.uint8,
                      device=_dev())
     rc = lib.ck_backward(x.data_ptr(), dy.data_ptr(), x.shape[0], i, o, lut.handle, prep_ptr, prep_bytes, 1,
-                         dx.data_ptr(), None, None, ws.data_ptr(), ws.numel(), None, 0, _lib.stream_handle(_dev()))
+                         dx.data_ptr(), None, None, ws.data_ptr(), ws.numel(), None, 0, None,
+                         _lib.stream_handle(_dev()))
     _lib.check(rc, "ck_backward")
     return dx
 

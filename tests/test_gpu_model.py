@@ -176,3 +176,62 @@ def test_cuda_graph_training_step_matches_eager():
     # 3 warm-up + 4 replays = 7 updates (capture records, it does not execute)
     for pe, pg in zip(eager.parameters(), graphed.parameters()):
         assert torch.allclose(pe, pg, rtol=1e-5, atol=1e-6), (pe - pg).abs().max()
+
+
+def _net_cases():
+    # mirrors NET_CASES in tests/golden/make_golden_train.py (BASELINE configs C2 / C3 at full width)
+    return {
+        "c2_tabular": ((ck.LayerSpec(64, 512, 5), ck.LayerSpec(512, 512, 5), ck.LayerSpec(512, 1, 5)), 2, 32768, 1,
+                       1e-4, 64, 1e-3),
+        "c3_speech": ((ck.LayerSpec(257, 512, 15), ck.LayerSpec(512, 512, 15), ck.LayerSpec(512, 257, 15)), 2, 32768,
+                      2, 3e-5, 64, 2e-3),
+    }
+
+
+@pytest.mark.parametrize("name", ["c2_tabular", "c3_speech"])
+def test_c2_c3_nets_follow_reference_trajectory(name):
+    """network_train on the C2 tabular net [64->512->512->1] d5 and the C3
+    speech FFN [257->512->512->257] d15 (256 rows, 2 epochs of 4 Adam steps,
+    cosine decay) against the reference trainer's float64 run.
+
+    Bars: epoch losses within 1e-3 relative; the
+    trained network's outputs on a probe batch within 1e-3 (C2) / 2e-3 (C3)
+    normwise -- the reference's own outputs move by 1.1e-4 / 5.8e-4 when
+    1e-5 * max|g| of additive noise (the size of a BF16x3 gradient error)
+    perturbs its gradients (tests/golden/make_golden_train.py).  The
+    coefficients (a fixed-stride subsample) are compared elementwise at
+    1e-3 of their range for all but <= 0.1 % of the elements, the biases for
+    all but <= 1 % (one element of a head): Adam's first
+    step is ~lr * sign(g), so an element whose gradient lies below the
+    round-off can take the opposite first step -- a discrete difference of
+    2 lr, not a drift."""
+    g = np.load(GOLDEN / f"train_{name}.npz")
+    layers, epochs, lut_size, seed, lr, batch, probe_tol = _net_cases()[name]
+    ds = ck.Dataset(g["x"].astype(np.float64), g["y"].astype(np.float64), name=name)
+    res = ck.network_train(ck.NetworkSpec(layers, ck.Loss.MSE), ds, epochs, ck.AdamHParams(lr=lr), seed=seed,
+                           batch_size=batch, lut_size=lut_size, cosine_decay=True)
+    got = np.array(res.trace.epoch_losses)
+    want = g["epoch_losses"]
+    loss_err = float(np.abs(got - want).max() / np.abs(want).max())
+    probe = res.network.forward(g["x"][: g["probe_y"].shape[0]].astype(np.float64))
+    probe_err = orc.normwise_err(probe.cpu().numpy(), g["probe_y"])
+    print(name, "losses", got, want, f"rel {loss_err:.2e}", f"probe {probe_err:.2e}")
+    assert loss_err <= TRAIN_TOL
+    assert probe_err <= probe_tol
+    for i, layer in enumerate(res.network.layers):
+        c = layer.coeff.as3d().permute(2, 1, 0).contiguous().cpu().numpy()
+        assert tuple(c.shape) == tuple(g[f"coeff_jod_shape_{i}"])
+        sub = c.reshape(-1)[::997]
+        want_sub = g[f"coeff_jod_sub_{i}"]
+        scale = np.abs(want_sub).max()
+        bad = np.abs(sub - want_sub) > TRAIN_TOL * scale
+        print(f"  layer {i}: coeff subsample normwise {orc.normwise_err(sub, want_sub):.2e}, "
+              f"{int(bad.sum())}/{bad.size} beyond 1e-3")
+        assert bad.mean() <= 1e-3
+        if layer.bias is not None:
+            # biases start at 0 and move by ~lr per step: the same sign-flip
+            # mechanism, at most 1 % of the elements (one for a head)
+            gb, wb = layer.bias.cpu().numpy(), g[f"bias_{i}"]
+            bad_b = np.abs(gb - wb) > TRAIN_TOL * np.abs(wb).max()
+            print(f"  layer {i}: bias normwise {orc.normwise_err(gb, wb):.2e}, {int(bad_b.sum())}/{bad_b.size} beyond")
+            assert bad_b.sum() <= max(1, 0.01 * bad_b.size)
