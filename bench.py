@@ -27,6 +27,7 @@ Python reference itself cannot travel to the GPU box) on the host cores.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import pathlib
@@ -330,6 +331,9 @@ def run_ours(args, wl):
                 print(f"peer allreduce unavailable ({exc}); using NCCL", file=sys.stderr)
         if reducer is None:
             reducer, reducer_kind = ck.GradientAllreducer(params), "NCCL all_reduce (Ring)"
+        # dC / db written by ck_backward straight into the exchange buffer; the
+        # peer exchange starts on the grads-ready event, before the last dX GEMM
+        reducer.bind(model)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
     if is_net:
@@ -506,14 +510,17 @@ def run_ours(args, wl):
                 pending["next"] = g + 1
             cur.wait_event(ready[k])
             xin = xb[k][: hi - lo].detach().requires_grad_(not is_net)
-            y = model(xin)
-            if is_net:
-                part = torch.nn.functional.mse_loss(y, dyb[k][: hi - lo], reduction="sum") / rows
-                part.backward()
-                loss += part.detach()
-            else:
-                loss += (y.detach() * dyb[k][: hi - lo]).sum()
-                y.backward(dyb[k][: hi - lo])
+            # micro-batches before the last accumulate without starting the exchange
+            sync_ctx = reducer.no_sync() if (reducer is not None and j + 1 < n_mb) else contextlib.nullcontext()
+            with sync_ctx:
+                y = model(xin)
+                if is_net:
+                    part = torch.nn.functional.mse_loss(y, dyb[k][: hi - lo], reduction="sum") / rows
+                    part.backward()
+                    loss += part.detach()
+                else:
+                    loss += (y.detach() * dyb[k][: hi - lo]).sum()
+                    y.backward(dyb[k][: hi - lo])
             free[k].record(cur)
         if reducer is not None:
             reducer()

@@ -101,10 +101,13 @@ struct KArgs {
 // reduction is biased (the error grows linearly with the chain: 1.06e-4
 // normwise for the 32768-term C4 forward, 5.5e-5 / 2.6e-5 / 1.2e-5 with 2 /
 // 4 / 8 reduction splits -- tools/accum_error.py), so store GEMMs accumulate
-// kSegIters pipeline iterations (1024 reduction terms at BK = 64) in one
+// kSegIters pipeline iterations (2048 reduction terms at BK = 64) in one
 // TMEM buffer, then the epilogue warps add the segment into fp32 registers
-// (round to nearest) while the MMAs fill the other buffer.
-constexpr int kSegIters = 16;
+// (round to nearest) while the MMAs fill the other buffer.  C4 forward
+// error / time vs segment length (tools/seg_sweep.py): 16 it. 4.5e-6, +3-5 %;
+// 32 it. 7.3e-6, +1-2 %; 64 it. 1.4e-5, +2 %; 128 it. 2.8e-5, +0-2 %;
+// whole tile 1.06e-4.
+constexpr int kSegIters = 32;
 __host__ __device__ inline int seg_len(int seg_iters, int iters) { return seg_iters > 0 ? seg_iters : iters; }
 
 namespace {

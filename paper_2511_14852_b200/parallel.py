@@ -25,6 +25,7 @@ kernel (ck_set_gemm_sm_reserve).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import weakref
@@ -108,6 +109,7 @@ class GradientAllreducer:
         self.flat = self._storage[:self.layout.n]
         self.views = [self.layout.view(self.flat, i) for i in range(len(self.params))]
         self._sinks: list = []
+        self._no_sync = False
 
     @property
     def nbytes(self) -> int:
@@ -135,6 +137,16 @@ class GradientAllreducer:
             m._state.grad_sink = sink
             self._sinks.append(sink)
         return self
+
+    @contextlib.contextmanager
+    def no_sync(self):
+        """Backward passes inside accumulate gradients without starting an
+        exchange (micro-batches before the last one of a step)."""
+        prev, self._no_sync = self._no_sync, True
+        try:
+            yield
+        finally:
+            self._no_sync = prev
 
     def _pack(self) -> list:
         """Copy gradients that are not already the buffer's views into it."""
@@ -366,13 +378,15 @@ class _GradSink:
             return None
         if layer.coeff_doj.grad is not None or (layer.bias is not None and layer.bias.grad is not None):
             return None  # accumulating over micro-batches: autograd adds to the existing .grad
-        if isinstance(red, PeerAllreducer) and red._peers is not None:
+        if isinstance(red, PeerAllreducer) and red._peers is not None and not red._no_sync:
             red._begin_backward()
         db = red.views[self.ib] if self.ib is not None else None
         return red.views[self.ic], db, self.event
 
     def done(self) -> None:
         red = self._reducer()
+        if red is None or red._no_sync:
+            return  # in place, but more micro-batches will add to it: exchanged at the step's call
         self.launched = True
         if isinstance(red, PeerAllreducer) and red._peers is not None:
             red._launch_layer(self)
