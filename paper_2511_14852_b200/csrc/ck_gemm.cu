@@ -42,9 +42,17 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   cuuint32_t box[3] = {static_cast<cuuint32_t>(mn_major ? 64 : bk), static_cast<cuuint32_t>(mn_major ? bk : box_rows),
                        1};
   cuuint32_t estr[3] = {1, 1, 1};
+  // L2 promotion of the TMA requests (CK_TMA_PROMO = 0 none, 1 64B, 2 128B, 3 256B; default 256B)
+  static const CUtensorMapL2promotion promo = [] {
+    const char* e = getenv("CK_TMA_PROMO");
+    const int v = e ? atoi(e) : 3;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                           : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(base), dims, strides, box,
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed with code " + std::to_string(static_cast<int>(r)));
     return kCudaError;
@@ -72,6 +80,20 @@ int gemm_group() {
     return v >= 1 && v <= 1024 ? v : 8;
   }();
   return g;
+}
+
+int gemm_pace() {
+  static int v = [] {
+    const char* e = getenv("CK_GEMM_PACE");
+    const int n = e ? atoi(e) : 0;
+    return n > 0 ? n : 0;
+  }();
+  return v;
+}
+
+uint32_t next_pace_tag() {
+  static std::atomic<uint32_t> tag{0};
+  return tag.fetch_add(1) + 1;  // never 0 (the zero-initialised table)
 }
 
 int gemm_seg() {

@@ -45,7 +45,15 @@ int gen_max_o() {
 // (d >= 4) and the reduction is long enough to amortise the fill (d*I >=
 // 1536); below that the materialised planes are as fast or faster.
 // CK_GEN=all drops the degree / length rule (tests).
-constexpr int kGenMaxChain = 8192;  // reduction terms
+// longest reduction (terms) the generated forward takes (CK_GEN_MAX_CHAIN
+// overrides it for timing experiments; results past it are less accurate)
+int gen_max_chain() {
+  static int v = [] {
+    const char* e = getenv("CK_GEN_MAX_CHAIN");
+    return e ? atoi(e) : 8192;
+  }();
+  return v;
+}
 
 bool gen_layer(int I, int O, int K) {
   static const bool all = [] {
@@ -59,7 +67,7 @@ bool gen_layer(int I, int O, int K) {
   // spare), so it is limited to reductions whose biased tensor-core
   // accumulation stays <= ~3e-5 normwise (8192 terms; ck_gemm_impl.cuh,
   // kSegIters); longer ones take expand + the segmented store GEMM
-  if (gen_chunks(I, d) * 64 > kGenMaxChain) return false;
+  if (gen_chunks(I, d) * 64 > gen_max_chain()) return false;
   return all || (d >= 4 && static_cast<int64_t>(d) * I >= 1536);
 }
 

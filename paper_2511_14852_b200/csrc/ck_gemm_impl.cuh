@@ -40,6 +40,9 @@ int gemm_group();
 // pipeline iterations per accumulation segment of the store GEMMs
 // (kSegIters; CK_GEMM_SEG overrides, 0 = whole tile)
 int gemm_seg();
+// wave pacing (experiment, CK_GEMM_PACE = window in pipeline iterations, 0 off)
+int gemm_pace();
+uint32_t next_pace_tag();
 // Store-GEMM N tile: a multiple of 32 (64 per CTA for MN-major B slabs) <= BN
 // spreading N evenly over ceil(N/BN) tiles.
 inline int store_ntile(int64_t N, int BN, int CG, bool mn_major) {
@@ -95,7 +98,41 @@ struct KArgs {
   // store GEMMs: pipeline iterations accumulated in TMEM per segment before
   // the epilogue folds the segment into fp32 registers (0: whole tile)
   int seg_iters;
+  // wave pacing: units publish the window (pace_window iterations) they are
+  // in; a producer does not start window w until every unit of this launch
+  // reached w - pace_slack (0: off)
+  int pace_window, pace_slack;
+  uint32_t pace_tag;
 };
+
+// Per-unit progress of the paced GEMMs: (launch tag << 32) | window.  An
+// entry of another launch counts as "not started"; a unit that finished
+// writes window 0xffffffff.  Waits time out (pacing is an optimisation, never
+// a dependency), so concurrent GEMMs on other streams cannot deadlock.
+constexpr int kPaceSlots = 256;
+__device__ unsigned long long g_pace[kPaceSlots];
+
+__device__ __forceinline__ void pace_publish(int unit, uint32_t tag, uint32_t w) {
+  *reinterpret_cast<volatile unsigned long long*>(&g_pace[unit]) = (static_cast<unsigned long long>(tag) << 32) | w;
+}
+
+__device__ __forceinline__ void pace_wait(int n_units, uint32_t tag, uint32_t need) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t lo = 0xffffffffu;
+    for (int u = 0; u < n_units; ++u) {
+      const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&g_pace[u]);
+      const uint32_t w = (static_cast<uint32_t>(e >> 32) == tag) ? static_cast<uint32_t>(e) : 0u;
+      lo = w < lo ? w : lo;
+    }
+    if (lo >= need) return;
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 200000ull) return;  // 200 us: give up pacing this window
+    __nanosleep(256);
+  }
+}
 
 // Accumulation segments.  The tensor core's fp32 accumulation of a long
 // reduction is biased (the error grows linearly with the chain: 1.06e-4
@@ -113,7 +150,13 @@ __host__ __device__ inline int seg_len(int seg_iters, int iters) { return seg_it
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
+// Warpgroup 0 = control warps (TMA producer, MMA issuer, TMEM allocator),
+// warpgroups 1-2 = epilogue.  The store epilogue keeps a row's 128 segment
+// sums in registers (kSegIters): the control warpgroup hands registers to
+// the epilogue warpgroups (setmaxnreg), 168 -> 56 / 224 per thread.
+constexpr int kThreads = 384;
+constexpr int kEpiWarp0 = 4;
+constexpr int kCtrlRegs = 56, kEpiRegs = 224;
 constexpr int kEpiWarps = 8;
 constexpr int kMaxDFused = 16;       // fused dX epilogue: degree <= 16
 
@@ -536,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) {
+  if (warp == 1) {
     if constexpr (CG == 2) {
       tmem_alloc_pair(tmem_slot, C::kTmemCols);
     } else {
@@ -554,6 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // everything above is CTA-local; operands and outputs are touched below
   pdl_wait();
 
+  if (warp < kEpiWarp0) {
+  reg_dealloc<kCtrlRegs>();  // (warpgroup-uniform)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
@@ -562,6 +607,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = unit; t < total; t += n_units) {
         const TileCoord tc = decode_tile(p, t, kBM * CG);
         for (int it = 0; it < tc.iters; ++it, ++g) {
+          if (p.pace_window > 0 && g % p.pace_window == 0) {
+            const uint32_t w = g / p.pace_window;
+            if (leader) pace_publish(unit, p.pace_tag, w);
+            if (w > static_cast<uint32_t>(p.pace_slack)) pace_wait(n_units, p.pace_tag, w - p.pace_slack);
+          }
           const int stage = g % STAGES;
           const uint32_t phase = (g / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -615,6 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.pace_window > 0 && leader) pace_publish(unit, p.pace_tag, 0xffffffffu);
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
@@ -686,9 +737,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
-    const int q = warp & 3;          // TMEM lane quarter this warp may access
-    const int h = (warp - 4) >> 2;   // which half of the tile's columns
+  }
+  } else {
+    reg_alloc<kEpiRegs>();
+    const int q = warp & 3;                  // TMEM lane quarter this warp may access
+    const int h = (warp - kEpiWarp0) >> 2;   // which half of the tile's columns
     uint32_t seg = 0;
     for (int t = unit; t < total; t += n_units) {
       const TileCoord tc = decode_tile(p, t, kBM * CG);
@@ -762,7 +815,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // see kSegIters).  Each drained buffer is released before the next
         // wait, so the MMAs of the following segment overlap the fold.
         constexpr int NCH = BN / 64;
-        uint32_t sums[NCH][32];
+        float sums[NCH][32];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sums[ch][e] = 0.0f;
         const int D = seg_len(p.seg_iters, tc.iters);
         const int nseg = (tc.iters + D - 1) / D;
         for (int j = 0; j < nseg; ++j, ++seg) {
@@ -770,21 +827,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&tfull[acc], use & 1);
           tc_fence_after();
           const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+          // every chunk of the buffer (columns past a narrow tile's n_tile
+          // are allocated and never stored), 16 columns per load
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {
-            const int c = 32 * h + 64 * ch;
-            if (c < p.n_tile) {
-              // 8 columns per load: the 128 sums + one load stay in registers
 #pragma unroll
-              for (int e0 = 0; e0 < 32; e0 += 8) {
-                uint32_t r[8];
-                tmem_ld_32x32b_x8(tbase + c + e0, r);
-                tmem_ld_wait();
+            for (int e0 = 0; e0 < 32; e0 += 16) {
+              uint32_t r[16];
+              tmem_ld_32x32b_x16(tbase + 32 * h + 64 * ch + e0, r);
+              tmem_ld_wait();
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  sums[ch][e0 + e] =
-                      j == 0 ? r[e] : __float_as_uint(__uint_as_float(sums[ch][e0 + e]) + __uint_as_float(r[e]));
-              }
+              for (int e = 0; e < 16; ++e) sums[ch][e0 + e] += __uint_as_float(r[e]);
             }
           }
           tc_fence_before();
@@ -801,7 +854,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      static_cast<long long>(tc.split) * p.out_split_stride;
         const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
         float* tile = reinterpret_cast<float*>(smem + STAGES * C::kStageBytes + C::kBarrierBytes) +
-                      (warp - 4) * (kEpiTileBytes / 4);
+                      (warp - kEpiWarp0) * (kEpiTileBytes / 4);
         const int row0 = tc.m0 + row_off + q * 32;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
@@ -816,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int e = 0; e < 32; ++e) {
                 const int n = nb + e;
                 if (n < p.N) {
-                  float o = __uint_as_float(sums[ch][e]);
+                  float o = sums[ch][e];
                   if (p.bias0) o += p.bias0[n];
                   if (p.bias1) o += p.bias1[n];
                   float* dst = out + static_cast<long long>(n) * p.ldo + row;
@@ -826,8 +879,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else {
-            store_chunk_coalesced(sums[ch], tile, lane, row0, p.M, nb, p.N, out, p.ldo, p.bias0, p.bias1,
-                                  p.accumulate, vec);
+            store_chunk_coalesced(reinterpret_cast<const uint32_t(&)[32]>(sums[ch]), tile, lane, row0, p.M, nb, p.N,
+                                  out, p.ldo, p.bias0, p.bias1, p.accumulate, vec);
           }
         }
       }
@@ -837,13 +890,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) {
     tc_fence_before();
     cluster_sync();  // no CTA leaves while its peer may still signal it
-    if (warp == 2) {
+    if (warp == 1) {
       tc_fence_after();
       tmem_dealloc_pair(tmem_base, C::kTmemCols);
     }
   } else {
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 1) {
       tc_fence_after();
       tmem_dealloc(tmem_base, C::kTmemCols);
     }
@@ -910,6 +963,9 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.bias1 = splits == 1 ? p.bias1 : nullptr;
   k.accumulate = accumulate;
   k.seg_iters = EPI == kEpiStore ? gemm_seg() : 0;
+  k.pace_window = gemm_pace();
+  k.pace_slack = 2;
+  k.pace_tag = k.pace_window > 0 ? next_pace_tag() : 0;
   k.out_trans = p.out_trans;
   auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM>;
   // store kernels: + a 4 KB staging tile per epilogue warp

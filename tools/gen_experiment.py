@@ -21,6 +21,9 @@ os.makedirs(out, exist_ok=True)
 shapes = [(16384, 256, 256, 3), (16384, 256, 256, 5), (16384, 256, 256, 8), (16384, 512, 256, 4),
           (16384, 1024, 256, 8), (16384, 256, 128, 3), (16384, 257, 200, 16), (65536, 256, 256, 3),
           (16384, 64, 256, 1), (16384, 4096, 256, 8), (1000, 100, 60, 7), (16384, 512, 512, 5)]
+if os.environ.get("GEN_WIDE"):
+    # the wide layers of C1 / C4 (16 and 8 N tiles)
+    shapes = [(16384, 4096, 4096, 8), (16384, 2048, 2048, 5), (16384, 4096, 4096, 3), (16384, 1024, 1024, 8)]
 for (b, i, o, d) in shapes:
     g = torch.Generator(device="cpu").manual_seed(b + i + o + d)
     x = (torch.rand(b, i, generator=g) * 3 - 1.5).to(dev)

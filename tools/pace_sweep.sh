@@ -1,0 +1,11 @@
+#!/bin/bash
+# DRAM traffic and time of the C4 GEMMs with wave pacing (CK_GEMM_PACE =
+# window in pipeline iterations; 0 = off).  gpurun_out/pace_w<W>.csv
+set -u
+mkdir -p gpurun_out
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sector_op_read_hit_rate.pct,sm__cycles_elapsed.avg.per_second"
+for W in "${@:-0 4 16 64}"; do
+  CK_GEMM_PACE=$W timeout 600 ncu --metrics "$M" --clock-control none -k regex:gemm_bf16x3 --launch-skip 3 --launch-count 3 \
+    --csv --log-file gpurun_out/pace_w$W.csv python tools/profile_step.py 32768 4096 4096 8 32768 > /dev/null 2>&1
+  echo "pace $W rc=$?"
+done
