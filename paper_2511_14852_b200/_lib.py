@@ -13,6 +13,8 @@ import pathlib
 import threading
 
 LIB_PATH = pathlib.Path(__file__).resolve().parent / "lib" / "libchebykan.so"
+if os.environ.get("CK_LIB_PATH"):  # A/B experiments with a variant build (tools/build_variant.py)
+    LIB_PATH = pathlib.Path(os.environ["CK_LIB_PATH"]).resolve()
 
 # ck_status codes (include/chebykan.h)
 CK_OK = 0

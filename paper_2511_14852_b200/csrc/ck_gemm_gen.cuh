@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(kGenThreads, 1)
             const uint64_t dal = umma_desc_kmajor<kRowBytes>(a_lo + kk * 32);
             const uint64_t dbh = umma_desc_kmajor<kRowBytes>(b_hi + kk * 32);
             const uint64_t dbl = umma_desc_kmajor<kRowBytes>(b_lo + kk * 32);
-            umma_bf16_pair(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
-            umma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);
+            umma_bf16_pair<kCollector>(d_tmem, dah, dbh, idesc, (it | kk) != 0 ? 1u : 0u);
+            umma_bf16_pair<kCollector ? 2 : 0>(d_tmem, dah, dbl, idesc, 1u);
             umma_bf16_pair(d_tmem, dal, dbh, idesc, 1u);
           }
           umma_commit_pair(&empty[stage]);

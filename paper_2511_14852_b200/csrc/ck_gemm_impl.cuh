@@ -145,6 +145,14 @@ __device__ __forceinline__ void pace_wait(int n_units, uint32_t tag, uint32_t ne
 // 32 it. 7.3e-6, +1-2 %; 64 it. 1.4e-5, +2 %; 128 it. 2.8e-5, +0-2 %;
 // whole tile 1.06e-4.
 constexpr int kSegIters = 32;
+
+// A-operand collector reuse across the hi*hi / hi*lo MMA pair (1 = on; see
+// umma_bf16_pair).  CK_BUILD_NO_COLLECTOR builds it off for comparison.
+#ifdef CK_BUILD_NO_COLLECTOR
+constexpr int kCollector = 0;
+#else
+constexpr int kCollector = 1;
+#endif
 __host__ __device__ inline int seg_len(int seg_iters, int iters) { return seg_iters > 0 ? seg_iters : iters; }
 
 namespace {
@@ -713,12 +721,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const uint32_t accum = ((it - s0) | kk) != 0 ? 1u : 0u;
             if constexpr (CG == 2) {
-              umma_bf16_pair(d_tmem, dah, dbh, idesc, accum);
-              umma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);
+              umma_bf16_pair<kCollector>(d_tmem, dah, dbh, idesc, accum);
+              umma_bf16_pair<kCollector ? 2 : 0>(d_tmem, dah, dbl, idesc, 1u);
               umma_bf16_pair(d_tmem, dal, dbh, idesc, 1u);
             } else {
-              umma_bf16(d_tmem, dah, dbh, idesc, accum);
-              umma_bf16(d_tmem, dah, dbl, idesc, 1u);
+              umma_bf16<kCollector>(d_tmem, dah, dbh, idesc, accum);
+              umma_bf16<kCollector ? 2 : 0>(d_tmem, dah, dbl, idesc, 1u);
               umma_bf16(d_tmem, dal, dbh, idesc, 1u);
             }
           }
