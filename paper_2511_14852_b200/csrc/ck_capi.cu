@@ -142,7 +142,7 @@ struct FwdLayout {
     ldI = L.ldI;
     const int d = K - 1;
     planes = 0;
-    split_elems = d > 0 ? gemm_split_ws_elems(chunk, O, 1, I) : 0;
+    split_elems = d > 0 ? gemm_split_ws_elems(chunk, O, 1, d * ceil_div(I, 64)) : 0;
     split = planes + L.per_chunk;
     total = split + align_up(sizeof(float) * split_elems) + kAlign;
   }
@@ -165,9 +165,9 @@ struct BwdLayout {
     fused_dx = dx_tile_inputs(static_cast<int>(d)) > 0;
     const size_t gb = fused_dx ? 0 : align_up(sizeof(float) * d * chunk * I);
     const size_t dbp = align_up(sizeof(double) * n_chunks * kDbSlots * O);
-    int64_t s1 = d > 0 ? gemm_split_ws_elems(chunk, I, static_cast<int>(d), O) : 0;
-    int64_t s2 = d > 0 ? gemm_split_ws_elems(O, I, static_cast<int>(d), chunk) : 0;
-    const int64_t s3 = d > 0 ? gemm_split_ws_elems(I, O, static_cast<int>(d), chunk) : 0;  // transposed dC
+    int64_t s1 = d > 0 ? gemm_split_ws_elems(chunk, I, static_cast<int>(d), ceil_div(O, 64)) : 0;
+    int64_t s2 = d > 0 ? gemm_split_ws_elems(O, I, static_cast<int>(d), ceil_div(chunk, 64)) : 0;
+    const int64_t s3 = d > 0 ? gemm_split_ws_elems(I, O, static_cast<int>(d), ceil_div(chunk, 64)) : 0;  // transposed dC
     if (s3 > s2) s2 = s3;
     split_elems = s1 > s2 ? s1 : s2;
     dy_hi = 0;

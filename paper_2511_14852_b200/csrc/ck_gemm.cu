@@ -146,11 +146,11 @@ StoreCfg pick_store(int64_t N) { return N <= 128 ? StoreCfg{128, 1} : StoreCfg{2
 // (1024^2, d5) ran as two rounds, the second 8 % full; 8 splits run 9 rounds
 // of 1/8 the length.  >= 4 K blocks per split, <= 64 splits, partials
 // <= 1.5 GB.
-int choose_splits(int64_t M, int64_t N, int nz, int64_t R, const StoreCfg& c, bool mn_major) {
+int choose_splits(int64_t M, int64_t N, int nz, int64_t kchunks, const StoreCfg& c, bool mn_major) {
   const int nt = store_ntile(N, c.bn, c.cg, mn_major);
   const int64_t tiles = ceil_div(M, static_cast<int64_t>(kBM) * c.cg) * ceil_div(N, nt) * nz;
   const int64_t units = num_sms() / c.cg;
-  const int64_t chunks = ceil_div(R, 64);
+  const int64_t chunks = kchunks;  // 64-wide K chunks over all segments
   const double t_it = 0.8e-6 * nt / 256.0 * (c.cg == 2 ? 1.0 : 0.5);
   const double out_bytes = 4.0 * static_cast<double>(nz) * static_cast<double>(M) * static_cast<double>(N);
   int64_t max_splits = chunks / 4 > 1 ? chunks / 4 : 1;
@@ -182,12 +182,12 @@ int forced_splits() {
   return v;
 }
 
-int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R) {
+int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t kchunks) {
   // the larger of the two operand majornesses' choices (the workspace is
   // sized before the caller knows which GEMM runs)
   int splits = forced_splits() > 0 ? forced_splits() : 1;
   for (bool mn : {false, true}) {
-    const int sp = choose_splits(M, N, nz, R, pick_store(N), mn);
+    const int sp = choose_splits(M, N, nz, kchunks, pick_store(N), mn);
     if (sp > splits) splits = sp;
   }
   return splits > 1 ? static_cast<int64_t>(splits) * nz * M * N : 0;
@@ -224,7 +224,7 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   CK_CHECK(p.a.rows < (1ll << 31) && p.b.rows < (1ll << 31), "gemm: extent too large");
   const bool mn = p.a.mn_major || p.b.mn_major;
   const StoreCfg cfg = pick_store(p.b.rows);
-  int splits = choose_splits(p.a.rows, p.b.rows, p.nz, p.R, cfg, mn);
+  int splits = choose_splits(p.a.rows, p.b.rows, p.nz, p.S * ceil_div(p.R, 64), cfg, mn);
   if (forced_splits() > 0) splits = forced_splits();  // experiments (CK_GEMM_SPLITS)
   const int64_t need = static_cast<int64_t>(splits) * p.nz * p.a.rows * p.b.rows;
   if (splits > 1 && (p.split_ws == nullptr || p.split_ws_elems < need)) splits = 1;

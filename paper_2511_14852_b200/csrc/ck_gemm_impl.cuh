@@ -192,7 +192,7 @@ constexpr int kDxmChord = 8;  // DXM offset of the chord-slope LUT epilogues
 // Tile decode shared by all roles (persistent static schedule: CTA c takes
 // tiles c, c + grid, ...; n fastest so co-resident CTAs share A rows in L2).
 struct TileCoord {
-  int n0, m0, z, split, c_begin, per_seg, iters;
+  int n0, m0, z, split, f_begin, iters;
 };
 
 // Grouped rasterisation: consecutive tiles walk kGroupM m-tiles for one n,
@@ -212,10 +212,11 @@ __device__ __forceinline__ TileCoord decode_tile(const KArgs& p, int t, int m_ti
   c.n0 = (rr / gm) * p.n_tile;
   c.z = zs / p.splits;
   c.split = zs % p.splits;
-  c.c_begin = static_cast<int>(static_cast<long long>(c.split) * p.r_chunks / p.splits);
-  const int c_end = static_cast<int>(static_cast<long long>(c.split + 1) * p.r_chunks / p.splits);
-  c.per_seg = c_end - c.c_begin;
-  c.iters = p.S * c.per_seg;
+  // reduction splits cut the flattened (segment, K chunk) iteration space
+  // into contiguous ranges (a split may cross segment boundaries)
+  const long long flat = static_cast<long long>(p.S) * p.r_chunks;
+  c.f_begin = static_cast<int>(static_cast<long long>(c.split) * flat / p.splits);
+  c.iters = static_cast<int>(static_cast<long long>(c.split + 1) * flat / p.splits) - c.f_begin;
   return c;
 }
 
@@ -624,8 +625,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t phase = (g / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * C::kStageBytes;
-          const int s = it / tc.per_seg;
-          const int r0 = (tc.c_begin + it % tc.per_seg) * BK;
+          const int f = tc.f_begin + it;
+          const int s = f / p.r_chunks;
+          const int r0 = (f - s * p.r_chunks) * BK;
           const int aseg = p.a_seg0 + s + p.a_seg_z * tc.z;
           const int bseg = p.b_seg0 + s + p.b_seg_z * tc.z;
           const int arow = tc.m0 + row_off;

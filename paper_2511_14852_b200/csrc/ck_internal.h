@@ -228,7 +228,8 @@ int gemm_gen_forward(const float* x, int64_t M, int I, int O, const LutView& v, 
                      const __nv_bfloat16* c_lo, const float* bias0, const float* bias1, float* y, cudaStream_t s);
 // Output cells a store GEMM computes, tile padding included (orientation choice).
 int64_t gemm_store_padded(int64_t M, int64_t N, bool mn_major);
-// Workspace (floats) the split-R path may want for this problem shape.
-int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t R);
+// Workspace (floats) the split-R path may want for this problem shape;
+// kchunks = 64-wide K chunks of the whole reduction (segments x ceil(R/64)).
+int64_t gemm_split_ws_elems(int64_t M, int64_t N, int nz, int64_t kchunks);
 
 }  // namespace ck

@@ -110,6 +110,9 @@ def test_c4_chunked_dc_equals_one_chunk_dc():
     (2048, 257, 512, 15, 32768, 11),   # C3 first layer (ragged I)
     (2048, 512, 512, 15, 32768, 12),   # C3 hidden layer
     (2048, 512, 257, 15, 32768, 13),   # C3 output layer (ragged O, transposed dC)
+    (128, 40, 256, 8, 32768, 14),      # paper configs (perf.py:137-143): few rows, reduction
+    (64, 256, 512, 15, 32768, 15),     # splits across the (segment, K chunk) space
+    (32, 512, 1024, 24, 32768, 16),    # d = 24: unfused dX
 ], ids=lambda s: "x".join(map(str, s[:4])))
 def test_reported_shapes_vs_oracle(shape):
     want = _oracle(*shape)
