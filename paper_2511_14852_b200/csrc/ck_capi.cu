@@ -363,10 +363,10 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
   }
   ck::PrepHeader h{ck::kPrepMagic, ck::kPrepVersion, d_in, d_out, n_feat, (L.skinny ? 1 : 0) | (L.gen ? 2 : 0),
                    static_cast<uint64_t>(ck_coeff_prep_bytes(d_in, d_out, n_feat))};
-  CK_TRY(ck::launch_prep_header(ck::at<void>(prep, L.hdr), h, s));
   if (L.skinny) {
-    CK_CUDA(cudaMemcpyAsync(ck::at<float>(prep, L.f32), coeff_doj, sizeof(float) * K * O * I, cudaMemcpyDeviceToDevice,
-                            s));
+    // the fp32 copy and the header in one launch
+    CK_TRY(ck::launch_copy_with_header(coeff_doj, ck::at<float>(prep, L.f32), K * O * I, ck::at<void>(prep, L.hdr), h,
+                                       s));
   } else {
     // DOJ copies: rows (k,o), unit stride in i
     CK_TRY(ck::launch_split_rows(coeff_doj, 1, K * O, I, 0, ck::at<__nv_bfloat16>(prep, L.doj_hi),
@@ -381,7 +381,7 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
                                         ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, I * L.ldO, s));
     }
     // k = 0 term: T_0 == 1 so its contribution is the per-output constant
-    CK_TRY(ck::launch_row_sum(coeff_doj, O, I, ck::at<float>(prep, L.c0sum), s));
+    CK_TRY(ck::launch_row_sum(coeff_doj, O, I, ck::at<float>(prep, L.c0sum), s, ck::at<void>(prep, L.hdr), &h));
     if (L.gen) {
       CK_TRY(ck::launch_gen_coeff(coeff_doj, d_in, d_out, n_feat - 1, ck::at<__nv_bfloat16>(prep, L.gen_hi),
                                   ck::at<__nv_bfloat16>(prep, L.gen_lo), s));

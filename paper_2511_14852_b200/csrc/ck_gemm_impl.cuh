@@ -820,57 +820,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         // ------------- store epilogue -------------
-        // Fold the tile's accumulation segments into fp32 registers: this
-        // thread's row, columns 32 h + 64 ch + [0, 32) (round-to-nearest adds;
-        // see kSegIters).  Each drained buffer is released before the next
-        // wait, so the MMAs of the following segment overlap the fold.
-        constexpr int NCH = BN / 64;
-        float sums[NCH][32];
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) sums[ch][e] = 0.0f;
-        const int D = seg_len(p.seg_iters, tc.iters);
-        const int nseg = (tc.iters + D - 1) / D;
-        for (int j = 0; j < nseg; ++j, ++seg) {
-          const uint32_t acc = seg & 1, use = seg >> 1;
-          mbar_wait(&tfull[acc], use & 1);
-          tc_fence_after();
-          const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-          // every chunk of the buffer (columns past a narrow tile's n_tile
-          // are allocated and never stored), 16 columns per load
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-#pragma unroll
-            for (int e0 = 0; e0 < 32; e0 += 16) {
-              uint32_t r[16];
-              tmem_ld_32x32b_x16(tbase + 32 * h + 64 * ch + e0, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 16; ++e) sums[ch][e0 + e] += __uint_as_float(r[e]);
-            }
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (CG == 2) {
-              mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits on it
-            } else {
-              mbar_arrive(&tempty[acc]);
-            }
-          }
-        }
         float* out = p.out + static_cast<long long>(tc.z) * p.out_z_stride +
                      static_cast<long long>(tc.split) * p.out_split_stride;
         const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
         float* tile = reinterpret_cast<float*>(smem + STAGES * C::kStageBytes + C::kBarrierBytes) +
                       (warp - kEpiWarp0) * (kEpiTileBytes / 4);
         const int row0 = tc.m0 + row_off + q * 32;
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          const int c = 32 * h + 64 * ch;  // 32-column chunks alternate between the quarter's two warps
+        // one 32-column chunk (this thread's row) to the output, + bias
+        auto store32 = [&](const uint32_t (&v)[32], int c) {
           const int nb = tc.n0 + c;
-          if (c >= p.n_tile || nb >= p.N) continue;
+          if (c >= p.n_tile || nb >= p.N) return;
           if (p.out_trans) {
             // transposed: column n of the tile is a row of the output; lanes
             // (= tile rows) are contiguous there, so each store is 128 bytes
@@ -879,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int e = 0; e < 32; ++e) {
                 const int n = nb + e;
                 if (n < p.N) {
-                  float o = sums[ch][e];
+                  float o = __uint_as_float(v[e]);
                   if (p.bias0) o += p.bias0[n];
                   if (p.bias1) o += p.bias1[n];
                   float* dst = out + static_cast<long long>(n) * p.ldo + row;
@@ -889,9 +848,72 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else {
-            store_chunk_coalesced(reinterpret_cast<const uint32_t(&)[32]>(sums[ch]), tile, lane, row0, p.M, nb, p.N,
-                                  out, p.ldo, p.bias0, p.bias1, p.accumulate, vec);
+            store_chunk_coalesced(v, tile, lane, row0, p.M, nb, p.N, out, p.ldo, p.bias0, p.bias1, p.accumulate, vec);
           }
+        };
+        auto release = [&](uint32_t acc) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) {
+              mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits on it
+            } else {
+              mbar_arrive(&tempty[acc]);
+            }
+          }
+        };
+        const int D = seg_len(p.seg_iters, tc.iters);
+        const int nseg = (tc.iters + D - 1) / D;
+        if (nseg == 1) {
+          // one segment: nothing to fold -- stream 32-column chunks from TMEM
+          // to the output (loads and stores interleaved; short-K tiles are
+          // epilogue-bound)
+          const uint32_t acc = seg & 1, use = seg >> 1;
+          ++seg;
+          mbar_wait(&tfull[acc], use & 1);
+          tc_fence_after();
+          const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+          for (int c = 32 * h; c < p.n_tile; c += 64) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tbase + c, r);
+            tmem_ld_wait();
+            store32(r, c);
+          }
+          release(acc);
+        } else {
+          // Fold the tile's accumulation segments into fp32 registers: this
+          // thread's row, columns 32 h + 64 ch + [0, 32) (round-to-nearest
+          // adds; see kSegIters).  Each drained buffer is released before the
+          // next wait, so the MMAs of the following segment overlap the fold.
+          constexpr int NCH = BN / 64;
+          float sums[NCH][32];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) sums[ch][e] = 0.0f;
+          for (int j = 0; j < nseg; ++j, ++seg) {
+            const uint32_t acc = seg & 1, use = seg >> 1;
+            mbar_wait(&tfull[acc], use & 1);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+            // every chunk of the buffer (columns past a narrow tile's n_tile
+            // are allocated and never stored), 16 columns per load
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) {
+#pragma unroll
+              for (int e0 = 0; e0 < 32; e0 += 16) {
+                uint32_t r[16];
+                tmem_ld_32x32b_x16(tbase + 32 * h + 64 * ch + e0, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) sums[ch][e0 + e] += __uint_as_float(r[e]);
+              }
+            }
+            release(acc);
+          }
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) store32(reinterpret_cast<const uint32_t(&)[32]>(sums[ch]), 32 * h + 64 * ch);
         }
       }
     }

@@ -119,7 +119,8 @@ int launch_split_transpose(const float* in, int64_t nz, int64_t rows, int64_t co
 int launch_split_transpose_stacked(const float* c_doj, int64_t K, int64_t O, int64_t I, int n_i, __nv_bfloat16* hi,
                                    __nv_bfloat16* lo, int64_t ld, cudaStream_t s);
 // out[r] = sum_c in[r][c]  (float64 accumulation in a fixed order)
-int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s);
+int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s, void* hdr = nullptr,
+                   const struct PrepHeader* h = nullptr);
 // part[slot][c] = sum over rows of in[rows][cols]  (float64, fixed order)
 int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part, int slots,
                        cudaStream_t s);
@@ -147,7 +148,8 @@ struct PrepHeader {
 };
 constexpr uint32_t kPrepMagic = 0x52504b43u;  // "CKPR"
 constexpr uint32_t kPrepVersion = 2;
-int launch_prep_header(void* dst, const PrepHeader& h, cudaStream_t s);
+// out[0..n) = in[0..n) and the prep header, one launch
+int launch_copy_with_header(const float* in, float* out, int64_t n, void* hdr, const PrepHeader& h, cudaStream_t s);
 
 // --- skinny-output layers (ck_skinny.cu) ----------------------------------
 // d_out <= 8 with n_feat * round_up_pow2(d_out) <= 32: CUDA-core kernels on

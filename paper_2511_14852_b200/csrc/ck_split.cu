@@ -170,8 +170,10 @@ __global__ void split_transpose_stacked_kernel(const float* __restrict__ c, int6
 }
 
 // one warp per row, float64 lane partials combined by a fixed shuffle tree
-__global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, float* __restrict__ out) {
+__global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, float* __restrict__ out,
+                               PrepHeader* hdr, PrepHeader h) {
   pdl_wait();
+  if (hdr != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *hdr = h;  // (coefficient prep: same launch)
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -184,9 +186,18 @@ __global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64
   }
 }
 
-__global__ void prep_header_kernel(PrepHeader* dst, PrepHeader h) {
+// fp32 copy of the coefficients (skinny layers' prep) plus the prep header
+__global__ void copy_header_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n, PrepHeader* hdr,
+                                   PrepHeader h) {
   pdl_wait();
-  *dst = h;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *hdr = h;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t e = t0; e < n4; e += stride)
+    reinterpret_cast<float4*>(out)[e] = reinterpret_cast<const float4*>(in)[e];
+  for (int64_t e = 4 * n4 + t0; e < n; e += stride) out[e] = in[e];
 }
 
 // part[s][c] = sum of rows [s*chunk, min((s+1)*chunk, rows)) of column c
@@ -342,17 +353,20 @@ int launch_split_transpose_stacked(const float* c_doj, int64_t K, int64_t O, int
   return kOk;
 }
 
-int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s) {
+int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cudaStream_t s, void* hdr,
+                   const PrepHeader* h) {
   if (rows == 0) return kOk;
   LaunchScope scope(kKReduce, s);
-  CK_CUDA(launch_k((row_sum_kernel), blocks_for(rows * 32), kThreads, 0, s, in, rows, cols, out));
+  CK_CUDA(launch_k((row_sum_kernel), blocks_for(rows * 32), kThreads, 0, s, in, rows, cols, out,
+                   static_cast<PrepHeader*>(hdr), h ? *h : PrepHeader{}));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
 
-int launch_prep_header(void* dst, const PrepHeader& h, cudaStream_t s) {
+int launch_copy_with_header(const float* in, float* out, int64_t n, void* hdr, const PrepHeader& h, cudaStream_t s) {
   LaunchScope scope(kKSplit, s);
-  CK_CUDA(launch_k((prep_header_kernel), 1, 1, 0, s, static_cast<PrepHeader*>(dst), h));
+  CK_CUDA(launch_k((copy_header_kernel), blocks_for(n / 4 > 0 ? n / 4 : 1), kThreads, 0, s, in, out, n,
+                   static_cast<PrepHeader*>(hdr), h));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }

@@ -166,3 +166,30 @@ def test_c4_full_batch_properties():
     # db: float64 column sums
     want_db = dy.double().sum(0)
     assert float((db_full.double() - want_db).abs().max() / want_db.abs().max()) <= 1e-6
+
+
+def test_c4_full_batch_rank1_dc():
+    """dC at the full bench batch (262144 rows = 8 accumulated 32768-row
+    chunks) for a rank-1 dy[b, o] = u[b]: every output row of dC equals
+    sum_b u_b B_k(x_bi), a matrix-vector product computed here in float64
+    from the expansion kernel's basis values (ck_expand, pinned to the
+    reference's interp_rows by test_expand_matches_reference_interp)."""
+    b_full, chunk = 262144, 32768
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(123)
+    x = torch.rand(b_full, 4096, device=dev, generator=g) * 3 - 1.5
+    u = torch.randn(b_full, device=dev, generator=g)
+    layer = ck.ChebyKANLayer(4096, 4096, 8, lut_size=32768).to(dev)
+    layer(x).backward(u[:, None].expand(b_full, 4096).contiguous())
+    dc = layer.coeff_doj.grad  # [9, 4096, 4096]
+    table = ck.lut_build(ck.BasisKind.CHEBYSHEV, 8, 32768, device=dev)
+    ref = torch.zeros(9, 4096, dtype=torch.float64, device=dev)
+    for r0 in range(0, b_full, chunk):
+        phi = ck.expand(x[r0:r0 + chunk], table)  # [rows, 4096, 9] fp32
+        ref += torch.einsum("b,bik->ki", u[r0:r0 + chunk].double(), phi.double())
+        del phi
+    err = float((dc.double() - ref[:, None, :]).abs().amax() / ref.abs().amax())
+    spread = float((dc - dc[:, :1, :]).abs().amax() / dc.abs().amax())
+    print("C4 full batch rank-1 dC", f"{err:.2e}", "row spread", f"{spread:.2e}")
+    assert err <= TOL
+    assert spread <= 1e-6  # every output row of dC is the same reduction
