@@ -52,7 +52,7 @@ struct PrepLayout {
     ldI = round_up(I, 8);
     ldO = round_up(O, 8);
     const int d = K - 1;
-    n_i = dx_tile_inputs(d);
+    n_i = dx_tile_inputs(d, I);
     dxb_rows = n_i > 0 ? ceil_div(I, n_i) * d * n_i : static_cast<int64_t>(K) * I;
     const size_t doj = align_up(sizeof(__nv_bfloat16) * K * O * ldI);
     const size_t dxb = align_up(sizeof(__nv_bfloat16) * dxb_rows * ldO);
@@ -162,7 +162,7 @@ struct BwdLayout {
     ldO = round_up(O, 8);
     const int64_t d = K - 1;
     const size_t dy = align_up(sizeof(__nv_bfloat16) * chunk * ldO);
-    fused_dx = dx_tile_inputs(static_cast<int>(d)) > 0;
+    fused_dx = dx_tile_inputs(static_cast<int>(d), I) > 0;
     const size_t gb = fused_dx ? 0 : align_up(sizeof(float) * d * chunk * I);
     const size_t dbp = align_up(sizeof(double) * n_chunks * kDbSlots * O);
     int64_t s1 = d > 0 ? gemm_split_ws_elems(chunk, I, static_cast<int>(d), ceil_div(O, 64)) : 0;

@@ -199,18 +199,30 @@ int64_t gemm_store_padded(int64_t M, int64_t N, bool mn_major) {
   return ceil_div(M, static_cast<int64_t>(kBM) * c.cg) * kBM * c.cg * (ceil_div(N, nt) * nt);
 }
 
-int dx_tile_inputs(int d) {
+// Inputs per stacked dX tile: a multiple of 8 with d * n_i <= 256 (one MMA,
+// a multiple of 16) chosen for the layer width -- the fewest padded columns
+// plus a per-tile overhead of 8 columns (I = 256, d = 3: 4 tiles of 64, not
+// 4 x 80 with a 16-wide last tile; I = 512, d = 5: 11 x 48).
+int dx_tile_inputs(int d, int64_t I) {
   if (d < 1 || d > kMaxDFused) return 0;
-  for (int n_i = (256 / d) / 8 * 8; n_i >= 8; n_i -= 8)
-    if ((d * n_i) % 16 == 0 && d * n_i <= 256) return n_i;
-  return 0;
+  int best = 0;
+  int64_t best_cost = 0;
+  for (int n_i = (256 / d) / 8 * 8; n_i >= 8; n_i -= 8) {
+    if ((d * n_i) % 16 != 0 || d * n_i > 256) continue;
+    const int64_t cost = ceil_div(I, n_i) * (n_i + 8);
+    if (best == 0 || cost < best_cost) {
+      best = n_i;
+      best_cost = cost;
+    }
+  }
+  return best;
 }
 
 int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   CK_CHECK(p.S >= 1 && p.nz >= 1 && p.R >= 1, "gemm: empty reduction");
   if (p.dx != nullptr) {
     // fused dX: B = d stacked boxes (S = d features), N = cols of dx
-    CK_CHECK(p.nz == 1 && p.dx->n_i == dx_tile_inputs(p.S), "gemm: bad fused-dx configuration");
+    CK_CHECK(p.nz == 1 && p.dx->n_i == dx_tile_inputs(p.S, p.dx->cols), "gemm: bad fused-dx configuration");
     if (p.dx->lut.exact) return launch_dx_exact(p, s);
     const bool bk64 = gemm_bk() == 64;
     if (dx_chord() && bk64 && gemm_cg() == 2 && chord_kind(p.dx->lut.kind)) return launch_dx_chord(p, s);

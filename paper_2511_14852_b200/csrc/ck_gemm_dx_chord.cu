@@ -5,14 +5,29 @@
 
 namespace ck {
 
+// epilogue warps of the chord-slope dX GEMM: 16 (default) or 8 (CK_DX_EW=8)
+int dx_epi_warps() {
+  static int v = [] {
+    const char* e = getenv("CK_DX_EW");
+    return (e && std::string(e) == "8") ? 8 : 16;
+  }();
+  return v;
+}
+
+template <int KIND>
+int launch_chord(const GemmProblem& p, cudaStream_t s) {
+  if (dx_epi_warps() == 16) return launch<256, 64, 3, kEpiDx, 2, 0, 0, kDxmChord + KIND, 16>(p, 1, nullptr, 0, 0, s);
+  return launch<256, 64, 3, kEpiDx, 2, 0, 0, kDxmChord + KIND, 8>(p, 1, nullptr, 0, 0, s);
+}
+
 int launch_dx_chord(const GemmProblem& p, cudaStream_t s) {
   switch (p.dx->lut.kind) {
     case kCheb:
-      return launch<256, 64, 3, kEpiDx, 2, 0, 0, kDxmChord + kCheb>(p, 1, nullptr, 0, 0, s);
+      return launch_chord<kCheb>(p, s);
     case kLegendre:
-      return launch<256, 64, 3, kEpiDx, 2, 0, 0, kDxmChord + kLegendre>(p, 1, nullptr, 0, 0, s);
+      return launch_chord<kLegendre>(p, s);
     case kHermite:
-      return launch<256, 64, 3, kEpiDx, 2, 0, 0, kDxmChord + kHermite>(p, 1, nullptr, 0, 0, s);
+      return launch_chord<kHermite>(p, s);
     default:
       set_error("gemm: no chord-slope epilogue for this basis kind");
       return kUnsupported;

@@ -166,6 +166,23 @@ constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
 constexpr int kCtrlRegs = 56, kEpiRegs = 224;
 constexpr int kEpiWarps = 8;
+// Input-gradient kernels may run EW = 16 epilogue warps (640 threads, 112
+// registers each): the fused dX fold of a short-K tile is latency-bound at
+// two epilogue warps per scheduler (ncu: 9 cycles per issued instruction,
+// tensor pipe 28 % active at 256^2 d3), so four per scheduler overlap twice
+// the gathers / tanh chains.  The store epilogue keeps 8 warps (its segment
+// fold holds 128 running sums per thread).
+__host__ __device__ constexpr int gemm_threads(int ew) { return 128 + 32 * ew; }
+// setmaxnreg moves registers within the CTA's launch allocation (threads x
+// the launch-bound register count, a multiple of 8): what the control warps
+// release is all the epilogue warps can take, or their setmaxnreg.inc waits
+// forever.  384 threads: 168 at launch -> 56 / 224; 640 threads: 96 -> 56 / 104.
+__host__ __device__ constexpr int launch_regs(int threads) { return (65536 / threads) / 8 * 8 > 168 ? 168 : (65536 / threads) / 8 * 8; }
+__host__ __device__ constexpr int epi_regs(int ew) {
+  return (launch_regs(gemm_threads(ew)) * gemm_threads(ew) - 128 * kCtrlRegs) / (32 * ew) / 8 * 8;
+}
+static_assert(epi_regs(8) == kEpiRegs, "register budget (EW = 8)");
+static_assert(epi_regs(16) == 104, "register budget (EW = 16)");
 constexpr int kMaxDFused = 16;       // fused dX epilogue: degree <= 16
 
 // BK = reduction elements per pipeline stage: 64 (128-byte rows, SWIZZLE_128B)
@@ -270,7 +287,7 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[W]) {
 // the exact reference cell without float64 work.  Then fold with the d
 // accumulators and apply the Jacobian.  (Each gather is one L1 wavefront per
 // lane: the load count, not the bytes, bounds short-K tiles.)
-template <int D>
+template <int D, int NH = 2>
 __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok, int h) {
   constexpr int K = DxBlock<D>::K, S = DxBlock<D>::S, NS = DxBlock<D>::NS, W = DxBlock<D>::W;
   const int n_i = p.n_tile, N = p.lutN;
@@ -283,7 +300,7 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
   float xv[W];
   if (cb < n_i) dx_load_x(p, xr, row_ok, n0 + cb, xv);
 #pragma unroll 1
-  for (; cb < n_i; cb += 2 * W) {
+  for (; cb < n_i; cb += NH * W) {
     uint32_t r[D][W];
 #pragma unroll
     for (int k = 0; k < D; ++k) tmem_ld_cols<W>(tbase + k * n_i + cb, r[k]);
@@ -304,7 +321,7 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
 #pragma unroll
       for (int j = 0; j < NS; ++j) sl[e][j] = __ldg(rows4 + static_cast<long long>(c) * (S / 4) + j);
     }
-    if (cb + 2 * W < n_i) dx_load_x(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
+    if (cb + NH * W < n_i) dx_load_x(p, xr, row_ok, n0 + cb + NH * W, xv);  // next block's x
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       if (near[e]) {
@@ -352,40 +369,43 @@ __device__ __forceinline__ void dx_epilogue(const KArgs& p, uint32_t tbase, int 
 // slopes from chord_slopes at its float32 grid nodes -- the node recomputation
 // the expansion kernels use for the values (DESIGN decision 2).  No per-element
 // table gather: short-K dX tiles were bound by that gather's L2 round trip.
-template <int KIND, int D>
+template <int KIND, int D, int NH = 2>
 __device__ __forceinline__ void dx_epilogue_chord(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok,
                                                   int h) {
-  // no slope registers to hold: 8 columns per block up to d = 8
-  constexpr int K = DxBlock<D>::K, S = DxBlock<D>::S, W = D <= 8 ? 8 : 4;
+  // no slope registers to hold: 8 columns per block up to d = 8 (d = 4 with
+  // the 112-register budget of 16 epilogue warps)
+  constexpr int K = DxBlock<D>::K, S = DxBlock<D>::S, W = D <= (NH > 2 ? 4 : 8) ? 8 : 4;
   const int n_i = p.n_tile, N = p.lutN;
   const float* xr = p.x + static_cast<long long>(row) * p.ldo;
   float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
   const bool vec = ((p.ldo & 3) == 0);
   const float hN = 0.5f * static_cast<float>(N - 1);
   const float stepf = 2.0f / static_cast<float>(N - 1);
+  // columns past d_in (a ragged last tile) are skipped, not folded
+  const int n_lim = min(n_i, p.N - n0);
   int cb = W * h;
   float xv[W];
-  if (cb < n_i) dx_load_x(p, xr, row_ok, n0 + cb, xv);
+  if (cb < n_lim) dx_load_x(p, xr, row_ok, n0 + cb, xv);
 #pragma unroll 1
-  for (; cb < n_i; cb += 2 * W) {
+  for (; cb < n_lim; cb += NH * W) {
     uint32_t r[D][W];
 #pragma unroll
     for (int k = 0; k < D; ++k) tmem_ld_cols<W>(tbase + k * n_i + cb, r[k]);
-    float x_cur[W], t[W];
+    float x_cur[W], jac[W];
     int cell[W];
     bool near[W];
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       x_cur[e] = xv[e];
-      const float tt = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
-      t[e] = tt;
+      float tt;
+      tanh_jac(xv[e], tt, jac[e]);
       const float pos = fmaf(tt, hN, hN);
       const int c = min(static_cast<int>(pos), N - 2);
       const float fr = pos - static_cast<float>(c);
       cell[e] = c;
       near[e] = fr < p.guard || fr > 1.0f - p.guard;
     }
-    if (cb + 2 * W < n_i) dx_load_x(p, xr, row_ok, n0 + cb + 2 * W, xv);  // next block's x
+    if (cb + NH * W < n_lim) dx_load_x(p, xr, row_ok, n0 + cb + NH * W, xv);  // next block's x
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       if (near[e]) {
@@ -404,7 +424,7 @@ __device__ __forceinline__ void dx_epilogue_chord(const KArgs& p, uint32_t tbase
       float a = 0.0f;
 #pragma unroll
       for (int k = 0; k < D; ++k) a = fmaf(sl[k], __uint_as_float(r[k][e]), a);
-      acc[e] = p.jacobian ? a * (1.0f - t[e] * t[e]) : a;
+      acc[e] = p.jacobian ? a * jac[e] : a;
     }
     const int i0 = n0 + cb;
     if (row_ok) {
@@ -426,7 +446,7 @@ __device__ __forceinline__ void dx_epilogue_chord(const KArgs& p, uint32_t tbase
 // slopes are the analytic derivatives derivative_rows(kind, t)
 // (basis.py:155-204, kernels.py:224) at float32 t = tanh(x), recomputed in
 // registers; no table and no cell.
-template <int KIND, int D>
+template <int KIND, int D, int NH = 2>
 __device__ __forceinline__ void dx_epilogue_exact(const KArgs& p, uint32_t tbase, int n0, int row, bool row_ok,
                                                   int h) {
   constexpr int W = D <= 8 ? 4 : 2;
@@ -435,7 +455,7 @@ __device__ __forceinline__ void dx_epilogue_exact(const KArgs& p, uint32_t tbase
   float* dxr = p.dx + static_cast<long long>(row) * p.ldo;
   const bool vec = ((p.ldo & 3) == 0);
 #pragma unroll 1
-  for (int cb = W * h; cb < n_i; cb += 2 * W) {
+  for (int cb = W * h; cb < n_i; cb += NH * W) {
     uint32_t r[D][W];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -550,8 +570,8 @@ __device__ __forceinline__ void store_chunk_coalesced(const uint32_t (&r)[32], f
 // DXM: input-gradient epilogue flavour -- 0 = LUT slopes gathered from the
 // dX rows (exact reference cell), 1 + kind = analytic derivatives of that
 // basis kind (exact mode), kDxmChord + kind = LUT slopes recomputed as chords.
-template <int BN, int BK, int STAGES, int EPI, int CG, int AMN, int BMN, int DXM = 0>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int BK, int STAGES, int EPI, int CG, int AMN, int BMN, int DXM = 0, int EW = kEpiWarps>
+__global__ void __launch_bounds__(gemm_threads(EW), 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                        const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                        const KArgs p) {
@@ -584,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], CG * kEpiWarps);  // one arrive per epilogue warp (of both CTAs)
+      mbar_init(&tempty[a], CG * EW);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
@@ -749,7 +769,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   } else {
-    reg_alloc<kEpiRegs>();
+    static_assert(EW == kEpiWarps || EPI == kEpiDx, "the store epilogue runs 8 warps");
+    reg_alloc<epi_regs(EW)>();
     const int q = warp & 3;                  // TMEM lane quarter this warp may access
     const int h = (warp - kEpiWarp0) >> 2;   // which half of the tile's columns
     uint32_t seg = 0;
@@ -769,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           switch (p.b_boxes) {
 #define CK_DX_CASE(D) \
   case D:             \
-    dx_epilogue<D>(p, tbase, tc.n0, row, row_ok, h); \
+    dx_epilogue<D, EW / 4>(p, tbase, tc.n0, row, row_ok, h); \
     break;
             CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
             CK_DX_CASE(8) CK_DX_CASE(9) CK_DX_CASE(10) CK_DX_CASE(11) CK_DX_CASE(12) CK_DX_CASE(13)
@@ -783,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           switch (p.b_boxes) {
 #define CK_DX_CASE(D)                                            \
   case D:                                                        \
-    dx_epilogue_chord<KIND, D>(p, tbase, tc.n0, row, row_ok, h); \
+    dx_epilogue_chord<KIND, D, EW / 4>(p, tbase, tc.n0, row, row_ok, h); \
     break;
             CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
             CK_DX_CASE(8) CK_DX_CASE(9) CK_DX_CASE(10) CK_DX_CASE(11) CK_DX_CASE(12) CK_DX_CASE(13)
@@ -798,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define CK_DX_CASE(D)                                                   \
   case D:                                                               \
     if constexpr (KIND != kFourier || D % 2 == 0) {                     \
-      dx_epilogue_exact<KIND, D>(p, tbase, tc.n0, row, row_ok, h);      \
+      dx_epilogue_exact<KIND, D, EW / 4>(p, tbase, tc.n0, row, row_ok, h); \
     }                                                                   \
     break;
             CK_DX_CASE(1) CK_DX_CASE(2) CK_DX_CASE(3) CK_DX_CASE(4) CK_DX_CASE(5) CK_DX_CASE(6) CK_DX_CASE(7)
@@ -938,7 +959,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ----------------------------------------------------------------------------
 // Host side: launch
 
-template <int BN, int BK, int STAGES, int EPI, int CG, int AMN = 0, int BMN = 0, int DXM = 0>
+template <int BN, int BK, int STAGES, int EPI, int CG, int AMN = 0, int BMN = 0, int DXM = 0, int EW = kEpiWarps>
 int launch(const GemmProblem& p, int splits, float* out, long long out_split_stride, int accumulate,
            cudaStream_t s) {
   static_assert(!(AMN || BMN) || BK == 64, "MN-major operands use 128-byte (BK = 64) K slabs");
@@ -999,7 +1020,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.pace_slack = 2;
   k.pace_tag = k.pace_window > 0 ? next_pace_tag() : 0;
   k.out_trans = p.out_trans;
-  auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM>;
+  auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM, EW>;
   // store kernels: + a 4 KB staging tile per epilogue warp
   constexpr int kSmem = C::kSmemBytes + (EPI == kEpiStore ? kEpiWarps * kEpiTileBytes : 0);
   static_assert(kSmem <= 232448, "smem budget");
@@ -1023,7 +1044,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   LaunchScope scope(p.kclass, s);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(units * CG));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(gemm_threads(EW));
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];

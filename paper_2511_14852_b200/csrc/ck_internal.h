@@ -147,7 +147,7 @@ struct PrepHeader {
   uint64_t bytes;     // ck_coeff_prep_bytes(d_in, d_out, n_feat)
 };
 constexpr uint32_t kPrepMagic = 0x52504b43u;  // "CKPR"
-constexpr uint32_t kPrepVersion = 2;
+constexpr uint32_t kPrepVersion = 3;  // 3: stacked dX tile width chosen per d_in
 // out[0..n) = in[0..n) and the prep header, one launch
 int launch_copy_with_header(const float* in, float* out, int64_t n, void* hdr, const PrepHeader& h, cudaStream_t s);
 
@@ -194,8 +194,8 @@ struct DxEpilogue {
   int64_t cols;        // I
   int n_i;             // inputs per N tile; the MMA N is d * n_i
 };
-// n_i for degree d, or 0 when the stacked layout does not fit one MMA.
-int dx_tile_inputs(int d);
+// n_i for degree d and I inputs, or 0 when the stacked layout does not fit one MMA.
+int dx_tile_inputs(int d, int64_t I);
 
 struct GemmProblem {
   GemmOperand a, b;

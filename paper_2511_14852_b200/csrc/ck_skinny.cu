@@ -295,6 +295,301 @@ __global__ void __launch_bounds__(256) skinny_bwd_kernel(const float* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// LUT-mode kernels of the three-term families (Chebyshev / Legendre /
+// Hermite): the hot skinny path (the tabular head [512 -> 1]).  The kernels
+// above spend ~115 (forward) / ~200 (backward) instructions per element
+// (runtime kind switch per element, C reloaded per element and feature, tanh
+// and both nodes' recurrences evaluated twice in the backward); these are
+// issue-bound, so the per-element work is cut to the minimum:
+//   forward : lanes own 4 consecutive inputs per 128-wide chunk (float4 x and
+//             C loads, one C load per 4 elements and feature), one recurrence
+//             per grid node, interpolate, dot;
+//   backward: one tanh; the exact reference cell as in the fused dX
+//             epilogue; ONE divided-difference recurrence over the cell
+//             gives the chord slopes S_k (dX) and the left node's values
+//             B_k(b), and the interpolated values follow as
+//             B_k(b) + f (a - b) S_k  (= lerp(B_k(b), B_k(a), f)).
+
+// S[k-1] = chord slope of feature k (k = 1..P) over [b, a] and vb[k] = B_k(b)
+// (k = 0..P): chord_slopes (ck_basis.cuh) extended by the last value.
+template <int KIND, int P>
+__device__ __forceinline__ void chord_and_values(float b, float a, float (&S)[P], float (&vb)[P + 1]) {
+  float pv = 1.0f, cv = KIND == kHermite ? 2.0f * b : b;  // B_0(b), B_1(b)
+  float sp = 0.0f, sc = KIND == kHermite ? 2.0f : 1.0f;   // S_0, S_1
+  vb[0] = 1.0f;
+  vb[1] = cv;
+  S[0] = sc;
+#pragma unroll
+  for (int k = 1; k < P; ++k) {
+    float sn, vn;
+    if constexpr (KIND == kCheb) {
+      sn = fmaf(2.0f * a, sc, fmaf(2.0f, cv, -sp));
+      vn = fmaf(2.0f * b, cv, -pv);
+    } else if constexpr (KIND == kLegendre) {
+      const float c2 = static_cast<float>(2 * k + 1), ck = static_cast<float>(k);
+      const float inv = 1.0f / static_cast<float>(k + 1);
+      sn = fmaf(c2, fmaf(a, sc, cv), -ck * sp) * inv;
+      vn = fmaf(c2 * b, cv, -ck * pv) * inv;
+    } else {
+      const float c2k = static_cast<float>(2 * k);
+      sn = fmaf(2.0f, fmaf(a, sc, cv), -c2k * sp);
+      vn = fmaf(2.0f * b, cv, -c2k * pv);
+    }
+    S[k] = sn;
+    vb[k + 1] = vn;
+    sp = sc;
+    sc = sn;
+    pv = cv;
+    cv = vn;
+  }
+}
+
+// x, 4 consecutive inputs i0..i0+3 of a row (zero past I); vec: 16-byte path
+__device__ __forceinline__ void load4(const float* p, int i0, int I, bool vec, float (&v)[4]) {
+  if (vec && i0 + 4 <= I) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p + i0));
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = i0 + e < I ? __ldg(p + i0 + e) : 0.0f;
+  }
+}
+
+template <int KIND, int O, int P>
+__device__ __forceinline__ void skinny_fwd_lut_rows(const float* __restrict__ x, int64_t rows, int I, int K,
+                                                    const float* __restrict__ c, const float* __restrict__ bias,
+                                                    int N, bool vec, float* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t plane = static_cast<int64_t>(O) * I;
+  const float hN = 0.5f * static_cast<float>(N - 1);
+  const float stepf = 2.0f / static_cast<float>(N - 1);
+  for (int64_t b = warp; b < rows; b += nwarps) {
+    float acc[O];
+#pragma unroll
+    for (int o = 0; o < O; ++o) acc[o] = 0.0f;
+    const float* xr = x + b * I;
+    for (int i0 = 4 * lane; i0 < I; i0 += 128) {
+      float xv[4];
+      load4(xr, i0, I, vec, xv);
+      float v[4][P + 1];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        // cell_f32 (the forward's float32 cell; values are continuous)
+        const float t = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
+        const int idx = min(static_cast<int>(fmaf(t, hN, hN)), N - 2);
+        const float f = fmaf(t, hN, hN - static_cast<float>(idx));
+        float v0[P + 1], v1[P + 1];
+        basis_f32<KIND, P>(grid_node_f(idx, N, stepf), v0);
+        basis_f32<KIND, P>(grid_node_f(idx + 1, N, stepf), v1);
+#pragma unroll
+        for (int k = 1; k <= P; ++k) v[e][k] = lerp_ref(v0[k], v1[k], f);
+        v[e][0] = i0 + e < I ? 1.0f : 0.0f;  // (padded inputs: zero coefficients below)
+      }
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        if (k < K) {
+#pragma unroll
+          for (int o = 0; o < O; ++o) {
+            float cv[4];
+            load4(c + k * plane + static_cast<int64_t>(o) * I, i0, I, vec, cv);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[o] = fmaf(v[e][k], cv[e], acc[o]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < O; ++o) {
+      float a = acc[o];
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) a += __shfl_xor_sync(0xffffffffu, a, s);
+      acc[o] = a;
+    }
+    if (lane < O) {
+      float out = acc[0];
+#pragma unroll
+      for (int o = 1; o < O; ++o)
+        if (lane == o) out = acc[o];
+      y[b * O + lane] = out + (bias ? bias[lane] : 0.0f);
+    }
+  }
+}
+
+template <int O, int P>
+__global__ void __launch_bounds__(256) skinny_fwd_lut_kernel(const float* __restrict__ x, int64_t rows, int I, int K,
+                                                             const float* __restrict__ c,
+                                                             const float* __restrict__ bias, LutView L, int vec,
+                                                             float* __restrict__ y) {
+  pdl_wait();
+  switch (L.kind) {  // uniform: one body runs
+    case kLegendre:
+      skinny_fwd_lut_rows<kLegendre, O, P>(x, rows, I, K, c, bias, L.N, vec != 0, y);
+      break;
+    case kHermite:
+      skinny_fwd_lut_rows<kHermite, O, P>(x, rows, I, K, c, bias, L.N, vec != 0, y);
+      break;
+    default:
+      skinny_fwd_lut_rows<kCheb, O, P>(x, rows, I, K, c, bias, L.N, vec != 0, y);
+      break;
+  }
+}
+
+template <int KIND, int O, int P>
+__device__ __forceinline__ void skinny_bwd_lut_body(const float* __restrict__ x, const float* __restrict__ dy,
+                                                    int64_t rows, int I, int K, const float* __restrict__ c,
+                                                    const LutView& L, int jacobian, int64_t rb,
+                                                    float* __restrict__ dx, float* __restrict__ part_c,
+                                                    double* __restrict__ part_b, float (*red)[(P + 1) * O][32],
+                                                    double (*redb)[O]) {
+  constexpr int KMAX = P + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.y * 32 + lane;
+  const bool col_ok = i < I;
+  const int ic = col_ok ? i : I - 1;
+  const int64_t plane = static_cast<int64_t>(O) * I;
+  const int N = L.N, S = dxrow_stride(K);
+  const float hN = 0.5f * static_cast<float>(N - 1);
+  const float stepf = 2.0f / static_cast<float>(N - 1);
+  const float guard = fminf(0.5f, fmaxf(1e-3f, 4e-7f * static_cast<float>(N)));
+  float cr[KMAX][O], acc[KMAX][O];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+    for (int o = 0; o < O; ++o) {
+      cr[k][o] = k < K ? __ldg(c + k * plane + static_cast<int64_t>(o) * I + ic) : 0.0f;
+      acc[k][o] = 0.0f;
+    }
+  double db[O];
+#pragma unroll
+  for (int o = 0; o < O; ++o) db[o] = 0.0;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rb;
+  const int64_t r1 = r0 + rb < rows ? r0 + rb : rows;
+  constexpr int R = KMAX * O <= 8 ? 4 : (KMAX * O <= 16 ? 2 : 1);  // rows in flight (register budget)
+  float xn[R], gn[R][O];
+  auto load_group = [&](int64_t bg) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int64_t b = bg + 8 * u;
+      const bool ok = b < r1;
+      xn[u] = ok ? __ldg(x + b * I + ic) : 0.0f;
+#pragma unroll
+      for (int o = 0; o < O; ++o) gn[u][o] = ok ? __ldg(dy + b * O + o) : 0.0f;
+    }
+  };
+  load_group(r0 + w);
+  for (int64_t bg = r0 + w; bg < r1; bg += 8 * R) {
+    float xg[R], g[R][O];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      xg[u] = xn[u];
+#pragma unroll
+      for (int o = 0; o < O; ++o) g[u][o] = gn[u][o];
+    }
+    load_group(bg + 8 * R);
+    if (blockIdx.y == 0 && lane == 0) {
+#pragma unroll
+      for (int u = 0; u < R; ++u)
+#pragma unroll
+        for (int o = 0; o < O; ++o) db[o] += static_cast<double>(g[u][o]);  // zero past r1
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int64_t b = bg + 8 * u;
+      if (b >= r1) break;
+      const float xv = xg[u];
+      float t, jac;
+      tanh_jac(xv, t, jac);
+      const float pos = fmaf(t, hN, hN);
+      int cell = min(static_cast<int>(pos), N - 2);
+      const float fr = pos - static_cast<float>(cell);
+      if (fr < guard || fr > 1.0f - guard) {
+        // exact reference cell b_c <= x < b_{c+1} (at most one step off)
+        const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
+        const float bl = __ldg(row + K - 1), bh = __ldg(row + K);
+        cell = min(cell + (xv < bl ? -1 : (xv < bh ? 0 : 1)), N - 2);  // x = +inf: N-2 as the reference
+      }
+      const float f = fmaf(t, hN, hN - static_cast<float>(cell));
+      const float nb = grid_node_f(cell, N, stepf), na = grid_node_f(cell + 1, N, stepf);
+      float sl[P], vb[P + 1];
+      chord_and_values<KIND, P>(nb, na, sl, vb);
+      const float fs = f * (na - nb);
+      float gx = 0.0f;
+#pragma unroll
+      for (int k = 1; k < KMAX; ++k) {
+        float gk = 0.0f;
+#pragma unroll
+        for (int o = 0; o < O; ++o) gk = fmaf(g[u][o], cr[k][o], gk);
+        gx = fmaf(sl[k - 1], gk, gx);
+      }
+#pragma unroll
+      for (int o = 0; o < O; ++o) acc[0][o] += g[u][o];
+#pragma unroll
+      for (int k = 1; k < KMAX; ++k) {
+        const float v = fmaf(fs, sl[k - 1], vb[k]);  // lerp(B_k(b), B_k(a), f)
+#pragma unroll
+        for (int o = 0; o < O; ++o) acc[k][o] = fmaf(g[u][o], v, acc[k][o]);
+      }
+      if (dx && col_ok) dx[b * I + i] = jacobian ? gx * jac : gx;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+    for (int o = 0; o < O; ++o) red[w][k * O + o][lane] = acc[k][o];
+  if (lane == 0) {
+#pragma unroll
+    for (int o = 0; o < O; ++o) redb[w][o] = db[o];
+  }
+  __syncthreads();
+  for (int e = w; e < K * O; e += 8) {  // fold the 8 warps in order
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += red[j][e][lane];
+    const int k = e / O, o = e - k * O;
+    if (col_ok) part_c[(static_cast<int64_t>(blockIdx.x) * K + k) * plane + static_cast<int64_t>(o) * I + i] = s;
+  }
+  if (blockIdx.y == 0 && threadIdx.x < O) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += redb[j][threadIdx.x];
+    part_b[static_cast<int64_t>(blockIdx.x) * O + threadIdx.x] = s;
+  }
+}
+
+template <int O, int P>
+__global__ void __launch_bounds__(256) skinny_bwd_lut_kernel(const float* __restrict__ x, const float* __restrict__ dy,
+                                                             int64_t rows, int I, int K, const float* __restrict__ c,
+                                                             LutView L, int jacobian, int64_t rb,
+                                                             float* __restrict__ dx, float* __restrict__ part_c,
+                                                             double* __restrict__ part_b) {
+  __shared__ float red[8][(P + 1) * O][32];
+  __shared__ double redb[8][O];
+  pdl_wait();
+  switch (L.kind) {
+    case kLegendre:
+      skinny_bwd_lut_body<kLegendre, O, P>(x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b, red, redb);
+      break;
+    case kHermite:
+      skinny_bwd_lut_body<kHermite, O, P>(x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b, red, redb);
+      break;
+    default:
+      skinny_bwd_lut_body<kCheb, O, P>(x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b, red, redb);
+      break;
+  }
+}
+
+// the LUT kernels above serve the three-term families; exact handles and
+// Fourier tables take the generic kernels
+bool skinny_lut_fast(const LutView& L) {
+  return !L.exact && (L.kind == kCheb || L.kind == kLegendre || L.kind == kHermite);
+}
+
 int round_o(int O) { return O <= 1 ? 1 : O <= 2 ? 2 : O <= 4 ? 4 : 8; }
 
 int skinny_p(int O, int K) {
@@ -317,9 +612,9 @@ int skinny_bwd_blocks_per_sm(int O, int K) {
   int n = 0;
 #define CK_OCC(OO, PP)                                                                           \
   if (O == OO && pm == PP) {                                                                     \
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, skinny_bwd_kernel<OO, PP>, 256, 0) != \
-        cudaSuccess)                                                                             \
-      n = 0;                                                                                     \
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, skinny_bwd_lut_kernel<OO, PP>, 256, 0) != \
+        cudaSuccess)                                                                                 \
+      n = 0;                                                                                         \
   } else
   CK_OCC(1, 1) CK_OCC(1, 2) CK_OCC(1, 3) CK_OCC(1, 5) CK_OCC(1, 6) CK_OCC(1, 7)
   CK_OCC(1, 4) CK_OCC(1, 8) CK_OCC(1, 16) CK_OCC(1, 32) CK_OCC(2, 4) CK_OCC(2, 8) CK_OCC(2, 16)
@@ -344,16 +639,30 @@ int launch_skinny_forward(const float* x, int64_t rows, int I, int O, const floa
   if (rows == 0) return kOk;
   const LutView L = view(lut);
   const int64_t want = ceil_div(rows * 32, 256);  // one warp per row
-  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
-  const int blocks = static_cast<int>(want < cap ? want : cap);
   const int K = L.K;
   LaunchScope scope(kKSkinny, s);
   // P: smallest of 4 / 8 / 16 / 32 with P + 1 >= K (even, as Fourier needs);
   // single-output heads get P = K - 1 exactly up to K = 9
   const int pm = skinny_p(O, K);
-#define CK_SK(OO, PP)                                                                              \
-  if (O == OO && pm == PP) {                                                                       \
-    CK_CUDA(launch_k((skinny_fwd_kernel<OO, PP>), blocks, 256, 0, s, x, rows, I, K, c, bias, L, y));                \
+  const bool fast = skinny_lut_fast(L);
+  // 16-byte x / C loads when every row and coefficient row starts aligned
+  const int vec = (I % 4 == 0) && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
+  // grid: one wave of resident blocks (grid-stride over rows)
+  auto blocks_for = [&](auto kernel) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+    const int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
+    return static_cast<int>(want < cap ? want : cap);
+  };
+#define CK_SK(OO, PP)                                                                                            \
+  if (O == OO && pm == PP) {                                                                                     \
+    if (fast) {                                                                                                  \
+      CK_CUDA(launch_k((skinny_fwd_lut_kernel<OO, PP>), blocks_for(skinny_fwd_lut_kernel<OO, PP>), 256, 0, s, x, \
+                       rows, I, K, c, bias, L, vec, y));                                                         \
+    } else {                                                                                                     \
+      CK_CUDA(launch_k((skinny_fwd_kernel<OO, PP>), blocks_for(skinny_fwd_kernel<OO, PP>), 256, 0, s, x, rows, I, \
+                       K, c, bias, L, y));                                                                       \
+    }                                                                                                            \
   } else
   CK_SK(1, 1) CK_SK(1, 2) CK_SK(1, 3) CK_SK(1, 5) CK_SK(1, 6) CK_SK(1, 7)
   CK_SK(1, 4) CK_SK(1, 8) CK_SK(1, 16) CK_SK(1, 32) CK_SK(2, 4) CK_SK(2, 8) CK_SK(2, 16)
@@ -381,7 +690,13 @@ int launch_skinny_backward(const float* x, const float* dy, int64_t rows, int I,
   const int pm = skinny_p(O, K);
 #define CK_SKB(OO, PP)                                                                                        \
   if (O == OO && pm == PP) {                                                                                  \
-    CK_CUDA(launch_k((skinny_bwd_kernel<OO, PP>), grid, 256, 0, s, x, dy, rows, I, K, c, L, jacobian, rb, dx, part_c, part_b)); \
+    if (skinny_lut_fast(L)) {                                                                                 \
+      CK_CUDA(launch_k((skinny_bwd_lut_kernel<OO, PP>), grid, 256, 0, s, x, dy, rows, I, K, c, L, jacobian, rb, dx, \
+                       part_c, part_b));                                                                      \
+    } else {                                                                                                  \
+      CK_CUDA(launch_k((skinny_bwd_kernel<OO, PP>), grid, 256, 0, s, x, dy, rows, I, K, c, L, jacobian, rb, dx, \
+                       part_c, part_b));                                                                      \
+    }                                                                                                         \
   } else
   CK_SKB(1, 1) CK_SKB(1, 2) CK_SKB(1, 3) CK_SKB(1, 5) CK_SKB(1, 6) CK_SKB(1, 7)
   CK_SKB(1, 4) CK_SKB(1, 8) CK_SKB(1, 16) CK_SKB(1, 32) CK_SKB(2, 4) CK_SKB(2, 8) CK_SKB(2, 16)
