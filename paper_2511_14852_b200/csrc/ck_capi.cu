@@ -123,7 +123,7 @@ struct BasisLayout {
     chunk = B < cr ? B : cr;
     if (chunk < 1) chunk = 1;
     n_chunks = ceil_div(B > 0 ? B : 1, chunk);
-    ldI = round_up(I, 8);
+    ldI = round_up(I, 16);  // 32-byte rows: whole-sector plane stores (I = 257: 2.5 -> 4.8 TB/s)
     plane = chunk * ldI;
     const int d = K - 1;
     half = align_up(sizeof(__nv_bfloat16) * (d > 0 ? d : 0) * plane);
@@ -159,7 +159,7 @@ struct BwdLayout {
     const BasisLayout L(B, I, K);
     chunk = L.chunk;
     n_chunks = L.n_chunks;
-    ldO = round_up(O, 8);
+    ldO = round_up(O, 16);  // 32-byte rows (whole-sector stores)
     const int64_t d = K - 1;
     const size_t dy = align_up(sizeof(__nv_bfloat16) * chunk * ldO);
     fused_dx = dx_tile_inputs(static_cast<int>(d), I) > 0;
@@ -367,6 +367,16 @@ extern "C" int ck_coeff_prepare(const float* coeff_doj, int d_in, int d_out, int
     // the fp32 copy and the header in one launch
     CK_TRY(ck::launch_copy_with_header(coeff_doj, ck::at<float>(prep, L.f32), K * O * I, ck::at<void>(prep, L.hdr), h,
                                        s));
+  } else if (L.n_i > 0) {
+    // DOJ copies, the stacked input-gradient operand, c0sum and the header: one launch
+    CK_TRY(ck::launch_prep_fused(coeff_doj, K, O, I, L.n_i, ck::at<__nv_bfloat16>(prep, L.doj_hi),
+                                 ck::at<__nv_bfloat16>(prep, L.doj_lo), L.ldI, ck::at<__nv_bfloat16>(prep, L.dxb_hi),
+                                 ck::at<__nv_bfloat16>(prep, L.dxb_lo), L.ldO, ck::at<float>(prep, L.c0sum),
+                                 ck::at<void>(prep, L.hdr), h, s));
+    if (L.gen) {
+      CK_TRY(ck::launch_gen_coeff(coeff_doj, d_in, d_out, n_feat - 1, ck::at<__nv_bfloat16>(prep, L.gen_hi),
+                                  ck::at<__nv_bfloat16>(prep, L.gen_lo), s));
+    }
   } else {
     // DOJ copies: rows (k,o), unit stride in i
     CK_TRY(ck::launch_split_rows(coeff_doj, 1, K * O, I, 0, ck::at<__nv_bfloat16>(prep, L.doj_hi),
@@ -545,8 +555,13 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
     CK_TRY(ck::launch_skinny_backward(x, dy, batch, d_in, d_out, ck::at<float>(const_cast<void*>(prep), P.f32), lut,
                                       include_tanh_jacobian, dx, part_c, part_b, SW.slots, s));
     // second stage: ordered slot merges (kernels.py:438-442 order semantics)
-    if (dc_doj) CK_TRY(ck::launch_merge(part_c, SW.slots, n, n, dc_doj, 0, s));
-    if (db) CK_TRY(ck::launch_col_finish(part_b, SW.slots, d_out, db, s));
+    // (db's ordered slot fold runs in the same launch as the dC merge)
+    const ck::ColFinishJob fin{part_b, SW.slots, d_out, db, nullptr, 0};
+    if (dc_doj) {
+      CK_TRY(ck::launch_merge(part_c, SW.slots, n, n, dc_doj, 0, s, db ? &fin : nullptr));
+    } else if (db) {
+      CK_TRY(ck::launch_col_finish(part_b, SW.slots, d_out, db, s));
+    }
     if (grads_ready != nullptr) CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
     return kOk;
   }
@@ -578,12 +593,17 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
   // db is needed for dC_0 as well; keep a private copy when the caller skips it
   const bool need_db = db != nullptr || dc_doj != nullptr;
 
-  bool db_done = false;
+  bool event_done = false;
+  // db, and dC_0 = db (T_0 == 1), from the row-block partials: one job, run
+  // by the last chunk's dC GEMM (inside its split merge launch when it
+  // splits) or on its own
+  float* dbo = db != nullptr ? db : ck::at<float>(workspace, W.db_tmp);
+  const ck::ColFinishJob fin_job{db_part, static_cast<int>(W.n_chunks * ck::kDbSlots), O, dbo, dc_doj, I};
+  bool db_done = !need_db;
   auto finish_db = [&]() -> int {
-    if (!need_db) return kOk;
-    float* dbo = db != nullptr ? db : ck::at<float>(workspace, W.db_tmp);
-    // db, and dC_0 = db (T_0 == 1) written by the same launch
-    CK_TRY(ck::launch_col_finish(db_part, static_cast<int>(W.n_chunks * ck::kDbSlots), O, dbo, s, dc_doj, I));
+    if (db_done) return kOk;
+    CK_TRY(ck::launch_col_finish(fin_job.part, fin_job.slots, O, dbo, s, dc_doj, I));
+    db_done = true;
     return kOk;
   };
   int64_t ci = 0;
@@ -677,7 +697,10 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
         gc.split_ws = split_ws;
         gc.split_ws_elems = W.split_elems;
         gc.kclass = ck::kKGemmDc;
+        const bool fold_db = !db_done && r0 + rows >= batch;  // the last chunk: db partials are complete
+        if (fold_db) gc.fin = &fin_job;
         CK_TRY(ck::gemm_bf16x3(gc, s));
+        if (fold_db) db_done = true;
       }
       return kOk;
     };
@@ -688,17 +711,15 @@ extern "C" int ck_backward(const float* x, const float* dy, int64_t batch, int d
       CK_TRY(run_dc());
       CK_TRY(finish_db());
       CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
-      db_done = true;
+      event_done = true;
       CK_TRY(run_dx());
     } else {
       CK_TRY(run_dx());
       CK_TRY(run_dc());
     }
   }
-  if (!db_done) {
-    CK_TRY(finish_db());
-    if (grads_ready != nullptr) CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
-  }
+  CK_TRY(finish_db());
+  if (grads_ready != nullptr && !event_done) CK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(grads_ready), s));
   return kOk;
 }
 

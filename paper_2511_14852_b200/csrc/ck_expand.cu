@@ -116,6 +116,23 @@ __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __r
   const int sq = static_cast<int>(stride - sr * quads);
   int64_t r = it0 / quads;
   int q = static_cast<int>(it0 - r * quads);
+  // x of the next item is loaded before this item is expanded: the loop was
+  // bound by the load latency at the occupancy the high-degree planes leave
+  // (ncu, 32000 x 257 d15: 71 % long-scoreboard stalls, 29 % issue)
+  auto load_x = [&](int64_t rr, int qq, float (&v4)[4]) {
+    if (rr >= rows) return;
+    const int cc = qq * 4;
+    const float* xr = x + rr * cols + cc;
+    if (vec) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xr));
+      v4[0] = v.x; v4[1] = v.y; v4[2] = v.z; v4[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v4[e] = cc + e < cols ? __ldg(xr + e) : 0.0f;
+    }
+  };
+  float xn[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  load_x(r, q, xn);
   for (; r < rows; r += sr, q += sq) {
     if (q >= quads) {
       q -= quads;
@@ -123,14 +140,15 @@ __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __r
       if (r >= rows) break;
     }
     const int c = q * 4;
-    const float* xr = x + r * cols + c;
-    float xv[4];
-    if (vec) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(xr));
-      xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) xv[e] = c + e < cols ? __ldg(xr + e) : 0.0f;
+    float xv[4] = {xn[0], xn[1], xn[2], xn[3]};
+    {
+      int64_t rn = r + sr;
+      int qn = q + sq;
+      if (qn >= quads) {
+        qn -= quads;
+        ++rn;
+      }
+      load_x(rn, qn, xn);
     }
     uint32_t h0[D], l0[D], h1[D], l1[D];
     {

@@ -278,10 +278,16 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
   }
   if (rc != kOk) return rc;
   if (splits > 1) {
-    CK_TRY(launch_merge(p.split_ws, splits, split_stride, split_stride, p.out, p.accumulate, s));
-    if (p.bias0 || p.bias1) {
+    const bool bias = p.bias0 || p.bias1;
+    CK_TRY(launch_merge(p.split_ws, splits, split_stride, split_stride, p.out, p.accumulate, s, bias ? nullptr : p.fin));
+    if (bias) {
       CK_TRY(launch_add_rows(p.out, p.nz * p.a.rows, p.b.rows, p.bias0, p.bias1, s));
     }
+    if (bias && p.fin) {
+      CK_TRY(launch_col_finish(p.fin->part, p.fin->slots, p.fin->cols, p.fin->out, s, p.fin->bcast, p.fin->bcast_cols));
+    }
+  } else if (p.fin) {
+    CK_TRY(launch_col_finish(p.fin->part, p.fin->slots, p.fin->cols, p.fin->out, s, p.fin->bcast, p.fin->bcast_cols));
   }
   return kOk;
 }

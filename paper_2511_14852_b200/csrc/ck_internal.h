@@ -129,9 +129,19 @@ int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part
 // bcast[c][0..bcast_cols) = out[c]
 int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s,
                       float* bcast = nullptr, int64_t bcast_cols = 0);
-// out[n] = (accumulate ? out[n] : 0) + sum_{s<S} partials[s * stride + n]
+// A col_finish (above) folded into another reduction launch.
+struct ColFinishJob {
+  const double* part;
+  int slots;
+  int64_t cols;
+  float* out;
+  float* bcast;        // nullable
+  int64_t bcast_cols;
+};
+// out[n] = (accumulate ? out[n] : 0) + sum_{s<S} partials[s * stride + n];
+// fin (nullable): a col_finish job run by extra blocks of the same launch
 int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate,
-                 cudaStream_t s);
+                 cudaStream_t s, const ColFinishJob* fin = nullptr);
 // out[r][c] = a[c] + b[c] (either nullable)
 int launch_fill_rows(float* out, int64_t rows, int64_t cols, const float* a, const float* b,
                      cudaStream_t s);
@@ -148,6 +158,12 @@ struct PrepHeader {
 };
 constexpr uint32_t kPrepMagic = 0x52504b43u;  // "CKPR"
 constexpr uint32_t kPrepVersion = 3;  // 3: stacked dX tile width chosen per d_in
+// The coefficient prep of a stacked-dX layer in one launch: DOJ hi/lo
+// [K][O][ldI], the stacked operand (see launch_split_transpose_stacked),
+// c0sum[o] = sum_i C[0][o][i] (float64, fixed order) and the header.
+int launch_prep_fused(const float* c_doj, int64_t K, int64_t O, int64_t I, int n_i, __nv_bfloat16* doj_hi,
+                      __nv_bfloat16* doj_lo, int64_t ldI, __nv_bfloat16* dxb_hi, __nv_bfloat16* dxb_lo, int64_t ldO,
+                      float* c0sum, void* hdr, const PrepHeader& h, cudaStream_t s);
 // out[0..n) = in[0..n) and the prep header, one launch
 int launch_copy_with_header(const float* in, float* out, int64_t n, void* hdr, const PrepHeader& h, cudaStream_t s);
 
@@ -213,6 +229,7 @@ struct GemmProblem {
   int kclass = kKGemmFwd;  // timing / counting class
   int out_trans = 0;       // 1: store out[z][n][m] (row pitch ldo) -- the transposed orientation
   const DxEpilogue* dx = nullptr;  // non-null: stacked-B fused dX path
+  const ColFinishJob* fin = nullptr;  // run after the GEMM (in its merge launch when it splits)
 };
 int gemm_bf16x3(const GemmProblem& p, cudaStream_t s);
 

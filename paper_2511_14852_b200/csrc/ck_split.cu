@@ -186,6 +186,72 @@ __global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64
   }
 }
 
+// The whole coefficient prep of a stacked-dX layer in one launch (it was
+// three: DOJ split, stacked transpose, row sums): blocks [0, sum_blocks)
+// compute c0sum[o] = sum_i C[0][o][i] (one warp per row, float64 lane
+// partials, fixed shuffle tree -- as row_sum_kernel); the other blocks take
+// 32 (o) x 32 (i) tiles of every plane k, write the DOJ hi/lo copy (unit
+// stride in i) and, for k >= 1, the stacked input-gradient operand through a
+// shared-memory transpose (unit stride in o; padded inputs zeroed).
+__global__ void __launch_bounds__(256) prep_fused_kernel(const float* __restrict__ c, int64_t K, int64_t O, int64_t I,
+                                                         int n_i, int sum_blocks, __nv_bfloat16* __restrict__ doj_hi,
+                                                         __nv_bfloat16* __restrict__ doj_lo, int64_t ldI,
+                                                         __nv_bfloat16* __restrict__ dxb_hi,
+                                                         __nv_bfloat16* __restrict__ dxb_lo, int64_t ldO,
+                                                         float* __restrict__ c0sum, PrepHeader* hdr, PrepHeader h) {
+  pdl_wait();
+  __shared__ float tile[32][33];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *hdr = h;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t d = K - 1;
+  const int64_t i_pad = ceil_div(I, n_i) * n_i;
+  const int64_t ot = ceil_div(O, 32), it_ = ceil_div(i_pad, 32);
+  const int64_t tiles = K * ot * it_;
+  for (int64_t t = blockIdx.x; t < sum_blocks + tiles; t += gridDim.x) {
+    if (t < sum_blocks) {
+      const int64_t o = t * 8 + ty;
+      if (o < O) {
+        double acc = 0.0;
+        for (int64_t i = tx; i < I; i += 32) acc += static_cast<double>(c[o * I + i]);
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+        if (tx == 0) c0sum[o] = static_cast<float>(acc);
+      }
+      continue;
+    }
+    const int64_t u = t - sum_blocks;
+    const int64_t k = u / (ot * it_);
+    const int64_t rem = u - k * ot * it_;
+    const int64_t o0 = (rem / it_) * 32, i0 = (rem % it_) * 32;
+    const float* src = c + k * O * I;
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t o = o0 + j, i = i0 + tx;
+      const float v = (o < O && i < I) ? src[o * I + i] : 0.0f;
+      tile[j][tx] = v;
+      if (o < O && i < I) {
+        __nv_bfloat16 hv, lv;
+        split_bf16(v, hv, lv);
+        const int64_t q = (k * O + o) * ldI + i;
+        doj_hi[q] = hv;
+        doj_lo[q] = lv;
+      }
+    }
+    if (k == 0) continue;  // (uniform per block: no barrier skipped by part of it)
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t i = i0 + j, o = o0 + tx;
+      if (i < i_pad && o < ldO) {
+        __nv_bfloat16 hv, lv;
+        split_bf16(tile[tx][j], hv, lv);
+        const int64_t row = (i / n_i) * d * n_i + (k - 1) * n_i + i % n_i;
+        dxb_hi[row * ldO + o] = hv;
+        dxb_lo[row * ldO + o] = lv;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // fp32 copy of the coefficients (skinny layers' prep) plus the prep header
 __global__ void copy_header_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n, PrepHeader* hdr,
                                    PrepHeader h) {
@@ -218,17 +284,19 @@ __global__ void col_partial_kernel(const float* __restrict__ in, int64_t rows, i
 // out[c] = sum_s part[s][c]: block = 32 columns x 8 warps; warp w sums
 // slots w, w+8, ... and the 8 partials are folded in warp order (fixed
 // order for a given slot count: deterministic).
-// With bcast != nullptr the block also writes bcast[c][0..bcast_cols) =
-// out[c] for its 32 columns (dC_0 = db, the B_0 == 1 fold) -- one launch
-// instead of a separate broadcast.
-__global__ void __launch_bounds__(256) col_finish_kernel(const double* __restrict__ part, int slots, int64_t cols,
-                                                         float* __restrict__ out, float* __restrict__ bcast,
-                                                         int64_t bcast_cols) {
-  pdl_wait();
+// With bcast != nullptr the block also writes bcast[c][i] = out[c] for its
+// 32 columns and bcast columns i in [i0, i1) (dC_0 = db, the B_0 == 1 fold)
+// -- one launch instead of a separate broadcast.  Blocks that share the 32
+// columns (different broadcast ranges) recompute the same sums; only the
+// first writes out[c].
+__device__ __forceinline__ void col_finish_block(const double* __restrict__ part, int slots, int64_t cols,
+                                                 float* __restrict__ out, float* __restrict__ bcast,
+                                                 int64_t bcast_cols, int64_t cb, int64_t i0, int64_t i1,
+                                                 bool write_out) {
   __shared__ double red[8][32];
   __shared__ float val[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t c0 = cb * 32;
   const int64_t c = c0 + lane;
   double acc = 0.0;
   if (c < cols)
@@ -240,7 +308,7 @@ __global__ void __launch_bounds__(256) col_finish_kernel(const double* __restric
 #pragma unroll
     for (int j = 0; j < 8; ++j) t += red[j][lane];
     val[lane] = static_cast<float>(t);
-    if (c < cols) out[c] = static_cast<float>(t);
+    if (write_out && c < cols) out[c] = static_cast<float>(t);
   }
   if (bcast == nullptr) return;
   __syncthreads();
@@ -248,18 +316,49 @@ __global__ void __launch_bounds__(256) col_finish_kernel(const double* __restric
   for (int r = 0; r < nr; ++r) {
     float* row = bcast + (c0 + r) * bcast_cols;
     const float v = val[r];
-    for (int64_t i = threadIdx.x; i < bcast_cols; i += blockDim.x) row[i] = v;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) row[i] = v;
   }
 }
 
-// out[n] = (acc ? out[n] : 0) + sum_s partials[s*stride + n], ascending s
-__global__ void merge_kernel(const float* __restrict__ partials, int S, int64_t stride, int64_t n,
-                             float* __restrict__ out, int accumulate) {
+// broadcast column ranges per 32 output columns: enough blocks to fill the
+// GPU (16 blocks wrote the 1 MB dC_0 of a 512 x 512 layer in 7.5 us)
+int64_t bcast_split(int64_t cols, int64_t bcast_cols) {
+  if (bcast_cols <= 0) return 1;
+  const int64_t cb = ceil_div(cols, 32);
+  int64_t by = ceil_div(static_cast<int64_t>(num_sms()) * 2, cb);
+  const int64_t max_by = ceil_div(bcast_cols, 256);
+  if (by > max_by) by = max_by;
+  return by < 1 ? 1 : by;
+}
+
+__global__ void __launch_bounds__(256) col_finish_kernel(const double* __restrict__ part, int slots, int64_t cols,
+                                                         float* __restrict__ out, float* __restrict__ bcast,
+                                                         int64_t bcast_cols) {
   pdl_wait();
+  const int64_t by = gridDim.y, span = ceil_div(bcast_cols, by);
+  const int64_t i0 = blockIdx.y * span, i1 = i0 + span < bcast_cols ? i0 + span : bcast_cols;
+  col_finish_block(part, slots, cols, out, bcast, bcast_cols, blockIdx.x, i0, i1, blockIdx.y == 0);
+}
+
+// out[n] = (acc ? out[n] : 0) + sum_s partials[s*stride + n], ascending s.
+// The first `fin_blocks` blocks run a col_finish job (the bias gradient and
+// dC_0 that follow a split dC GEMM) in the same launch, alongside the merge.
+__global__ void merge_kernel(const float* __restrict__ partials, int S, int64_t stride, int64_t n,
+                             float* __restrict__ out, int accumulate, int merge_blocks, ColFinishJob fin,
+                             int64_t fin_by, int fin_blocks) {
+  pdl_wait();
+  if (static_cast<int>(blockIdx.x) < fin_blocks) {
+    const int64_t j = blockIdx.x;
+    const int64_t cb = j / fin_by, y = j - cb * fin_by;
+    const int64_t span = ceil_div(fin.bcast_cols, fin_by);
+    const int64_t i0 = y * span, i1 = i0 + span < fin.bcast_cols ? i0 + span : fin.bcast_cols;
+    col_finish_block(fin.part, fin.slots, fin.cols, fin.out, fin.bcast, fin.bcast_cols, cb, i0, i1, y == 0);
+    return;
+  }
   const bool vec = (stride % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(partials) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t step = static_cast<int64_t>(merge_blocks) * blockDim.x;
+  const int64_t t0 = (blockIdx.x - fin_blocks) * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (vec) {
     for (int64_t i = t0; i < n / 4; i += step) {
       float4 a = accumulate ? reinterpret_cast<const float4*>(out)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -363,6 +462,21 @@ int launch_row_sum(const float* in, int64_t rows, int64_t cols, float* out, cuda
   return kOk;
 }
 
+int launch_prep_fused(const float* c_doj, int64_t K, int64_t O, int64_t I, int n_i, __nv_bfloat16* doj_hi,
+                      __nv_bfloat16* doj_lo, int64_t ldI, __nv_bfloat16* dxb_hi, __nv_bfloat16* dxb_lo, int64_t ldO,
+                      float* c0sum, void* hdr, const PrepHeader& h, cudaStream_t s) {
+  CK_CHECK(n_i > 0 && K >= 1 && O >= 1 && I >= 1, "prep: bad stacked layout");
+  const int sum_blocks = static_cast<int>(ceil_div(O, 8));
+  const int64_t tiles = K * ceil_div(O, 32) * ceil_div(ceil_div(I, n_i) * n_i, 32);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  const int64_t want = sum_blocks + tiles;
+  LaunchScope scope(kKSplit, s);
+  CK_CUDA(launch_k((prep_fused_kernel), static_cast<int>(want < cap ? want : cap), kThreads, 0, s, c_doj, K, O, I, n_i,
+                   sum_blocks, doj_hi, doj_lo, ldI, dxb_hi, dxb_lo, ldO, c0sum, static_cast<PrepHeader*>(hdr), h));
+  CK_CUDA(cudaGetLastError());
+  return kOk;
+}
+
 int launch_copy_with_header(const float* in, float* out, int64_t n, void* hdr, const PrepHeader& h, cudaStream_t s) {
   LaunchScope scope(kKSplit, s);
   CK_CUDA(launch_k((copy_header_kernel), blocks_for(n / 4 > 0 ? n / 4 : 1), kThreads, 0, s, in, out, n,
@@ -383,17 +497,31 @@ int launch_col_partial(const float* in, int64_t rows, int64_t cols, double* part
 int launch_col_finish(const double* part, int slots, int64_t cols, float* out, cudaStream_t s, float* bcast,
                       int64_t bcast_cols) {
   if (cols == 0) return kOk;
+  const int64_t by = bcast != nullptr ? bcast_split(cols, bcast_cols) : 1;
   LaunchScope scope(kKReduce, s);
-  CK_CUDA(launch_k((col_finish_kernel), static_cast<unsigned>(ceil_div(cols, 32)), 256, 0, s, part, slots, cols, out,
-                   bcast, bcast_cols));
+  CK_CUDA(launch_k((col_finish_kernel), dim3(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(by)),
+                   256, 0, s, part, slots, cols, out, bcast, bcast ? bcast_cols : 0));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
 
-int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate, cudaStream_t s) {
-  if (n == 0) return kOk;
+int launch_merge(const float* partials, int S, int64_t stride, int64_t n, float* out, int accumulate, cudaStream_t s,
+                 const ColFinishJob* fin) {
+  if (n == 0) return fin ? launch_col_finish(fin->part, fin->slots, fin->cols, fin->out, s, fin->bcast,
+                                             fin->bcast_cols)
+                         : kOk;
+  ColFinishJob f{};
+  int64_t fin_blocks = 0, fin_by = 1;
+  if (fin != nullptr && fin->cols > 0) {
+    f = *fin;
+    if (f.bcast == nullptr) f.bcast_cols = 0;
+    fin_by = f.bcast ? bcast_split(f.cols, f.bcast_cols) : 1;
+    fin_blocks = ceil_div(f.cols, 32) * fin_by;
+  }
+  const int mb = blocks_for(ceil_div(n, 4));
   LaunchScope scope(kKReduce, s);
-  CK_CUDA(launch_k((merge_kernel), blocks_for(ceil_div(n, 4)), kThreads, 0, s, partials, S, stride, n, out, accumulate));
+  CK_CUDA(launch_k((merge_kernel), static_cast<unsigned>(mb + fin_blocks), kThreads, 0, s, partials, S, stride, n, out,
+                   accumulate, mb, f, fin_by, static_cast<int>(fin_blocks)));
   CK_CUDA(cudaGetLastError());
   return kOk;
 }
