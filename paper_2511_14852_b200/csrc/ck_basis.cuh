@@ -24,13 +24,31 @@ __host__ __device__ inline int basis_features(int kind, int degree) {
   return kind == kFourier ? 2 * degree + 1 : degree + 1;
 }
 
+// tanh(x) in 5 instructions (ex2 / rcp approximations; tanhf is ~14 plus a
+// branch): with r = 1 / (1 + e^{2|x|}) in (0, 1/2], t = sign(x) (1 - 2r),
+// |t| <= 1 by construction, +-inf -> +-1.  Absolute error ~1e-7 over the
+// whole range -- what the LUT paths consume: the cell position has ~1e-7 * N
+// cells of error (the same order as a 2-ulp tanhf near |t| = 1), and the
+// interpolated values are continuous in t.  (Exact-mode bases keep tanhf:
+// there t itself is the argument of the polynomial.)
+__device__ __forceinline__ float tanh_r(float x, float& r) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(x) * 2.8853900817779268f));  // e^{2|x|}
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+  return copysignf(fmaf(-2.0f, r, 1.0f), x);
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+  float r;
+  return tanh_r(x, r);
+}
+
 // Fast cell choice for value interpolation (float32).  frac is formed with
 // one rounding (fma of t*h against the exact h - idx), so the interpolated
 // value is accurate to ~k^2 * ulp(t); a cell flip at an edge is harmless for
 // values because the interpolant is continuous.
 __device__ __forceinline__ void cell_f32(float xv, int n, int& idx, float& frac) {
-  float t = tanhf(xv);
-  t = fminf(fmaxf(t, -1.0f), 1.0f);
+  const float t = tanh_fast(xv);  // in [-1, 1]
   const float h = 0.5f * static_cast<float>(n - 1);
   const float pos = fmaf(t, h, h);
   int i = static_cast<int>(pos);
@@ -48,10 +66,8 @@ __device__ __forceinline__ void cell_f32(float xv, int n, int& idx, float& frac)
 // guard band (4e-7 * N cells) where the cell is settled against the exact
 // float32 boundaries; the values interpolate continuously in t.
 __device__ __forceinline__ void tanh_jac(float x, float& t, float& jac) {
-  float e, r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(x) * 2.8853900817779268f));  // e^{2|x|}
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
-  t = copysignf(fmaf(-2.0f, r, 1.0f), x);
+  float r;
+  t = tanh_r(x, r);
   jac = 4.0f * r * (1.0f - r);
 }
 

@@ -359,49 +359,107 @@ __device__ __forceinline__ void load4(const float* p, int i0, int I, bool vec, f
   }
 }
 
+// Interpolated LUT values v[1..P] of one element (the forward's float32
+// cell; the interpolant is continuous, so no boundary check): one recurrence
+// per grid node, then lerp.  ~4P + 16 instructions.
+template <int KIND, int P>
+__device__ __forceinline__ void lut_values(float xv, float hN, float stepf, int N, float (&v)[P + 1]) {
+  const float t = tanh_fast(xv);  // in [-1, 1]
+  const int idx = min(static_cast<int>(fmaf(t, hN, hN)), N - 2);
+  const float fi = static_cast<float>(idx);
+  const float f = fmaf(t, hN, hN - fi);
+  const float x0 = fmaf(fi, stepf, -1.0f);
+  const float x1 = idx + 1 >= N - 1 ? 1.0f : fmaf(fi + 1.0f, stepf, -1.0f);  // grid_node_f(idx + 1)
+  float v0[P + 1], v1[P + 1];
+  basis_f32<KIND, P>(x0, v0);
+  basis_f32<KIND, P>(x1, v1);
+#pragma unroll
+  for (int k = 1; k <= P; ++k) v[k] = lerp_ref(v0[k], v1[k], f);
+}
+
+// One pass of a lane: QJ quads of inputs p0 + 4 (lane + 32 j).  FULL: all
+// in range and 16-byte aligned (no checks); otherwise C loads past I read as
+// zero, so padded inputs (x = 0, finite values) contribute nothing.
+template <int KIND, int O, int P, int QJ, bool FULL>
+__device__ __forceinline__ void skinny_fwd_pass(const float (&xq)[QJ][4], int p0, int lane, int I, int K,
+                                                const float* __restrict__ c, int64_t plane, float hN, float stepf,
+                                                int N, float (&acc)[O]) {
+#pragma unroll
+  for (int j = 0; j < QJ; ++j) {
+    const int i0 = p0 + 4 * (lane + 32 * j);
+    if (!FULL && i0 >= I) break;
+    float v[4][P + 1];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) lut_values<KIND, P>(xq[j][e], hN, stepf, N, v[e]);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+      if (k < K) {
+#pragma unroll
+        for (int o = 0; o < O; ++o) {
+          const float* cp = c + k * plane + static_cast<int64_t>(o) * I + i0;
+          float cv[4];
+          if (FULL) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(cp));
+            cv[0] = q.x; cv[1] = q.y; cv[2] = q.z; cv[3] = q.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cv[e] = i0 + e < I ? __ldg(cp + e) : 0.0f;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[o] = k == 0 ? acc[o] + cv[e] : fmaf(v[e][k], cv[e], acc[o]);  // B_0 == 1
+        }
+      }
+    }
+  }
+}
+
+// One warp per row (grid-stride over rows); a pass covers 512 inputs of the
+// row: lane l owns the 4-input quads l, l + 32, l + 64, l + 96 (float4 x and C
+// loads).  The x of the next pass (this row's next 512 inputs or the next
+// row's first) is loaded before the current pass is evaluated, so the HBM
+// latency of x overlaps the basis work (ncu: the row loop stalled on x,
+// 33 % long-scoreboard).  Full passes (16-byte aligned, 512 inputs in range)
+// skip every bounds check.
 template <int KIND, int O, int P>
 __device__ __forceinline__ void skinny_fwd_lut_rows(const float* __restrict__ x, int64_t rows, int I, int K,
                                                     const float* __restrict__ c, const float* __restrict__ bias,
                                                     int N, bool vec, float* __restrict__ y) {
+  constexpr int QJ = 4, PASS = 128 * QJ;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int64_t plane = static_cast<int64_t>(O) * I;
   const float hN = 0.5f * static_cast<float>(N - 1);
   const float stepf = 2.0f / static_cast<float>(N - 1);
+  const int passes = (I + PASS - 1) / PASS;
+  auto load_pass = [&](int64_t b, int p0, float (&xq)[QJ][4]) {
+    if (b >= rows) return;
+    const float* xr = x + b * I;
+#pragma unroll
+    for (int j = 0; j < QJ; ++j) load4(xr, p0 + 4 * (lane + 32 * j), I, vec, xq[j]);
+  };
+  float xn[QJ][4];
+  load_pass(warp, 0, xn);
   for (int64_t b = warp; b < rows; b += nwarps) {
     float acc[O];
 #pragma unroll
     for (int o = 0; o < O; ++o) acc[o] = 0.0f;
-    const float* xr = x + b * I;
-    for (int i0 = 4 * lane; i0 < I; i0 += 128) {
-      float xv[4];
-      load4(xr, i0, I, vec, xv);
-      float v[4][P + 1];
+    for (int p = 0; p < passes; ++p) {
+      const int p0 = p * PASS;
+      float xq[QJ][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        // cell_f32 (the forward's float32 cell; values are continuous)
-        const float t = fminf(fmaxf(tanhf(xv[e]), -1.0f), 1.0f);
-        const int idx = min(static_cast<int>(fmaf(t, hN, hN)), N - 2);
-        const float f = fmaf(t, hN, hN - static_cast<float>(idx));
-        float v0[P + 1], v1[P + 1];
-        basis_f32<KIND, P>(grid_node_f(idx, N, stepf), v0);
-        basis_f32<KIND, P>(grid_node_f(idx + 1, N, stepf), v1);
+      for (int j = 0; j < QJ; ++j)
 #pragma unroll
-        for (int k = 1; k <= P; ++k) v[e][k] = lerp_ref(v0[k], v1[k], f);
-        v[e][0] = i0 + e < I ? 1.0f : 0.0f;  // (padded inputs: zero coefficients below)
+        for (int e = 0; e < 4; ++e) xq[j][e] = xn[j][e];
+      if (p + 1 < passes) {
+        load_pass(b, p0 + PASS, xn);
+      } else {
+        load_pass(b + nwarps, 0, xn);
       }
-#pragma unroll
-      for (int k = 0; k <= P; ++k) {
-        if (k < K) {
-#pragma unroll
-          for (int o = 0; o < O; ++o) {
-            float cv[4];
-            load4(c + k * plane + static_cast<int64_t>(o) * I, i0, I, vec, cv);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[o] = fmaf(v[e][k], cv[e], acc[o]);
-          }
-        }
+      if (vec && p0 + PASS <= I) {
+        skinny_fwd_pass<KIND, O, P, QJ, true>(xq, p0, lane, I, K, c, plane, hN, stepf, N, acc);
+      } else {
+        skinny_fwd_pass<KIND, O, P, QJ, false>(xq, p0, lane, I, K, c, plane, hN, stepf, N, acc);
       }
     }
 #pragma unroll
@@ -468,22 +526,34 @@ __device__ __forceinline__ void skinny_bwd_lut_body(const float* __restrict__ x,
   double db[O];
 #pragma unroll
   for (int o = 0; o < O; ++o) db[o] = 0.0;
+  // this warp's rows: first, first + 8, ... < r1 (n of them); running
+  // pointers, one 64-bit add per row instead of an index product
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rb;
   const int64_t r1 = r0 + rb < rows ? r0 + rb : rows;
+  const int64_t first = r0 + w;
+  const int n = first < r1 ? static_cast<int>((r1 - first + 7) / 8) : 0;
+  const int64_t xs = 8 * static_cast<int64_t>(I);
+  const float* xp = x + first * I + ic;
+  const float* gp = dy + first * O;
+  float* dxp = (dx != nullptr && col_ok) ? dx + first * I + i : nullptr;
+  const bool db_block = blockIdx.y == 0;  // uniform
   constexpr int R = KMAX * O <= 8 ? 4 : (KMAX * O <= 16 ? 2 : 1);  // rows in flight (register budget)
   float xn[R], gn[R][O];
-  auto load_group = [&](int64_t bg) {
+  auto load_group = [&](int j0) {
+    const float* xq = xp;
+    const float* gq = gp;
 #pragma unroll
     for (int u = 0; u < R; ++u) {
-      const int64_t b = bg + 8 * u;
-      const bool ok = b < r1;
-      xn[u] = ok ? __ldg(x + b * I + ic) : 0.0f;
+      const bool ok = j0 + u < n;
+      xn[u] = ok ? __ldg(xq) : 0.0f;
 #pragma unroll
-      for (int o = 0; o < O; ++o) gn[u][o] = ok ? __ldg(dy + b * O + o) : 0.0f;
+      for (int o = 0; o < O; ++o) gn[u][o] = ok ? __ldg(gq + o) : 0.0f;
+      xq += xs;
+      gq += 8 * O;
     }
   };
-  load_group(r0 + w);
-  for (int64_t bg = r0 + w; bg < r1; bg += 8 * R) {
+  load_group(0);
+  for (int j = 0; j < n; j += R) {
     float xg[R], g[R][O];
 #pragma unroll
     for (int u = 0; u < R; ++u) {
@@ -491,17 +561,18 @@ __device__ __forceinline__ void skinny_bwd_lut_body(const float* __restrict__ x,
 #pragma unroll
       for (int o = 0; o < O; ++o) g[u][o] = gn[u][o];
     }
-    load_group(bg + 8 * R);
-    if (blockIdx.y == 0 && lane == 0) {
+    xp += R * xs;
+    gp += R * 8 * O;
+    load_group(j + R);
+    if (db_block) {
 #pragma unroll
       for (int u = 0; u < R; ++u)
 #pragma unroll
-        for (int o = 0; o < O; ++o) db[o] += static_cast<double>(g[u][o]);  // zero past r1
+        for (int o = 0; o < O; ++o) db[o] += static_cast<double>(g[u][o]);  // zero past n
     }
 #pragma unroll
     for (int u = 0; u < R; ++u) {
-      const int64_t b = bg + 8 * u;
-      if (b >= r1) break;
+      if (j + u >= n) break;
       const float xv = xg[u];
       float t, jac;
       tanh_jac(xv, t, jac);
@@ -514,28 +585,29 @@ __device__ __forceinline__ void skinny_bwd_lut_body(const float* __restrict__ x,
         const float bl = __ldg(row + K - 1), bh = __ldg(row + K);
         cell = min(cell + (xv < bl ? -1 : (xv < bh ? 0 : 1)), N - 2);  // x = +inf: N-2 as the reference
       }
-      const float f = fmaf(t, hN, hN - static_cast<float>(cell));
-      const float nb = grid_node_f(cell, N, stepf), na = grid_node_f(cell + 1, N, stepf);
+      const float fc = static_cast<float>(cell);
+      const float f = fmaf(t, hN, hN - fc);
+      const float nb = fmaf(fc, stepf, -1.0f);
+      const float na = cell + 1 >= N - 1 ? 1.0f : fmaf(fc + 1.0f, stepf, -1.0f);  // grid_node_f(cell + 1)
       float sl[P], vb[P + 1];
       chord_and_values<KIND, P>(nb, na, sl, vb);
       const float fs = f * (na - nb);
       float gx = 0.0f;
 #pragma unroll
-      for (int k = 1; k < KMAX; ++k) {
-        float gk = 0.0f;
+      for (int o = 0; o < O; ++o) {
+        float so = 0.0f;
 #pragma unroll
-        for (int o = 0; o < O; ++o) gk = fmaf(g[u][o], cr[k][o], gk);
-        gx = fmaf(sl[k - 1], gk, gx);
+        for (int k = 1; k < KMAX; ++k) so = fmaf(sl[k - 1], cr[k][o], so);
+        gx = fmaf(g[u][o], so, gx);
+        acc[0][o] += g[u][o];
       }
-#pragma unroll
-      for (int o = 0; o < O; ++o) acc[0][o] += g[u][o];
 #pragma unroll
       for (int k = 1; k < KMAX; ++k) {
         const float v = fmaf(fs, sl[k - 1], vb[k]);  // lerp(B_k(b), B_k(a), f)
 #pragma unroll
         for (int o = 0; o < O; ++o) acc[k][o] = fmaf(g[u][o], v, acc[k][o]);
       }
-      if (dx && col_ok) dx[b * I + i] = jacobian ? gx * jac : gx;
+      if (dxp != nullptr) dxp[static_cast<int64_t>(j + u) * xs] = jacobian ? gx * jac : gx;
     }
   }
 #pragma unroll

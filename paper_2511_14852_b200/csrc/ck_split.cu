@@ -44,7 +44,7 @@ __global__ void split_rows_kernel(const float* __restrict__ in, int64_t nz, int6
 // [s*rb, min((s+1)*rb, rows)) and columns [64 cb, 64 cb + 64): warp w takes
 // rows w, w+8, ...; lane l the column pair 64 cb + 2 l.  The 8 warp partials
 // are folded in warp order, so part[s][c] is deterministic.
-__global__ void __launch_bounds__(256) split_rows_colsum_kernel(const float* __restrict__ in, int64_t rows,
+__global__ void __launch_bounds__(256, 3) split_rows_colsum_kernel(const float* __restrict__ in, int64_t rows,
                                                                 int64_t cols, int64_t rb, uint32_t* __restrict__ hi,
                                                                 uint32_t* __restrict__ lo, int64_t ld,
                                                                 double* __restrict__ part) {
@@ -58,11 +58,13 @@ __global__ void __launch_bounds__(256) split_rows_colsum_kernel(const float* __r
   if (c < cols) {
     const bool two = c + 1 < cols;
     const bool vec = two && ((cols & 1) == 0);
-    // 4 rows per iteration (independent loads in flight); sums in row order
-    for (int64_t rr = r0 + w; rr < r1; rr += 32) {
-      float a[4], b[4];
+    // 8 rows per iteration (independent loads in flight: 4 left the HBM
+    // pipe a third full, ncu 27 % DRAM); sums in row order
+    constexpr int RU = 8;
+    for (int64_t rr = r0 + w; rr < r1; rr += 8 * RU) {
+      float a[RU], b[RU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < RU; ++u) {
         const int64_t r = rr + 8 * u;
         a[u] = b[u] = 0.0f;
         if (r < r1) {
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(256) split_rows_colsum_kernel(const float* __r
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < RU; ++u) {
         const int64_t r = rr + 8 * u;
         if (r >= r1) break;
         s0 += static_cast<double>(a[u]);
@@ -190,9 +192,12 @@ __global__ void row_sum_kernel(const float* __restrict__ in, int64_t rows, int64
 // three: DOJ split, stacked transpose, row sums): blocks [0, sum_blocks)
 // compute c0sum[o] = sum_i C[0][o][i] (one warp per row, float64 lane
 // partials, fixed shuffle tree -- as row_sum_kernel); the other blocks take
-// 32 (o) x 32 (i) tiles of every plane k, write the DOJ hi/lo copy (unit
-// stride in i) and, for k >= 1, the stacked input-gradient operand through a
-// shared-memory transpose (unit stride in o; padded inputs zeroed).
+// 64 (o) x 64 (i) tiles of every plane k: lanes own input pairs (8-byte
+// loads, bf16x2 stores of the DOJ hi/lo copy, unit stride in i) and, for
+// k >= 1, after a shared-memory transpose, output pairs of the stacked
+// input-gradient operand (unit stride in o; padded inputs zeroed).  The
+// stacked row of an input is computed once per warp (the index division was
+// most of the kernel's instructions when every element did it).
 __global__ void __launch_bounds__(256) prep_fused_kernel(const float* __restrict__ c, int64_t K, int64_t O, int64_t I,
                                                          int n_i, int sum_blocks, __nv_bfloat16* __restrict__ doj_hi,
                                                          __nv_bfloat16* __restrict__ doj_lo, int64_t ldI,
@@ -200,52 +205,78 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const float* __restrict
                                                          __nv_bfloat16* __restrict__ dxb_lo, int64_t ldO,
                                                          float* __restrict__ c0sum, PrepHeader* hdr, PrepHeader h) {
   pdl_wait();
-  __shared__ float tile[32][33];
+  __shared__ float tile[64][65];
   if (blockIdx.x == 0 && threadIdx.x == 0) *hdr = h;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t d = K - 1;
   const int64_t i_pad = ceil_div(I, n_i) * n_i;
-  const int64_t ot = ceil_div(O, 32), it_ = ceil_div(i_pad, 32);
+  const int64_t ot = ceil_div(O, 64), it_ = ceil_div(i_pad, 64);
   const int64_t tiles = K * ot * it_;
+  const bool pairs = (I % 2 == 0) && (reinterpret_cast<uintptr_t>(c) & 7) == 0;
+  uint32_t* dh = reinterpret_cast<uint32_t*>(doj_hi);
+  uint32_t* dl = reinterpret_cast<uint32_t*>(doj_lo);
+  uint32_t* xh = reinterpret_cast<uint32_t*>(dxb_hi);
+  uint32_t* xl = reinterpret_cast<uint32_t*>(dxb_lo);
   for (int64_t t = blockIdx.x; t < sum_blocks + tiles; t += gridDim.x) {
     if (t < sum_blocks) {
-      const int64_t o = t * 8 + ty;
+      const int64_t o = t * 8 + w;
       if (o < O) {
         double acc = 0.0;
-        for (int64_t i = tx; i < I; i += 32) acc += static_cast<double>(c[o * I + i]);
+        for (int64_t i = lane; i < I; i += 32) acc += static_cast<double>(c[o * I + i]);
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
-        if (tx == 0) c0sum[o] = static_cast<float>(acc);
+        if (lane == 0) c0sum[o] = static_cast<float>(acc);
       }
       continue;
     }
     const int64_t u = t - sum_blocks;
     const int64_t k = u / (ot * it_);
     const int64_t rem = u - k * ot * it_;
-    const int64_t o0 = (rem / it_) * 32, i0 = (rem % it_) * 32;
+    const int64_t o0 = (rem / it_) * 64, i0 = (rem % it_) * 64;
     const float* src = c + k * O * I;
-    for (int j = ty; j < 32; j += 8) {
-      const int64_t o = o0 + j, i = i0 + tx;
-      const float v = (o < O && i < I) ? src[o * I + i] : 0.0f;
-      tile[j][tx] = v;
-      if (o < O && i < I) {
-        __nv_bfloat16 hv, lv;
-        split_bf16(v, hv, lv);
-        const int64_t q = (k * O + o) * ldI + i;
-        doj_hi[q] = hv;
-        doj_lo[q] = lv;
+    const int64_t i = i0 + 2 * lane;
+#pragma unroll 4
+    for (int r = 0; r < 8; ++r) {
+      const int ol = w + 8 * r;
+      const int64_t o = o0 + ol;
+      float a = 0.0f, b = 0.0f;
+      if (o < O) {
+        const float* p = src + o * I + i;
+        if (pairs && i < I) {
+          const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+          a = v.x;
+          b = v.y;
+        } else {
+          a = i < I ? __ldg(p) : 0.0f;
+          b = i + 1 < I ? __ldg(p + 1) : 0.0f;
+        }
+        if (i < I) {  // (i + 1 = I odd: the pad element of the row gets 0)
+          uint32_t h2, l2;
+          split_pack2(a, b, h2, l2);
+          const int64_t q = ((k * O + o) * ldI + i) >> 1;
+          dh[q] = h2;
+          dl[q] = l2;
+        }
       }
+      tile[ol][2 * lane] = a;
+      tile[ol][2 * lane + 1] = b;
     }
     if (k == 0) continue;  // (uniform per block: no barrier skipped by part of it)
     __syncthreads();
-    for (int j = ty; j < 32; j += 8) {
-      const int64_t i = i0 + j, o = o0 + tx;
-      if (i < i_pad && o < ldO) {
-        __nv_bfloat16 hv, lv;
-        split_bf16(tile[tx][j], hv, lv);
-        const int64_t row = (i / n_i) * d * n_i + (k - 1) * n_i + i % n_i;
-        dxb_hi[row * ldO + o] = hv;
-        dxb_lo[row * ldO + o] = lv;
+    const int64_t o = o0 + 2 * lane;
+#pragma unroll 4
+    for (int r = 0; r < 8; ++r) {
+      const int il = w + 8 * r;
+      const int64_t ii = i0 + il;
+      if (ii >= i_pad) break;  // uniform per warp (ii grows with r)
+      const int64_t blk = ii / n_i;
+      const int64_t row = blk * d * n_i + (k - 1) * n_i + (ii - blk * n_i);
+      if (o < ldO) {
+        uint32_t h2, l2;
+        split_pack2(tile[2 * lane][il], tile[2 * lane + 1][il], h2, l2);
+        const int64_t q = (row * ldO + o) >> 1;
+        xh[q] = h2;
+        xl[q] = l2;
       }
     }
     __syncthreads();
@@ -299,8 +330,18 @@ __device__ __forceinline__ void col_finish_block(const double* __restrict__ part
   const int64_t c0 = cb * 32;
   const int64_t c = c0 + lane;
   double acc = 0.0;
-  if (c < cols)
-    for (int s = w; s < slots; s += 8) acc += part[s * cols + c];
+  if (c < cols) {
+    int s = w;
+    for (; s + 24 < slots; s += 32) {  // four loads in flight, added in slot order
+      const double p0 = part[s * cols + c], p1 = part[(s + 8) * cols + c];
+      const double p2 = part[(s + 16) * cols + c], p3 = part[(s + 24) * cols + c];
+      acc += p0;
+      acc += p1;
+      acc += p2;
+      acc += p3;
+    }
+    for (; s < slots; s += 8) acc += part[s * cols + c];
+  }
   red[w][lane] = acc;
   __syncthreads();
   if (w == 0) {
@@ -359,11 +400,30 @@ __global__ void merge_kernel(const float* __restrict__ partials, int S, int64_t 
                    ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   const int64_t step = static_cast<int64_t>(merge_blocks) * blockDim.x;
   const int64_t t0 = (blockIdx.x - fin_blocks) * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  // the slot loads are issued 8 at a time, then added in ascending slot
+  // order: a plain loop waited one L2 round trip per slot (27 slots of the
+  // C2 head's dC took 11 us for 0.4 MB)
+  constexpr int U = 8;
   if (vec) {
+    const float4* pp = reinterpret_cast<const float4*>(partials);
+    const int64_t st4 = stride / 4;
     for (int64_t i = t0; i < n / 4; i += step) {
       float4 a = accumulate ? reinterpret_cast<const float4*>(out)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int s = 0; s < S; ++s) {
-        const float4 p = __ldg(reinterpret_cast<const float4*>(partials + s * stride) + i);
+      int s = 0;
+      for (; s + U <= S; s += U) {
+        float4 p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) p[u] = __ldg(pp + (s + u) * st4 + i);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          a.x += p[u].x;
+          a.y += p[u].y;
+          a.z += p[u].z;
+          a.w += p[u].w;
+        }
+      }
+      for (; s < S; ++s) {
+        const float4 p = __ldg(pp + s * st4 + i);
         a.x += p.x;
         a.y += p.y;
         a.z += p.z;
@@ -374,7 +434,15 @@ __global__ void merge_kernel(const float* __restrict__ partials, int S, int64_t 
   } else {
     for (int64_t i = t0; i < n; i += step) {
       float a = accumulate ? out[i] : 0.0f;
-      for (int s = 0; s < S; ++s) a += partials[s * stride + i];
+      int s = 0;
+      for (; s + U <= S; s += U) {
+        float p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) p[u] = __ldg(partials + (s + u) * stride + i);
+#pragma unroll
+        for (int u = 0; u < U; ++u) a += p[u];
+      }
+      for (; s < S; ++s) a += partials[s * stride + i];
       out[i] = a;
     }
   }
@@ -467,7 +535,8 @@ int launch_prep_fused(const float* c_doj, int64_t K, int64_t O, int64_t I, int n
                       float* c0sum, void* hdr, const PrepHeader& h, cudaStream_t s) {
   CK_CHECK(n_i > 0 && K >= 1 && O >= 1 && I >= 1, "prep: bad stacked layout");
   const int sum_blocks = static_cast<int>(ceil_div(O, 8));
-  const int64_t tiles = K * ceil_div(O, 32) * ceil_div(ceil_div(I, n_i) * n_i, 32);
+  CK_CHECK(ldI % 2 == 0 && ldO % 2 == 0, "prep: pitches must be even (bf16x2 stores)");
+  const int64_t tiles = K * ceil_div(O, 64) * ceil_div(ceil_div(I, n_i) * n_i, 64);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   const int64_t want = sum_blocks + tiles;
   LaunchScope scope(kKSplit, s);
