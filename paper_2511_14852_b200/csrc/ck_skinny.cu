@@ -380,7 +380,7 @@ __device__ __forceinline__ void lut_values(float xv, float hN, float stepf, int 
 // One pass of a lane: QJ quads of inputs p0 + 4 (lane + 32 j).  FULL: all
 // in range and 16-byte aligned (no checks); otherwise C loads past I read as
 // zero, so padded inputs (x = 0, finite values) contribute nothing.
-template <int KIND, int O, int P, int QJ, bool FULL>
+template <int KIND, int O, int P, int QJ, bool FULL, bool KX>
 __device__ __forceinline__ void skinny_fwd_pass(const float (&xq)[QJ][4], int p0, int lane, int I, int K,
                                                 const float* __restrict__ c, int64_t plane, float hN, float stepf,
                                                 int N, float (&acc)[O]) {
@@ -393,7 +393,7 @@ __device__ __forceinline__ void skinny_fwd_pass(const float (&xq)[QJ][4], int p0
     for (int e = 0; e < 4; ++e) lut_values<KIND, P>(xq[j][e], hN, stepf, N, v[e]);
 #pragma unroll
     for (int k = 0; k <= P; ++k) {
-      if (k < K) {
+      if (KX || k < K) {  // KX: K == P + 1 (compile-time)
 #pragma unroll
         for (int o = 0; o < O; ++o) {
           const float* cp = c + k * plane + static_cast<int64_t>(o) * I + i0;
@@ -457,9 +457,13 @@ __device__ __forceinline__ void skinny_fwd_lut_rows(const float* __restrict__ x,
         load_pass(b + nwarps, 0, xn);
       }
       if (vec && p0 + PASS <= I) {
-        skinny_fwd_pass<KIND, O, P, QJ, true>(xq, p0, lane, I, K, c, plane, hN, stepf, N, acc);
+        if (K == P + 1) {
+          skinny_fwd_pass<KIND, O, P, QJ, true, true>(xq, p0, lane, I, K, c, plane, hN, stepf, N, acc);
+        } else {
+          skinny_fwd_pass<KIND, O, P, QJ, true, false>(xq, p0, lane, I, K, c, plane, hN, stepf, N, acc);
+        }
       } else {
-        skinny_fwd_pass<KIND, O, P, QJ, false>(xq, p0, lane, I, K, c, plane, hN, stepf, N, acc);
+        skinny_fwd_pass<KIND, O, P, QJ, false, false>(xq, p0, lane, I, K, c, plane, hN, stepf, N, acc);
       }
     }
 #pragma unroll
@@ -570,20 +574,37 @@ __device__ __forceinline__ void skinny_bwd_lut_body(const float* __restrict__ x,
 #pragma unroll
         for (int o = 0; o < O; ++o) db[o] += static_cast<double>(g[u][o]);  // zero past n
     }
+    // phase 1, all rows of the group: tanh, float32 cell and, inside the
+    // guard band, the loads of the cell's reference boundaries -- issued for
+    // the whole group before any is consumed (a band element in ~half the
+    // warps made every row wait one L2 round trip: 31 % long-scoreboard
+    // stalls on the boundary compare)
+    float tg[R], jg[R], bl[R], bh[R];
+    int cg[R];
+    bool band[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      tanh_jac(xg[u], tg[u], jg[u]);
+      const float pos = fmaf(tg[u], hN, hN);
+      cg[u] = min(static_cast<int>(pos), N - 2);
+      const float fr = pos - static_cast<float>(cg[u]);
+      band[u] = fr < guard || fr > 1.0f - guard;
+      bl[u] = bh[u] = 0.0f;
+      if (band[u]) {
+        const float* row = L.dxrows + static_cast<int64_t>(cg[u]) * S;
+        bl[u] = __ldg(row + K - 1);
+        bh[u] = __ldg(row + K);
+      }
+    }
 #pragma unroll
     for (int u = 0; u < R; ++u) {
       if (j + u >= n) break;
       const float xv = xg[u];
-      float t, jac;
-      tanh_jac(xv, t, jac);
-      const float pos = fmaf(t, hN, hN);
-      int cell = min(static_cast<int>(pos), N - 2);
-      const float fr = pos - static_cast<float>(cell);
-      if (fr < guard || fr > 1.0f - guard) {
+      const float t = tg[u], jac = jg[u];
+      int cell = cg[u];
+      if (band[u]) {
         // exact reference cell b_c <= x < b_{c+1} (at most one step off)
-        const float* row = L.dxrows + static_cast<int64_t>(cell) * S;
-        const float bl = __ldg(row + K - 1), bh = __ldg(row + K);
-        cell = min(cell + (xv < bl ? -1 : (xv < bh ? 0 : 1)), N - 2);  // x = +inf: N-2 as the reference
+        cell = min(cell + (xv < bl[u] ? -1 : (xv < bh[u] ? 0 : 1)), N - 2);  // x = +inf: N-2 as the reference
       }
       const float fc = static_cast<float>(cell);
       const float f = fmaf(t, hN, hN - fc);

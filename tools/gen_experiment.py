@@ -24,6 +24,10 @@ shapes = [(16384, 256, 256, 3), (16384, 256, 256, 5), (16384, 256, 256, 8), (163
 if os.environ.get("GEN_WIDE"):
     # the wide layers of C1 / C4 (16 and 8 N tiles)
     shapes = [(16384, 4096, 4096, 8), (16384, 2048, 2048, 5), (16384, 4096, 4096, 3), (16384, 1024, 1024, 8)]
+if os.environ.get("GEN_NETS"):
+    # the C2 / C3 net layers (2 N tiles for the 512-wide outputs)
+    shapes = [(16384, 64, 512, 5), (16384, 512, 512, 5), (32000, 257, 512, 15), (32000, 512, 512, 15),
+              (32000, 512, 257, 15), (16384, 256, 256, 3), (16384, 512, 512, 3)]
 for (b, i, o, d) in shapes:
     g = torch.Generator(device="cpu").manual_seed(b + i + o + d)
     x = (torch.rand(b, i, generator=g) * 3 - 1.5).to(dev)
