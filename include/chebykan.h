@@ -264,6 +264,10 @@ CK_API int ck_allreduce_peers_flags(float* const* bufs, unsigned long long* cons
 CK_API long long ck_launch_count(void);
 CK_API int ck_timing_enable(int on);
 CK_API int ck_timing_collect(double* ms_per_class, long long* launches_per_class, int n_classes);
+/* ck_debug_gemm_trace: per-CTA globaltimer stamps (8 per CTA) of the last
+ * tensor-core GEMM launch, copied to out[max_ctas][8]; returns the CTA rows
+ * copied, 0 when the library was built without CK_GEMM_TRACE (the default). */
+CK_API int ck_debug_gemm_trace(unsigned long long* out, int max_ctas);
 
 #ifdef __cplusplus
 }

@@ -293,3 +293,16 @@ int gemm_bf16x3(const GemmProblem& p, cudaStream_t s) {
 }
 
 }  // namespace ck
+
+// Timeline of the last GEMM launch (CK_GEMM_TRACE builds; 0 = not built in).
+extern "C" int ck_debug_gemm_trace(unsigned long long* out, int max_ctas) {
+#ifdef CK_GEMM_TRACE
+  const int n = max_ctas < 512 ? max_ctas : 512;
+  CK_CUDA(cudaMemcpyFromSymbol(out, ck::g_gemm_trace, sizeof(unsigned long long) * ck::kTraceEvents * n));
+  return n;
+#else
+  (void)out;
+  (void)max_ctas;
+  return 0;
+#endif
+}

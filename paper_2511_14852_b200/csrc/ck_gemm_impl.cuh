@@ -134,6 +134,23 @@ __device__ __forceinline__ void pace_wait(int n_units, uint32_t tag, uint32_t ne
   }
 }
 
+// Per-CTA timeline of the last launch (CK_GEMM_TRACE builds only; dev tool
+// tools/gemm_trace.py): globaltimer at kernel entry, after the prologue
+// barrier, after griddepcontrol.wait, first stage landed (MMA warp), last
+// MMA committed, first accumulator drained (epilogue), last tile stored, exit.
+constexpr int kTraceEvents = 8;
+#ifdef CK_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[512][kTraceEvents];
+__device__ __forceinline__ void gemm_trace(int ev) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (blockIdx.x < 512) g_gemm_trace[blockIdx.x][ev] = t;
+}
+#define CK_TRACE(ev) gemm_trace(ev)
+#else
+#define CK_TRACE(ev) ((void)0)
+#endif
+
 // Accumulation segments.  The tensor core's fp32 accumulation of a long
 // reduction is biased (the error grows linearly with the chain: 1.06e-4
 // normwise for the 32768-term C4 forward, 5.5e-5 / 2.6e-5 / 1.2e-5 with 2 /
@@ -510,23 +527,43 @@ __device__ __forceinline__ void dx_epilogue_exact(const KArgs& p, uint32_t tbase
 // epilogue of a one-tile-per-CTA launch take ~7 us.
 constexpr int kEpiTileBytes = 32 * 32 * 4;
 
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+
+// One 32 x 32 accumulator chunk (this warp's 32 rows, columns nb..nb+31)
+// to the output through the warp's XOR-swizzled 4 KB staging tile: each
+// store instruction then writes four whole 128-byte row segments.  The
+// staging tile is addressed in the shared window (ld/st.shared: generic
+// accesses cost an address-space check each) and all eight row groups'
+// loads are issued before the stores.
 __device__ __forceinline__ void store_chunk_coalesced(const uint32_t (&r)[32], float* tile, int lane, int row0,
                                                       int M, int nb, int N, float* out, long long ldo,
                                                       const float* bias0, const float* bias1, int accumulate,
                                                       bool vec) {
+  const uint32_t ts = smem_u32(tile);
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
     const int slot = c4 ^ (lane & 7);
-    *reinterpret_cast<float4*>(tile + lane * 32 + slot * 4) =
-        make_float4(__uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1]), __uint_as_float(r[4 * c4 + 2]),
-                    __uint_as_float(r[4 * c4 + 3]));
+    sts128(ts + (lane * 32 + slot * 4) * 4, __uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1]),
+           __uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3]));
   }
   __syncwarp();
+#ifdef CK_EPI_NOSTORE
+  if (M > 0) return;  // timing experiment: stage only, no global stores
+#endif
   const int c4 = lane & 7;      // this lane's 4 columns
   const int rsub = lane >> 3;   // row within each group of 4
   const int n = nb + 4 * c4;
+  const bool full = vec && n + 4 <= N;
   float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (vec && n + 4 <= N) {
+  if (full) {
     if (bias0) {
       const float4 b = __ldg(reinterpret_cast<const float4*>(bias0 + n));
       bv.x += b.x; bv.y += b.y; bv.z += b.z; bv.w += b.w;
@@ -536,22 +573,28 @@ __device__ __forceinline__ void store_chunk_coalesced(const uint32_t (&r)[32], f
       bv.x += b.x; bv.y += b.y; bv.z += b.z; bv.w += b.w;
     }
   }
-#pragma unroll 4
-  for (int rg = 0; rg < 32; rg += 4) {
-    const int lr = rg + rsub;
-    const int row = row0 + lr;
-    float4 v = *reinterpret_cast<const float4*>(tile + lr * 32 + ((c4 ^ (lr & 7)) * 4));
-    if (row >= M) continue;
-    float* dst = out + static_cast<long long>(row) * ldo + n;
-    if (vec && n + 4 <= N) {
-      v.x += bv.x; v.y += bv.y; v.z += bv.z; v.w += bv.w;
+  float4 v[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const int lr = 4 * g + rsub;
+    v[g] = lds128(ts + (lr * 32 + ((c4 ^ (lr & 7)) * 4)) * 4);
+  }
+  __syncwarp();
+  float* dst = out + static_cast<long long>(row0 + rsub) * ldo + n;
+  const long long step = 4 * ldo;
+#pragma unroll
+  for (int g = 0; g < 8; ++g, dst += step) {
+    if (row0 + 4 * g + rsub >= M) continue;
+    float4 w = v[g];
+    if (full) {
+      w.x += bv.x; w.y += bv.y; w.z += bv.z; w.w += bv.w;
       if (accumulate) {
         const float4 prev = *reinterpret_cast<const float4*>(dst);
-        v.x += prev.x; v.y += prev.y; v.z += prev.z; v.w += prev.w;
+        w.x += prev.x; w.y += prev.y; w.z += prev.z; w.w += prev.w;
       }
-      *reinterpret_cast<float4*>(dst) = v;
+      *reinterpret_cast<float4*>(dst) = w;
     } else {
-      const float e[4] = {v.x, v.y, v.z, v.w};
+      const float e[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (n + q < N) {
@@ -564,7 +607,6 @@ __device__ __forceinline__ void store_chunk_coalesced(const uint32_t (&r)[32], f
       }
     }
   }
-  __syncwarp();
 }
 
 // DXM: input-gradient epilogue flavour -- 0 = LUT slopes gathered from the
@@ -592,6 +634,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   const bool leader = rank == 0;
   const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;
   const int row_off = static_cast<int>(rank) * kBM;  // this CTA's rows inside a pair tile
+  if (threadIdx.x == 0) CK_TRACE(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a_hi);
@@ -623,8 +666,10 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) CK_TRACE(1);
   // everything above is CTA-local; operands and outputs are touched below
   pdl_wait();
+  if (threadIdx.x == 0) CK_TRACE(2);
 
   if (warp < kEpiWarp0) {
   reg_dealloc<kCtrlRegs>();  // (warpgroup-uniform)
@@ -717,6 +762,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           const uint32_t phase = (g / STAGES) & 1;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (g == 0) CK_TRACE(3);
           const uint32_t a_hi = smem_u32(smem + stage * C::kStageBytes);
           const uint32_t a_lo = a_hi + C::kABytes;
           const uint32_t b_hi = a_hi + 2 * C::kABytes;
@@ -766,6 +812,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         }
         }
       }
+      CK_TRACE(4);
     }
   }
   } else {
@@ -893,6 +940,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           ++seg;
           mbar_wait(&tfull[acc], use & 1);
           tc_fence_after();
+          if (seg == 1 && warp == kEpiWarp0 && lane == 0) CK_TRACE(5);
           const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
           for (int c = 32 * h; c < p.n_tile; c += 64) {
@@ -939,10 +987,12 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       }
     }
   }
+  if (warp == kEpiWarp0 && lane == 0) CK_TRACE(6);
   __syncwarp();  // reconverge the role warps before the aligned barriers
   if constexpr (CG == 2) {
     tc_fence_before();
     cluster_sync();  // no CTA leaves while its peer may still signal it
+    if (threadIdx.x == 0) CK_TRACE(7);
     if (warp == 1) {
       tc_fence_after();
       tmem_dealloc_pair(tmem_base, C::kTmemCols);
