@@ -60,6 +60,34 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
   return kOk;
 }
 
+// Output map of the TMA-store epilogue (see store_chunk_tma).  The copy
+// engine needs 16-byte aligned base and pitches; other layouts keep the
+// per-thread stores.
+int make_out_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t planes, int64_t ld,
+                 int64_t plane_stride) {
+  auto encode = get_encode();
+  if (!encode || (reinterpret_cast<uintptr_t>(base) & 15) != 0 || ld % 4 != 0 || plane_stride % 4 != 0 ||
+      rows < 1 || cols < 1 || planes < 1)
+    return kUnsupported;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(planes)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 4), static_cast<cuuint64_t>(plane_stride * 4)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? kOk : kUnsupported;
+}
+
+// CK_TMA_STORE=0: the store epilogue uses per-thread coalesced stores (A/B)
+bool tma_store_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CK_TMA_STORE");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 namespace {
 
 int gemm_bk() {

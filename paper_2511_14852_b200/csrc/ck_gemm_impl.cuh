@@ -36,6 +36,11 @@ namespace ck {
 // shared host helpers (ck_gemm.cu)
 int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t rows, int64_t segs, int64_t ld,
              int64_t seg_stride, int box_rows, int bk, int mn_major = 0);
+// fp32 output map for the TMA-store epilogue: dims (cols, rows, planes),
+// 32 x 32 boxes, SWIZZLE_128B; kUnsupported when the layout does not allow it
+int make_out_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t planes, int64_t ld,
+                 int64_t plane_stride);
+bool tma_store_enabled();
 int gemm_group();
 // pipeline iterations per accumulation segment of the store GEMMs
 // (kSegIters; CK_GEMM_SEG overrides, 0 = whole tile)
@@ -92,6 +97,8 @@ struct KArgs {
   const float* bias1;
   int accumulate;
   int out_trans;   // store out[n][m] (see GemmProblem::out_trans)
+  int tma_store;   // store epilogue writes through the output tensor map (TMA bulk store / reduce-add)
+  int tma_zmul;    // output map plane = split * tma_zmul + z
   // generated-operand forward (ck_gemm_gen.cu): x pitch and input count
   long long gen_ldx;
   int gen_I;
@@ -537,6 +544,64 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   return v;
 }
 
+// One 32 x 32 accumulator chunk through the TMA: the warp stages its rows
+// (+ bias) in its 1 KB-aligned 4 KB tile in the SWIZZLE_128B layout of the
+// output map's 32 x 32 box, and lane 0 issues one bulk tensor store (or
+// reduce-add for out +=) -- the copy engine writes the 4 KB, no per-thread
+// global stores.  Rows >= M / columns >= N of the box are clipped by the TMA.
+// The previous chunk's bulk read of the tile must be done before it is
+// rewritten (wait_group.read).
+__device__ __forceinline__ void store_chunk_tma(const uint32_t (&r)[32], float* tile, int lane, int row0, int nb,
+                                               int N, int plane, const CUtensorMap* map, const float* bias0,
+                                               const float* bias1, int accumulate) {
+  const uint32_t ts = smem_u32(tile);
+  float b[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) b[e] = 0.0f;
+  if (bias0 || bias1) {
+    if (nb + 32 <= N) {
+#pragma unroll
+      for (int e4 = 0; e4 < 8; ++e4) {
+        if (bias0) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(bias0 + nb) + e4);
+          b[4 * e4] += q.x; b[4 * e4 + 1] += q.y; b[4 * e4 + 2] += q.z; b[4 * e4 + 3] += q.w;
+        }
+        if (bias1) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(bias1 + nb) + e4);
+          b[4 * e4] += q.x; b[4 * e4 + 1] += q.y; b[4 * e4 + 2] += q.z; b[4 * e4 + 3] += q.w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        if (nb + e < N) {
+          if (bias0) b[e] += __ldg(bias0 + nb + e);
+          if (bias1) b[e] += __ldg(bias1 + nb + e);
+        }
+      }
+    }
+  }
+  if (lane == 0) bulk_wait_read_all();
+  __syncwarp();
+#pragma unroll
+  for (int c4 = 0; c4 < 8; ++c4) {
+    const int slot = c4 ^ (lane & 7);
+    sts128(ts + (lane * 32 + slot * 4) * 4, __uint_as_float(r[4 * c4]) + b[4 * c4],
+           __uint_as_float(r[4 * c4 + 1]) + b[4 * c4 + 1], __uint_as_float(r[4 * c4 + 2]) + b[4 * c4 + 2],
+           __uint_as_float(r[4 * c4 + 3]) + b[4 * c4 + 3]);
+  }
+  fence_proxy_async_smem();  // generic-proxy smem writes -> the bulk copy
+  __syncwarp();
+  if (lane == 0) {
+    if (accumulate) {
+      tma_reduce_add_3d(map, ts, nb, row0, plane);
+    } else {
+      tma_store_3d(map, ts, nb, row0, plane);
+    }
+    bulk_commit();
+  }
+}
+
 // One 32 x 32 accumulator chunk (this warp's 32 rows, columns nb..nb+31)
 // to the output through the warp's XOR-swizzled 4 KB staging tile: each
 // store instruction then writes four whole 128-byte row segments.  The
@@ -616,12 +681,15 @@ template <int BN, int BK, int STAGES, int EPI, int CG, int AMN, int BMN, int DXM
 __global__ void __launch_bounds__(gemm_threads(EW), 1)
     gemm_bf16x3_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                        const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
-                       const KArgs p) {
+                       const __grid_constant__ CUtensorMap tm_out, const KArgs p) {
   using C = Cfg<BN, BK, STAGES, CG>;
   constexpr int kRowBytes = C::kRowBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
+  // layout: operand stages | store epilogue staging tiles (4 KB per warp,
+  // 1 KB-aligned for the SWIZZLE_128B TMA box) | barriers
+  constexpr int kTileRegion = EPI == kEpiStore ? kEpiWarps * kEpiTileBytes : 0;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes + kTileRegion);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready (MMA -> epilogue)
   uint64_t* tempty = tfull + 2;      // [2] accumulator drained (epilogue -> MMA)
@@ -641,6 +709,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     tma_prefetch_desc(&tm_a_lo);
     tma_prefetch_desc(&tm_b_hi);
     tma_prefetch_desc(&tm_b_lo);
+    if (p.tma_store) tma_prefetch_desc(&tm_out);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -891,8 +960,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         float* out = p.out + static_cast<long long>(tc.z) * p.out_z_stride +
                      static_cast<long long>(tc.split) * p.out_split_stride;
         const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-        float* tile = reinterpret_cast<float*>(smem + STAGES * C::kStageBytes + C::kBarrierBytes) +
-                      (warp - kEpiWarp0) * (kEpiTileBytes / 4);
+        float* tile = reinterpret_cast<float*>(smem + STAGES * C::kStageBytes + (warp - kEpiWarp0) * kEpiTileBytes);
+        const int plane = tc.split * p.tma_zmul + tc.z;
         const int row0 = tc.m0 + row_off + q * 32;
         // one 32-column chunk (this thread's row) to the output, + bias
         auto store32 = [&](const uint32_t (&v)[32], int c) {
@@ -915,6 +984,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
                 }
               }
             }
+          } else if (p.tma_store) {
+            store_chunk_tma(v, tile, lane, row0, nb, p.N, plane, &tm_out, p.bias0, p.bias1, p.accumulate);
           } else {
             store_chunk_coalesced(v, tile, lane, row0, p.M, nb, p.N, out, p.ldo, p.bias0, p.bias1, p.accumulate, vec);
           }
@@ -987,6 +1058,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       }
     }
   }
+  if (EPI == kEpiStore && p.tma_store && warp >= kEpiWarp0 && lane == 0) bulk_wait_all();  // stores complete
   if (warp == kEpiWarp0 && lane == 0) CK_TRACE(6);
   __syncwarp();  // reconverge the role warps before the aligned barriers
   if constexpr (CG == 2) {
@@ -1070,6 +1142,18 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.pace_slack = 2;
   k.pace_tag = k.pace_window > 0 ? next_pace_tag() : 0;
   k.out_trans = p.out_trans;
+  // TMA-store epilogue: partial slots [split][z] must be one plane sequence
+  CUtensorMap to{};
+  k.tma_store = 0;
+  k.tma_zmul = 0;
+  if (EPI == kEpiStore && !p.out_trans && tma_store_enabled() &&
+      (splits == 1 || out_split_stride == static_cast<long long>(p.nz) * p.out_z_stride)) {
+    const int64_t planes = static_cast<int64_t>(p.nz) * splits;
+    if (make_out_map(&to, out, k.M, k.N, planes, p.ldo, planes > 1 ? p.out_z_stride : p.ldo * k.M) == kOk) {
+      k.tma_store = 1;
+      k.tma_zmul = splits > 1 ? p.nz : 0;
+    }
+  }
   auto kernel = gemm_bf16x3_kernel<BN, BK, STAGES, EPI, CG, AMN, BMN, DXM, EW>;
   // store kernels: + a 4 KB staging tile per epilogue warp
   constexpr int kSmem = C::kSmemBytes + (EPI == kEpiStore ? kEpiWarps * kEpiTileBytes : 0);
@@ -1113,7 +1197,7 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  CK_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta_hi, ta_lo, tb_hi, tb_lo, k));
+  CK_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta_hi, ta_lo, tb_hi, tb_lo, to, k));
   return kOk;
 }
 

@@ -35,8 +35,10 @@ fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = np.zeros((512, 8), dtype=np.uint64)
 for rep in range(4):
     forward_raw(x, prep, lut, None, cache)
-    if which != "fwd":
-        backward_raw(x, dy, prep, lut, True, cache=cache)
+    if which == "dx":
+        backward_raw(x, dy, prep, lut, True, want_dc=False, want_db=False, cache=cache)
+    elif which == "dc":
+        backward_raw(x, dy, prep, lut, True, want_dx=False, want_db=False, cache=cache)
     torch.cuda.synchronize()
 n = fn(buf.ctypes.data, 512)
 assert n > 0, "library built without CK_GEMM_TRACE"
