@@ -74,6 +74,7 @@ SIGNATURES = {
     "ck_launch_count": (ctypes.c_longlong, []),
     "ck_timing_enable": (_c_int, [_c_int]),
     "ck_timing_collect": (_c_int, [_c_dp, ctypes.POINTER(ctypes.c_longlong), _c_int]),
+    "ck_debug_gemm_trace": (_c_int, [ctypes.c_void_p, _c_int]),
 }
 
 KERNEL_CLASSES = ("gemm_fwd", "gemm_dx", "gemm_dc", "expand", "expand_t", "dx_combine", "split", "reduce", "lut",

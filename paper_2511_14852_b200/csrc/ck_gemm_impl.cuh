@@ -1142,11 +1142,18 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
   k.pace_slack = 2;
   k.pace_tag = k.pace_window > 0 ? next_pace_tag() : 0;
   k.out_trans = p.out_trans;
-  // TMA-store epilogue: partial slots [split][z] must be one plane sequence
+  // TMA-store epilogue for short reductions (<= 256 K chunks per tile), where
+  // the last tile's store is exposed: 256^2 d3 forward 24.3 -> 21.8 us, the
+  // C2 step 511 -> 501 us.  Long tiles (C4: 512 chunks) keep the per-thread
+  // stores: there the store hides behind the next tile's MMAs and the bulk
+  // stores, sharing the TMA unit with the operand loads, measured 0.3 %
+  // slower (3 alternating runs each, profiles/r02_session3.md).  Partial
+  // slots [split][z] must form one plane sequence.
   CUtensorMap to{};
   k.tma_store = 0;
   k.tma_zmul = 0;
-  if (EPI == kEpiStore && !p.out_trans && tma_store_enabled() &&
+  const int64_t chunks_per_tile = ceil_div(static_cast<int64_t>(k.S) * r_chunks, static_cast<int64_t>(splits));
+  if (EPI == kEpiStore && !p.out_trans && tma_store_enabled() && chunks_per_tile <= 256 &&
       (splits == 1 || out_split_stride == static_cast<long long>(p.nz) * p.out_z_stride)) {
     const int64_t planes = static_cast<int64_t>(p.nz) * splits;
     if (make_out_map(&to, out, k.M, k.N, planes, p.ldo, planes > 1 ? p.out_z_stride : p.ldo * k.M) == kOk) {

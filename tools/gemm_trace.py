@@ -9,7 +9,6 @@ done, 2 griddepcontrol.wait done, 3 first stage landed (MMA warp, leader),
 4 last MMA committed (leader), 5 first accumulator drained (epilogue warp 4),
 6 epilogue done (warp 4), 7 exit barrier passed.
 """
-import ctypes
 import sys
 
 import numpy as np
@@ -31,7 +30,6 @@ prep = PreparedCoeff(c)
 cache = torch.empty(ck.kernels.basis_cache_bytes(b, i, o, d + 1), dtype=torch.uint8, device=dev)
 lib = _lib.lib()
 fn = lib.ck_debug_gemm_trace
-fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = np.zeros((512, 8), dtype=np.uint64)
 for rep in range(4):
     forward_raw(x, prep, lut, None, cache)
