@@ -67,9 +67,22 @@ int gemm_sms();
 // the previous grid has completed and its memory is visible -- before it
 // touches global memory.  CK_PDL=0 disables the attribute (then the wait is a
 // no-op).
+//
+// Right after its own wait, every kernel signals griddepcontrol.launch_dependents:
+// the next kernel's grid may then launch as soon as every CTA of this one is
+// running, so its launch and its CTAs' prologues fill SMs as this kernel's
+// CTAs retire instead of after the whole grid (without the signal the
+// trigger is implicit at exit).  Safe by construction: every dependent
+// kernel still waits (griddepcontrol.wait) for this grid's completion and
+// memory before it reads anything.  CK_PDL_EARLY=0 builds omit the signal.
 bool pdl_enabled();
 
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#if !defined(CK_PDL_EARLY) || CK_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 template <typename... KArgsT, typename... Args>
 cudaError_t launch_k(void (*kernel)(KArgsT...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
