@@ -532,39 +532,56 @@ def run_ours(args, wl):
     e2e_mode = (f"eager, {n_mb} micro-batches of {mb} rows; the copy of micro-batch g+1 (the next step's first "
                 f"included) overlaps the compute of g")
     if graph is not None and n_mb == 1:
-        # launch-bound nets: the whole e2e step -- H2D copies of x/dy from
-        # pinned memory, forward, backward, Adam, D2H copy of the loss -- is
-        # one captured CUDA graph; every step still moves its inputs in and
-        # reads its loss back on the host
-        loss_h = torch.zeros((), dtype=torch.float32, pin_memory=True)
+        # launch-bound nets: the e2e step's compute -- forward, backward, Adam,
+        # D2H copy of the loss -- is one captured CUDA graph per input buffer;
+        # the H2D copy of step s+1's x/dy (pinned memory, copy stream) runs
+        # while step s computes, and every step's loss is read on the host
+        loss_h = [torch.zeros((), dtype=torch.float32, pin_memory=True) for _ in range(2)]
 
-        def e2e_body():
-            xb[0][:rows].copy_(x_h, non_blocking=True)
-            dyb[0][:rows].copy_(dy_h, non_blocking=True)
-            y = model(xb[0][:rows])
-            loss = torch.nn.functional.mse_loss(y, dyb[0][:rows])
+        def e2e_body(k):
+            y = model(xb[k][:rows])
+            loss = torch.nn.functional.mse_loss(y, dyb[k][:rows])
             loss.backward()
             opt.step()
             opt.zero_grad(set_to_none=True)
-            loss_h.copy_(loss.detach(), non_blocking=True)
+            loss_h[k].copy_(loss.detach(), non_blocking=True)
 
+        for k in range(2):
+            xb[k][:rows].copy_(x_h)
+            dyb[k][:rows].copy_(dy_h)
         side2 = torch.cuda.Stream(device=dev)
         side2.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side2):
-            for _ in range(2):
-                e2e_body()
+            for k in (0, 1, 0, 1):
+                e2e_body(k)
         torch.cuda.current_stream(dev).wait_stream(side2)
+        torch.cuda.synchronize(dev)
         barrier()
-        g_e2e = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_e2e):
-            e2e_body()
+        g_e2e = []
+        for k in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                e2e_body(k)
+            g_e2e.append(g)
+        torch.cuda.synchronize(dev)
 
         def e2e_step(step_no=0, prefetch_next_step=True):  # noqa: F811 (graph-replay form)
-            g_e2e.replay()
-            torch.cuda.current_stream(dev).synchronize()
-            return float(loss_h)
+            cur = torch.cuda.current_stream(dev)
+            k = step_no & 1
+            if pending["next"] != step_no:
+                issue_copy(step_no)
+            pending["next"] = None
+            if prefetch_next_step:
+                issue_copy(step_no + 1)  # overlaps this step's compute
+                pending["next"] = step_no + 1
+            cur.wait_event(ready[k])
+            g_e2e[k].replay()
+            free[k].record(cur)
+            cur.synchronize()
+            return float(loss_h[k])
 
-        e2e_mode = "one captured CUDA graph per step (H2D x/dy from pinned memory, step, D2H loss)"
+        e2e_mode = ("one captured CUDA graph per step (forward, backward, Adam, D2H loss, read on the host every "
+                    "step); the H2D copy of the next step's x/dy from pinned memory overlaps this step's compute")
     e2e_step(0, prefetch_next_step=False)  # warm the copy path; no copy left in flight
     barrier()
     e2e_steps = max(10, args.steps)
