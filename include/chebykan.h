@@ -252,6 +252,18 @@ CK_API int ck_allreduce_peers_flags(float* const* bufs, unsigned long long* cons
                                     int64_t lo, int64_t n, unsigned long long epoch, int max_blocks,
                                     void* stream);
 
+/* --- Loss ---------------------------------------------------------------------
+ * ck_mse_loss: the trainer's mean squared error (model.py:184-218): loss =
+ * mean((pred - target)^2) (float64 sums, deterministic) and/or grad = 2 (pred
+ * - target) / n, times *grad_scale when given (a device scalar, e.g.
+ * autograd's grad_output), in one pass; either output may be NULL.  The
+ * workspace (ck_mse_workspace_bytes, 16-byte aligned) must be zero-filled
+ * before its first use; each call leaves it ready for the next on the same
+ * stream. */
+CK_API size_t ck_mse_workspace_bytes(int64_t n);
+CK_API int ck_mse_loss(const float* pred, const float* target, int64_t n, float* loss, float* grad,
+                       const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream);
+
 /* --- Diagnostics --------------------------------------------------------------
  * ck_launch_count: kernels this library has launched in the process.
  * ck_timing_enable(1): bracket every launch with CUDA events on its stream;

@@ -82,6 +82,7 @@ from .model import (
     save_checkpoint,
     loss_fn,
     make_synthetic,
+    mse,
     mse_loss,
     network_train,
     rmsle_loss,

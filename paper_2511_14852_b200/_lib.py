@@ -75,6 +75,8 @@ SIGNATURES = {
     "ck_timing_enable": (_c_int, [_c_int]),
     "ck_timing_collect": (_c_int, [_c_dp, ctypes.POINTER(ctypes.c_longlong), _c_int]),
     "ck_debug_gemm_trace": (_c_int, [ctypes.c_void_p, _c_int]),
+    "ck_mse_workspace_bytes": (ctypes.c_size_t, [_c_i64]),
+    "ck_mse_loss": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, ctypes.c_size_t, _c_p]),
 }
 
 KERNEL_CLASSES = ("gemm_fwd", "gemm_dx", "gemm_dc", "expand", "expand_t", "dx_combine", "split", "reduce", "lut",

@@ -430,14 +430,22 @@ __device__ __forceinline__ void dx_epilogue_chord(const KArgs& p, uint32_t tbase
       near[e] = fr < p.guard || fr > 1.0f - p.guard;
     }
     if (cb + NH * W < n_lim) dx_load_x(p, xr, row_ok, n0 + cb + NH * W, xv);  // next block's x
+    // the block's guard-band boundary loads are all issued before any is
+    // consumed (one L2 round trip per block, not per band element)
+    float bl[W], bh[W];
 #pragma unroll
     for (int e = 0; e < W; ++e) {
+      bl[e] = bh[e] = 0.0f;
       if (near[e]) {
-        // exact reference cell: b_c <= x < b_{c+1}; at most one step off
         const float* rw = p.dxrows + static_cast<long long>(cell[e]) * S;
-        const float bl = __ldg(rw + D), bh = __ldg(rw + K);
-        cell[e] = min(cell[e] + (x_cur[e] < bl ? -1 : (x_cur[e] < bh ? 0 : 1)), N - 2);  // x = +inf: N-2
+        bl[e] = __ldg(rw + D);
+        bh[e] = __ldg(rw + K);
       }
+    }
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      // exact reference cell: b_c <= x < b_{c+1}; at most one step off
+      if (near[e]) cell[e] = min(cell[e] + (x_cur[e] < bl[e] ? -1 : (x_cur[e] < bh[e] ? 0 : 1)), N - 2);  // x = +inf: N-2
     }
     tmem_ld_wait();
     float acc[W];

@@ -132,8 +132,105 @@ int adam_launch(float* param, const float* grad, float* m, float* v, int64_t n, 
   return kOk;
 }
 
+// ---------------------------------------------------------------------------
+// Mean squared error (model.py:184-218 mse: mean((p - t)^2), gradient
+// 2 (p - t) / n) in one pass: each block sums its (p - t)^2 in float64 over a
+// fixed grid-stride partition and a fixed shared-memory tree; the last block
+// to finish (a counter in the workspace, reset by that block) adds the block
+// partials in block order -- deterministic for a given n and device.  The
+// gradient, optionally times a device scalar (autograd's grad_output), is
+// written in the same pass.
+constexpr int kMseThreads = 256;
+
+__global__ void __launch_bounds__(kMseThreads) mse_kernel(const float* __restrict__ pred,
+                                                          const float* __restrict__ target, int64_t n,
+                                                          float* __restrict__ loss, float* __restrict__ grad,
+                                                          const float* __restrict__ grad_scale,
+                                                          double* __restrict__ part, unsigned int* counter) {
+  pdl_wait();
+  __shared__ double red[kMseThreads];
+  __shared__ bool last;
+  const float gscale = (grad_scale ? grad_scale[0] : 1.0f);
+  const float nf = static_cast<float>(n);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  double acc = 0.0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(target) |
+                     reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+  auto one = [&](float p, float t) -> float {
+    const float d = p - t;
+    acc += static_cast<double>(d) * static_cast<double>(d);
+    return __fmul_rn(__fdiv_rn(__fmul_rn(2.0f, d), nf), gscale);  // 2 * diff / n (model.py order), x grad_out
+  };
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t i = t0; i < n4; i += stride) {
+    const float4 p = __ldg(reinterpret_cast<const float4*>(pred) + i);
+    const float4 t = __ldg(reinterpret_cast<const float4*>(target) + i);
+    float4 g;
+    g.x = one(p.x, t.x);
+    g.y = one(p.y, t.y);
+    g.z = one(p.z, t.z);
+    g.w = one(p.w, t.w);
+    if (grad) reinterpret_cast<float4*>(grad)[i] = g;
+  }
+  for (int64_t i = 4 * n4 + t0; i < n; i += stride) {
+    const float g = one(pred[i], target[i]);
+    if (grad) grad[i] = g;
+  }
+  if (loss == nullptr) return;
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = kMseThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = red[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += *reinterpret_cast<volatile double*>(part + b);
+    *loss = static_cast<float>(s / static_cast<double>(n));
+    *counter = 0u;  // ready for the next call
+  }
+}
+
+int mse_blocks(int64_t n) {
+  const int64_t want = ceil_div(ceil_div(n > 0 ? n : 1, 4), kMseThreads);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 4;
+  return static_cast<int>(want < cap ? want : cap);
+}
+
 }  // namespace
 }  // namespace ck
+
+extern "C" size_t ck_mse_workspace_bytes(int64_t n) {
+  // block partials (float64) + the completion counter
+  (void)n;  // the partials are per block; the grid is capped at 4 blocks per SM
+  return sizeof(double) * static_cast<size_t>(ck::num_sms()) * 4 + 16;
+}
+
+extern "C" int ck_mse_loss(const float* pred, const float* target, int64_t n, float* loss, float* grad,
+                           const float* grad_scale, void* workspace, size_t workspace_bytes, void* stream) {
+  CK_CHECK(n >= 1, "ck_mse_loss: empty input");
+  CK_CHECK(pred && target && (loss || grad), "ck_mse_loss: NULL tensor");
+  CK_CHECK(loss == nullptr || (workspace != nullptr && workspace_bytes >= ck_mse_workspace_bytes(n)),
+           "ck_mse_loss: workspace too small");
+  CK_CHECK((reinterpret_cast<uintptr_t>(workspace) & 15) == 0, "ck_mse_loss: workspace must be 16-byte aligned");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int blocks = ck::mse_blocks(n);
+  double* part = static_cast<double*>(workspace);
+  unsigned int* counter = loss ? reinterpret_cast<unsigned int*>(part + static_cast<size_t>(ck::num_sms()) * 4) : nullptr;
+  ck::LaunchScope scope(ck::kKOptim, s);
+  CK_CUDA(ck::launch_k((ck::mse_kernel), blocks, ck::kMseThreads, 0, s, pred, target, n, loss, grad, grad_scale, part,
+                       counter));
+  CK_CUDA(cudaGetLastError());
+  return ck::kOk;
+}
 
 extern "C" int ck_adam_step(float* param, const float* grad, float* m, float* v, int64_t n, double lr,
                             double beta1, double beta2, double eps, int64_t step, void* stream) {

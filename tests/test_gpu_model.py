@@ -236,3 +236,34 @@ def test_c2_c3_nets_follow_reference_trajectory(name):
             gb, wb = layer.bias.cpu().numpy(), g[f"bias_{i}"]
             print(f"  layer {i}: bias normwise {orc.normwise_err(gb, wb):.2e}")
             assert orc.normwise_err(gb, wb) <= 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 7, 4096, 1 << 20])
+def test_fused_mse_matches_float64_and_is_deterministic(n):
+    # ck_mse_loss: loss = mean((p - t)^2), grad = 2 (p - t) / n (model.py:184-218)
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cpu").manual_seed(n)
+    p = torch.randn(n, generator=g).to(dev)
+    t = torch.randn(n, generator=g).to(dev)
+    loss, grad = ck.model.mse_device(p, t)
+    pd, td = p.double().cpu().numpy(), t.double().cpu().numpy()
+    want = np.mean((pd - td) ** 2)
+    assert abs(float(loss) - want) <= 1e-6 * want
+    np.testing.assert_allclose(grad.cpu().numpy(), 2.0 * (pd - td) / n, rtol=2e-7, atol=1e-12)
+    again, _ = ck.model.mse_device(p, t)
+    assert float(again) == float(loss)  # fixed-order reduction
+
+
+@pytest.mark.gpu
+def test_fused_mse_autograd_matches_torch():
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(3)
+    y = torch.randn(333, 5, device=dev, requires_grad=True)
+    tgt = torch.randn(333, 5, device=dev, requires_grad=True)
+    (3.0 * ck.mse(y, tgt)).backward()
+    gy, gt = y.grad.clone(), tgt.grad.clone()
+    y.grad, tgt.grad = None, None
+    (3.0 * torch.nn.functional.mse_loss(y, tgt)).backward()
+    torch.testing.assert_close(gy, y.grad, rtol=1e-6, atol=1e-9)
+    torch.testing.assert_close(gt, tgt.grad, rtol=1e-6, atol=1e-9)
