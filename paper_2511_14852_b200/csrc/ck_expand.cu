@@ -97,6 +97,215 @@ __global__ void __launch_bounds__(kThreads) basis_eval_kernel(const float* __res
 }
 
 // --- specialized planes kernels ----------------------------------------------
+// Expand the 4 x values of one quad (row r, columns c..c+3) into planes
+// k = 1..D and store one 8-byte hi and lo word per plane; padded columns
+// (c+e >= cols) are written as zeros inside [cols, ld).
+template <int kSrc, int KIND, int D>
+__device__ __forceinline__ void quad_emit(const float (&xv)[4], int64_t r, int c, int cols, int lut_n,
+                                          uint2* __restrict__ hi, uint2* __restrict__ lo, int64_t ld, int64_t pq) {
+  uint32_t h0[D], l0[D], h1[D], l1[D];
+  {
+    float a[D], b[D];
+    elem_planes<kSrc, KIND, D>(xv[0], lut_n, a);
+    elem_planes<kSrc, KIND, D>(xv[1], lut_n, b);
+#pragma unroll
+    for (int k = 0; k < D; ++k) split_pack2(a[k], b[k], h0[k], l0[k]);
+  }
+  {
+    float a[D], b[D];
+    elem_planes<kSrc, KIND, D>(xv[2], lut_n, a);
+    elem_planes<kSrc, KIND, D>(xv[3], lut_n, b);
+#pragma unroll
+    for (int k = 0; k < D; ++k) split_pack2(a[k], b[k], h1[k], l1[k]);
+  }
+  const uint32_t m0 = c + 1 < cols ? 0xffffffffu : (c < cols ? 0xffffu : 0u);
+  const uint32_t m1 = c + 3 < cols ? 0xffffffffu : (c + 2 < cols ? 0xffffu : 0u);
+  uint2* hp = hi + ((r * ld + c) >> 2);
+  uint2* lp = lo + ((r * ld + c) >> 2);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    *hp = make_uint2(h0[k] & m0, h1[k] & m1);
+    *lp = make_uint2(l0[k] & m0, l1[k] & m1);
+    hp += pq;
+    lp += pq;
+  }
+  // the row's last quad also zero-fills the pitch padding [c + 4, ld): a
+  // partly written 32-byte sector at every row end made the L2 fetch it from
+  // DRAM first (ncu, 32000 x 257 d15: +31 MB of reads, half the write rate)
+  if (c + 4 >= cols && c + 4 < ld) {
+    for (int64_t w = c + 4; w < ld; w += 4) {
+      uint2* hz = hi + ((r * ld + w) >> 2);
+      uint2* lz = lo + ((r * ld + w) >> 2);
+      for (int k = 0; k < D; ++k) {
+        *hz = make_uint2(0u, 0u);
+        *lz = make_uint2(0u, 0u);
+        hz += pq;
+        lz += pq;
+      }
+    }
+  }
+}
+
+// B_{k+1} from B_k (cur) and B_{k-1} (prev): basis_f32's recurrence step k,
+// the same operations (bitwise the same values).
+template <int KIND>
+__device__ __forceinline__ float rec_next(int k, float x, float cur, float prev) {
+  if constexpr (KIND == kCheb) {
+    return fmaf(2.0f * x, cur, -prev);
+  } else if constexpr (KIND == kLegendre) {
+    const float num = fmaf(static_cast<float>(2 * k + 1) * x, cur, -static_cast<float>(k) * prev);
+    return num * (1.0f / static_cast<float>(k + 1));
+  } else {
+    return fmaf(2.0f * x, cur, -static_cast<float>(2 * k) * prev);
+  }
+}
+
+// quad_emit for the LUT path of the three-term families, streamed plane by
+// plane: the 8 node recurrences (4 elements x 2 grid nodes) advance one
+// feature at a time and each plane's hi/lo words are stored as soon as they
+// exist, so the state is 16 floats instead of 4 D-element arrays (d15: 114
+// registers, 23 % occupancy, issue-bound at ~13 instructions per value).
+// Bitwise the values of quad_emit.
+template <int KIND, int D>
+__device__ __forceinline__ void quad_emit_stream(const float (&xv)[4], int64_t r, int c, int cols, int lut_n,
+                                                 uint2* __restrict__ hi, uint2* __restrict__ lo, int64_t ld,
+                                                 int64_t pq) {
+  float f[4], xn[8], pv[8], cv[8];
+  const float step = 2.0f / static_cast<float>(lut_n - 1);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int idx;
+    cell_f32(xv[e], lut_n, idx, f[e]);
+    xn[2 * e] = grid_node_f(idx, lut_n, step);
+    xn[2 * e + 1] = grid_node_f(idx + 1, lut_n, step);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    pv[j] = 1.0f;
+    cv[j] = KIND == kHermite ? 2.0f * xn[j] : xn[j];  // B_1
+  }
+  const uint32_t m0 = c + 1 < cols ? 0xffffffffu : (c < cols ? 0xffffu : 0u);
+  const uint32_t m1 = c + 3 < cols ? 0xffffffffu : (c + 2 < cols ? 0xffffu : 0u);
+  uint2* hp = hi + ((r * ld + c) >> 2);
+  uint2* lp = lo + ((r * ld + c) >> 2);
+#pragma unroll
+  for (int k = 1; k <= D; ++k) {
+    if (k > 1) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float nv = rec_next<KIND>(k - 1, xn[j], cv[j], pv[j]);
+        pv[j] = cv[j];
+        cv[j] = nv;
+      }
+    }
+    uint32_t h0, l0, h1, l1;
+    split_pack2(lerp_ref(cv[0], cv[1], f[0]), lerp_ref(cv[2], cv[3], f[1]), h0, l0);
+    split_pack2(lerp_ref(cv[4], cv[5], f[2]), lerp_ref(cv[6], cv[7], f[3]), h1, l1);
+    *hp = make_uint2(h0 & m0, h1 & m1);
+    *lp = make_uint2(l0 & m0, l1 & m1);
+    hp += pq;
+    lp += pq;
+  }
+  if (c + 4 >= cols && c + 4 < ld) {  // pitch padding (see quad_emit)
+    for (int64_t w = c + 4; w < ld; w += 4) {
+      uint2* hz = hi + ((r * ld + w) >> 2);
+      uint2* lz = lo + ((r * ld + w) >> 2);
+      for (int k = 0; k < D; ++k) {
+        *hz = make_uint2(0u, 0u);
+        *lz = make_uint2(0u, 0u);
+        hz += pq;
+        lz += pq;
+      }
+    }
+  }
+}
+
+template <int kSrc, int KIND, int D>
+__device__ __forceinline__ void quad_out(const float (&xv)[4], int64_t r, int c, int cols, int lut_n,
+                                         uint2* __restrict__ hi, uint2* __restrict__ lo, int64_t ld, int64_t pq) {
+  if constexpr (kSrc == kSrcNodes && (KIND == kCheb || KIND == kLegendre || KIND == kHermite)) {
+    quad_emit_stream<KIND, D>(xv, r, c, cols, lut_n, hi, lo, ld, pq);
+  } else {
+    quad_emit<kSrc, KIND, D>(xv, r, c, cols, lut_n, hi, lo, ld, pq);
+  }
+}
+
+// Ragged rows (cols % 4 != 0: x rows are not 16-byte aligned, e.g. the 257
+// spectrogram bins of the C3 input layer): a block's 256 consecutive quads
+// cover one contiguous stretch of x, loaded cooperatively with aligned
+// 16-byte loads into shared memory; each thread then reads its quad there.
+// (Per-thread scalar loads left this case at half the aligned layers' write
+// rate: ncu 12 long-scoreboard stalls per issue, LSU throttle.)
+template <int kSrc, int KIND, int D>
+__device__ __forceinline__ void quads_ragged(const float* __restrict__ x, int64_t rows, int cols, int lut_n,
+                                             uint2* __restrict__ hi, uint2* __restrict__ lo, int64_t ld,
+                                             int64_t pq) {
+  __shared__ float sx[4 * (kThreads + 2)];
+  const int quads = (cols + 3) >> 2;
+  const int64_t n_items = rows * quads;
+  const int64_t total = rows * cols;
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int64_t bstride = static_cast<int64_t>(gridDim.x) * kThreads;
+  // stretch of x covered by the block's quads [base, base + 256): first
+  // aligned float index and the number of 16-byte slots
+  auto stretch = [&](int64_t base, int64_t& rb, int& qb, int64_t& a0) -> int {
+    const int64_t last = (base + kThreads < n_items ? base + kThreads : n_items) - 1;
+    rb = base / quads;
+    qb = static_cast<int>(base - rb * quads);
+    const int64_t rl = last / quads;
+    const int ql = static_cast<int>(last - rl * quads);
+    const int64_t f1 = rl * cols + (4 * ql + 4 < cols ? 4 * ql + 4 : cols);  // exclusive
+    a0 = (rb * cols + 4 * qb) & ~static_cast<int64_t>(3);
+    return static_cast<int>((f1 - a0 + 3) >> 2);  // <= kThreads + 2
+  };
+  auto load_slot = [&](int64_t a) -> float4 {
+    float4 v;
+    if (aligned && a + 4 <= total) {
+      v = __ldg(reinterpret_cast<const float4*>(x + a));
+    } else {
+      v.x = a < total ? __ldg(x + a) : 0.0f;
+      v.y = a + 1 < total ? __ldg(x + a + 1) : 0.0f;
+      v.z = a + 2 < total ? __ldg(x + a + 2) : 0.0f;
+      v.w = a + 3 < total ? __ldg(x + a + 3) : 0.0f;
+    }
+    return v;
+  };
+  // the next stretch is loaded into registers while the current one is
+  // expanded (slots tid and, for tid < 2, 256 + tid)
+  float4 nx0 = make_float4(0.f, 0.f, 0.f, 0.f), nx1 = nx0;
+  auto prefetch = [&](int64_t base) {
+    if (base >= n_items) return;
+    int64_t rb, a0;
+    int qb;
+    const int nv = stretch(base, rb, qb, a0);
+    if (static_cast<int>(threadIdx.x) < nv) nx0 = load_slot(a0 + 4 * threadIdx.x);
+    if (static_cast<int>(threadIdx.x) + kThreads < nv) nx1 = load_slot(a0 + 4 * (threadIdx.x + kThreads));
+  };
+  int64_t base = blockIdx.x * static_cast<int64_t>(kThreads);
+  prefetch(base);
+  for (; base < n_items; base += bstride) {
+    int64_t rb, a0;
+    int qb;
+    const int nv = stretch(base, rb, qb, a0);
+    __syncthreads();  // the previous stretch's readers are done
+    if (static_cast<int>(threadIdx.x) < nv) *reinterpret_cast<float4*>(sx + 4 * threadIdx.x) = nx0;
+    if (static_cast<int>(threadIdx.x) + kThreads < nv) *reinterpret_cast<float4*>(sx + 4 * (threadIdx.x + kThreads)) = nx1;
+    __syncthreads();
+    prefetch(base + bstride);
+    const int64_t it = base + threadIdx.x;
+    if (it < n_items) {
+      const int qq = qb + static_cast<int>(threadIdx.x);
+      const int64_t r = rb + qq / quads;
+      const int c = (qq % quads) * 4;
+      const int64_t off = r * cols + c - a0;
+      float xv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) xv[e] = c + e < cols ? sx[off + e] : 0.0f;
+      quad_out<kSrc, KIND, D>(xv, r, c, cols, lut_n, hi, lo, ld, pq);
+    }
+  }
+}
+
 // Planes k = 1..D, hi/lo [k-1][r][ld]: each thread expands 4 adjacent
 // columns of one row (two bf16x2 pairs) and writes one 8-byte word per plane
 // for hi and lo (a warp stores 256 contiguous bytes per plane).
@@ -108,6 +317,10 @@ __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __r
   const int64_t pq = plane >> 2;  // plane stride in 8-byte words
   const int quads = (cols + 3) >> 2;
   const bool vec = (cols & 3) == 0;
+  if (!vec) {
+    quads_ragged<kSrc, KIND, D>(x, rows, cols, lut_n, hi, lo, ld, pq);
+    return;
+  }
   // grid-stride over (row, quad) items, advanced incrementally (one division
   // per thread instead of a 64-bit division per item)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -150,33 +363,7 @@ __global__ void __launch_bounds__(kThreads) expand_quads_kernel(const float* __r
       }
       load_x(rn, qn, xn);
     }
-    uint32_t h0[D], l0[D], h1[D], l1[D];
-    {
-      float a[D], b[D];
-      elem_planes<kSrc, KIND, D>(xv[0], lut_n, a);
-      elem_planes<kSrc, KIND, D>(xv[1], lut_n, b);
-#pragma unroll
-      for (int k = 0; k < D; ++k) split_pack2(a[k], b[k], h0[k], l0[k]);
-    }
-    {
-      float a[D], b[D];
-      elem_planes<kSrc, KIND, D>(xv[2], lut_n, a);
-      elem_planes<kSrc, KIND, D>(xv[3], lut_n, b);
-#pragma unroll
-      for (int k = 0; k < D; ++k) split_pack2(a[k], b[k], h1[k], l1[k]);
-    }
-    // padded columns (c+e >= cols) are written as zeros inside [cols, ld)
-    const uint32_t m0 = c + 1 < cols ? 0xffffffffu : (c < cols ? 0xffffu : 0u);
-    const uint32_t m1 = c + 3 < cols ? 0xffffffffu : (c + 2 < cols ? 0xffffu : 0u);
-    uint2* hp = hi + ((r * ld + c) >> 2);
-    uint2* lp = lo + ((r * ld + c) >> 2);
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      *hp = make_uint2(h0[k] & m0, h1[k] & m1);
-      *lp = make_uint2(l0[k] & m0, l1[k] & m1);
-      hp += pq;
-      lp += pq;
-    }
+    quad_out<kSrc, KIND, D>(xv, r, c, cols, lut_n, hi, lo, ld, pq);
   }
 }
 

@@ -157,10 +157,12 @@ __global__ void __launch_bounds__(kMseThreads) mse_kernel(const float* __restric
   double acc = 0.0;
   const bool vec = ((reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(target) |
                      reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+  const bool want_grad = grad != nullptr;
   auto one = [&](float p, float t) -> float {
     const float d = p - t;
     acc += static_cast<double>(d) * static_cast<double>(d);
-    return __fmul_rn(__fdiv_rn(__fmul_rn(2.0f, d), nf), gscale);  // 2 * diff / n (model.py order), x grad_out
+    // 2 * diff / n (model.py order), x grad_out
+    return want_grad ? __fmul_rn(__fdiv_rn(__fmul_rn(2.0f, d), nf), gscale) : 0.0f;
   };
   const int64_t n4 = vec ? n / 4 : 0;
   for (int64_t i = t0; i < n4; i += stride) {
@@ -190,11 +192,21 @@ __global__ void __launch_bounds__(kMseThreads) mse_kernel(const float* __restric
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += *reinterpret_cast<volatile double*>(part + b);
-    *loss = static_cast<float>(s / static_cast<double>(n));
+  if (!last) return;
+  // the last block folds the block partials: thread j sums partials j, j +
+  // 256, ... in order, then the same fixed tree (a serial fold of ~600
+  // partials took 30 us of L2 round trips)
+  __threadfence();
+  double s = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += kMseThreads) s += __ldcg(part + b);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kMseThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *loss = static_cast<float>(red[0] / static_cast<double>(n));
     *counter = 0u;  // ready for the next call
   }
 }
