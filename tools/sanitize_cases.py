@@ -58,6 +58,22 @@ def case_partial():
     torch.cuda.synchronize()
 
 
+def case_short():
+    # TMA-store epilogue (<= 256 K chunks, 16-byte pitches): forward with
+    # bias, split-R partial planes, multi-chunk dC with bulk reduce-add
+    layer_step(600, 96, 300, 5, chunk=256)
+    layer_step(512, 64, 512, 5)
+    layer_step(4000, 64, 256, 3, chunk=1024)
+
+
+def case_mse():
+    for n in (1, 7, 4099, 1 << 20):
+        p = torch.randn(n, device=dev, requires_grad=True)
+        t = torch.randn(n, device=dev)
+        (2.0 * ck.mse(p, t)).backward()
+    torch.cuda.synchronize()
+
+
 def case_adam():
     ps = [torch.nn.Parameter(torch.randn(n, device=dev)) for n in (1, 0, 5, 4099, 70000)]
     for p in ps:
@@ -82,7 +98,7 @@ def case_peer():
     torch.cuda.synchronize()
 
 
-CASES = {"gemm": case_gemm, "gen": case_gen, "skinny": case_skinny, "partial": case_partial, "adam": case_adam,
+CASES = {"short": case_short, "mse": case_mse, "gemm": case_gemm, "gen": case_gen, "skinny": case_skinny, "partial": case_partial, "adam": case_adam,
          "peer": case_peer}
 
 if __name__ == "__main__":
