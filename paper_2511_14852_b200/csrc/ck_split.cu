@@ -221,8 +221,17 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const float* __restrict
     if (t < sum_blocks) {
       const int64_t o = t * 8 + w;
       if (o < O) {
+        // 8 loads in flight per lane, added in index order
         double acc = 0.0;
-        for (int64_t i = lane; i < I; i += 32) acc += static_cast<double>(c[o * I + i]);
+        int64_t i = lane;
+        for (; i + 7 * 32 < I; i += 8 * 32) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldg(c + o * I + i + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc += static_cast<double>(v[u]);
+        }
+        for (; i < I; i += 32) acc += static_cast<double>(c[o * I + i]);
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
         if (lane == 0) c0sum[o] = static_cast<float>(acc);
@@ -235,31 +244,38 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const float* __restrict
     const int64_t o0 = (rem / it_) * 64, i0 = (rem % it_) * 64;
     const float* src = c + k * O * I;
     const int64_t i = i0 + 2 * lane;
-#pragma unroll 4
+    // all 8 row loads in flight before any store (the tile loop was a chain
+    // of L2 round trips: ~35 % of HBM at 512^2)
+    float av[8], bv[8];
+#pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const int ol = w + 8 * r;
-      const int64_t o = o0 + ol;
-      float a = 0.0f, b = 0.0f;
+      const int64_t o = o0 + w + 8 * r;
+      av[r] = bv[r] = 0.0f;
       if (o < O) {
         const float* p = src + o * I + i;
         if (pairs && i < I) {
           const float2 v = __ldg(reinterpret_cast<const float2*>(p));
-          a = v.x;
-          b = v.y;
+          av[r] = v.x;
+          bv[r] = v.y;
         } else {
-          a = i < I ? __ldg(p) : 0.0f;
-          b = i + 1 < I ? __ldg(p + 1) : 0.0f;
-        }
-        if (i < I) {  // (i + 1 = I odd: the pad element of the row gets 0)
-          uint32_t h2, l2;
-          split_pack2(a, b, h2, l2);
-          const int64_t q = ((k * O + o) * ldI + i) >> 1;
-          dh[q] = h2;
-          dl[q] = l2;
+          av[r] = i < I ? __ldg(p) : 0.0f;
+          bv[r] = i + 1 < I ? __ldg(p + 1) : 0.0f;
         }
       }
-      tile[ol][2 * lane] = a;
-      tile[ol][2 * lane + 1] = b;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int ol = w + 8 * r;
+      const int64_t o = o0 + ol;
+      if (o < O && i < I) {  // (i + 1 = I odd: the pad element of the row gets 0)
+        uint32_t h2, l2;
+        split_pack2(av[r], bv[r], h2, l2);
+        const int64_t q = ((k * O + o) * ldI + i) >> 1;
+        dh[q] = h2;
+        dl[q] = l2;
+      }
+      tile[ol][2 * lane] = av[r];
+      tile[ol][2 * lane + 1] = bv[r];
     }
     if (k == 0) continue;  // (uniform per block: no barrier skipped by part of it)
     __syncthreads();
@@ -269,8 +285,9 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const float* __restrict
       const int il = w + 8 * r;
       const int64_t ii = i0 + il;
       if (ii >= i_pad) break;  // uniform per warp (ii grows with r)
-      const int64_t blk = ii / n_i;
-      const int64_t row = blk * d * n_i + (k - 1) * n_i + (ii - blk * n_i);
+      const int iiw = static_cast<int>(ii);  // (32-bit division: inputs < 2^31)
+      const int blk = iiw / n_i;
+      const int64_t row = static_cast<int64_t>(blk) * d * n_i + (k - 1) * n_i + (iiw - blk * n_i);
       if (o < ldO) {
         uint32_t h2, l2;
         split_pack2(tile[2 * lane][il], tile[2 * lane + 1][il], h2, l2);
