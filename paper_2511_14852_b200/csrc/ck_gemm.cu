@@ -100,14 +100,20 @@ int gemm_bk() {
 
 }  // namespace
 
-// Rasterisation group size (m-tiles per group; CK_GEMM_GROUP overrides).
-int gemm_group() {
+// Rasterisation group size (m-tiles per group) for a problem with m_tiles
+// rows of tiles; CK_GEMM_GROUP overrides.  16 for tall problems (>= 128
+// m-tiles: the C4 chunks of 32768 rows): the C4 training step went 517-523k
+// -> 542-547k samples/s against 8 (eight interleaved runs on one box,
+// profiles/r02_session3.md) -- the same work per clock at ~5 % higher
+// power-capped clocks, ~9 % less L2->SM traffic for the forward and dC GEMMs
+// (ncu).  8 below that (the 16384-row C1 layers: 8 measured 0.3-1.5 % faster).
+int gemm_group(int m_tiles) {
   static int g = [] {
     const char* e = getenv("CK_GEMM_GROUP");
-    const int v = e ? atoi(e) : 8;
-    return v >= 1 && v <= 1024 ? v : 8;
+    const int v = e ? atoi(e) : 0;
+    return v >= 1 && v <= 1024 ? v : 0;
   }();
-  return g;
+  return g > 0 ? g : (m_tiles >= 128 ? 16 : 8);
 }
 
 int gemm_pace() {

@@ -122,9 +122,9 @@ int gemm_gen_forward(const float* x, int64_t M, int I, int O, const LutView& v, 
   k.ldo = O;
   k.bias0 = bias0;
   k.bias1 = bias1;
-  k.group_m = gemm_group();
   k.n_tiles = static_cast<int>(ceil_div(O, n_tile));
   k.m_tiles = static_cast<int>(ceil_div(M, 256));
+  k.group_m = gemm_group(k.m_tiles);
   const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles;
   CK_CHECK(total < (1ll << 31), "gemm_gen: too many tiles");
   k.total_tiles = static_cast<int>(total);

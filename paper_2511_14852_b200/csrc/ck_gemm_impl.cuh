@@ -41,7 +41,7 @@ int make_map(CUtensorMap* map, const __nv_bfloat16* base, int64_t R, int64_t row
 int make_out_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t planes, int64_t ld,
                  int64_t plane_stride);
 bool tma_store_enabled();
-int gemm_group();
+int gemm_group(int m_tiles);
 // pipeline iterations per accumulation segment of the store GEMMs
 // (kSegIters; CK_GEMM_SEG overrides, 0 = whole tile)
 int gemm_seg();
@@ -1182,9 +1182,9 @@ int launch(const GemmProblem& p, int splits, float* out, long long out_split_str
     CK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr_set.fetch_or(bit);
   }
-  k.group_m = gemm_group();
   k.n_tiles = static_cast<int>(ceil_div(k.N, n_tile));
   k.m_tiles = static_cast<int>(ceil_div(k.M, kBM * CG));
+  k.group_m = gemm_group(k.m_tiles);
   const long long total = static_cast<long long>(k.n_tiles) * k.m_tiles * p.nz * splits;
   CK_CHECK(total < (1ll << 31), "gemm: too many tiles");
   k.total_tiles = static_cast<int>(total);
