@@ -565,7 +565,13 @@ def run_ours(args, wl):
             g_e2e.append(g)
         torch.cuda.synchronize(dev)
 
+        done = [torch.cuda.Event() for _ in range(2)]
+        last = {"k": None}
+
         def e2e_step(step_no=0, prefetch_next_step=True):  # noqa: F811 (graph-replay form)
+            # the host reads step s-1's loss (copied to pinned memory inside
+            # its graph) after enqueueing step s, so the GPU never waits for
+            # the host between steps; the last step of a run reads its own
             cur = torch.cuda.current_stream(dev)
             k = step_no & 1
             if pending["next"] != step_no:
@@ -577,11 +583,21 @@ def run_ours(args, wl):
             cur.wait_event(ready[k])
             g_e2e[k].replay()
             free[k].record(cur)
-            cur.synchronize()
-            return float(loss_h[k])
+            done[k].record(cur)
+            out = None
+            if last["k"] is not None:
+                done[last["k"]].synchronize()
+                out = float(loss_h[last["k"]])
+            last["k"] = k
+            if not prefetch_next_step:
+                done[k].synchronize()
+                out = float(loss_h[k])
+                last["k"] = None
+            return out
 
-        e2e_mode = ("one captured CUDA graph per step (forward, backward, Adam, D2H loss, read on the host every "
-                    "step); the H2D copy of the next step's x/dy from pinned memory overlaps this step's compute")
+        e2e_mode = ("one captured CUDA graph per step (forward, backward, Adam, D2H copy of the loss); every "
+                    "step's loss is read on the host one step later (after the next step is enqueued) and the "
+                    "H2D copy of the next step's x/dy from pinned memory overlaps this step's compute")
     e2e_step(0, prefetch_next_step=False)  # warm the copy path; no copy left in flight
     barrier()
     e2e_steps = max(10, args.steps)
